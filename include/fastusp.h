@@ -1,0 +1,158 @@
+/* fastusp -- B200-native USP (Ulysses x Ring) joint-attention layer, C ABI.
+ *
+ * Drop-in for the reference's uspsim USP attention API
+ * (/root/reference/proj/include/uspsim/protocols.hpp, tensor.hpp, fp8.hpp, mesh.hpp).
+ * Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers unless a function says "_host".
+ *  - Tensors are dense [B,H,S,D], row-major, d fastest (= uspsim::Tensor4T, tensor.hpp:29-61).
+ *  - Every function returns fusp_status; the message of the last failure on the calling
+ *    thread is fusp_last_error() (same text as the reference exception's what()).
+ *  - Stream-ordered: functions enqueue on `stream` and return; they do not synchronize
+ *    unless documented (options.check_finite, the _host variants).
+ *  - Collective functions (usp/ulysses/ring) must be called by every rank of the mesh in
+ *    the same order, like uspsim::run_protocol programs (fabric.cpp:211-213) and NCCL.
+ */
+#ifndef FASTUSP_H_
+#define FASTUSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fusp_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+/* Status codes map 1:1 onto the reference's exception classes. */
+typedef enum {
+  FUSP_OK = 0,
+  FUSP_ERR_SHAPE = 1,            /* uspsim::ShapeError           tensor.hpp:13-16  */
+  FUSP_ERR_MESH = 2,             /* uspsim::MeshError            mesh.hpp:17-20    */
+  FUSP_ERR_COMM = 3,             /* uspsim::FabricError          fabric.hpp:106    */
+  FUSP_ERR_INVALID_ARGUMENT = 4, /* std::invalid_argument (non-finite input) protocols.cpp:103, fp8.cpp:112 */
+  FUSP_ERR_DEADLOCK = 5,         /* uspsim::DeadlockError        fabric.hpp:112    */
+  FUSP_ERR_CUDA = 10,
+  FUSP_ERR_NCCL = 11,
+  FUSP_ERR_OOM = 12,
+  FUSP_ERR_UNSUPPORTED = 13
+} fusp_status;
+
+typedef enum { FUSP_F32 = 0, FUSP_F16 = 1, FUSP_BF16 = 2, FUSP_E4M3 = 3 } fusp_dtype;
+
+/* = uspsim::Shape4 (tensor.hpp:18-26) */
+typedef struct {
+  int64_t b, h, s, d;
+} fusp_shape4;
+
+/* = uspsim::CommOptions (protocols.hpp:12-15) plus B200 extensions. */
+typedef struct {
+  int fp8_kv;         /* quantize K/V payloads (scale + E4M3 codes), protocols.hpp:13 */
+  int pipelined_ring; /* double-buffered ring on a side stream, protocols.hpp:14 */
+  int out_dtype;      /* fusp_dtype of the layer output (F32 = reference) */
+  int check_finite;   /* 1: validate inputs like check_local_qkv (protocols.cpp:97-105); syncs */
+  int fp8_block;      /* 0 = per-tensor scale (reference); 1 = one scale per (b,h) head slab */
+} fusp_comm_options;
+
+const char* fusp_last_error(void);
+const char* fusp_version(void);
+/* Number of fastusp CUDA kernels launched so far by this process (all devices). */
+uint64_t fusp_kernel_launch_count(void);
+
+/* ---- FP8 E4M3 codec (fp8.hpp:23-49) ---------------------------------------------------- */
+/* encode_e4m3 (fp8.cpp:45-68), elementwise: f32 -> code.  Bit-exact. */
+fusp_status fusp_encode_e4m3(const float* x, int64_t n, uint8_t* codes, fusp_stream_t stream);
+/* decode_e4m3 (fp8.cpp:39-43), elementwise: code -> f32 (NaN codes -> NaN). */
+fusp_status fusp_decode_e4m3(const uint8_t* codes, int64_t n, float* y, fusp_stream_t stream);
+/* quantize (fp8.cpp:107-123): *scale_dev = max|x|/448 (1 if all zero), codes = RNE(x/scale).
+ * x dtype F32/F16/BF16.  Bit-exact codes and scale.  Non-finite input -> FUSP_ERR_INVALID_ARGUMENT
+ * (synchronizes to report it; pass check_finite=0 to skip the check and stay async). */
+fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8_t* codes,
+                               float* scale_dev, int check_finite, fusp_stream_t stream);
+/* dequantize (fp8.cpp:125-130): y = decode(code) * (*scale_dev), written as `dtype`. */
+fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, int64_t n, void* y,
+                                 fusp_dtype dtype, fusp_stream_t stream);
+
+/* ---- single-GPU attention numerics (tensor.hpp:91-98) ----------------------------------- */
+/* attention_with_lse (tensor.cpp:193-202): q [B,H,Sq,D], k,v [B,H,Skv,D], all `in_dtype`
+ * (F32/BF16/F16; computed as bf16 Q.K^T and f16 P.V with f32 accumulation).
+ * out [B,H,Sq,D] in out_dtype; lse [B,H,Sq] f32 natural log (nullable). Skv = 0 gives
+ * out = 0, lse = -inf (tensor.cpp:161-164).  D must be 128. */
+fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
+                                    fusp_dtype in_dtype, fusp_shape4 q_shape, int64_t skv,
+                                    void* out, fusp_dtype out_dtype, float* lse,
+                                    fusp_stream_t stream);
+/* merge_lse (tensor.cpp:204-243): f32 o1,o2 [B,H,S,D], l1,l2 [B,H,S] -> out, lse (may alias o1/l1). */
+fusp_status fusp_merge_lse(const float* o1, const float* l1, const float* o2, const float* l2,
+                           fusp_shape4 shape, float* out, float* lse, fusp_stream_t stream);
+
+/* ---- mesh (mesh.hpp:27-50) -------------------------------------------------------------- */
+/* build_mesh (mesh.cpp:57-79): largest feasible R <= max_ring with n%R==0 and heads%(n/R)==0. */
+fusp_status fusp_mesh_build(int n, int max_ring_dim_size, int heads, int* r, int* u);
+/* make_mesh (mesh.cpp:34-55): ulysses_groups [R][U], ring_groups [U][R] (rank = ring*U + uly). */
+fusp_status fusp_mesh_make(int n, int r, int* ulysses_groups, int* ring_groups);
+
+/* ---- per-rank context (replaces uspsim::WorkerContext, fabric.hpp:136-166) --------------- */
+typedef struct fusp_fabric_s* fusp_fabric; /* in-process fabric: threads as ranks (fabric.cpp:280) */
+typedef struct fusp_ctx_s* fusp_ctx;
+
+fusp_status fusp_fabric_create(int world, fusp_fabric* out);
+fusp_status fusp_fabric_destroy(fusp_fabric f);
+/* A rank of an in-process fabric; `device` may be shared by several ranks (tests). */
+fusp_status fusp_ctx_create_local(fusp_fabric f, int rank, int device, fusp_ctx* out);
+/* One process (or thread) per GPU over NCCL; uid from fusp_nccl_unique_id on one rank. */
+fusp_status fusp_nccl_unique_id(uint8_t uid[128]);
+fusp_status fusp_ctx_create_nccl(const uint8_t uid[128], int world, int rank, int device,
+                                 fusp_ctx* out);
+fusp_status fusp_ctx_destroy(fusp_ctx ctx);
+int fusp_ctx_rank(fusp_ctx ctx);
+int fusp_ctx_world(fusp_ctx ctx);
+/* Bytes this rank put on the wire since creation, self-traffic excluded, per op:
+ * = TrafficLog::bytes_for("all_to_all"|"send", rank) (fabric.cpp:44-49). */
+fusp_status fusp_ctx_traffic(fusp_ctx ctx, uint64_t* all_to_all_bytes, uint64_t* send_bytes);
+fusp_status fusp_ctx_reset_traffic(fusp_ctx ctx);
+/* Per-step device timings of the last ring call (ms): compute[i], comm[i] for i < R. */
+fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms, float* comm_ms,
+                                  int* steps);
+
+/* ---- distributed protocols (protocols.hpp:47-71) ------------------------------------------ */
+/* usp_attention (protocols.cpp:321-340) on mesh make_mesh(world, ring_dim).
+ * q,k,v: local shards [B,H,S/N,D] (in_dtype F32/BF16/F16); out: [B,H,S/N,D] in opts->out_dtype. */
+fusp_status fusp_usp_attention(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                               const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                               void* out, const fusp_comm_options* opts, fusp_stream_t stream);
+/* ulysses_attention (protocols.cpp:207-214) over the whole world. */
+fusp_status fusp_ulysses_attention(fusp_ctx ctx, const void* q, const void* k, const void* v,
+                                   fusp_dtype in_dtype, fusp_shape4 local_shape, void* out,
+                                   const fusp_comm_options* opts, fusp_stream_t stream);
+/* ring_attention_{serial,pipelined} (protocols.cpp:237-319) over the whole world:
+ * out [B,H,S/N,D] in opts->out_dtype and lse [B,H,S/N] f32 (nullable). */
+fusp_status fusp_ring_attention(fusp_ctx ctx, const void* q, const void* k, const void* v,
+                                fusp_dtype in_dtype, fusp_shape4 local_shape, void* out,
+                                float* lse, const fusp_comm_options* opts, fusp_stream_t stream);
+
+/* Host-buffer variant of fusp_usp_attention (the reference's calling convention: host
+ * tensors in, host tensor out).  Copies H2D, runs, copies D2H, synchronizes. */
+fusp_status fusp_usp_attention_host(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                                    const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                    void* out, const fusp_comm_options* opts,
+                                    fusp_stream_t stream);
+
+/* ---- CUDA Graph of the per-layer launch sequence (no reference counterpart) -------------- */
+typedef struct fusp_graph_s* fusp_graph;
+/* Captures `layers` back-to-back fusp_usp_attention calls (layer i reads q/k/v + i*layer_stride
+ * bytes and writes out + i*out_stride bytes) into one CUDA graph. NCCL or world-1 contexts. */
+fusp_status fusp_graph_capture_usp(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                                   const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                   void* out, const fusp_comm_options* opts, int layers,
+                                   int64_t in_layer_stride_bytes, int64_t out_layer_stride_bytes,
+                                   fusp_stream_t stream, fusp_graph* graph);
+fusp_status fusp_graph_launch(fusp_graph graph, fusp_stream_t stream);
+fusp_status fusp_graph_destroy(fusp_graph graph);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTUSP_H_ */

@@ -1,0 +1,13 @@
+"""fastusp for B200: the FastUSP (arXiv 2602.10940) USP joint-attention layer.
+
+Host-side mirror of the reference's uspsim API over the C ABI in
+include/fastusp.h (libfastusp.so: hand-written sm_100a kernels + NCCL).
+"""
+from ._lib import (BF16, E4M3, F16, F32, FabricError, FuspError, InvalidArgument, MeshError,
+                   ShapeError, build)
+from .api import (AttnResult, Mesh2D, ProcessGroup, QuantizedTensor, attention_reference,
+                  attention_with_lse, build_mesh, decode_e4m3, dequantize, encode_e4m3,
+                  kernel_launch_count, make_mesh, merge_lse, quantize, kFp8Max, kFp8MaxCode,
+                  kFp8NanCode)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

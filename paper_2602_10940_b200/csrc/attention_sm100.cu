@@ -1,0 +1,388 @@
+// tcgen05 / TMEM / TMA flash-attention forward for sm_100a with natural-log LSE
+// output and an optional fused online-softmax merge into a running accumulator.
+//
+// Replaces the reference's scalar attention_with_lse -> attention_core
+// (reference proj/src/tensor.cpp:143-202) and, when `acc_o` is given, folds in
+// merge_lse (tensor.cpp:204-243) so a ring step's partial result is merged in
+// the epilogue instead of in a separate pass.
+//
+// Non-causal, head dim D = 128.  Q/K are bf16, V is f16 (P.V runs in f16:
+// bf16 P cannot meet rel-L2 <= 1e-3 against the fp32 oracle).
+//
+// CTA = one head x 256 query rows as two 128-row tiles that ping-pong on the
+// tensor core; KV tiles of 128 rows stream through a 2-stage TMA ring.
+//   warp 0      TMA producer for Q and K
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 2      TMA producer for V
+//   warp 3      idle
+//   warps 4-7   softmax / correction / epilogue for Q tile 0 (one row per thread)
+//   warps 8-11  same for Q tile 1
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_t (f16
+// pairs) overwrites columns [0,64) of S_t after the softmax has read S_t.
+#include <cmath>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "fastusp_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fusp {
+namespace {
+
+using namespace ptx;
+
+constexpr int kBM = 128;   // rows per Q tile (one softmax warpgroup)
+constexpr int kBN = 128;   // keys per KV tile
+constexpr int kD = 128;    // head dim
+constexpr int kStages = 2; // KV ring depth
+constexpr int kThreads = 384;
+constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: [2 halves][128 rows][128 B]
+constexpr uint32_t kHalfBytes = kTileBytes / 2;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: lazy O rescale (P <= 2^8 in f16)
+
+struct __align__(1024) Smem {
+  uint8_t q[2][kTileBytes];
+  uint8_t k[kStages][kTileBytes];
+  uint8_t v[kStages][kTileBytes];
+  uint64_t q_full;
+  uint64_t k_full[kStages], k_empty[kStages];
+  uint64_t v_full[kStages], v_empty[kStages];
+  uint64_t s_full[2], p_full[2], o_done[2];
+  uint32_t tmem_base;
+};
+
+struct Params {
+  int sq, skv, heads;
+  float scale_log2;  // log2(e) / sqrt(D)
+  void* out;
+  int out_dtype;     // FUSP_F32 / FUSP_F16 / FUSP_BF16
+  int out_chunk;     // rows per output chunk (row -> (row / chunk, row % chunk))
+  int64_t out_hs, out_cs, out_rs;  // element strides: head, chunk, row
+  float* lse;        // [heads][lse_hs] natural-log LSE or null
+  int64_t lse_hs;
+  const float* acc_o;    // fp32 [heads][sq][D] running accumulator or null
+  const float* acc_lse;  // [heads][sq]
+};
+
+__device__ __forceinline__ float merge_coeffs(float l1, float l2, float& c1, float& c2) {
+  // merge_lse per row (reference tensor.cpp:219-240), identity rows pass through.
+  if (l2 == -INFINITY) { c1 = 1.f; c2 = 0.f; return l1; }
+  if (l1 == -INFINITY) { c1 = 0.f; c2 = 1.f; return l2; }
+  const float m = l1 > l2 ? l1 : l2;
+  const float lse = m + logf(expf(l1 - m) + expf(l2 - m));
+  c1 = expf(l1 - lse);
+  c2 = expf(l2 - lse);
+  return lse;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int row0 = blockIdx.x * (2 * kBM);
+  const int n_kv = (p.skv + kBN - 1) / kBN;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], kBM);
+      mbar_init(&sm.o_done[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: Q tiles, then K tiles ----------------
+    if (lane == 0) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(sm.q[t] + h * kHalfBytes, &tm_q, &sm.q_full, h * 64, row0 + t * kBM, head);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        mbar_wait(&sm.k_empty[st], ph ^ 1);
+        mbar_expect_tx(&sm.k_full[st], kTileBytes);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(sm.k[st] + h * kHalfBytes, &tm_k, &sm.k_full[st], h * 64, j * kBN, head);
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------- TMA producer: V tiles ----------------
+    if (lane == 0) {
+      prefetch_tmap(&tm_v);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        mbar_wait(&sm.v_empty[st], ph ^ 1);
+        mbar_expect_tx(&sm.v_full[st], kTileBytes);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(sm.v[st] + h * kHalfBytes, &tm_v, &sm.v_full[st], h * 64, j * kBN, head);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- single-thread tcgen05.mma issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_f16(1, 1, 0, 0, kBM, kBN);  // bf16 x bf16, K-major
+      constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);   // f16 P(tmem) x f16 V(MN)
+      const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
+      auto issue_pv = [&](int t, int jj) {
+        const int st = jj % kStages;
+        const uint32_t vbase = smem_u32(sm.v[st]);
+        const uint32_t t_o = tmem + 256 + t * 128;
+        const uint32_t t_p = tmem + t * 128;
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k) {
+          // B = V tile, MN-major SW128: LBO = d-half stride (16 KB), SBO = 8-row group (1 KB)
+          const uint64_t bdesc = umma_desc_sw128(vbase + k * 16 * 128, kHalfBytes, 1024);
+          mma_ts(t_o, t_p + k * 8, bdesc, idesc_pv, (jj > 0 || k > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&sm.q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        mbar_wait(&sm.k_full[st], ph);
+        tc_fence_after();
+        const uint32_t kbase = smem_u32(sm.k[st]);
+        for (int t = 0; t < 2; ++t) {
+          if (j > 0) {
+            // O_t += P_t(j-1) V(j-1): needs the softmax to have published P_t(j-1)
+            mbar_wait(&sm.p_full[t], (j - 1) & 1);
+            if (t == 0) mbar_wait(&sm.v_full[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+            tc_fence_after();
+            issue_pv(t, j - 1);
+            if (t == 1) mma_commit(&sm.v_empty[(j - 1) % kStages]);
+          }
+          // S_t = Q_t K_j^T  (executes after PV_t(j-1) has read P_t: tcgen05.mma is in-order)
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+            const uint64_t adesc = umma_desc_sw128(q_addr[t] + off, 16, 1024);
+            const uint64_t bdesc = umma_desc_sw128(kbase + off, 16, 1024);
+            mma_ss(tmem + t * 128, adesc, bdesc, idesc_qk, k > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.s_full[t]);
+        }
+        mma_commit(&sm.k_empty[st]);
+      }
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&sm.p_full[t], (n_kv - 1) & 1);
+        if (t == 0) mbar_wait(&sm.v_full[(n_kv - 1) % kStages], ((n_kv - 1) / kStages) & 1);
+        tc_fence_after();
+        issue_pv(t, n_kv - 1);
+        mma_commit(&sm.o_done[t]);
+      }
+      mma_commit(&sm.v_empty[(n_kv - 1) % kStages]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax warpgroups ----------------
+    const int t = (warp - 4) >> 2;          // Q tile 0 / 1
+    const int quad = warp & 3;              // TMEM lane quadrant of this warp
+    const int r_in_tile = quad * 32 + lane; // row within the 128-row tile
+    const int row = row0 + t * kBM + r_in_tile;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + t * 128;
+    const uint32_t t_o = tmem + lane_off + 256 + t * 128;
+    const float sl2 = p.scale_log2;
+
+    float m_use = -INFINITY;  // max used for the exponent (raw logit units)
+    float l_sum = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&sm.s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t s[128];
+      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+      tmem_wait_ld();
+      const int valid = p.skv - j * kBN;  // keys in this tile (mask the tail)
+      if (valid < kBN) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) s[c] = __float_as_uint(-INFINITY);
+      }
+      float mx = __uint_as_float(s[0]);
+#pragma unroll
+      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+      // Lazy rescale: keep the old max unless the new one exceeds it by > 8 (log2 units).
+      float alpha = 1.f;
+      if (m_use == -INFINITY) {
+        m_use = mx;
+      } else if ((mx - m_use) * sl2 > kRescaleThreshold) {
+        alpha = ex2((m_use - mx) * sl2);
+        m_use = mx;
+      }
+      const float neg_m = -m_use * sl2;
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) {
+        const float p0 = ex2(fmaf(__uint_as_float(s[c]), sl2, neg_m));
+        const float p1 = ex2(fmaf(__uint_as_float(s[c + 1]), sl2, neg_m));
+        rs0 += p0;
+        rs1 += p1;
+        s[c >> 1] = pack_f16x2(p0, p1);  // P packs into the first 64 slots
+      }
+      l_sum = l_sum * alpha + (rs0 + rs1);
+      tmem_st32(t_s + 0, &s[0]);
+      tmem_st32(t_s + 32, &s[32]);
+      // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
+      // s_full commit for S_t(j) covers every MMA issued before it.
+      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(t_o + c * 32, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full[t]);
+    }
+
+    // ---------------- epilogue: O / l, LSE, optional merge, store ----------------
+    mbar_wait(&sm.o_done[t], 0);
+    tc_fence_after();
+    const bool in_range = row < p.sq;
+    const float lse2 = m_use * sl2 + __log2f(l_sum);
+    float lse_b = lse2 * 0.69314718055994530942f;
+    // recompute in accurate math for the exported value
+    lse_b = m_use * (sl2 * 0.69314718055994530942f) + logf(l_sum);
+    const float inv_l = 1.f / l_sum;
+    float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
+    const float* acc_row = nullptr;
+    if (p.acc_o != nullptr && in_range) {
+      const float l1 = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
+      lse_out = merge_coeffs(l1, lse_b, c_acc, c_new);
+      acc_row = p.acc_o + (static_cast<int64_t>(head) * p.sq + row) * kD;
+    }
+    const float scale_new = c_new * inv_l;
+    const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
+                          static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
+                          static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tmem_ld32(t_o + c * 32, o);
+      tmem_wait_ld();
+      if (!in_range) continue;
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * scale_new;
+      if (acc_row != nullptr) {
+        const float4* a4 = reinterpret_cast<const float4*>(acc_row + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 a = a4[i];
+          v[4 * i + 0] = fmaf(c_acc, a.x, v[4 * i + 0]);
+          v[4 * i + 1] = fmaf(c_acc, a.y, v[4 * i + 1]);
+          v[4 * i + 2] = fmaf(c_acc, a.z, v[4 * i + 2]);
+          v[4 * i + 3] = fmaf(c_acc, a.w, v[4 * i + 3]);
+        }
+      }
+      if (p.out_dtype == FUSP_F32) {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + obase + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + obase + c * 32);
+        const bool f16 = p.out_dtype == FUSP_F16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = v[8 * i + 2 * e], b = v[8 * i + 2 * e + 1];
+            w[e] = f16 ? pack_f16x2(a, b) : pack_bf16x2(a, b);
+          }
+          dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+    (void)lse2;
+    if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+// Host launcher. q,k: bf16 [heads][sq|skv][128] (row stride 128); v: f16 [heads][skv][128].
+fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
+  if (a.d != kD) return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(a.d) +
+                                                      " unsupported by the sm_100a kernel (D=128)");
+  if (a.sq <= 0 || a.heads <= 0) return FUSP_OK;
+  CUtensorMap tq, tk, tv;
+  fusp_status st;
+  if ((st = make_tmap_rows(&tq, a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.heads, a.sq, a.q_hs)) != FUSP_OK)
+    return st;
+  if ((st = make_tmap_rows(&tk, a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.heads, a.skv, a.k_hs)) != FUSP_OK)
+    return st;
+  if ((st = make_tmap_rows(&tv, a.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.heads, a.skv, a.v_hs)) != FUSP_OK)
+    return st;
+  Params p{};
+  p.sq = a.sq;
+  p.skv = a.skv;
+  p.heads = a.heads;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a.d)));
+  p.out = a.out;
+  p.out_dtype = a.out_dtype;
+  p.out_chunk = a.out_chunk > 0 ? a.out_chunk : a.sq;
+  p.out_hs = a.out_hs;
+  p.out_cs = a.out_cs;
+  p.out_rs = a.out_rs;
+  p.lse = a.lse;
+  p.lse_hs = a.lse_hs;
+  p.acc_o = a.acc_o;
+  p.acc_lse = a.acc_lse;
+  static bool attr_set = false;
+  const int smem = static_cast<int>(sizeof(Smem)) + 1024;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(attn_fwd_kernel)");
+    attr_set = true;
+  }
+  dim3 grid((a.sq + 2 * kBM - 1) / (2 * kBM), a.heads);
+  attn_fwd_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_kernel launch");
+  return FUSP_OK;
+}
+
+}  // namespace fusp

@@ -1,0 +1,103 @@
+// Internal declarations shared by the fastusp translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/fastusp.h"
+
+namespace fusp {
+
+// ---- errors (thread-local last error, fastusp.h) --------------------------------------
+fusp_status set_error(fusp_status code, const std::string& msg);
+fusp_status set_cuda_error(cudaError_t e, const std::string& where);
+void clear_error();
+
+#define FUSP_CHECK(expr)                      \
+  do {                                        \
+    fusp_status _st = (expr);                 \
+    if (_st != FUSP_OK) return _st;           \
+  } while (0)
+#define FUSP_CUDA(expr)                                              \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) return set_cuda_error(_e, #expr);         \
+  } while (0)
+
+void count_launch(int n = 1);
+
+// ---- TMA descriptors ------------------------------------------------------------------
+// 3-D map over [heads][rows][128] 16-bit elements with a head stride of `head_stride`
+// elements (rows are 128 elements apart); box = 64 elements x 128 rows x 1 head, 128B swizzle.
+fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int heads,
+                           int rows, int64_t head_stride);
+
+// ---- attention kernel -----------------------------------------------------------------
+struct AttnLaunch {
+  const void* q;  // bf16 [heads][sq][128], head stride q_hs elements
+  const void* k;  // bf16 [heads][skv][128]
+  const void* v;  // f16  [heads][skv][128]
+  int64_t q_hs, k_hs, v_hs;
+  int heads, sq, skv, d;
+  void* out;
+  int out_dtype;
+  int out_chunk;  // rows per output chunk; 0 = sq
+  int64_t out_hs, out_cs, out_rs;
+  float* lse;
+  int64_t lse_hs;
+  const float* acc_o;    // merge into (acc_o, acc_lse) when non-null
+  const float* acc_lse;
+};
+fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
+
+// ---- elementwise / data-movement kernels (kernels.cu) -----------------------------------
+fusp_status launch_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,
+                           cudaStream_t s);
+fusp_status launch_encode(const float* x, int64_t n, uint8_t* codes, cudaStream_t s);
+fusp_status launch_decode(const uint8_t* c, int64_t n, float* y, cudaStream_t s);
+// amax over n elements of x (any float dtype) into *amax_bits (u32 float bits, atomicMax),
+// sets *nonfinite = 1 on NaN/Inf.  The buffer must be zeroed first (done by launch_amax).
+fusp_status launch_amax(const void* x, int dtype, int64_t n, uint32_t* amax_bits,
+                        uint32_t* nonfinite, cudaStream_t s);
+// scale = amax/448 (1 if 0) from amax_bits; codes = RNE(x/scale)
+fusp_status launch_quantize(const void* x, int dtype, int64_t n, const uint32_t* amax_bits,
+                            float* scale_out, uint8_t* codes, cudaStream_t s);
+fusp_status launch_dequantize(const uint8_t* codes, const float* scale, int64_t n, void* y,
+                              int y_dtype, cudaStream_t s);
+fusp_status launch_merge(const float* o1, const float* l1, const float* o2, const float* l2,
+                         int64_t rows, int d, float* out, float* lse, cudaStream_t s);
+fusp_status launch_fill(void* p, int dtype, int64_t n, float value, cudaStream_t s);
+
+// Ulysses pack: src [B][H][SL][D] (dtype src_dt) -> dst [U][B][hp][SL][D] (dst_dt), slot-major.
+struct PackDesc {
+  const void* src;
+  int src_dtype;
+  void* dst;
+  int dst_dtype;
+  int64_t dst_slot_stride;  // elements (or bytes for e4m3) between destination slots
+  int b, h, sl, d, u;
+  const float* scale;       // e4m3: quantization scale (device)
+};
+fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
+// Ulysses unpack: src slots [U][B][hp][SL][D] -> dst [B][hp][U*SL][D]; e4m3 src uses per-slot
+// scales scale[j] (device) -- value = decode(code) * scale[j] in f32, then cast to dst dtype.
+struct UnpackDesc {
+  const void* src;
+  int src_dtype;
+  int64_t src_slot_stride;
+  const float* scales;       // [U] for e4m3
+  int64_t scale_stride;      // floats between consecutive slot scales
+  void* dst;
+  int dst_dtype;
+  int b, hp, sl, d, u;
+};
+fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s);
+// Output unpack for B>1: src slots [U][B][hp][SL][D] -> dst [B][H][SL][D].
+fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst, int dtype, int b,
+                                int hp, int sl, int d, int u, cudaStream_t s);
+
+size_t dtype_size(int dt);
+
+}  // namespace fusp

@@ -1,0 +1,297 @@
+// fastusp runtime: error state, TMA descriptor encoding, per-device scratch, and the
+// single-GPU C-ABI entry points (codec, attention_with_lse, merge_lse, mesh).
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "fastusp_internal.h"
+
+namespace fusp {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+fusp_status set_error(fusp_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+fusp_status set_cuda_error(cudaError_t e, const std::string& where) {
+  if (e == cudaErrorMemoryAllocation)
+    return set_error(FUSP_ERR_OOM, where + ": " + cudaGetErrorString(e));
+  return set_error(FUSP_ERR_CUDA, where + ": " + cudaGetErrorString(e));
+}
+
+void clear_error() { g_last_error.clear(); }
+
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+// ---- TMA ------------------------------------------------------------------------------
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int heads,
+                           int rows, int64_t head_stride) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(FUSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention operand not 16-byte aligned");
+  cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
+  cuuint64_t strides[2] = {128 * 2, static_cast<cuuint64_t>(head_stride) * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(FUSP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return FUSP_OK;
+}
+
+// ---- per-device scratch used by the context-free single-GPU API -------------------------
+namespace {
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_scratch_mu;
+std::vector<Scratch> g_scratch;  // indexed by device
+
+fusp_status scratch(size_t bytes, void** out) {
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  if (g_scratch.size() <= static_cast<size_t>(dev)) g_scratch.resize(dev + 1);
+  Scratch& s = g_scratch[dev];
+  if (s.bytes < bytes) {
+    if (s.ptr) {
+      FUSP_CUDA(cudaDeviceSynchronize());
+      FUSP_CUDA(cudaFree(s.ptr));
+      s.ptr = nullptr;
+      s.bytes = 0;
+    }
+    FUSP_CUDA(cudaMalloc(&s.ptr, bytes));
+    s.bytes = bytes;
+  }
+  *out = s.ptr;
+  return FUSP_OK;
+}
+
+std::string shape_str(const fusp_shape4& s) {
+  std::ostringstream os;
+  os << "[" << s.b << "," << s.h << "," << s.s << "," << s.d << "]";
+  return os.str();
+}
+
+bool valid_float_dtype(int dt) { return dt == FUSP_F32 || dt == FUSP_F16 || dt == FUSP_BF16; }
+}  // namespace
+
+}  // namespace fusp
+
+using namespace fusp;
+
+extern "C" {
+
+const char* fusp_last_error(void) { return g_last_error.c_str(); }
+const char* fusp_version(void) { return "fastusp 0.1 (sm_100a)"; }
+uint64_t fusp_kernel_launch_count(void) { return g_launches.load(); }
+
+fusp_status fusp_encode_e4m3(const float* x, int64_t n, uint8_t* codes, fusp_stream_t stream) {
+  clear_error();
+  return launch_encode(x, n, codes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_decode_e4m3(const uint8_t* codes, int64_t n, float* y, fusp_stream_t stream) {
+  clear_error();
+  return launch_decode(codes, n, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8_t* codes,
+                               float* scale_dev, int check_finite, fusp_stream_t stream) {
+  clear_error();
+  if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: bad dtype");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  void* ws = nullptr;
+  FUSP_CHECK(scratch(256, &ws));
+  uint32_t* amax = static_cast<uint32_t*>(ws);
+  uint32_t* bad = amax + 1;
+  FUSP_CHECK(launch_amax(x, dtype, n, amax, bad, s));
+  if (check_finite) {
+    uint32_t flag = 0;
+    FUSP_CUDA(cudaMemcpyAsync(&flag, bad, 4, cudaMemcpyDeviceToHost, s));
+    FUSP_CUDA(cudaStreamSynchronize(s));
+    if (flag) {
+      // locate the first non-finite element like the reference message (fp8.cpp:112-113)
+      std::vector<float> hv;
+      int64_t idx = -1;
+      const size_t es = dtype_size(dtype);
+      std::vector<uint8_t> raw(static_cast<size_t>(n) * es);
+      FUSP_CUDA(cudaMemcpy(raw.data(), x, raw.size(), cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n && idx < 0; ++i) {
+        float f;
+        if (dtype == FUSP_F32) {
+          std::memcpy(&f, &raw[i * 4], 4);
+        } else {
+          uint16_t h;
+          std::memcpy(&h, &raw[i * 2], 2);
+          if (dtype == FUSP_BF16) {
+            uint32_t u = uint32_t(h) << 16;
+            std::memcpy(&f, &u, 4);
+          } else {
+            const bool exp_all = ((h >> 10) & 0x1F) == 0x1F;
+            f = exp_all ? NAN : 0.f;
+          }
+        }
+        if (!std::isfinite(f)) idx = i;
+      }
+      return set_error(FUSP_ERR_INVALID_ARGUMENT,
+                       "quantize: non-finite element at flat index " + std::to_string(idx));
+    }
+  }
+  return launch_quantize(x, dtype, n, amax, scale_dev, codes, s);
+}
+
+fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, int64_t n, void* y,
+                                 fusp_dtype dtype, fusp_stream_t stream) {
+  clear_error();
+  if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "dequantize: bad dtype");
+  return launch_dequantize(codes, scale_dev, n, y, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
+                                    fusp_dtype in_dtype, fusp_shape4 qs, int64_t skv, void* out,
+                                    fusp_dtype out_dtype, float* lse, fusp_stream_t stream) {
+  clear_error();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!valid_float_dtype(in_dtype) || !valid_float_dtype(out_dtype))
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention: bad dtype");
+  if (qs.b < 0 || qs.h < 0 || qs.s < 0 || qs.d <= 0 || skv < 0)
+    return set_error(FUSP_ERR_SHAPE, "attention: bad shape " + shape_str(qs));
+  const int64_t heads = qs.b * qs.h;
+  const int64_t nq = heads * qs.s * qs.d;
+  if (heads == 0 || qs.s == 0) return FUSP_OK;
+  if (skv == 0) {  // merge identity: out 0, lse -inf (tensor.cpp:161-164)
+    FUSP_CHECK(launch_fill(out, out_dtype, nq, 0.f, s));
+    if (lse) FUSP_CHECK(launch_fill(lse, FUSP_F32, heads * qs.s, -INFINITY, s));
+    return FUSP_OK;
+  }
+  if (qs.d != 128)
+    return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(qs.d) +
+                                         " unsupported by the sm_100a kernel (D=128)");
+  const int64_t nkv = heads * skv * qs.d;
+  // Operand staging: Q,K -> bf16, V -> f16 (one HBM pass each, skipped when already in place).
+  size_t need = 0;
+  if (in_dtype != FUSP_BF16) need += static_cast<size_t>(nq + nkv) * 2;
+  if (in_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
+  uint8_t* ws = nullptr;
+  if (need) FUSP_CHECK(scratch(need + 256, reinterpret_cast<void**>(&ws)));
+  const void* qb = q;
+  const void* kb = k;
+  const void* vh = v;
+  size_t off = 0;
+  if (in_dtype != FUSP_BF16) {
+    void* tq = ws + off;
+    off += static_cast<size_t>(nq) * 2;
+    void* tk = ws + off;
+    off += static_cast<size_t>(nkv) * 2;
+    FUSP_CHECK(launch_convert(q, in_dtype, tq, FUSP_BF16, nq, s));
+    FUSP_CHECK(launch_convert(k, in_dtype, tk, FUSP_BF16, nkv, s));
+    qb = tq;
+    kb = tk;
+  }
+  if (in_dtype != FUSP_F16) {
+    void* tv = ws + off;
+    FUSP_CHECK(launch_convert(v, in_dtype, tv, FUSP_F16, nkv, s));
+    vh = tv;
+  }
+  AttnLaunch a{};
+  a.q = qb;
+  a.k = kb;
+  a.v = vh;
+  a.q_hs = qs.s * 128;
+  a.k_hs = skv * 128;
+  a.v_hs = skv * 128;
+  a.heads = static_cast<int>(heads);
+  a.sq = static_cast<int>(qs.s);
+  a.skv = static_cast<int>(skv);
+  a.d = static_cast<int>(qs.d);
+  a.out = out;
+  a.out_dtype = out_dtype;
+  a.out_chunk = static_cast<int>(qs.s);
+  a.out_hs = qs.s * 128;
+  a.out_cs = 0;
+  a.out_rs = 128;
+  a.lse = lse;
+  a.lse_hs = qs.s;
+  return launch_attention(a, s);
+}
+
+fusp_status fusp_merge_lse(const float* o1, const float* l1, const float* o2, const float* l2,
+                           fusp_shape4 shape, float* out, float* lse, fusp_stream_t stream) {
+  clear_error();
+  return launch_merge(o1, l1, o2, l2, shape.b * shape.h * shape.s, static_cast<int>(shape.d), out,
+                      lse, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_mesh_build(int n, int max_ring, int heads, int* r, int* u) {
+  clear_error();
+  if (n < 1) return set_error(FUSP_ERR_MESH, "worker count must be >= 1, got " + std::to_string(n));
+  if (max_ring < 1)
+    return set_error(FUSP_ERR_MESH,
+                     "max_ring_dim_size must be >= 1, got " + std::to_string(max_ring));
+  if (heads < 1) return set_error(FUSP_ERR_MESH, "head count must be >= 1, got " + std::to_string(heads));
+  for (int rr = (n < max_ring ? n : max_ring); rr >= 1; --rr) {
+    if (n % rr != 0 || heads % (n / rr) != 0) continue;
+    *r = rr;
+    *u = n / rr;
+    return FUSP_OK;
+  }
+  std::ostringstream os;
+  os << "no feasible (R,U) mesh for N=" << n << ", max_ring_dim_size=" << max_ring
+     << ", H=" << heads << ":";
+  for (int rr = 1; rr <= n; ++rr) {
+    if (n % rr != 0) continue;
+    os << " (R=" << rr << ",U=" << n / rr << ")";
+    if (rr > max_ring) os << " violates R<=" << max_ring << ";";
+    else os << " violates H%" << n / rr << "==0;";
+  }
+  return set_error(FUSP_ERR_MESH, os.str());
+}
+
+fusp_status fusp_mesh_make(int n, int r, int* ulysses_groups, int* ring_groups) {
+  clear_error();
+  if (n < 1) return set_error(FUSP_ERR_MESH, "worker count must be >= 1, got " + std::to_string(n));
+  if (r < 1 || n % r != 0)
+    return set_error(FUSP_ERR_MESH, "ring dimension " + std::to_string(r) +
+                                        " does not divide worker count " + std::to_string(n));
+  const int u = n / r;
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < u; ++j) ulysses_groups[i * u + j] = i * u + j;
+  for (int j = 0; j < u; ++j)
+    for (int i = 0; i < r; ++i) ring_groups[j * r + i] = i * u + j;
+  return FUSP_OK;
+}
+
+}  // extern "C"
