@@ -238,3 +238,269 @@ def build_mesh(n: int, max_ring_dim_size: int, heads: int) -> Mesh2D:
 
 def kernel_launch_count() -> int:
     return int(lib().fusp_kernel_launch_count())
+
+
+# ---- communication options (protocols.hpp:12-15) ----------------------------------------------
+@dataclass
+class CommOptions:
+    """= uspsim::CommOptions plus B200 extensions (out_dtype, check_finite, fp8_block)."""
+    fp8_kv: bool = False
+    pipelined_ring: bool = False
+    out_dtype: torch.dtype = torch.float32
+    check_finite: bool = True
+    fp8_block: int = 0
+
+    def _c(self) -> _CommOptions:
+        return _CommOptions(int(self.fp8_kv), int(self.pipelined_ring), _DT[self.out_dtype],
+                            int(self.check_finite), int(self.fp8_block))
+
+
+# ---- per-rank contexts (fabric.hpp:136-166) ------------------------------------------------------
+class Fabric:
+    """In-process fabric: `world` ranks living in this process (threads as ranks)."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        check(lib().fusp_fabric_create(world, ctypes.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def close(self):
+        if self.handle:
+            lib().fusp_fabric_destroy(self.handle)
+            self.handle = None
+
+
+class WorkerContext:
+    """= uspsim::WorkerContext: one rank, bound to one CUDA device."""
+
+    def __init__(self, handle, device: int):
+        self.handle = handle
+        self.device = device
+
+    @classmethod
+    def local(cls, fabric: Fabric, rank: int, device: int = 0) -> "WorkerContext":
+        h = ctypes.c_void_p()
+        check(lib().fusp_ctx_create_local(fabric.handle, rank, device, ctypes.byref(h)))
+        return cls(h, device)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib().fusp_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid: bytes, world: int, rank: int, device: int) -> "WorkerContext":
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        check(lib().fusp_ctx_create_nccl(buf, world, rank, device, ctypes.byref(h)))
+        return cls(h, device)
+
+    def rank(self) -> int:
+        return lib().fusp_ctx_rank(self.handle)
+
+    def world_size(self) -> int:
+        return lib().fusp_ctx_world(self.handle)
+
+    def traffic(self):
+        """(all_to_all bytes, send bytes) this rank put on the wire (TrafficLog::bytes_for)."""
+        a, s = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().fusp_ctx_traffic(self.handle, ctypes.byref(a), ctypes.byref(s)))
+        return a.value, s.value
+
+    def reset_traffic(self):
+        check(lib().fusp_ctx_reset_traffic(self.handle))
+
+    def ring_timings(self, max_steps: int = 32):
+        """Per ring step device times (ms) of the last call: (compute[], comm[])."""
+        c = (ctypes.c_float * max_steps)()
+        m = (ctypes.c_float * max_steps)()
+        n = ctypes.c_int()
+        check(lib().fusp_ctx_ring_timings(self.handle, max_steps, c, m, ctypes.byref(n)))
+        return list(c[:n.value]), list(m[:n.value])
+
+    def close(self):
+        if self.handle:
+            lib().fusp_ctx_destroy(self.handle)
+            self.handle = None
+
+
+@dataclass
+class RunReport:
+    results: list
+    traffic: list  # per rank (all_to_all bytes, send bytes)
+
+
+def run_protocol(n_workers: int, program: Callable[[WorkerContext], object], device: int = 0,
+                 devices: Optional[List[int]] = None) -> RunReport:
+    """= uspsim::run_protocol (fabric.hpp:180): one host thread per rank, each with its own
+    CUDA stream; ranks may share a device.  Raises the first rank's exception."""
+    if n_workers < 1:
+        raise FabricError(3, "run_protocol: need at least one worker")
+    fab = Fabric(n_workers)
+    devs = devices or [device] * n_workers
+    ctxs = [WorkerContext.local(fab, r, devs[r]) for r in range(n_workers)]
+    results = [None] * n_workers
+    errors = [None] * n_workers
+
+    def body(r):
+        try:
+            torch.cuda.set_device(devs[r])
+            s = torch.cuda.Stream(device=devs[r])
+            with torch.cuda.stream(s):
+                results[r] = program(ctxs[r])
+            s.synchronize()
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            errors[r] = e
+
+    try:
+        if n_workers == 1:
+            body(0)
+        else:
+            th = [threading.Thread(target=body, args=(r,)) for r in range(n_workers)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+        for e in errors:
+            if e is not None:
+                raise e
+        return RunReport(results, [c.traffic() for c in ctxs])
+    finally:
+        for c in ctxs:
+            c.close()
+        fab.close()
+
+
+# ---- protocols (protocols.hpp:28-71) --------------------------------------------------------------
+def split_sequence(full: torch.Tensor, count: int) -> List[torch.Tensor]:
+    """split_sequence (protocols.cpp:10-21)."""
+    if count < 1:
+        raise ShapeError(1, "split_sequence: count must be >= 1")
+    s = full.shape[2]
+    if s % count:
+        raise ShapeError(1, f"split_sequence: S={s} not divisible by shard count {count}")
+    c = s // count
+    return [full[:, :, i * c:(i + 1) * c].contiguous() for i in range(count)]
+
+
+def gather_output(shards: List[torch.Tensor]) -> torch.Tensor:
+    """gather_output (protocols.cpp:23): concatenation along S in rank order."""
+    return torch.cat(list(shards), dim=2)
+
+
+def _check_local(q, k, v, where):
+    if not (tuple(q.shape) == tuple(k.shape) == tuple(v.shape)):
+        raise ShapeError(1, f"{where}: local Q/K/V shapes differ: Q={list(q.shape)} "
+                            f"K={list(k.shape)} V={list(v.shape)}")
+    if q.dtype != k.dtype or q.dtype != v.dtype:
+        raise InvalidArgument(4, f"{where}: Q/K/V dtypes differ")
+
+
+def _inputs(q, k, v, where):
+    q, k, v = _dev(q), _dev(k), _dev(v)
+    _shape4(q)
+    _check_local(q, k, v, where)
+    if q.dtype not in _DT:
+        q, k, v = q.float(), k.float(), v.float()
+    return q, k, v
+
+
+def usp_attention(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
+                  opts: Optional[CommOptions] = None) -> torch.Tensor:
+    """usp_attention (protocols.cpp:321-340): local shards [B,H,S/N,D] -> [B,H,S/N,D]."""
+    opts = opts or CommOptions()
+    if mesh.n != ctx.world_size():
+        raise MeshError(2, f"mesh covers {mesh.n} workers but the fabric has {ctx.world_size()}")
+    q, k, v = _inputs(q, k, v, "usp")
+    out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    co = opts._c()
+    check(lib().fusp_usp_attention(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
+                                   _shape4(q), _ptr(out), ctypes.byref(co), _stream()))
+    return out
+
+
+def _world_group(ctx, group: Optional[ProcessGroup]):
+    if group is not None and list(group.members) != list(range(ctx.world_size())):
+        raise FabricError(3, "fastusp runs ulysses/ring protocols on the world group; "
+                             "use usp_attention with a Mesh2D for sub-groups")
+
+
+def ulysses_attention(ctx: WorkerContext, q, k, v, group: Optional[ProcessGroup] = None,
+                      opts: Optional[CommOptions] = None) -> torch.Tensor:
+    """ulysses_attention (protocols.cpp:207-214) over the world group."""
+    opts = opts or CommOptions()
+    _world_group(ctx, group)
+    q, k, v = _inputs(q, k, v, "ulysses")
+    out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    co = opts._c()
+    check(lib().fusp_ulysses_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
+                                       _shape4(q), _ptr(out), ctypes.byref(co), _stream()))
+    return out
+
+
+def _ring(ctx, q, k, v, group, opts, pipelined):
+    opts = opts or CommOptions()
+    _world_group(ctx, group)
+    q, k, v = _inputs(q, k, v, "ring")
+    out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    co = opts._c()
+    co.pipelined_ring = int(pipelined)
+    check(lib().fusp_ring_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
+                                    _shape4(q), _ptr(out), _ptr(lse), ctypes.byref(co), _stream()))
+    return AttnResult(out, lse)
+
+
+def ring_attention_serial(ctx, q, k, v, group=None, opts=None) -> AttnResult:
+    """ring_attention_serial (protocols.cpp:237-268) over the world group."""
+    return _ring(ctx, q, k, v, group, opts, False)
+
+
+def ring_attention_pipelined(ctx, q, k, v, group=None, opts=None) -> AttnResult:
+    """ring_attention_pipelined (protocols.cpp:270-319): double-buffered on a side stream."""
+    return _ring(ctx, q, k, v, group, opts, True)
+
+
+def usp_attention_host(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
+                       opts: Optional[CommOptions] = None):
+    """usp_attention on HOST tensors (H2D, layer, D2H inside one C-ABI call)."""
+    opts = opts or CommOptions()
+    if q.is_cuda:
+        raise InvalidArgument(4, "usp_attention_host expects host tensors")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    _check_local(q, k, v, "usp")
+    out = torch.empty(q.shape, dtype=opts.out_dtype)
+    co = opts._c()
+    check(lib().fusp_usp_attention_host(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
+                                        _DT[q.dtype], _shape4(q), _ptr(out), ctypes.byref(co),
+                                        _stream()))
+    return out
+
+
+class LayerGraph:
+    """CUDA graph of `layers` back-to-back usp_attention calls (fusp_graph_capture_usp)."""
+
+    def __init__(self, ctx: WorkerContext, q, k, v, out, mesh: Mesh2D,
+                 opts: Optional[CommOptions] = None, layers: int = 1):
+        opts = opts or CommOptions(check_finite=False)
+        co = opts._c()
+        # q/k/v/out: [layers, B, H, S, D]
+        per_in = q[0].numel() * q.element_size()
+        per_out = out[0].numel() * out.element_size()
+        h = ctypes.c_void_p()
+        self._keep = (q, k, v, out)
+        check(lib().fusp_graph_capture_usp(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
+                                           _DT[q.dtype], _shape4(q[0]), _ptr(out),
+                                           ctypes.byref(co), layers, per_in, per_out, _stream(),
+                                           ctypes.byref(h)))
+        self.handle = h
+
+    def launch(self, stream=None):
+        check(lib().fusp_graph_launch(self.handle, _stream(stream)))
+
+    def close(self):
+        if self.handle:
+            lib().fusp_graph_destroy(self.handle)
+            self.handle = None

@@ -54,6 +54,7 @@ struct __align__(1024) Smem {
 
 struct Params {
   int sq, skv, heads;
+  uint32_t idesc_qk;  // bf16 x bf16 or f16 x f16 Q.K^T
   float scale_log2;  // log2(e) / sqrt(D)
   void* out;
   int out_dtype;     // FUSP_F32 / FUSP_F16 / FUSP_BF16
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- single-thread tcgen05.mma issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_f16(1, 1, 0, 0, kBM, kBN);  // bf16 x bf16, K-major
+      const uint32_t idesc_qk = p.idesc_qk;                           // K-major x K-major
       constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);   // f16 P(tmem) x f16 V(MN)
       const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
       auto issue_pv = [&](int t, int jj) {
@@ -348,16 +349,17 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   if (a.sq <= 0 || a.heads <= 0) return FUSP_OK;
   CUtensorMap tq, tk, tv;
   fusp_status st;
-  if ((st = make_tmap_rows(&tq, a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.heads, a.sq, a.q_hs)) != FUSP_OK)
-    return st;
-  if ((st = make_tmap_rows(&tk, a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.heads, a.skv, a.k_hs)) != FUSP_OK)
-    return st;
+  const bool qk16 = a.qk_dtype == FUSP_F16;
+  const CUtensorMapDataType qkt = qk16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if ((st = make_tmap_rows(&tq, a.q, qkt, a.heads, a.sq, a.q_hs)) != FUSP_OK) return st;
+  if ((st = make_tmap_rows(&tk, a.k, qkt, a.heads, a.skv, a.k_hs)) != FUSP_OK) return st;
   if ((st = make_tmap_rows(&tv, a.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.heads, a.skv, a.v_hs)) != FUSP_OK)
     return st;
   Params p{};
   p.sq = a.sq;
   p.skv = a.skv;
   p.heads = a.heads;
+  p.idesc_qk = qk16 ? idesc_f16(0, 0, 0, 0, kBM, kBN) : idesc_f16(1, 1, 0, 0, kBM, kBN);
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a.d)));
   p.out = a.out;
   p.out_dtype = a.out_dtype;

@@ -1,0 +1,128 @@
+// Communication backends for the USP protocols.
+//
+// The reference moves bytes through an in-process fabric of threads
+// (reference proj/src/fabric.cpp:147-226): eager send, blocking recv, and an
+// all_to_all that is one logical round per group.  On B200 the same collective
+// semantics are provided by
+//   * NcclComm  -- one process (or thread) per GPU, NCCL grouped send/recv over
+//                  NVLink/NVSwitch on Ulysses / ring sub-communicators split from
+//                  the world communicator exactly like the mesh (mesh.cpp:44-53);
+//   * LocalComm -- ranks living in one process (threads as ranks, like
+//                  run_protocol): a host rendezvous exchanges buffer pointers and
+//                  CUDA events, and each receiver PULLS its slots with copy-engine
+//                  cudaMemcpyPeerAsync on its own stream.  Several ranks may share
+//                  one GPU, which is how the multi-rank protocols are exercised on a
+//                  single B200.
+// All operations are stream-ordered: they enqueue on the given stream and return.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fastusp_internal.h"
+
+namespace fusp {
+
+struct Group {
+  std::vector<int> members;  // world ranks, group order
+  int pos = -1;              // my position
+  std::string key() const;
+  int size() const { return static_cast<int>(members.size()); }
+};
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  // Slot t (t = group position) of `send` goes to member t; slot j of `recv` receives
+  // member j's slot for me.  `bytes` per slot, slots `stride` bytes apart.  The self
+  // slot is copied locally unless send and recv alias.
+  virtual fusp_status all_to_all(const Group& g, const void* send, void* recv, size_t stride,
+                                 size_t bytes, cudaStream_t s) = 0;
+  // Ring step: send `nparts` buffers to position (pos+1)%R and receive the same number
+  // from (pos-1+R)%R (the reference sends K then V, protocols.cpp:253-257).
+  virtual fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
+                                    const size_t* bytes, int nparts, cudaStream_t s) = 0;
+  virtual bool capturable() const = 0;
+};
+
+// ---- in-process fabric -------------------------------------------------------------------
+struct LocalFabric {
+  explicit LocalFabric(int n) : world(n) {}
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Post {
+    std::vector<const void*> sends;
+    int device = 0;
+    cudaEvent_t ready = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  struct Slot {
+    std::vector<Post> posts;
+    int arrived = 0;
+    int done_arrived = 0;
+    int left = 0;
+  };
+  std::map<std::pair<std::string, uint64_t>, Slot> slots;
+  std::map<std::string, std::vector<uint64_t>> seq;
+  double timeout_s = 120.0;
+};
+
+class LocalComm : public Comm {
+ public:
+  LocalComm(LocalFabric* f, int rank, int device);
+  ~LocalComm() override;
+  fusp_status all_to_all(const Group& g, const void* send, void* recv, size_t stride, size_t bytes,
+                         cudaStream_t s) override;
+  fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
+                            const size_t* bytes, int nparts, cudaStream_t s) override;
+  bool capturable() const override { return fabric_->world == 1; }
+
+ private:
+  // Generic pull-based exchange: for every peer j in `srcs`, copy the chunk at
+  // (peer send ptr + src_off[j]) into (recv + dst_off[j]).
+  struct Pull {
+    int from;        // group position of the sender
+    int part;        // which of the sender's posted buffers
+    size_t src_off;  // byte offset inside it
+    void* dst;
+    size_t bytes;
+  };
+  fusp_status exchange(const Group& g, const char* op, std::vector<const void*> sends,
+                       const std::vector<Pull>& pulls, cudaStream_t s);
+  LocalFabric* fabric_;
+  int rank_, device_;
+  cudaEvent_t ready_ = nullptr, done_ = nullptr;
+};
+
+// ---- NCCL --------------------------------------------------------------------------------
+class NcclComm : public Comm {
+ public:
+  NcclComm(ncclComm_t world, int rank, int nranks);
+  ~NcclComm() override;
+  fusp_status all_to_all(const Group& g, const void* send, void* recv, size_t stride, size_t bytes,
+                         cudaStream_t s) override;
+  fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
+                            const size_t* bytes, int nparts, cudaStream_t s) override;
+  bool capturable() const override { return true; }
+  // Collective over the world: make sure sub-communicators for every group of the
+  // (R,U) mesh exist (ncclCommSplit, color = ring / ulysses index).
+  fusp_status ensure_mesh(int r);
+
+ private:
+  fusp_status sub(const Group& g, ncclComm_t* out);
+  ncclComm_t world_;
+  int rank_, nranks_;
+  std::map<std::string, ncclComm_t> subs_;
+};
+
+fusp_status nccl_error(ncclResult_t r, const std::string& where);
+
+}  // namespace fusp

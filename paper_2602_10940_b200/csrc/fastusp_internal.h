@@ -36,11 +36,12 @@ fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType
 
 // ---- attention kernel -----------------------------------------------------------------
 struct AttnLaunch {
-  const void* q;  // bf16 [heads][sq][128], head stride q_hs elements
-  const void* k;  // bf16 [heads][skv][128]
+  const void* q;  // bf16|f16 [heads][sq][128], head stride q_hs elements
+  const void* k;  // bf16|f16 [heads][skv][128]
   const void* v;  // f16  [heads][skv][128]
   int64_t q_hs, k_hs, v_hs;
   int heads, sq, skv, d;
+  int qk_dtype;   // FUSP_BF16 (default) or FUSP_F16 for Q and K
   void* out;
   int out_dtype;
   int out_chunk;  // rows per output chunk; 0 = sq
@@ -99,5 +100,15 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
                                 int hp, int sl, int d, int u, cudaStream_t s);
 
 size_t dtype_size(int dt);
+
+// FP8 helpers for the protocols.
+fusp_status launch_scale_finalize(const uint32_t* amax_bits, float* scale, float* copies,
+                                  int64_t copy_stride, int count, cudaStream_t s);
+// amax + quantize over a chunk [heads][span][d] of codes whose row r uses
+// scales[(r / seg_rows) * sstride]; writes *scale_out and codes_out.
+fusp_status launch_requantize_seg(const uint8_t* codes, const float* scales, int64_t sstride, int d,
+                                  int span, int seg_rows, int64_t n, uint32_t* amax_bits,
+                                  float* scale_out, uint8_t* codes_out, cudaStream_t s);
+fusp_status launch_finite(const void* x, int dt, int64_t n, uint32_t* flag, cudaStream_t s);
 
 }  // namespace fusp

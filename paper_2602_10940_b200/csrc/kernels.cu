@@ -273,7 +273,12 @@ __global__ void unpack_kernel(const void* __restrict__ src, int sdt, int64_t slo
     const int64_t bh = row / sl;
     const int64_t o = (bh * span + int64_t(j) * sl + s) * d + dd;
     const int64_t si = j * slot_stride + r;
-    if (sdt == ddt && sdt != FUSP_E4M3) {
+    if (sdt == FUSP_E4M3 && ddt == FUSP_E4M3) {
+      *reinterpret_cast<uint2*>(static_cast<uint8_t*>(dst) + o) =
+          *reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(src) + si);
+      continue;
+    }
+    if (sdt == ddt) {
       if (sdt == FUSP_F32) {
         const float4* a = reinterpret_cast<const float4*>(static_cast<const float*>(src) + si);
         float4* z = reinterpret_cast<float4*>(static_cast<float*>(dst) + o);
@@ -322,6 +327,63 @@ __global__ void unpack_heads_kernel(const uint8_t* __restrict__ src, int64_t slo
     *reinterpret_cast<uint4*>(dst + o) =
         *reinterpret_cast<const uint4*>(src + j * slot_stride_bytes + r);
   }
+}
+
+// scale = max/448 (1 if all zero) (fp8.cpp:119) -> *scale and `count` strided copies.
+__global__ void scale_finalize_kernel(const uint32_t* __restrict__ amax_bits, float* __restrict__ scale,
+                                      float* __restrict__ copies, int64_t copy_stride, int count) {
+  const float amax = __uint_as_float(*amax_bits);
+  const float sc = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  if (threadIdx.x == 0 && scale) *scale = sc;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) copies[i * copy_stride] = sc;
+}
+
+// Values of a segmented FP8 chunk [heads][span][D]: decode(code) * scale[seg], seg = row/seg_rows
+// -- exactly the f32 values the reference's dequantize produced (fp8.cpp:125-130).
+__device__ __forceinline__ float seg_value(const uint8_t* c, const float* scales, int64_t sstride,
+                                           int d, int span, int seg_rows, int64_t i) {
+  const int row = static_cast<int>((i / d) % span);
+  return __fmul_rn(dec_e4m3(c[i]), scales[(row / seg_rows) * sstride]);
+}
+
+__global__ void amax_seg_kernel(const uint8_t* __restrict__ c, const float* __restrict__ scales,
+                                int64_t sstride, int d, int span, int seg_rows, int64_t n,
+                                uint32_t* __restrict__ amax_bits) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    m = fmaxf(m, fabsf(seg_value(c, scales, sstride, d, span, seg_rows, i)));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float wm[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bm = 0.f;
+    for (int w = 0; w < kBlock / 32; ++w) bm = fmaxf(bm, wm[w]);
+    atomicMax(amax_bits, __float_as_uint(bm));
+  }
+}
+
+// Re-quantize a segmented chunk (ring hop, protocols.cpp:113-115 / :303-311).
+__global__ void quantize_seg_kernel(const uint8_t* __restrict__ c, const float* __restrict__ scales,
+                                    int64_t sstride, int d, int span, int seg_rows, int64_t n,
+                                    const uint32_t* __restrict__ amax_bits,
+                                    float* __restrict__ scale_out, uint8_t* __restrict__ codes) {
+  const float amax = __uint_as_float(*amax_bits);
+  const float sc = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = sc;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    codes[i] = enc_e4m3(__fdiv_rn(seg_value(c, scales, sstride, d, span, seg_rows, i), sc));
+}
+
+// Finite check over several tensors at once (check_local_qkv, protocols.cpp:102-104).
+__global__ void finite_kernel(const void* __restrict__ x, int dt, int64_t n, uint32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    bad |= !isfinite(load_as_f32(x, dt, i));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 }  // namespace
@@ -444,6 +506,38 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
       static_cast<const uint8_t*>(src), slot_stride * esz, static_cast<uint8_t*>(dst), esz, b, hp,
       sl, d, u);
   FUSP_LAUNCHED("unpack_heads_kernel");
+  return FUSP_OK;
+}
+
+}  // namespace fusp
+
+namespace fusp {
+
+fusp_status launch_scale_finalize(const uint32_t* amax_bits, float* scale, float* copies,
+                                  int64_t copy_stride, int count, cudaStream_t s) {
+  scale_finalize_kernel<<<1, 32, 0, s>>>(amax_bits, scale, copies, copy_stride, count);
+  FUSP_LAUNCHED("scale_finalize_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_requantize_seg(const uint8_t* codes, const float* scales, int64_t sstride, int d,
+                                  int span, int seg_rows, int64_t n, uint32_t* amax_bits,
+                                  float* scale_out, uint8_t* codes_out, cudaStream_t s) {
+  FUSP_CUDA(cudaMemsetAsync(amax_bits, 0, sizeof(uint32_t), s));
+  if (n <= 0) return FUSP_OK;
+  amax_seg_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(codes, scales, sstride, d, span, seg_rows, n,
+                                                     amax_bits);
+  FUSP_LAUNCHED("amax_seg_kernel");
+  quantize_seg_kernel<<<grid_for(n), kBlock, 0, s>>>(codes, scales, sstride, d, span, seg_rows, n,
+                                                      amax_bits, scale_out, codes_out);
+  FUSP_LAUNCHED("quantize_seg_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_finite(const void* x, int dt, int64_t n, uint32_t* flag, cudaStream_t s) {
+  if (n <= 0) return FUSP_OK;
+  finite_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(x, dt, n, flag);
+  FUSP_LAUNCHED("finite_kernel");
   return FUSP_OK;
 }
 

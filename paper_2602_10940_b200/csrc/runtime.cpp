@@ -201,9 +201,11 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
     return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(qs.d) +
                                          " unsupported by the sm_100a kernel (D=128)");
   const int64_t nkv = heads * skv * qs.d;
-  // Operand staging: Q,K -> bf16, V -> f16 (one HBM pass each, skipped when already in place).
+  // Operand staging: Q,K -> bf16 (f16 inputs stay f16), V -> f16; one HBM pass each,
+  // skipped when the caller's tensor already has the MMA dtype.
+  const int qk_dt = in_dtype == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
   size_t need = 0;
-  if (in_dtype != FUSP_BF16) need += static_cast<size_t>(nq + nkv) * 2;
+  if (in_dtype != qk_dt) need += static_cast<size_t>(nq + nkv) * 2;
   if (in_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
   uint8_t* ws = nullptr;
   if (need) FUSP_CHECK(scratch(need + 256, reinterpret_cast<void**>(&ws)));
@@ -211,7 +213,7 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
   const void* kb = k;
   const void* vh = v;
   size_t off = 0;
-  if (in_dtype != FUSP_BF16) {
+  if (in_dtype != qk_dt) {
     void* tq = ws + off;
     off += static_cast<size_t>(nq) * 2;
     void* tk = ws + off;
@@ -230,6 +232,7 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
   a.q = qb;
   a.k = kb;
   a.v = vh;
+  a.qk_dtype = qk_dt;
   a.q_hs = qs.s * 128;
   a.k_hs = skv * 128;
   a.v_hs = skv * 128;

@@ -1,0 +1,827 @@
+// The USP protocols on B200: per-rank context, Ulysses all-to-all reshards, the
+// (serial or double-buffered) ring with the LSE merge fused into the attention
+// epilogue, FP8 K/V communication, and CUDA-Graph capture of the layer.
+//
+// Reference mapping (proj/src/protocols.cpp):
+//   usp_attention            :321-340  -> run_layer(kUsp)
+//   ulysses_attention        :207-214  -> run_layer(kUlysses)  (R = 1)
+//   ring_attention_serial    :237-268  -> ring()  with pipelined = false
+//   ring_attention_pipelined :270-319  -> ring()  with pipelined = true (side stream)
+//   ulysses_input_reshard    :125-180  -> ulysses_in()   pack -> all_to_all -> unpack
+//   ulysses_output_reshard   :182-203  -> ulysses_out()  epilogue writes send slots -> all_to_all
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "fastusp_internal.h"
+
+using namespace fusp;
+
+struct fusp_fabric_s {
+  explicit fusp_fabric_s(int n) : fabric(n) {}
+  LocalFabric fabric;
+};
+
+struct fusp_ctx_s {
+  int rank = 0, world = 1, device = 0;
+  std::unique_ptr<Comm> comm;
+  NcclComm* nccl = nullptr;
+  cudaStream_t side = nullptr;  // ring communication stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_attn[2] = {nullptr, nullptr};
+  static constexpr int kMaxSteps = 32;
+  cudaEvent_t tc0[kMaxSteps], tc1[kMaxSteps], tm0[kMaxSteps], tm1[kMaxSteps];
+  int timed_steps = 0;
+  bool capturing = false;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  void* host_stage = nullptr;
+  size_t host_stage_bytes = 0;
+  uint64_t a2a_bytes = 0, send_bytes = 0;
+};
+
+struct fusp_graph_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int device = 0;
+};
+
+namespace {
+
+enum class Mode { kUsp, kUlysses, kRing };
+
+const char* tag(Mode m) { return m == Mode::kUsp ? "usp" : m == Mode::kUlysses ? "ulysses" : "ring"; }
+
+std::string sstr(const fusp_shape4& s) {
+  std::ostringstream os;
+  os << "[" << s.b << "," << s.h << "," << s.s << "," << s.d << "]";
+  return os.str();
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over the context arena; the first (dry) pass only measures.
+struct Carve {
+  char* base = nullptr;
+  size_t off = 0;
+  void* take(size_t bytes) {
+    off = align_up(off, 256);
+    void* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+fusp_status ensure_arena(fusp_ctx_s* c, size_t bytes) {
+  if (c->arena_bytes >= bytes) return FUSP_OK;
+  if (c->capturing)
+    return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+  FUSP_CUDA(cudaDeviceSynchronize());
+  if (c->arena) FUSP_CUDA(cudaFree(c->arena));
+  c->arena = nullptr;
+  c->arena_bytes = 0;
+  FUSP_CUDA(cudaMalloc(&c->arena, bytes));
+  c->arena_bytes = bytes;
+  return FUSP_OK;
+}
+
+struct Layer {
+  Mode mode;
+  int B, H, SL, D, U, R, hp, heads_r, span;
+  int64_t blk, C;  // elements per (Q|K|V) slot piece, elements per ring chunk (= U*blk)
+  bool fp8, pipelined;
+  int in_dt, out_dt;
+  int qk_dt;  // MMA dtype of Q and K: f16 inputs stay f16, f32/bf16 travel as bf16
+  size_t wout;
+  Group ug, rg;
+  // Ulysses wire slot: [Q bf16 blk][K bf16|e4m3 blk][V f16|e4m3 blk]{[k scale][v scale]}
+  size_t slot_bytes, slot_stride;
+};
+
+struct Buffers {
+  // Ulysses in
+  char *send_in = nullptr, *recv_in = nullptr;
+  // attention operands of the local chunk
+  const void *Qr = nullptr, *Kr = nullptr, *Vr = nullptr;
+  void *Qr_w = nullptr, *Kr_w = nullptr, *Vr_w = nullptr;
+  // fp8 exact local chunk: codes [heads_r][span][D] + per-segment scales
+  uint8_t *Kc = nullptr, *Vc = nullptr;
+  const float *Ks = nullptr, *Vs = nullptr;
+  int64_t s_stride = 1;
+  int seg_rows = 0;
+  float* qscale = nullptr;  // [0]=k [1]=v scale of a locally quantized chunk
+  uint32_t* amax = nullptr; // scratch (4 words)
+  // ring
+  char* rb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buf][K|V] wire parts
+  char* sw[2] = {nullptr, nullptr};                           // fp8 send wire parts
+  void *Kd = nullptr, *Vd = nullptr;                          // fp8 dequantized operands
+  float *acc_o = nullptr, *acc_lse = nullptr;
+  // Ulysses out
+  char *send_out = nullptr, *recv_out = nullptr;
+};
+
+fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, int in_dt,
+                       const fusp_comm_options& o, Layer* L) {
+  if (mode != Mode::kUsp) r = mode == Mode::kRing ? c->world : 1;
+  if (r < 1 || c->world % r != 0)
+    return set_error(FUSP_ERR_MESH, "ring dimension " + std::to_string(r) +
+                                        " does not divide worker count " + std::to_string(c->world));
+  if (ls.b < 1 || ls.h < 1 || ls.s < 1 || ls.d < 1)
+    return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": bad local shape " + sstr(ls));
+  if (in_dt != FUSP_F32 && in_dt != FUSP_BF16 && in_dt != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "input dtype must be f32, bf16 or f16");
+  if (o.out_dtype != FUSP_F32 && o.out_dtype != FUSP_BF16 && o.out_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "out_dtype must be f32, bf16 or f16");
+  Layer& l = *L;
+  l.mode = mode;
+  l.B = static_cast<int>(ls.b);
+  l.H = static_cast<int>(ls.h);
+  l.SL = static_cast<int>(ls.s);
+  l.D = static_cast<int>(ls.d);
+  l.R = r;
+  l.U = mode == Mode::kRing ? 1 : c->world / r;
+  if (l.H % l.U != 0)
+    return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": head count H=" +
+                                         std::to_string(l.H) + " not divisible by ulysses dimension U=" +
+                                         std::to_string(l.U));
+  if (l.D != 128)
+    return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": head dim D=" + std::to_string(l.D) +
+                                         " unsupported by the sm_100a kernel (D=128)");
+  l.hp = l.H / l.U;
+  l.heads_r = l.B * l.hp;
+  l.span = l.U * l.SL;
+  l.blk = int64_t(l.B) * l.hp * l.SL * l.D;
+  l.C = l.blk * l.U;
+  l.fp8 = o.fp8_kv != 0;
+  l.pipelined = o.pipelined_ring != 0;
+  l.in_dt = in_dt;
+  l.qk_dt = in_dt == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
+  l.out_dt = o.out_dtype;
+  l.wout = dtype_size(o.out_dtype);
+  // mesh groups (mesh.cpp:44-53): rank = ring_idx * U + uly_idx
+  const int ri = c->rank / l.U, ui = c->rank % l.U;
+  for (int j = 0; j < l.U; ++j) l.ug.members.push_back(ri * l.U + j);
+  for (int i = 0; i < l.R; ++i) l.rg.members.push_back(i * l.U + ui);
+  l.ug.pos = ui;
+  l.rg.pos = ri;
+  l.slot_bytes = l.fp8 ? size_t(l.blk) * 4 + 8 : size_t(l.blk) * 6;
+  l.slot_stride = align_up(l.slot_bytes, 256);
+  return FUSP_OK;
+}
+
+// Assign workspace for a layer. `user_*` are the caller's tensors (zero-copy when possible).
+void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, const void* v,
+           void* out) {
+  const size_t C2 = size_t(l.C) * 2;
+  const bool uly = l.mode != Mode::kRing;
+  if (uly && l.U > 1) {
+    b->send_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
+    b->recv_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
+    b->Qr = b->Qr_w = cv.take(C2);
+    b->Kr = b->Kr_w = cv.take(C2);
+    b->Vr = b->Vr_w = cv.take(C2);
+    if (l.fp8) {
+      b->Kc = static_cast<uint8_t*>(cv.take(l.C));
+      b->Vc = static_cast<uint8_t*>(cv.take(l.C));
+    }
+  } else {
+    // U == 1: no transfer; operands are the caller's tensors when already in the MMA dtype.
+    if (l.in_dt == l.qk_dt) b->Qr = q; else b->Qr = b->Qr_w = cv.take(C2);
+    const bool fq = uly && l.fp8;  // Ulysses self slot still takes the FP8 round trip (D7)
+    if (l.in_dt == l.qk_dt && !fq) b->Kr = k; else b->Kr = b->Kr_w = cv.take(C2);
+    if (l.in_dt == FUSP_F16 && !fq) b->Vr = v; else b->Vr = b->Vr_w = cv.take(C2);
+    if (fq) {
+      b->Kc = static_cast<uint8_t*>(cv.take(l.C));
+      b->Vc = static_cast<uint8_t*>(cv.take(l.C));
+    }
+  }
+  b->qscale = static_cast<float*>(cv.take(64));
+  b->amax = static_cast<uint32_t*>(cv.take(64));
+  if (l.R > 1) {
+    const size_t part = l.fp8 ? align_up(size_t(l.C) + 4, 256) : C2;
+    for (int i = 0; i < 2; ++i)
+      for (int p = 0; p < 2; ++p) b->rb[i][p] = static_cast<char*>(cv.take(part));
+    if (l.fp8) {
+      for (int p = 0; p < 2; ++p) b->sw[p] = static_cast<char*>(cv.take(part));
+      b->Kd = cv.take(C2);
+      b->Vd = cv.take(C2);
+    }
+    b->acc_o = static_cast<float*>(cv.take(size_t(l.C) * 4));
+    b->acc_lse = static_cast<float*>(cv.take(size_t(l.heads_r) * l.span * 4));
+  }
+  if (uly && l.U > 1) {
+    b->send_out = static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
+    b->recv_out = l.B == 1 ? static_cast<char*>(out)
+                           : static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
+  }
+}
+
+// ---------------------------------------------------------------- Ulysses input reshard
+fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q, const void* k,
+                       const void* v, cudaStream_t s) {
+  const bool uly = l.mode != Mode::kRing;
+  if (!uly || l.U == 1) {
+    const int64_t n = l.C;
+    if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
+    if (uly && l.fp8) {
+      // quantize the whole local K and V (protocols.cpp:139-142), self slot dequantized (:163-179)
+      for (int p = 0; p < 2; ++p) {
+        const void* src = p == 0 ? k : v;
+        uint8_t* codes = p == 0 ? b.Kc : b.Vc;
+        FUSP_CHECK(launch_amax(src, l.in_dt, n, b.amax, b.amax + 1, s));
+        FUSP_CHECK(launch_quantize(src, l.in_dt, n, b.amax, b.qscale + p, codes, s));
+        FUSP_CHECK(launch_dequantize(codes, b.qscale + p, n, p == 0 ? b.Kr_w : b.Vr_w,
+                                     p == 0 ? l.qk_dt : FUSP_F16, s));
+      }
+      b.Ks = b.qscale;
+      b.Vs = b.qscale + 1;
+      b.s_stride = 1;
+      b.seg_rows = l.span;
+    } else {
+      if (b.Kr_w) FUSP_CHECK(launch_convert(k, l.in_dt, b.Kr_w, l.qk_dt, n, s));
+      if (b.Vr_w) FUSP_CHECK(launch_convert(v, l.in_dt, b.Vr_w, FUSP_F16, n, s));
+    }
+    return FUSP_OK;
+  }
+  // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153)
+  const int64_t se2 = int64_t(l.slot_stride) / 2;  // slot stride in 16-bit elements
+  PackDesc p{};
+  p.b = l.B;
+  p.h = l.H;
+  p.sl = l.SL;
+  p.d = l.D;
+  p.u = l.U;
+  p.src = q;
+  p.src_dtype = l.in_dt;
+  p.dst = b.send_in;
+  p.dst_dtype = l.qk_dt;
+  p.dst_slot_stride = se2;
+  FUSP_CHECK(launch_pack(p, s));
+  if (!l.fp8) {
+    p.src = k;
+    p.dst = b.send_in + l.blk * 2;
+    FUSP_CHECK(launch_pack(p, s));
+    p.src = v;
+    p.dst = b.send_in + l.blk * 4;
+    p.dst_dtype = FUSP_F16;
+    FUSP_CHECK(launch_pack(p, s));
+  } else {
+    // per-tensor scale over ALL local heads (fp8.cpp:107-123), copied into every slot's trailer
+    for (int part = 0; part < 2; ++part) {
+      const void* src = part == 0 ? k : v;
+      const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
+      FUSP_CHECK(launch_amax(src, l.in_dt, n, b.amax, b.amax + 1, s));
+      float* trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part;
+      FUSP_CHECK(launch_scale_finalize(b.amax, b.qscale + part, trailer,
+                                       int64_t(l.slot_stride / 4), l.U, s));
+      p.src = src;
+      p.dst = b.send_in + l.blk * 2 + part * l.blk;
+      p.dst_dtype = FUSP_E4M3;
+      p.dst_slot_stride = int64_t(l.slot_stride);
+      p.scale = b.qscale + part;
+      FUSP_CHECK(launch_pack(p, s));
+    }
+  }
+  FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
+  c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
+  // unpack: source j contributed our heads over its sequence shard (protocols.cpp:163-179)
+  UnpackDesc u{};
+  u.b = l.B;
+  u.hp = l.hp;
+  u.sl = l.SL;
+  u.d = l.D;
+  u.u = l.U;
+  u.src = b.recv_in;
+  u.src_dtype = l.qk_dt;
+  u.src_slot_stride = se2;
+  u.dst = b.Qr_w;
+  u.dst_dtype = l.qk_dt;
+  FUSP_CHECK(launch_unpack(u, s));
+  if (!l.fp8) {
+    u.src = b.recv_in + l.blk * 2;
+    u.dst = b.Kr_w;
+    FUSP_CHECK(launch_unpack(u, s));
+    u.src = b.recv_in + l.blk * 4;
+    u.src_dtype = FUSP_F16;
+    u.dst = b.Vr_w;
+    u.dst_dtype = FUSP_F16;
+    FUSP_CHECK(launch_unpack(u, s));
+  } else {
+    const float* scales = reinterpret_cast<const float*>(b.recv_in + l.blk * 4);
+    for (int part = 0; part < 2; ++part) {
+      u.src = b.recv_in + l.blk * 2 + part * l.blk;
+      u.src_dtype = FUSP_E4M3;
+      u.src_slot_stride = int64_t(l.slot_stride);
+      u.scales = scales + part;
+      u.scale_stride = int64_t(l.slot_stride / 4);
+      u.dst = part == 0 ? b.Kr_w : b.Vr_w;
+      u.dst_dtype = part == 0 ? l.qk_dt : FUSP_F16;
+      FUSP_CHECK(launch_unpack(u, s));
+      u.dst = part == 0 ? static_cast<void*>(b.Kc) : static_cast<void*>(b.Vc);
+      u.dst_dtype = FUSP_E4M3;
+      FUSP_CHECK(launch_unpack(u, s));
+    }
+    b.Ks = scales;
+    b.Vs = scales + 1;
+    b.s_stride = int64_t(l.slot_stride / 4);
+    b.seg_rows = l.SL;
+  }
+  return FUSP_OK;
+}
+
+// ---------------------------------------------------------------- attention step
+fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* V, bool first,
+                   bool last, void* out, float* lse_out, cudaStream_t s) {
+  AttnLaunch a{};
+  a.qk_dtype = l.qk_dt;
+  a.q = b.Qr;
+  a.k = K;
+  a.v = V;
+  a.q_hs = a.k_hs = a.v_hs = int64_t(l.span) * l.D;
+  a.heads = l.heads_r;
+  a.sq = l.span;
+  a.skv = l.span;
+  a.d = l.D;
+  const bool direct_out = l.mode == Mode::kRing || l.U == 1;
+  if (last) {
+    a.out = direct_out ? out : b.send_out;
+    a.out_dtype = l.out_dt;
+    if (direct_out) {
+      a.out_chunk = l.span;
+      a.out_hs = int64_t(l.span) * l.D;
+      a.out_cs = 0;
+      a.out_rs = l.D;
+    } else {  // epilogue stores O straight into the output all-to-all slots (t = row / SL)
+      a.out_chunk = l.SL;
+      a.out_hs = int64_t(l.SL) * l.D;
+      a.out_cs = l.blk;
+      a.out_rs = l.D;
+    }
+    a.lse = lse_out;
+    a.lse_hs = l.span;
+  } else {
+    a.out = b.acc_o;
+    a.out_dtype = FUSP_F32;
+    a.out_chunk = l.span;
+    a.out_hs = int64_t(l.span) * l.D;
+    a.out_cs = 0;
+    a.out_rs = l.D;
+    a.lse = b.acc_lse;
+    a.lse_hs = l.span;
+  }
+  if (!first) {  // merge_lse(acc, part) fused into the epilogue (protocols.cpp:265-266, :315-316)
+    a.acc_o = b.acc_o;
+    a.acc_lse = b.acc_lse;
+  }
+  return launch_attention(a, s);
+}
+
+// ---------------------------------------------------------------- ring
+fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, const void* v_src,
+                 void* out, float* lse_out, cudaStream_t s) {
+  const int R = l.R;
+  const bool timing = !c->capturing && R <= fusp_ctx_s::kMaxSteps;
+  c->timed_steps = timing ? R : 0;
+  const size_t C2 = size_t(l.C) * 2;
+  const size_t part_bytes = l.fp8 ? size_t(l.C) + 4 : C2;  // reference: 4-byte scale + codes
+  if (R == 1) {
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
+    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, true, out, lse_out, s));
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
+    return FUSP_OK;
+  }
+  const bool usp_local = l.mode != Mode::kRing;
+  // Fill the FP8 send wire [codes][f32 scale] for one hop from the chunk we hold.
+  auto quantize_hop = [&](int hop, int from_buf, cudaStream_t st) -> fusp_status {
+    for (int p = 0; p < 2; ++p) {
+      uint8_t* codes = reinterpret_cast<uint8_t*>(b.sw[p]);
+      float* scale = reinterpret_cast<float*>(b.sw[p] + l.C);
+      if (hop == 1 && !usp_local) {  // pure ring: quantize the caller's local chunk
+        const void* src = p == 0 ? k_src : v_src;
+        FUSP_CHECK(launch_amax(src, l.in_dt, l.C, b.amax + 2 * p, b.amax + 2 * p + 1, st));
+        FUSP_CHECK(launch_quantize(src, l.in_dt, l.C, b.amax + 2 * p, scale, codes, st));
+      } else if (hop == 1) {  // USP: exact f32 values of the (multi-scale) resharded chunk
+        FUSP_CHECK(launch_requantize_seg(p == 0 ? b.Kc : b.Vc, p == 0 ? b.Ks : b.Vs, b.s_stride,
+                                         l.D, l.span, b.seg_rows, l.C, b.amax + 2 * p, scale,
+                                         codes, st));
+      } else {  // forward: re-quantize the dequantized chunk just received (protocols.cpp:309-310)
+        const char* w = b.rb[from_buf][p];
+        FUSP_CHECK(launch_requantize_seg(reinterpret_cast<const uint8_t*>(w),
+                                         reinterpret_cast<const float*>(w + l.C), 1, l.D, l.span,
+                                         l.span, l.C, b.amax + 2 * p, scale, codes, st));
+      }
+    }
+    return FUSP_OK;
+  };
+  auto exchange = [&](int hop, cudaStream_t st) -> fusp_status {
+    const int into = hop % 2, from = (hop - 1) % 2;
+    const void* snd[2];
+    if (l.fp8) {
+      FUSP_CHECK(quantize_hop(hop, from, st));
+      snd[0] = b.sw[0];
+      snd[1] = b.sw[1];
+    } else if (hop == 1) {
+      snd[0] = b.Kr;
+      snd[1] = b.Vr;
+    } else {
+      snd[0] = b.rb[from][0];
+      snd[1] = b.rb[from][1];
+    }
+    void* rcv[2] = {b.rb[into][0], b.rb[into][1]};
+    const size_t bytes[2] = {part_bytes, part_bytes};
+    FUSP_CHECK(c->comm->ring_exchange(l.rg, snd, rcv, bytes, 2, st));
+    c->send_bytes += 2 * part_bytes;
+    return FUSP_OK;
+  };
+  auto operands = [&](int hop, cudaStream_t st, const void** K, const void** V) -> fusp_status {
+    const int buf = hop % 2;
+    if (!l.fp8) {
+      *K = b.rb[buf][0];
+      *V = b.rb[buf][1];
+      return FUSP_OK;
+    }
+    const char* wk = b.rb[buf][0];
+    const char* wv = b.rb[buf][1];
+    FUSP_CHECK(launch_dequantize(reinterpret_cast<const uint8_t*>(wk),
+                                 reinterpret_cast<const float*>(wk + l.C), l.C, b.Kd, l.qk_dt, st));
+    FUSP_CHECK(launch_dequantize(reinterpret_cast<const uint8_t*>(wv),
+                                 reinterpret_cast<const float*>(wv + l.C), l.C, b.Vd, FUSP_F16, st));
+    *K = b.Kd;
+    *V = b.Vd;
+    return FUSP_OK;
+  };
+
+  if (!l.pipelined) {
+    // ring_attention_serial (protocols.cpp:237-268): compute, then send/recv/compute per round.
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
+    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s));
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
+    for (int i = 1; i < R; ++i) {
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tm0[i], s));
+      FUSP_CHECK(exchange(i, s));
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[i], s));
+      const void *K, *V;
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[i], s));
+      FUSP_CHECK(operands(i, s, &K, &V));
+      FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s));
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[i], s));
+    }
+    return FUSP_OK;
+  }
+  // ring_attention_pipelined (Alg. 2, protocols.cpp:270-319): round i+1's transfer runs on
+  // the side stream while round i computes; buffers alternate, WAR hazards are events.
+  cudaStream_t m = c->side;
+  FUSP_CUDA(cudaEventRecord(c->ev_fork, s));
+  FUSP_CUDA(cudaStreamWaitEvent(m, c->ev_fork, 0));
+  if (timing) FUSP_CUDA(cudaEventRecord(c->tm0[1], m));
+  FUSP_CHECK(exchange(1, m));
+  if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[1], m));
+  FUSP_CUDA(cudaEventRecord(c->ev_recv[1], m));
+  if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
+  FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s));
+  if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
+  FUSP_CUDA(cudaEventRecord(c->ev_attn[0], s));
+  for (int i = 1; i < R; ++i) {
+    FUSP_CUDA(cudaStreamWaitEvent(s, c->ev_recv[i % 2], 0));
+    if (i < R - 1) {
+      // buffer (i+1)%2 was last read by compute step i-1
+      FUSP_CUDA(cudaStreamWaitEvent(m, c->ev_attn[(i - 1) % 2], 0));
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tm0[i + 1], m));
+      FUSP_CHECK(exchange(i + 1, m));
+      if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[i + 1], m));
+      FUSP_CUDA(cudaEventRecord(c->ev_recv[(i + 1) % 2], m));
+    }
+    const void *K, *V;
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[i], s));
+    FUSP_CHECK(operands(i, s, &K, &V));
+    FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s));
+    if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[i], s));
+    FUSP_CUDA(cudaEventRecord(c->ev_attn[i % 2], s));
+  }
+  FUSP_CUDA(cudaEventRecord(c->ev_join, m));
+  FUSP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  return FUSP_OK;
+}
+
+// ---------------------------------------------------------------- Ulysses output reshard
+fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, cudaStream_t s) {
+  if (l.mode == Mode::kRing || l.U == 1) return FUSP_OK;  // epilogue wrote `out` directly
+  const size_t slot = size_t(l.blk) * l.wout;
+  FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
+  c->a2a_bytes += uint64_t(l.U - 1) * slot;
+  if (l.B > 1)  // concat_heads (protocols.cpp:196-202)
+    FUSP_CHECK(launch_unpack_heads(b.recv_out, l.blk, out, l.out_dt, l.B, l.hp, l.SL, l.D, l.U, s));
+  return FUSP_OK;
+}
+
+fusp_status check_inputs(fusp_ctx_s* c, Mode mode, const Layer& l, const void* q, const void* k,
+                         const void* v, cudaStream_t s) {
+  size_t need = 256;
+  FUSP_CHECK(ensure_arena(c, need));
+  uint32_t* flag = static_cast<uint32_t*>(c->arena);
+  FUSP_CUDA(cudaMemsetAsync(flag, 0, 4, s));
+  const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
+  FUSP_CHECK(launch_finite(q, l.in_dt, n, flag, s));
+  FUSP_CHECK(launch_finite(k, l.in_dt, n, flag, s));
+  FUSP_CHECK(launch_finite(v, l.in_dt, n, flag, s));
+  uint32_t h = 0;
+  FUSP_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s));
+  FUSP_CUDA(cudaStreamSynchronize(s));
+  if (h)  // check_local_qkv (protocols.cpp:102-104)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT,
+                     std::string(tag(mode)) + ": non-finite element in protocol input");
+  return FUSP_OK;
+}
+
+fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void* k,
+                      const void* v, int in_dt, fusp_shape4 ls, void* out, float* lse_out,
+                      const fusp_comm_options* opts, cudaStream_t s, bool size_only = false) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  fusp_comm_options o{};
+  o.out_dtype = FUSP_F32;
+  if (opts) o = *opts;
+  Layer l;
+  FUSP_CHECK(plan_layer(c, mode, r, ls, in_dt, o, &l));
+  if (c->nccl && l.U > 1 && l.R > 1) FUSP_CHECK(c->nccl->ensure_mesh(l.R));
+  if (o.check_finite && !size_only) FUSP_CHECK(check_inputs(c, mode, l, q, k, v, s));
+  Carve cv;
+  Buffers b;
+  carve(l, cv, &b, q, k, v, out);
+  FUSP_CHECK(ensure_arena(c, cv.off + 256));
+  if (size_only) return FUSP_OK;
+  cv = Carve{static_cast<char*>(c->arena), 0};
+  b = Buffers{};
+  carve(l, cv, &b, q, k, v, out);
+  FUSP_CHECK(ulysses_in(c, l, b, q, k, v, s));
+  FUSP_CHECK(ring(c, l, b, k, v, out, lse_out, s));
+  FUSP_CHECK(ulysses_out(c, l, b, out, s));
+  return FUSP_OK;
+}
+
+fusp_status init_ctx(fusp_ctx_s* c) {
+  FUSP_CUDA(cudaSetDevice(c->device));
+  FUSP_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  FUSP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  FUSP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    FUSP_CUDA(cudaEventCreateWithFlags(&c->ev_recv[i], cudaEventDisableTiming));
+    FUSP_CUDA(cudaEventCreateWithFlags(&c->ev_attn[i], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < fusp_ctx_s::kMaxSteps; ++i) {
+    FUSP_CUDA(cudaEventCreate(&c->tc0[i]));
+    FUSP_CUDA(cudaEventCreate(&c->tc1[i]));
+    FUSP_CUDA(cudaEventCreate(&c->tm0[i]));
+    FUSP_CUDA(cudaEventCreate(&c->tm1[i]));
+  }
+  return FUSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fusp_status fusp_fabric_create(int world, fusp_fabric* out) {
+  clear_error();
+  if (world < 1) return set_error(FUSP_ERR_COMM, "run_protocol: need at least one worker");
+  *out = new fusp_fabric_s(world);
+  return FUSP_OK;
+}
+
+fusp_status fusp_fabric_destroy(fusp_fabric f) {
+  delete f;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_create_local(fusp_fabric f, int rank, int device, fusp_ctx* out) {
+  clear_error();
+  if (!f) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null fabric");
+  if (rank < 0 || rank >= f->fabric.world)
+    return set_error(FUSP_ERR_COMM, "rank " + std::to_string(rank) + " out of range [0," +
+                                        std::to_string(f->fabric.world) + ")");
+  auto* c = new fusp_ctx_s;
+  c->rank = rank;
+  c->world = f->fabric.world;
+  c->device = device;
+  fusp_status st = init_ctx(c);
+  if (st != FUSP_OK) {
+    delete c;
+    return st;
+  }
+  c->comm = std::make_unique<LocalComm>(&f->fabric, rank, device);
+  *out = c;
+  return FUSP_OK;
+}
+
+fusp_status fusp_nccl_unique_id(uint8_t uid[128]) {
+  clear_error();
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_error(r, "ncclGetUniqueId");
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(uid, &id, 128);
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_create_nccl(const uint8_t uid[128], int world, int rank, int device,
+                                 fusp_ctx* out) {
+  clear_error();
+  auto* c = new fusp_ctx_s;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  fusp_status st = init_ctx(c);
+  if (st != FUSP_OK) {
+    delete c;
+    return st;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, uid, 128);
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_error(r, "ncclCommInitRank");
+  }
+  auto nc = std::make_unique<NcclComm>(comm, rank, world);
+  c->nccl = nc.get();
+  c->comm = std::move(nc);
+  *out = c;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_destroy(fusp_ctx c) {
+  if (!c) return FUSP_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  c->comm.reset();
+  if (c->arena) cudaFree(c->arena);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_recv[0], c->ev_recv[1], c->ev_attn[0], c->ev_attn[1]})
+    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < fusp_ctx_s::kMaxSteps; ++i)
+    for (cudaEvent_t e : {c->tc0[i], c->tc1[i], c->tm0[i], c->tm1[i]})
+      if (e) cudaEventDestroy(e);
+  delete c;
+  return FUSP_OK;
+}
+
+int fusp_ctx_rank(fusp_ctx c) { return c ? c->rank : -1; }
+int fusp_ctx_world(fusp_ctx c) { return c ? c->world : 0; }
+
+fusp_status fusp_ctx_traffic(fusp_ctx c, uint64_t* a2a, uint64_t* snd) {
+  if (a2a) *a2a = c->a2a_bytes;
+  if (snd) *snd = c->send_bytes;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_reset_traffic(fusp_ctx c) {
+  c->a2a_bytes = 0;
+  c->send_bytes = 0;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_ring_timings(fusp_ctx c, int max_steps, float* compute_ms, float* comm_ms,
+                                  int* steps) {
+  clear_error();
+  FUSP_CUDA(cudaSetDevice(c->device));
+  const int n = c->timed_steps < max_steps ? c->timed_steps : max_steps;
+  *steps = n;
+  for (int i = 0; i < n; ++i) {
+    FUSP_CUDA(cudaEventSynchronize(c->tc1[i]));
+    FUSP_CUDA(cudaEventElapsedTime(&compute_ms[i], c->tc0[i], c->tc1[i]));
+    comm_ms[i] = 0.f;
+    if (i > 0) {
+      FUSP_CUDA(cudaEventSynchronize(c->tm1[i]));
+      FUSP_CUDA(cudaEventElapsedTime(&comm_ms[i], c->tm0[i], c->tm1[i]));
+    }
+  }
+  return FUSP_OK;
+}
+
+fusp_status fusp_usp_attention(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                               const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                               const fusp_comm_options* opts, fusp_stream_t stream) {
+  return run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_ulysses_attention(fusp_ctx c, const void* q, const void* k, const void* v,
+                                   fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                   const fusp_comm_options* opts, fusp_stream_t stream) {
+  return run_layer(c, Mode::kUlysses, 1, q, k, v, in_dtype, ls, out, nullptr, opts,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_ring_attention(fusp_ctx c, const void* q, const void* k, const void* v,
+                                fusp_dtype in_dtype, fusp_shape4 ls, void* out, float* lse,
+                                const fusp_comm_options* opts, fusp_stream_t stream) {
+  return run_layer(c, Mode::kRing, c ? c->world : 1, q, k, v, in_dtype, ls, out, lse, opts,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                                    const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                    const fusp_comm_options* opts, fusp_stream_t stream) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int out_dt = opts ? opts->out_dtype : FUSP_F32;
+  const size_t n = size_t(ls.b * ls.h * ls.s * ls.d);
+  const size_t in_b = n * dtype_size(in_dtype), out_b = n * dtype_size(out_dt);
+  // device staging lives in its own allocation (the arena belongs to the layer)
+  static thread_local void* dstage = nullptr;
+  static thread_local size_t dstage_bytes = 0;
+  const size_t need = 3 * align_up(in_b, 256) + align_up(out_b, 256);
+  if (dstage_bytes < need) {
+    if (dstage) FUSP_CUDA(cudaFree(dstage));
+    FUSP_CUDA(cudaMalloc(&dstage, need));
+    dstage_bytes = need;
+  }
+  char* d = static_cast<char*>(dstage);
+  void* dq = d;
+  void* dk = d + align_up(in_b, 256);
+  void* dv = d + 2 * align_up(in_b, 256);
+  void* dout = d + 3 * align_up(in_b, 256);
+  FUSP_CUDA(cudaMemcpyAsync(dq, q, in_b, cudaMemcpyHostToDevice, s));
+  FUSP_CUDA(cudaMemcpyAsync(dk, k, in_b, cudaMemcpyHostToDevice, s));
+  FUSP_CUDA(cudaMemcpyAsync(dv, v, in_b, cudaMemcpyHostToDevice, s));
+  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, dq, dk, dv, in_dtype, ls, dout, nullptr, opts, s));
+  FUSP_CUDA(cudaMemcpyAsync(out, dout, out_b, cudaMemcpyDeviceToHost, s));
+  FUSP_CUDA(cudaStreamSynchronize(s));
+  return FUSP_OK;
+}
+
+fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                                   const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                   const fusp_comm_options* opts, int layers,
+                                   int64_t in_stride, int64_t out_stride, fusp_stream_t stream,
+                                   fusp_graph* graph) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  if (!c->comm->capturable())
+    return set_error(FUSP_ERR_UNSUPPORTED,
+                     "graph capture needs an NCCL context (or a world-1 local context)");
+  if (opts && opts->check_finite)
+    return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // size the workspace before capture (no allocation inside the graph)
+  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts, s, true));
+  FUSP_CUDA(cudaStreamSynchronize(s));
+  auto* g = new fusp_graph_s;
+  g->device = c->device;
+  c->capturing = true;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  fusp_status st = e == cudaSuccess ? FUSP_OK : set_cuda_error(e, "cudaStreamBeginCapture");
+  for (int i = 0; i < layers && st == FUSP_OK; ++i) {
+    const char* qi = static_cast<const char*>(q) + i * in_stride;
+    const char* ki = static_cast<const char*>(k) + i * in_stride;
+    const char* vi = static_cast<const char*>(v) + i * in_stride;
+    char* oi = static_cast<char*>(out) + i * out_stride;
+    st = run_layer(c, Mode::kUsp, ring_dim, qi, ki, vi, in_dtype, ls, oi, nullptr, opts, s);
+  }
+  cudaGraph_t graph_raw = nullptr;
+  e = cudaStreamEndCapture(s, &graph_raw);
+  c->capturing = false;
+  if (st == FUSP_OK && e != cudaSuccess) st = set_cuda_error(e, "cudaStreamEndCapture");
+  if (st == FUSP_OK) {
+    g->graph = graph_raw;
+    e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) st = set_cuda_error(e, "cudaGraphInstantiate");
+  } else if (graph_raw) {
+    cudaGraphDestroy(graph_raw);
+  }
+  if (st != FUSP_OK) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return st;
+  }
+  *graph = g;
+  return FUSP_OK;
+}
+
+fusp_status fusp_graph_launch(fusp_graph g, fusp_stream_t stream) {
+  clear_error();
+  FUSP_CUDA(cudaSetDevice(g->device));
+  FUSP_CUDA(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)));
+  return FUSP_OK;
+}
+
+fusp_status fusp_graph_destroy(fusp_graph g) {
+  if (!g) return FUSP_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return FUSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+"""CPU: the C-ABI library loads, exports every symbol include/fastusp.h declares, and its
+host-only entry points (mesh, error reporting) match the reference.  No GPU compute."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fastusp.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fusp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_reference_roster():
+    syms = declared_symbols()
+    for s in ("fusp_usp_attention", "fusp_ulysses_attention", "fusp_ring_attention",
+              "fusp_attention_with_lse", "fusp_merge_lse", "fusp_quantize_e4m3",
+              "fusp_dequantize_e4m3", "fusp_encode_e4m3", "fusp_decode_e4m3", "fusp_mesh_build",
+              "fusp_mesh_make", "fusp_ctx_create_nccl", "fusp_ctx_create_local",
+              "fusp_graph_capture_usp", "fusp_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(fu):
+    from paper_2602_10940_b200 import _lib
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in declared_symbols() if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(declared_symbols()) <= set(_lib.EXPORTED) | {"fusp_kernel_launch_count"}
+
+
+def test_library_has_sm100a_code(fu):
+    import subprocess
+    from paper_2602_10940_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_version(fu):
+    from paper_2602_10940_b200._lib import lib
+    assert b"sm_100a" in lib().fusp_version()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("max_ring", [1, 2, 4, 8])
+@pytest.mark.parametrize("heads", [1, 3, 8, 24])
+def test_mesh_matches_reference_rules(fu, n, max_ring, heads):
+    from oracle import restate as R
+    try:
+        want = R.build_mesh(n, max_ring, heads)
+    except R.MeshError as e:
+        with pytest.raises(fu.MeshError) as got:
+            fu.build_mesh(n, max_ring, heads)
+        assert got.value.msg.startswith(str(e).split(":")[0])
+        return
+    m = fu.build_mesh(n, max_ring, heads)
+    assert (m.r, m.u) == want
+    ug, rg = R.make_mesh(n, m.r)
+    assert [g.members for g in m.ulysses_groups] == ug
+    assert [g.members for g in m.ring_groups] == rg
+    for rank in range(n):  # Mesh2D accessors (mesh.hpp:34-35, mesh.cpp:10-18)
+        assert rank in m.ring_group(rank).members and rank in m.ulysses_group(rank).members
+        assert m.ring_index(rank) * m.u + m.ulysses_index(rank) == rank
+
+
+def test_mesh_error_messages_match_reference(fu):
+    from oracle import ref, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    for args in ((4, 1, 3), (8, 2, 5), (0, 1, 1), (2, 0, 4), (2, 2, 0)):
+        with pytest.raises(Exception) as r:
+            ref.build_mesh(*args)
+        with pytest.raises(fu.MeshError) as g:
+            fu.build_mesh(*args)
+        assert g.value.msg == r.value.msg
+    with pytest.raises(fu.MeshError, match="does not divide"):
+        fu.make_mesh(6, 4)
+
+
+def test_cuda_tensors_required(fu):
+    import torch
+    x = torch.zeros(1, 1, 4, 128)
+    with pytest.raises(fu.InvalidArgument, match="no CPU fallback"):
+        fu.attention_with_lse(x, x, x)
