@@ -135,7 +135,7 @@ def test_flux_u8_on_one_gpu(cuda, fu):
     full = fu.attention_with_lse(single, torch.from_numpy(k).cuda().bfloat16(),
                                  torch.from_numpy(v).cuda().bfloat16()).out.cpu().numpy()
     assert rel_l2(out, full) <= REL_L2
-    assert rep.traffic[0][0] == 7 * (3 * 576 * 128) * (6 + 4)
+    assert rep.traffic[0][0] == 7 * (3 * 576 * 128) * (6 + 2)
 
 
 def test_errors_match_reference(cuda, fu):
