@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: FLUX-shape USP joint-attention layer on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fastusp|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+A step is one USP attention layer (Ulysses all-to-all -> ring attention -> Ulysses
+all-to-all) over FLUX-shaped synthetic tensors, B=1 S=4608 H=24 D=128, bf16 in, f16 out,
+U=N R=1 by default (BASELINE configs[1]); total work is fixed as N grows (strong scaling).
+`value` = whole-job TFLOP/s = 4*B*H*S^2*D / (max over ranks of the device time per step).
+L2 (126 MB) is flushed between timed steps by a 256 MiB write outside the per-step events.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, the
+uspsim library compiled from the reference sources) on this host's cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FLUX-shape USP attention layer latency (us) & TFLOP/s at 1/2/4/8 B200"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return FALLBACK_PEAKS, "fallback"
+
+
+def layer_flop(b, h, s, d):
+    return 4.0 * b * h * s * s * d
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def cpu_sample(nthreads: int, sq: int, s: int = 4608, d: int = 128):
+    """The reference's attention_with_lse (tensor.cpp:193-202, >99% of its layer time) on
+    `nthreads` host threads, one head x `sq` query rows x S keys each."""
+    from oracle import ref
+    sec, _ = ref.time_attention(nthreads, sq, s, d)
+    flop = nthreads * 4.0 * sq * s * d
+    return flop / sec, sec
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    b, h, s, d = 1, 24, args.seq, 128
+    nthreads = os.cpu_count() or 1
+    sq = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_sample(nthreads, sq, s, d)
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, _ = cpu_sample(nthreads, sq, s, d)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    rate = statistics.median(rates)
+    layer_s = layer_flop(b, h, s, d) / rate
+    sample = (f"{nthreads} threads x uspsim::attention_with_lse on 1 head x {sq} query rows x "
+              f"{s} keys (D={d}) per thread; the FLUX layer time is extrapolated from its FLOP "
+              f"count ({layer_flop(b, h, s, d):.3e})")
+    line = {
+        "metric": METRIC, "impl": "reference", "value": rate / 1e12, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": layer_s * 1e3, "latency_us": layer_s * 1e6, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"FLUX joint attention layer B={b} S={s} H={h} D={d}",
+                   "parallelism": "host threads", "wall_s": wall},
+        "cpu_baseline": {"value": rate / 1e12, "unit": "TFLOP/s", "cores": nthreads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": rate / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- fastusp arm
+def run_fastusp(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_10940_b200 as fu
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE",
+              file=sys.stderr)
+    n = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [fu.WorkerContext.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = fu.WorkerContext.nccl(obj[0], n, rank, local)
+    else:
+        fab = fu.Fabric(1)
+        ctx = fu.WorkerContext.local(fab, 0, local)
+
+    b, h, s, d = 1, args.heads, args.seq, 128
+    r = args.ring
+    if n % r:
+        raise SystemExit(f"ring {r} must divide {n}")
+    mesh = fu.make_mesh(n, r)
+    sl = s // n
+    flop = layer_flop(b, h, s, d)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    q = torch.empty(b, h, sl, d, device=dev, dtype=torch.bfloat16).uniform_(-1, 1, generator=gen)
+    k = torch.empty_like(q).uniform_(-1, 1, generator=gen)
+    v = torch.empty_like(q).uniform_(-1, 1, generator=gen)
+    out = torch.empty(b, h, sl, d, device=dev, dtype=torch.float16)
+    opts = fu.CommOptions(fp8_kv=args.fp8, pipelined_ring=not args.serial,
+                          out_dtype=torch.float16, check_finite=False)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        graph = None
+        if args.graph:
+            graph = fu.LayerGraph(ctx, q[None], k[None], v[None], out[None], mesh, opts, 1)
+
+        def step():
+            if graph is not None:
+                graph.launch(stream)
+            else:
+                fu.usp_attention(ctx, q, k, v, mesh, opts)
+
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        # ---- timed region: K layers, per-step CUDA events, L2 flushed between steps
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        clocks = ClockSampler(local)
+        clocks.start()
+        launches0 = fu.kernel_launch_count()
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches = fu.kernel_launch_count() - launches0
+        clk = clocks.stop()
+        step_ms = [a.elapsed_time(z) for a, z in ev]
+        t_ms = sum(step_ms) / len(step_ms)
+        if n > 1:
+            tt = torch.tensor([t_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_ms = float(tt.item())
+        # graph launches are counted by capture (kernels inside the graph): count per replay
+        if graph is not None:
+            per_layer = graph_kernel_count(fu, ctx, q, k, v, mesh, opts)
+            launches = per_layer * args.steps
+
+        # ---- dominant kernel alone (attention on resident bf16/f16 operands)
+        att = attention_roofline(fu, dev, stream, b, h, s, d, n, args)
+        # ---- ring hidden fraction when the mesh has a ring
+        hidden = ring_hidden(fu, ctx, q, k, v, mesh, opts, stream) if r > 1 else None
+        # ---- end to end through the reference-facing host-buffer call
+        e2e = end_to_end(fu, ctx, q, k, v, mesh, opts, stream, flop, n, args)
+    if graph is not None:
+        graph.close()
+
+    if rank == 0:
+        pk, kind = peaks()
+        roof = {"bound": "tensor", "achieved": att["tflops"], "peak": pk["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": att["tflops"] / pk["bf16_tflops"],
+                "traffic": att.get("traffic"), "kernel": "attn_fwd_kernel",
+                "peak_source": f"{kind} bf16 burst (MEASURED_PEAKS.json)",
+                "algorithmic_flop_per_launch": att["flop"], "avg_launch_us": att["us"]}
+        cpu = cpu_baseline(args)
+        line = {
+            "metric": METRIC, "value": flop / (t_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+            "latency_us": t_ms * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1])",
+            "config": {"workload": f"FLUX joint attention layer B={b} S={s} H={h} D={d} "
+                                   f"(4096 img + 512 txt tokens)",
+                       "mesh": {"ulysses": n // r, "ring": r}, "parallelism": f"usp_u{n // r}_r{r}",
+                       "fp8_kv": bool(args.fp8), "pipelined_ring": not args.serial,
+                       "cuda_graph": bool(args.graph), "out_dtype": "f16",
+                       "l2": "flushed between steps (256 MiB write outside the step events)",
+                       "flop_per_layer": flop},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if hidden is not None:
+            line["ring"] = hidden
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if n > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def graph_kernel_count(fu, ctx, q, k, v, mesh, opts):
+    """fastusp kernels one eager layer launches (== the kernels inside one graph replay)."""
+    import torch
+    c0 = fu.kernel_launch_count()
+    fu.usp_attention(ctx, q, k, v, mesh, opts)
+    torch.cuda.current_stream().synchronize()
+    return fu.kernel_launch_count() - c0
+
+
+def attention_roofline(fu, dev, stream, b, h, s, d, n, args):
+    """Average device time of the attention kernel alone on this rank's Ulysses shard
+    (H/U heads x S rows), CUDA events on its launching stream."""
+    import torch
+    u = n // args.ring
+    hp, span = h // u, s // args.ring
+    q = torch.randn(b, hp, span, d, device=dev, dtype=torch.bfloat16)
+    kk = torch.randn_like(q)
+    vv = torch.randn(b, hp, span, d, device=dev, dtype=torch.float16)
+    for _ in range(3):
+        fu.attention_with_lse(q, kk, vv, out_dtype=torch.float16)
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.current_stream().synchronize()
+    e0.record()
+    for _ in range(reps):
+        fu.attention_with_lse(q, kk, vv, out_dtype=torch.float16)
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    flop = layer_flop(b, hp, span, d)
+    res = {"us": us, "flop": flop, "tflops": flop / (us * 1e-6) / 1e12}
+    tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                t = json.load(f)
+            key = f"h{hp}_s{span}"
+            res["traffic"] = t.get(key)
+        except (OSError, ValueError):
+            pass
+    return res
+
+
+def ring_hidden(fu, ctx, q, k, v, mesh, opts, stream):
+    """hidden = 1 - (t_pipe - R*t_step)/((R-1)*t_comm) from per-step events."""
+    import dataclasses
+    import torch
+    ser = dataclasses.replace(opts, pipelined_ring=False)
+    fu.usp_attention(ctx, q, k, v, mesh, ser)
+    torch.cuda.current_stream().synchronize()
+    comp, comm = ctx.ring_timings()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pip = dataclasses.replace(opts, pipelined_ring=True)
+    e0.record()
+    fu.usp_attention(ctx, q, k, v, mesh, pip)
+    e1.record()
+    e1.synchronize()
+    r = len(comp)
+    t_step = sum(comp) / r
+    t_comm = sum(comm[1:]) / max(r - 1, 1)
+    t_pipe = e0.elapsed_time(e1)
+    hidden = 1.0 - (t_pipe - r * t_step) / ((r - 1) * t_comm) if t_comm > 0 else None
+    return {"steps": r, "t_step_ms": t_step, "t_comm_ms": t_comm, "t_pipelined_layer_ms": t_pipe,
+            "hidden_fraction": hidden}
+
+
+def end_to_end(fu, ctx, q, k, v, mesh, opts, stream, flop, n, args):
+    """Same metric through the host-buffer C-ABI call: pinned H2D of q,k,v, the layer,
+    D2H of the output, all inside the timed region."""
+    import torch
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
+    d2h = q.numel() * 2
+    for _ in range(2):
+        fu.usp_attention_host(ctx, hq, hk, hv, mesh, opts)
+    reps = max(3, min(args.steps, 10))
+    t = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fu.usp_attention_host(ctx, hq, hk, hv, mesh, opts)
+        e1.record(stream)
+        e1.synchronize()
+        t.append(e0.elapsed_time(e1))
+    ms = statistics.median(t)
+    if n > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=q.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": flop / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "fusp_usp_attention_host (pinned host bf16 in, host f16 out)"}
+
+
+def cpu_baseline(args):
+    if args.no_cpu_baseline:
+        return None
+    try:
+        nthreads = os.cpu_count() or 1
+        rate, sec = cpu_sample(nthreads, args.ref_rows, args.seq)
+        return {"value": rate / 1e12, "unit": "TFLOP/s", "cores": nthreads, "kind": "reference",
+                "sample": f"{nthreads} host threads x uspsim::attention_with_lse (oracle/_ref) on "
+                          f"1 head x {args.ref_rows} rows x {args.seq} keys each, {sec:.2f} s"}
+    except Exception as e:  # noqa: BLE001 -- the baseline is reported, never required
+        return {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["fastusp", "reference"], default="fastusp")
+    ap.add_argument("--seq", type=int, default=4608)
+    ap.add_argument("--heads", type=int, default=24)
+    ap.add_argument("--ring", type=int, default=1)
+    ap.add_argument("--fp8", action="store_true")
+    ap.add_argument("--serial", action="store_true", help="serial ring (default pipelined)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_fastusp(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -95,7 +95,7 @@ struct Layer {
   int64_t blk, C;  // elements per (Q|K|V) slot piece, elements per ring chunk (= U*blk)
   bool fp8, pipelined;
   int in_dt, out_dt;
-  int qk_dt;  // MMA dtype of Q and K: f16 inputs stay f16, f32/bf16 travel as bf16
+  int qk_dt;  // MMA dtype of Q and K: bf16, or f16 for f16 inputs and the FP8 path
   size_t wout;
   Group ug, rg;
   // Ulysses wire slot: [Q bf16 blk][K bf16|e4m3 blk][V f16|e4m3 blk]{[k scale][v scale]}
@@ -159,7 +159,9 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   l.fp8 = o.fp8_kv != 0;
   l.pipelined = o.pipelined_ring != 0;
   l.in_dt = in_dt;
-  l.qk_dt = in_dt == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
+  // FP8 K/V dequantize to decode(code)*scale (up to 28 significant bits): f16 keeps 2^-12 of
+  // it where bf16 keeps 2^-9, so the FP8 path runs Q.K^T in f16 (Q converts exactly).
+  l.qk_dt = (in_dt == FUSP_F16 || o.fp8_kv) ? FUSP_F16 : FUSP_BF16;
   l.out_dt = o.out_dtype;
   l.wout = dtype_size(o.out_dtype);
   // mesh groups (mesh.cpp:44-53): rank = ring_idx * U + uly_idx
