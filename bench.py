@@ -45,6 +45,53 @@ def layer_flop(b, h, s, d):
 
 
 # ---------------------------------------------------------------------------- clocks
+class NvmlClockSampler:
+    """SM clock + throttle reasons sampled every ~2 ms via NVML during the timed region
+    (the same fields as the profiling recipe's nvidia-smi clocks line)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except self.nv.NVMLError:
+                    pass
+                time.sleep(0.002)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 2:
+            time.sleep(0.001)
+
+    def stop(self):
+        self._stop.set()
+        self._t.join()
+        mx = self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        names = sorted(n for bit, n in self.REASONS.items() if self.reasons & bit)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": mx, "reasons": names, "samples": len(self.samples),
+                "source": "nvml"}
+
+
+def make_clock_sampler(device: int):
+    try:
+        return NvmlClockSampler(device)
+    except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -208,7 +255,7 @@ def run_fastusp(args):
         # ---- timed region: K layers, per-step CUDA events, L2 flushed between steps
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-        clocks = ClockSampler(local)
+        clocks = make_clock_sampler(local)
         clocks.start()
         launches0 = fu.kernel_launch_count()
         barrier()
@@ -290,9 +337,9 @@ def attention_roofline(fu, dev, stream, b, h, s, d, n, args):
     import torch
     u = n // args.ring
     hp, span = h // u, s // args.ring
-    q = torch.randn(b, hp, span, d, device=dev, dtype=torch.bfloat16)
-    kk = torch.randn_like(q)
-    vv = torch.randn(b, hp, span, d, device=dev, dtype=torch.float16)
+    q = torch.empty(b, hp, span, d, device=dev, dtype=torch.bfloat16).uniform_(-1, 1)
+    kk = torch.empty_like(q).uniform_(-1, 1)
+    vv = torch.empty(b, hp, span, d, device=dev, dtype=torch.float16).uniform_(-1, 1)
     for _ in range(3):
         fu.attention_with_lse(q, kk, vv, out_dtype=torch.float16)
     reps = 20

@@ -84,6 +84,12 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
                                     fusp_dtype in_dtype, fusp_shape4 q_shape, int64_t skv,
                                     void* out, fusp_dtype out_dtype, float* lse,
                                     fusp_stream_t stream);
+/* Same, with the operand dtypes the tensor cores consume given separately: Q,K in qk_dtype
+ * (BF16 or F16) and V in v_dtype (F16 runs with no staging pass at all). */
+fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void* v,
+                                       fusp_dtype qk_dtype, fusp_dtype v_dtype,
+                                       fusp_shape4 q_shape, int64_t skv, void* out,
+                                       fusp_dtype out_dtype, float* lse, fusp_stream_t stream);
 /* merge_lse (tensor.cpp:204-243): f32 o1,o2 [B,H,S,D], l1,l2 [B,H,S] -> out, lse (may alias o1/l1). */
 fusp_status fusp_merge_lse(const float* o1, const float* l1, const float* o2, const float* l2,
                            fusp_shape4 shape, float* out, float* lse, fusp_stream_t stream);

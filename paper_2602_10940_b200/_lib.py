@@ -80,6 +80,8 @@ _SIGS = {
     "fusp_dequantize_e4m3": (ctypes.c_int, [_P, _P, _I64, _P, ctypes.c_int, _P]),
     "fusp_attention_with_lse": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, Shape4, _I64, _P,
                                                ctypes.c_int, _P, _P]),
+    "fusp_attention_with_lse_ex": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int, Shape4,
+                                                  _I64, _P, ctypes.c_int, _P, _P]),
     "fusp_merge_lse": (ctypes.c_int, [_P, _P, _P, _P, Shape4, _P, _P, _P]),
     "fusp_mesh_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
     "fusp_mesh_make": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P]),

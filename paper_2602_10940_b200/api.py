@@ -140,13 +140,15 @@ def attention_with_lse(q, k, v, out_dtype=torch.float32) -> AttnResult:
         _shape4(t)
     _check_qkv(q, k, v)
     dt = q.dtype if q.dtype in _DT else torch.float32
-    q, k, v = q.to(dt), k.to(dt), v.to(dt)
+    q, k = q.to(dt), k.to(dt)
+    vdt = v.dtype if v.dtype in _DT else torch.float32
+    v = v.to(vdt)
     b, h, sq, d = q.shape
     out = torch.empty((b, h, sq, d), dtype=out_dtype, device=q.device)
     lse = torch.empty((b, h, sq), dtype=torch.float32, device=q.device)
-    check(lib().fusp_attention_with_lse(_ptr(q), _ptr(k), _ptr(v), _DT[dt], _shape4(q),
-                                        int(k.shape[2]), _ptr(out), _DT[out_dtype], _ptr(lse),
-                                        _stream()))
+    check(lib().fusp_attention_with_lse_ex(_ptr(q), _ptr(k), _ptr(v), _DT[dt], _DT[vdt],
+                                           _shape4(q), int(k.shape[2]), _ptr(out), _DT[out_dtype],
+                                           _ptr(lse), _stream()))
     return AttnResult(out, lse)
 
 

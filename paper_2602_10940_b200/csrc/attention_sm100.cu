@@ -40,6 +40,7 @@ constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: [2 halves][128 rows][128 B]
 constexpr uint32_t kHalfBytes = kTileBytes / 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: lazy O rescale (P <= 2^8 in f16)
+constexpr int kEmuEvery = 4;               // 1 exp2 pair in 4 is emulated on the FMA pipe
 
 struct __align__(1024) Smem {
   uint8_t q[2][kTileBytes];
@@ -110,7 +111,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-
+  // Register split: the producer/MMA warpgroup gives registers to the softmax warpgroups.
+  if (warp < 4) {
+  reg_dealloc<56>();
   if (warp == 0) {
     // ---------------- TMA producer: Q tiles, then K tiles ----------------
     if (lane == 0) {
@@ -198,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(&sm.v_empty[(n_kv - 1) % kStages]);
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    reg_alloc<224>();
     // ---------------- softmax warpgroups ----------------
     const int t = (warp - 4) >> 2;          // Q tile 0 / 1
     const int quad = warp & 3;              // TMEM lane quadrant of this warp
@@ -211,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     float m_use = -INFINITY;  // max used for the exponent (raw logit units)
     float l_sum = 0.f;
+    const float2 sl2x2 = make_float2(sl2, sl2);
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&sm.s_full[t], j & 1);
       tc_fence_after();
@@ -226,9 +232,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 128; ++c)
           if (c >= valid) s[c] = __float_as_uint(-INFINITY);
       }
-      float mx = __uint_as_float(s[0]);
+      // row max with independent chains (FMNMX3)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+      for (int c = 0; c < 128; c += 8) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          mx4[i] = fmaxf(mx4[i], fmaxf(__uint_as_float(s[c + i]), __uint_as_float(s[c + 4 + i])));
+      }
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       // Lazy rescale: keep the old max unless the new one exceeds it by > 8 (log2 units).
       float alpha = 1.f;
       if (m_use == -INFINITY) {
@@ -238,18 +250,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_use = mx;
       }
       const float neg_m = -m_use * sl2;
-      float rs0 = 0.f, rs1 = 0.f;
+      const float2 negm2 = make_float2(neg_m, neg_m);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(s[c]), sl2, neg_m));
-        const float p1 = ex2(fmaf(__uint_as_float(s[c + 1]), sl2, neg_m));
-        rs0 += p0;
-        rs1 += p1;
-        s[c >> 1] = pack_f16x2(p0, p1);  // P packs into the first 64 slots
+      for (int pi = 0; pi < 64; ++pi) {
+        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * pi]), __uint_as_float(s[2 * pi + 1])),
+                               sl2x2, negm2);
+        // one pair in kEmuEvery goes to the FMA pipe, the rest to MUFU.EX2
+        const float2 pp = (pi % kEmuEvery == kEmuEvery - 1) ? exp2_poly2(x)
+                                                           : make_float2(ex2(x.x), ex2(x.y));
+        acc[pi & 3] = fadd2(acc[pi & 3], pp);
+        s[pi] = pack_f16x2(pp.x, pp.y);  // P packs into the first 64 slots
+        if (pi == 31) tmem_st32(t_s + 0, &s[0]);  // first half of P goes out early
       }
-      l_sum = l_sum * alpha + (rs0 + rs1);
-      tmem_st32(t_s + 0, &s[0]);
       tmem_st32(t_s + 32, &s[32]);
+      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+      const float2 a = fadd2(a01, a23);
+      l_sum = fmaf(l_sum, alpha, a.x + a.y);
       // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
       // s_full commit for S_t(j) covers every MMA issued before it.
       if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
@@ -272,10 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&sm.o_done[t], 0);
     tc_fence_after();
     const bool in_range = row < p.sq;
-    const float lse2 = m_use * sl2 + __log2f(l_sum);
-    float lse_b = lse2 * 0.69314718055994530942f;
-    // recompute in accurate math for the exported value
-    lse_b = m_use * (sl2 * 0.69314718055994530942f) + logf(l_sum);
+    // natural-log LSE in accurate math: m/sqrt(D) + ln(l)  (tensor.cpp:177)
+    const float lse_b = m_use * (sl2 * 0.69314718055994530942f) + logf(l_sum);
     const float inv_l = 1.f / l_sum;
     float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
     const float* acc_row = nullptr;
@@ -328,7 +344,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    (void)lse2;
     if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
   }
 

@@ -180,12 +180,13 @@ fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, i
   return launch_dequantize(codes, scale_dev, n, y, dtype, reinterpret_cast<cudaStream_t>(stream));
 }
 
-fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
-                                    fusp_dtype in_dtype, fusp_shape4 qs, int64_t skv, void* out,
-                                    fusp_dtype out_dtype, float* lse, fusp_stream_t stream) {
+fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void* v,
+                                       fusp_dtype qk_dtype, fusp_dtype v_dtype, fusp_shape4 qs,
+                                       int64_t skv, void* out, fusp_dtype out_dtype, float* lse,
+                                       fusp_stream_t stream) {
   clear_error();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!valid_float_dtype(in_dtype) || !valid_float_dtype(out_dtype))
+  if (!valid_float_dtype(qk_dtype) || !valid_float_dtype(v_dtype) || !valid_float_dtype(out_dtype))
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention: bad dtype");
   if (qs.b < 0 || qs.h < 0 || qs.s < 0 || qs.d <= 0 || skv < 0)
     return set_error(FUSP_ERR_SHAPE, "attention: bad shape " + shape_str(qs));
@@ -201,31 +202,31 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
     return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(qs.d) +
                                          " unsupported by the sm_100a kernel (D=128)");
   const int64_t nkv = heads * skv * qs.d;
-  // Operand staging: Q,K -> bf16 (f16 inputs stay f16), V -> f16; one HBM pass each,
-  // skipped when the caller's tensor already has the MMA dtype.
-  const int qk_dt = in_dtype == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
+  // Operand staging: Q,K -> bf16 (f16 stays f16), V -> f16; one HBM pass each, skipped
+  // when the caller's tensor already has the MMA dtype.
+  const int qk_dt = qk_dtype == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
   size_t need = 0;
-  if (in_dtype != qk_dt) need += static_cast<size_t>(nq + nkv) * 2;
-  if (in_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
+  if (qk_dtype != qk_dt) need += static_cast<size_t>(nq + nkv) * 2;
+  if (v_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
   uint8_t* ws = nullptr;
   if (need) FUSP_CHECK(scratch(need + 256, reinterpret_cast<void**>(&ws)));
   const void* qb = q;
   const void* kb = k;
   const void* vh = v;
   size_t off = 0;
-  if (in_dtype != qk_dt) {
+  if (qk_dtype != qk_dt) {
     void* tq = ws + off;
     off += static_cast<size_t>(nq) * 2;
     void* tk = ws + off;
     off += static_cast<size_t>(nkv) * 2;
-    FUSP_CHECK(launch_convert(q, in_dtype, tq, FUSP_BF16, nq, s));
-    FUSP_CHECK(launch_convert(k, in_dtype, tk, FUSP_BF16, nkv, s));
+    FUSP_CHECK(launch_convert(q, qk_dtype, tq, qk_dt, nq, s));
+    FUSP_CHECK(launch_convert(k, qk_dtype, tk, qk_dt, nkv, s));
     qb = tq;
     kb = tk;
   }
-  if (in_dtype != FUSP_F16) {
+  if (v_dtype != FUSP_F16) {
     void* tv = ws + off;
-    FUSP_CHECK(launch_convert(v, in_dtype, tv, FUSP_F16, nkv, s));
+    FUSP_CHECK(launch_convert(v, v_dtype, tv, FUSP_F16, nkv, s));
     vh = tv;
   }
   AttnLaunch a{};
@@ -249,6 +250,13 @@ fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
   a.lse = lse;
   a.lse_hs = qs.s;
   return launch_attention(a, s);
+}
+
+fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
+                                    fusp_dtype in_dtype, fusp_shape4 qs, int64_t skv, void* out,
+                                    fusp_dtype out_dtype, float* lse, fusp_stream_t stream) {
+  return fusp_attention_with_lse_ex(q, k, v, in_dtype, in_dtype, qs, skv, out, out_dtype, lse,
+                                    stream);
 }
 
 fusp_status fusp_merge_lse(const float* o1, const float* l1, const float* o2, const float* l2,

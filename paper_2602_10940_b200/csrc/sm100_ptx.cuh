@@ -187,6 +187,51 @@ __device__ __forceinline__ void tmem_wait_st() {
 }
 
 // ---- misc math ----------------------------------------------------------------------------
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
+// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// 2^x on the FMA pipe for a pair (offloads the MUFU, which co-limits attention at D=128):
+// round-to-nearest split x = n + f with the 1.5*2^23 magic, degree-3 minimax for 2^f on
+// [-1/2, 1/2] (max rel. error 7.5e-5, below the f16 rounding P receives), exponent add.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.0f;
+  x.x = fmaxf(x.x, -126.f);  // -126: p(f) < 1 must not borrow into the sign bit
+  x.y = fmaxf(x.y, -126.f);
+  const float2 j = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 n = fadd2(j, make_float2(-kMagic, -kMagic));
+  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(f, make_float2(0.0551716685f, 0.0551716685f),
+                   make_float2(0.2426111549f, 0.2426111549f));
+  p = ffma2(p, f, make_float2(0.6932609677f, 0.6932609677f));
+  p = ffma2(p, f, make_float2(0.9999280572f, 0.9999280572f));
+  const int ex = (__float_as_int(j.x) - 0x4B400000) << 23;
+  const int ey = (__float_as_int(j.y) - 0x4B400000) << 23;
+  return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
