@@ -1,0 +1,10 @@
+# Round evidence: full GPU test suite, smoke, bench (fastusp + reference arms), ncu launch
+# list and one ncu --set full capture of the attention kernel.  Outputs in gpurun_out/.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:attn_fwd -s 3 -c 1 -o gpurun_out/attn_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_full.log 2>&1
+tail -3 gpurun_out/gpu_tests.log; tail -4 gpurun_out/smoke.log; cat gpurun_out/bench.json; cut -c1-300 gpurun_out/bench_ref.json

@@ -1,0 +1,100 @@
+"""Summarise ncu captures into profiles/ (run here, on the CPU box).
+
+    python tools/ncu_summary.py full  gpurun_out/attn_full.ncu-rep  profiles/r01_attn_full.md
+    python tools/ncu_summary.py launches gpurun_out/launches.csv   profiles/r01_launches.md
+
+`full` extracts the roofline-relevant raw metrics (duration, DRAM bytes, tensor / XU /
+FMA pipe utilisation, registers, occupancy, top warp-stall SASS lines); `launches`
+aggregates the per-launch duration list (cold-cache, serialised) into per-kernel shares.
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+from collections import defaultdict
+
+RAW_KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__cycles_elapsed.avg.per_second", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__average_warp_latency_per_inst_issued.ratio",
+]
+
+
+def ncu_csv(args):
+    out = subprocess.run(["ncu"] + args, capture_output=True, text=True, check=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def full(rep, dest):
+    rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
+    hdr, units = rows[0], rows[1]
+    lines = [f"# ncu --set full summary: `{rep}`", ""]
+    summary = []
+    for vals in rows[2:]:
+        name = vals[hdr.index("Kernel Name")]
+        lines.append(f"## {name[:120]}")
+        lines.append("")
+        lines.append("| metric | value | unit |")
+        lines.append("|---|---|---|")
+        rec = {"kernel": name}
+        for k in RAW_KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                lines.append(f"| {k} | {vals[i]} | {units[i]} |")
+                rec[k] = vals[i]
+        summary.append(rec)
+        lines.append("")
+    # top stall locations (SASS) for the first kernel
+    try:
+        src = ncu_csv(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"])
+        h = src[1]
+        data = src[2:]
+        ia, isrc = h.index("Address"), h.index("Source")
+        iss = h.index("Warp Stall Sampling (All Samples)")
+        tot = sum(float(r[iss] or 0) for r in data) or 1.0
+        lines += ["## top warp-stall SASS lines (all samples)", "", "| share | SASS |", "|---|---|"]
+        for r in sorted(data, key=lambda r: -float(r[iss] or 0))[:25]:
+            lines.append(f"| {float(r[iss]) / tot * 100:.1f}% | `{r[isrc].strip()[:100]}` |")
+    except (subprocess.CalledProcessError, ValueError, IndexError):
+        pass
+    with open(dest, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(dest.rsplit(".", 1)[0] + ".json", "w") as f:
+        json.dump(summary, f, indent=1)
+    print(dest)
+
+
+def launches(path, dest):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = defaultdict(list)
+    for r in rows[1:]:
+        name = re.sub(r"\(.*", "", r[ki])[:80]
+        agg[name].append(float(r[vi]))
+    tot = sum(sum(v) for v in agg.values())
+    lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none): `{path}`", "",
+             "Cold-cache, serialised per-launch times: compare shares, not absolutes.", "",
+             "| kernel | launches | avg us | total us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / 1e3:.1f} | "
+                     f"{sum(v) / tot * 100:.1f}% |")
+    with open(dest, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print(dest)
+
+
+if __name__ == "__main__":
+    mode, src, dst = sys.argv[1:4]
+    {"full": full, "launches": launches}[mode](src, dst)
