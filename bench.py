@@ -208,10 +208,10 @@ def run_fastusp(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if n > 1:
+        from paper_2602_10940_b200 import dist as fdist
         dist.init_process_group("nccl", device_id=dev)
-        obj = [fu.WorkerContext.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = fu.WorkerContext.nccl(obj[0], n, rank, local)
+        uid = fdist.broadcast_bytes(fu.WorkerContext.nccl_unique_id() if rank == 0 else None)
+        ctx = fu.WorkerContext.nccl(uid, n, rank, local)
     else:
         fab = fu.Fabric(1)
         ctx = fu.WorkerContext.local(fab, 0, local)
