@@ -71,6 +71,14 @@ fusp_status fusp_decode_e4m3(const uint8_t* codes, int64_t n, float* y, fusp_str
  * (synchronizes to report it; pass check_finite=0 to skip the check and stay async). */
 fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8_t* codes,
                                float* scale_dev, int check_finite, fusp_stream_t stream);
+/* Per-block variant (B200 extension; SPEC.md:167 makes per-block a reference non-goal): every
+ * run of `block` consecutive elements is quantized exactly as uspsim::quantize would quantize
+ * that slice alone -> scales_dev[n / block].  block = n is the reference's per-tensor case. */
+fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n, int64_t block,
+                                      uint8_t* codes, float* scales_dev, fusp_stream_t stream);
+fusp_status fusp_dequantize_e4m3_blocks(const uint8_t* codes, const float* scales_dev, int64_t n,
+                                        int64_t block, void* y, fusp_dtype dtype,
+                                        fusp_stream_t stream);
 /* dequantize (fp8.cpp:125-130): y = decode(code) * (*scale_dev), written as `dtype`. */
 fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, int64_t n, void* y,
                                  fusp_dtype dtype, fusp_stream_t stream);

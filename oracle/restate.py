@@ -100,9 +100,19 @@ def dequantize(codes, scale) -> np.ndarray:
     return (decode_e4m3(codes) * np.float32(scale)).astype(np.float32)
 
 
-def fake_quant(x) -> np.ndarray:
-    c, s = quantize(x)
-    return dequantize(c, s)
+def fake_quant(x, per_block: bool = False) -> np.ndarray:
+    """dequantize(quantize(x)); per_block quantizes every (b,h) slab on its own (the B200
+    per-block option: uspsim::quantize applied to each slab's Tensor4 slice)."""
+    x = np.asarray(x, np.float32)
+    if not per_block:
+        c, s = quantize(x)
+        return dequantize(c, s)
+    out = np.empty_like(x)
+    for b in range(x.shape[0]):
+        for h in range(x.shape[1]):
+            c, s = quantize(x[b:b + 1, h:h + 1])
+            out[b:b + 1, h:h + 1] = dequantize(c, s)
+    return out
 
 
 # ---- tensor.cpp:143-243 -----------------------------------------------------
@@ -182,7 +192,7 @@ def split_sequence(full, count: int):
     return [full[:, :, i * c:(i + 1) * c] for i in range(count)]
 
 
-def ulysses_input_reshard(qs, ks, vs, fp8: bool):
+def ulysses_input_reshard(qs, ks, vs, fp8: bool, per_block: bool = False):
     """detail::ulysses_input_reshard for one group (protocols.cpp:125-180).
 
     qs/ks/vs: the group members' local [B,H,S/N,D] shards in group order.
@@ -197,8 +207,8 @@ def ulysses_input_reshard(qs, ks, vs, fp8: bool):
         raise ValueError(f"ulysses: head count H={h} not divisible by ulysses dimension U={u}")
     hp = h // u
     if fp8:
-        ks = [fake_quant(k) for k in ks]
-        vs = [fake_quant(v) for v in vs]
+        ks = [fake_quant(k, per_block) for k in ks]
+        vs = [fake_quant(v, per_block) for v in vs]
     res = []
     for t in range(u):
         sl = slice(t * hp, (t + 1) * hp)
@@ -216,7 +226,7 @@ def ulysses_output_reshard(outs):
     return [np.concatenate([o[:, :, t * sp:(t + 1) * sp] for o in outs], axis=1) for t in range(u)]
 
 
-def ring_attention(qs, ks, vs, fp8: bool, attn=attention_with_lse):
+def ring_attention(qs, ks, vs, fp8: bool, attn=attention_with_lse, per_block: bool = False):
     """ring_attention_serial == ring_attention_pipelined (protocols.cpp:237-319).
 
     Member p: acc = attn(q_p, k_p, v_p); round i=1..R-1 receives the chunk that
@@ -234,14 +244,15 @@ def ring_attention(qs, ks, vs, fp8: bool, attn=attention_with_lse):
             kc, vc = ks[src], vs[src]
             if fp8:  # the chunk travelled i hops, re-quantized at each
                 for _ in range(i):
-                    kc, vc = fake_quant(kc), fake_quant(vc)
+                    kc, vc = fake_quant(kc, per_block), fake_quant(vc, per_block)
             po, pl = attn(qs[p], kc, vc)
             o, l = merge_lse(o, l, np.asarray(po, np.float32), np.asarray(pl, np.float32))
         res.append((o, l))
     return res
 
 
-def usp_attention(q, k, v, n: int, r: int, fp8: bool = False, attn=attention_with_lse):
+def usp_attention(q, k, v, n: int, r: int, fp8: bool = False, attn=attention_with_lse,
+                  per_block: bool = False):
     """usp_attention (protocols.cpp:321-340) over all n ranks; returns the gathered output.
 
     Ulysses-in within each ulysses group, ring within each ring group, Ulysses-out.
@@ -254,13 +265,13 @@ def usp_attention(q, k, v, n: int, r: int, fp8: bool = False, attn=attention_wit
     rs = {}
     for grp in ug:
         out = ulysses_input_reshard([qs[m] for m in grp], [ks[m] for m in grp],
-                                    [vs[m] for m in grp], fp8)
+                                    [vs[m] for m in grp], fp8, per_block)
         for pos, m in enumerate(grp):
             rs[m] = out[pos]
     red = {}
     for grp in rg:
         out = ring_attention([rs[m][0] for m in grp], [rs[m][1] for m in grp],
-                             [rs[m][2] for m in grp], fp8, attn)
+                             [rs[m][2] for m in grp], fp8, attn, per_block)
         for pos, m in enumerate(grp):
             red[m] = out[pos][0]
     final = {}

@@ -94,6 +94,27 @@ def quantize(x: torch.Tensor, check_finite: bool = True) -> QuantizedTensor:
     return QuantizedTensor(codes, scale)
 
 
+def quantize_blocks(x: torch.Tensor, block: int):
+    """Per-block quantize (B200 extension): each run of `block` elements is quantized like
+    uspsim::quantize on that slice alone.  Returns (codes, scales[numel // block])."""
+    x = _dev(x)
+    if x.dtype not in _DT:
+        x = x.float()
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    scales = torch.empty(max(x.numel() // max(block, 1), 1), dtype=torch.float32, device=x.device)
+    check(lib().fusp_quantize_e4m3_blocks(_ptr(x), _DT[x.dtype], x.numel(), block, _ptr(codes),
+                                          _ptr(scales), _stream()))
+    return codes, scales
+
+
+def dequantize_blocks(codes: torch.Tensor, scales: torch.Tensor, block: int,
+                      dtype=torch.float32) -> torch.Tensor:
+    out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
+    check(lib().fusp_dequantize_e4m3_blocks(_ptr(codes), _ptr(scales), codes.numel(), block,
+                                            _ptr(out), _DT[dtype], _stream()))
+    return out
+
+
 def dequantize(q: QuantizedTensor, dtype=torch.float32) -> torch.Tensor:
     """dequantize (fp8.cpp:125-130): decode(code) * scale."""
     out = torch.empty(q.codes.shape, dtype=dtype, device=q.codes.device)

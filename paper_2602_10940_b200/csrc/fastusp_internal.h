@@ -79,7 +79,8 @@ struct PackDesc {
   int dst_dtype;
   int64_t dst_slot_stride;  // elements (or bytes for e4m3) between destination slots
   int b, h, sl, d, u;
-  const float* scale;       // e4m3: quantization scale (device)
+  const float* scale;       // e4m3: quantization scale(s) (device)
+  int64_t scale_bh_stride;  // 0: one tensor-wide scale; 1: one scale per (b,h) slab
 };
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
 // Ulysses unpack: src slots [U][B][hp][SL][D] -> dst [B][hp][U*SL][D]; e4m3 src uses per-slot
@@ -89,7 +90,8 @@ struct UnpackDesc {
   int src_dtype;
   int64_t src_slot_stride;
   const float* scales;       // [U] for e4m3
-  int64_t scale_stride;      // floats between consecutive slot scales
+  int64_t scale_stride;      // floats between consecutive slot scale arrays
+  int64_t scale_bh_stride;   // 0: one scale per slot; 1: one per (b,h) slab inside the slot
   void* dst;
   int dst_dtype;
   int b, hp, sl, d, u;
@@ -101,14 +103,29 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
 
 size_t dtype_size(int dt);
 
-// FP8 helpers for the protocols.
-fusp_status launch_scale_finalize(const uint32_t* amax_bits, float* scale, float* copies,
-                                  int64_t copy_stride, int count, cudaStream_t s);
-// amax + quantize over a chunk [heads][span][d] of codes whose row r uses
-// scales[(r / seg_rows) * sstride]; writes *scale_out and codes_out.
-fusp_status launch_requantize_seg(const uint8_t* codes, const float* scales, int64_t sstride, int d,
-                                  int span, int seg_rows, int64_t n, uint32_t* amax_bits,
-                                  float* scale_out, uint8_t* codes_out, cudaStream_t s);
+// FP8 helpers for the protocols (blocked quantizer; one block = per-tensor reference mode).
+// Source of the values to quantize: a float tensor (dt = F32/F16/BF16), or an E4M3 chunk
+// [bh][span][d] whose value is decode(code) * scales[(row/seg_rows)*seg_stride + bh*bh_stride].
+struct Fp8Src {
+  const void* x;
+  int dt;
+  const float* scales;
+  int64_t seg_stride, bh_stride;
+  int d, span, seg_rows;
+};
+// amax per block of `block_elems` (into work[0..nblocks)), then work[k] = scale bits.
+fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nblocks,
+                               uint32_t* work, uint32_t* nonfinite, cudaStream_t s);
+fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_elems,
+                                   const float* scales, uint8_t* codes, cudaStream_t s);
+// amax + scales + codes in one call; `work` holds >= nblocks words.
+fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elems, uint32_t* work,
+                                float* scales, uint8_t* codes, uint32_t* nonfinite,
+                                cudaStream_t s);
+fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
+                                     int64_t n, void* y, int ydt, cudaStream_t s);
+fusp_status launch_scatter_slot_scales(const float* scales, float* base, int64_t slot_stride_f,
+                                       int b, int h, int u, int per_block, cudaStream_t s);
 fusp_status launch_finite(const void* x, int dt, int64_t n, uint32_t* flag, cudaStream_t s);
 
 }  // namespace fusp

@@ -185,10 +185,9 @@ __global__ void fill_kernel(void* p, int dt, int64_t n, float v) {
 // One thread per 8 consecutive d-elements.
 __global__ void pack_kernel(const void* __restrict__ src, int sdt, void* __restrict__ dst, int ddt,
                             int64_t slot_stride, int b, int h, int sl, int d, int u,
-                            const float* __restrict__ scale) {
+                            const float* __restrict__ scale, int64_t scale_bh_stride) {
   const int hp = h / u;
   const int64_t n = int64_t(b) * h * sl * d;  // multiple of 8 (d % 8 == 0)
-  const float qs = (ddt == FUSP_E4M3) ? *scale : 1.f;
   for (int64_t v8 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v8 < n / 8;
        v8 += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = v8 * 8;
@@ -226,6 +225,8 @@ __global__ void pack_kernel(const void* __restrict__ src, int sdt, void* __restr
       f[4] = c.x; f[5] = c.y; f[6] = c.z; f[7] = c.w;
     }
     if (ddt == FUSP_E4M3) {
+      // per-tensor (stride 0) or per-(b,h)-slab scale of the local tensor
+      const float qs = scale[bh * scale_bh_stride];
       uint32_t lo = 0, hi = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) lo |= uint32_t(enc_e4m3(__fdiv_rn(f[e], qs))) << (8 * e);
@@ -257,8 +258,8 @@ __global__ void pack_kernel(const void* __restrict__ src, int sdt, void* __restr
 // j-th sequence block; destination [B][hp][U*SL][D] in group-position sequence order.
 __global__ void unpack_kernel(const void* __restrict__ src, int sdt, int64_t slot_stride,
                               const float* __restrict__ scales, int64_t scale_stride,
-                              void* __restrict__ dst, int ddt, int b, int hp, int sl, int d,
-                              int u) {
+                              int64_t scale_bh_stride, void* __restrict__ dst, int ddt, int b,
+                              int hp, int sl, int d, int u) {
   const int64_t per_slot = int64_t(b) * hp * sl * d;
   const int64_t n = per_slot * u;
   const int64_t span = int64_t(u) * sl;
@@ -292,7 +293,7 @@ __global__ void unpack_kernel(const void* __restrict__ src, int sdt, int64_t slo
     }
     float f[8];
     if (sdt == FUSP_E4M3) {
-      const float sc = scales[j * scale_stride];
+      const float sc = scales[j * scale_stride + bh * scale_bh_stride];
       const uint2 w = *reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(src) + si);
 #pragma unroll
       for (int e = 0; e < 4; ++e) f[e] = __fmul_rn(dec_e4m3((w.x >> (8 * e)) & 0xFF), sc);
@@ -329,52 +330,93 @@ __global__ void unpack_heads_kernel(const uint8_t* __restrict__ src, int64_t slo
   }
 }
 
-// scale = max/448 (1 if all zero) (fp8.cpp:119) -> *scale and `count` strided copies.
-__global__ void scale_finalize_kernel(const uint32_t* __restrict__ amax_bits, float* __restrict__ scale,
-                                      float* __restrict__ copies, int64_t copy_stride, int count) {
-  const float amax = __uint_as_float(*amax_bits);
-  const float sc = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
-  if (threadIdx.x == 0 && scale) *scale = sc;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) copies[i * copy_stride] = sc;
+// ---- blocked FP8 (per-tensor = one block; per-(b,h)-slab = the B200 per-block option) ----
+// Source value i: a float tensor, or an E4M3 chunk [bh][span][d] whose value is
+// decode(code) * scales[(row / seg_rows) * seg_stride + bh * bh_stride] -- exactly the f32
+// values the reference's dequantize produced (fp8.cpp:125-130), so re-quantizing them
+// reproduces the reference's ring hops (protocols.cpp:113-115, :303-311) bit for bit.
+__device__ __forceinline__ float src_value(const Fp8Src& s, int64_t i) {
+  if (s.dt != FUSP_E4M3) return load_as_f32(s.x, s.dt, i);
+  const int64_t row = i / s.d;
+  const int64_t bh = row / s.span;
+  const int r = static_cast<int>(row - bh * s.span);
+  return __fmul_rn(dec_e4m3(static_cast<const uint8_t*>(s.x)[i]),
+                   s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride]);
 }
 
-// Values of a segmented FP8 chunk [heads][span][D]: decode(code) * scale[seg], seg = row/seg_rows
-// -- exactly the f32 values the reference's dequantize produced (fp8.cpp:125-130).
-__device__ __forceinline__ float seg_value(const uint8_t* c, const float* scales, int64_t sstride,
-                                           int d, int span, int seg_rows, int64_t i) {
-  const int row = static_cast<int>((i / d) % span);
-  return __fmul_rn(dec_e4m3(c[i]), scales[(row / seg_rows) * sstride]);
-}
-
-__global__ void amax_seg_kernel(const uint8_t* __restrict__ c, const float* __restrict__ scales,
-                                int64_t sstride, int d, int span, int seg_rows, int64_t n,
-                                uint32_t* __restrict__ amax_bits) {
+// Pass 1 (fp8.cpp:108-117) per block: grid.y = block, grid.x strides inside it.
+__global__ void amax_blocks_kernel(Fp8Src s, int64_t block_elems, uint32_t* __restrict__ amax,
+                                   uint32_t* __restrict__ nonfinite) {
+  const int64_t base = int64_t(blockIdx.y) * block_elems;
   float m = 0.f;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    m = fmaxf(m, fabsf(seg_value(c, scales, sstride, d, span, seg_rows, i)));
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < block_elems;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float v = src_value(s, base + i);
+    bad |= !isfinite(v);
+    m = fmaxf(m, fabsf(v));
+  }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  bad = __any_sync(0xffffffffu, bad);
   __shared__ float wm[kBlock / 32];
-  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __shared__ int wb[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) {
+    wm[threadIdx.x >> 5] = m;
+    wb[threadIdx.x >> 5] = bad;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     float bm = 0.f;
-    for (int w = 0; w < kBlock / 32; ++w) bm = fmaxf(bm, wm[w]);
-    atomicMax(amax_bits, __float_as_uint(bm));
+    int bb = 0;
+    for (int w = 0; w < kBlock / 32; ++w) {
+      bm = fmaxf(bm, wm[w]);
+      bb |= wb[w];
+    }
+    if (!(bm >= 0.f)) bm = 0.f;
+    atomicMax(&amax[blockIdx.y], __float_as_uint(bm));
+    if (bb && nonfinite) atomicOr(nonfinite, 1u);
   }
 }
 
-// Re-quantize a segmented chunk (ring hop, protocols.cpp:113-115 / :303-311).
-__global__ void quantize_seg_kernel(const uint8_t* __restrict__ c, const float* __restrict__ scales,
-                                    int64_t sstride, int d, int span, int seg_rows, int64_t n,
-                                    const uint32_t* __restrict__ amax_bits,
-                                    float* __restrict__ scale_out, uint8_t* __restrict__ codes) {
-  const float amax = __uint_as_float(*amax_bits);
-  const float sc = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = sc;
+// scale = max/448, 1 for an all-zero block (fp8.cpp:119).
+__global__ void finalize_scales_kernel(const uint32_t* __restrict__ amax, int nblocks,
+                                       float* __restrict__ scales) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nblocks; k += gridDim.x * blockDim.x) {
+    const float a = __uint_as_float(amax[k]);
+    scales[k] = a > 0.f ? __fdiv_rn(a, 448.0f) : 1.0f;
+  }
+}
+
+// Pass 2 (fp8.cpp:121): codes = encode(x / scale[block]), IEEE division.
+__global__ void quantize_blocks_kernel(Fp8Src s, int64_t n, int64_t block_elems,
+                                       const float* __restrict__ scales,
+                                       uint8_t* __restrict__ codes) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
-    codes[i] = enc_e4m3(__fdiv_rn(seg_value(c, scales, sstride, d, span, seg_rows, i), sc));
+    codes[i] = enc_e4m3(__fdiv_rn(src_value(s, i), scales[i / block_elems]));
+}
+
+__global__ void dequantize_blocks_kernel(const uint8_t* __restrict__ c,
+                                         const float* __restrict__ scales, int64_t block_elems,
+                                         int64_t n, void* __restrict__ y, int ydt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    store_from_f32(y, ydt, i, __fmul_rn(dec_e4m3(c[i]), scales[i / block_elems]));
+}
+
+// Slot trailers of the Ulysses FP8 wire: slot t carries the scales of its destination's
+// heads -- the tensor-wide scale (reference, QuantizedTensor::slice_heads, fp8.cpp:100-105)
+// or, per block, the scales of slabs (b, t*hp + hl) in [b][hl] order.
+__global__ void scatter_slot_scales_kernel(const float* __restrict__ scales, float* __restrict__ base,
+                                           int64_t slot_stride_f, int b, int h, int u,
+                                           int per_block) {
+  const int hp = h / u;
+  const int nsc = per_block ? b * hp : 1;
+  for (int idx = threadIdx.x; idx < u * nsc; idx += blockDim.x) {
+    const int t = idx / nsc, k = idx % nsc;
+    const int src = per_block ? (k / hp) * h + t * hp + (k % hp) : 0;
+    base[t * slot_stride_f + k] = scales[src];
+  }
 }
 
 // Finite check over several tensors at once (check_local_qkv, protocols.cpp:102-104).
@@ -479,7 +521,7 @@ fusp_status launch_pack(const PackDesc& p, cudaStream_t s) {
   if (p.d % 8 != 0) return set_error(FUSP_ERR_SHAPE, "pack: head dim must be a multiple of 8");
   pack_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(p.src, p.src_dtype, p.dst, p.dst_dtype,
                                                   p.dst_slot_stride, p.b, p.h, p.sl, p.d, p.u,
-                                                  p.scale);
+                                                  p.scale, p.scale_bh_stride);
   FUSP_LAUNCHED("pack_kernel");
   return FUSP_OK;
 }
@@ -489,8 +531,8 @@ fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s) {
   if (n <= 0) return FUSP_OK;
   if (p.d % 8 != 0) return set_error(FUSP_ERR_SHAPE, "unpack: head dim must be a multiple of 8");
   unpack_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(p.src, p.src_dtype, p.src_slot_stride, p.scales,
-                                                    p.scale_stride, p.dst, p.dst_dtype, p.b, p.hp,
-                                                    p.sl, p.d, p.u);
+                                                    p.scale_stride, p.scale_bh_stride, p.dst,
+                                                    p.dst_dtype, p.b, p.hp, p.sl, p.d, p.u);
   FUSP_LAUNCHED("unpack_kernel");
   return FUSP_OK;
 }
@@ -513,24 +555,51 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
 
 namespace fusp {
 
-fusp_status launch_scale_finalize(const uint32_t* amax_bits, float* scale, float* copies,
-                                  int64_t copy_stride, int count, cudaStream_t s) {
-  scale_finalize_kernel<<<1, 32, 0, s>>>(amax_bits, scale, copies, copy_stride, count);
-  FUSP_LAUNCHED("scale_finalize_kernel");
+fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nblocks,
+                               uint32_t* amax, uint32_t* nonfinite, cudaStream_t s) {
+  FUSP_CUDA(cudaMemsetAsync(amax, 0, sizeof(uint32_t) * nblocks, s));
+  if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
+  if (block_elems <= 0 || nblocks <= 0) return FUSP_OK;
+  int gx = grid_for(block_elems, 4);
+  const int cap = (kSMs * 8 + nblocks - 1) / nblocks;  // ~8 CTAs per SM in total
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  amax_blocks_kernel<<<dim3(gx, nblocks), kBlock, 0, s>>>(src, block_elems, amax, nonfinite);
+  FUSP_LAUNCHED("amax_blocks_kernel");
+  finalize_scales_kernel<<<(nblocks + kBlock - 1) / kBlock, kBlock, 0, s>>>(
+      amax, nblocks, reinterpret_cast<float*>(amax));
+  FUSP_LAUNCHED("finalize_scales_kernel");
   return FUSP_OK;
 }
 
-fusp_status launch_requantize_seg(const uint8_t* codes, const float* scales, int64_t sstride, int d,
-                                  int span, int seg_rows, int64_t n, uint32_t* amax_bits,
-                                  float* scale_out, uint8_t* codes_out, cudaStream_t s) {
-  FUSP_CUDA(cudaMemsetAsync(amax_bits, 0, sizeof(uint32_t), s));
+fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_elems,
+                                   const float* scales, uint8_t* codes, cudaStream_t s) {
   if (n <= 0) return FUSP_OK;
-  amax_seg_kernel<<<grid_for(n, 4), kBlock, 0, s>>>(codes, scales, sstride, d, span, seg_rows, n,
-                                                     amax_bits);
-  FUSP_LAUNCHED("amax_seg_kernel");
-  quantize_seg_kernel<<<grid_for(n), kBlock, 0, s>>>(codes, scales, sstride, d, span, seg_rows, n,
-                                                      amax_bits, scale_out, codes_out);
-  FUSP_LAUNCHED("quantize_seg_kernel");
+  quantize_blocks_kernel<<<grid_for(n), kBlock, 0, s>>>(src, n, block_elems, scales, codes);
+  FUSP_LAUNCHED("quantize_blocks_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elems, uint32_t* work,
+                                float* scales, uint8_t* codes, uint32_t* nonfinite,
+                                cudaStream_t s) {
+  const int nblocks = static_cast<int>((n + block_elems - 1) / block_elems);
+  FUSP_CHECK(launch_amax_blocks(src, block_elems, nblocks, work, nonfinite, s));
+  FUSP_CUDA(cudaMemcpyAsync(scales, work, sizeof(float) * nblocks, cudaMemcpyDeviceToDevice, s));
+  return launch_quantize_blocks(src, n, block_elems, scales, codes, s);
+}
+
+fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
+                                     int64_t n, void* y, int ydt, cudaStream_t s) {
+  if (n <= 0) return FUSP_OK;
+  dequantize_blocks_kernel<<<grid_for(n), kBlock, 0, s>>>(c, scales, block_elems, n, y, ydt);
+  FUSP_LAUNCHED("dequantize_blocks_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_scatter_slot_scales(const float* scales, float* base, int64_t slot_stride_f,
+                                       int b, int h, int u, int per_block, cudaStream_t s) {
+  scatter_slot_scales_kernel<<<1, 256, 0, s>>>(scales, base, slot_stride_f, b, h, u, per_block);
+  FUSP_LAUNCHED("scatter_slot_scales_kernel");
   return FUSP_OK;
 }
 

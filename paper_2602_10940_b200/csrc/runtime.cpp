@@ -173,6 +173,31 @@ fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8
   return launch_quantize(x, dtype, n, amax, scale_dev, codes, s);
 }
 
+fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n, int64_t block,
+                                      uint8_t* codes, float* scales_dev, fusp_stream_t stream) {
+  clear_error();
+  if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: bad dtype");
+  if (block <= 0 || n % block != 0)
+    return set_error(FUSP_ERR_SHAPE, "quantize: block " + std::to_string(block) +
+                                         " does not divide " + std::to_string(n) + " elements");
+  const int64_t nblocks = n / block;
+  void* ws = nullptr;
+  FUSP_CHECK(scratch(static_cast<size_t>(nblocks) * 4 + 256, &ws));
+  const Fp8Src src{x, dtype, nullptr, 0, 0, 1, 1, 1};
+  return launch_quantize_fp8(src, n, block, static_cast<uint32_t*>(ws), scales_dev, codes, nullptr,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_dequantize_e4m3_blocks(const uint8_t* codes, const float* scales_dev, int64_t n,
+                                        int64_t block, void* y, fusp_dtype dtype,
+                                        fusp_stream_t stream) {
+  clear_error();
+  if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "dequantize: bad dtype");
+  if (block <= 0) return set_error(FUSP_ERR_SHAPE, "dequantize: bad block");
+  return launch_dequantize_blocks(codes, scales_dev, block, n, y, dtype,
+                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
 fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, int64_t n, void* y,
                                  fusp_dtype dtype, fusp_stream_t stream) {
   clear_error();

@@ -98,8 +98,13 @@ struct Layer {
   int qk_dt;  // MMA dtype of Q and K: bf16, or f16 for f16 inputs and the FP8 path
   size_t wout;
   Group ug, rg;
-  // Ulysses wire slot: [Q bf16 blk][K bf16|e4m3 blk][V f16|e4m3 blk]{[k scale][v scale]}
+  // Ulysses wire slot: [Q blk][K bf16|e4m3 blk][V f16|e4m3 blk]{[k scales][v scales]}
   size_t slot_bytes, slot_stride;
+  // FP8 scale counts: per-tensor (reference) = 1; per block = one per (b,h) slab
+  bool fp8_block = false;
+  int nsc_local = 1;  // scales of the caller's local K (or V): B*H per block
+  int nsc_slot = 1;   // scales riding in one Ulysses slot: B*hp per block
+  int nsc_chunk = 1;  // scales of a ring chunk: heads_r per block
 };
 
 struct Buffers {
@@ -111,10 +116,11 @@ struct Buffers {
   // fp8 exact local chunk: codes [heads_r][span][D] + per-segment scales
   uint8_t *Kc = nullptr, *Vc = nullptr;
   const float *Ks = nullptr, *Vs = nullptr;
-  int64_t s_stride = 1;
+  int64_t s_stride = 1;     // floats between the scale arrays of consecutive sequence segments
+  int64_t bh_stride = 0;    // floats between the scales of consecutive (b,h) slabs
   int seg_rows = 0;
-  float* qscale = nullptr;  // [0]=k [1]=v scale of a locally quantized chunk
-  uint32_t* amax = nullptr; // scratch (4 words)
+  float* qscale = nullptr;  // K scales then V scales of a locally quantized chunk
+  uint32_t* amax = nullptr; // scratch: per-block amax / scale words
   // ring
   char* rb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buf][K|V] wire parts
   char* sw[2] = {nullptr, nullptr};                           // fp8 send wire parts
@@ -170,7 +176,13 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   for (int i = 0; i < l.R; ++i) l.rg.members.push_back(i * l.U + ui);
   l.ug.pos = ui;
   l.rg.pos = ri;
-  l.slot_bytes = l.fp8 ? size_t(l.blk) * 4 + 8 : size_t(l.blk) * 6;
+  l.fp8_block = l.fp8 && o.fp8_block != 0;
+  if (l.fp8_block) {
+    l.nsc_local = l.B * l.H;
+    l.nsc_slot = l.B * l.hp;
+    l.nsc_chunk = l.heads_r;
+  }
+  l.slot_bytes = l.fp8 ? size_t(l.blk) * 4 + 8 * size_t(l.nsc_slot) : size_t(l.blk) * 6;
   l.slot_stride = align_up(l.slot_bytes, 256);
   return FUSP_OK;
 }
@@ -201,10 +213,11 @@ void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, 
       b->Vc = static_cast<uint8_t*>(cv.take(l.C));
     }
   }
-  b->qscale = static_cast<float*>(cv.take(64));
-  b->amax = static_cast<uint32_t*>(cv.take(64));
+  const int nsc = l.nsc_local > l.nsc_chunk ? l.nsc_local : l.nsc_chunk;
+  b->qscale = static_cast<float*>(cv.take(sizeof(float) * 2 * nsc));
+  b->amax = static_cast<uint32_t*>(cv.take(sizeof(uint32_t) * 4 * (nsc + 1)));
   if (l.R > 1) {
-    const size_t part = l.fp8 ? align_up(size_t(l.C) + 4, 256) : C2;
+    const size_t part = l.fp8 ? align_up(size_t(l.C) + 4 * size_t(l.nsc_chunk), 256) : C2;
     for (int i = 0; i < 2; ++i)
       for (int p = 0; p < 2; ++p) b->rb[i][p] = static_cast<char*>(cv.take(part));
     if (l.fp8) {
@@ -230,18 +243,21 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     const int64_t n = l.C;
     if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
     if (uly && l.fp8) {
-      // quantize the whole local K and V (protocols.cpp:139-142), self slot dequantized (:163-179)
+      // quantize the whole local K and V (protocols.cpp:139-142; or per (b,h) slab), and the
+      // self slot takes the dequantized values (:163-179)
+      const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : n;
       for (int p = 0; p < 2; ++p) {
-        const void* src = p == 0 ? k : v;
+        const Fp8Src src{p == 0 ? k : v, l.in_dt, nullptr, 0, 0, l.D, l.span, l.span};
         uint8_t* codes = p == 0 ? b.Kc : b.Vc;
-        FUSP_CHECK(launch_amax(src, l.in_dt, n, b.amax, b.amax + 1, s));
-        FUSP_CHECK(launch_quantize(src, l.in_dt, n, b.amax, b.qscale + p, codes, s));
-        FUSP_CHECK(launch_dequantize(codes, b.qscale + p, n, p == 0 ? b.Kr_w : b.Vr_w,
-                                     p == 0 ? l.qk_dt : FUSP_F16, s));
+        float* sc = b.qscale + p * l.nsc_local;
+        FUSP_CHECK(launch_quantize_fp8(src, n, block, b.amax, sc, codes, nullptr, s));
+        FUSP_CHECK(launch_dequantize_blocks(codes, sc, block, n, p == 0 ? b.Kr_w : b.Vr_w,
+                                            p == 0 ? l.qk_dt : FUSP_F16, s));
       }
       b.Ks = b.qscale;
-      b.Vs = b.qscale + 1;
-      b.s_stride = 1;
+      b.Vs = b.qscale + l.nsc_local;
+      b.s_stride = 0;
+      b.bh_stride = l.fp8_block ? 1 : 0;
       b.seg_rows = l.span;
     } else {
       if (b.Kr_w) FUSP_CHECK(launch_convert(k, l.in_dt, b.Kr_w, l.qk_dt, n, s));
@@ -272,19 +288,23 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     p.dst_dtype = FUSP_F16;
     FUSP_CHECK(launch_pack(p, s));
   } else {
-    // per-tensor scale over ALL local heads (fp8.cpp:107-123), copied into every slot's trailer
+    // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --
+    // fused into the pack; every slot's trailer carries the scales of its heads
     for (int part = 0; part < 2; ++part) {
-      const void* src = part == 0 ? k : v;
+      const Fp8Src src{part == 0 ? k : v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL};
       const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
-      FUSP_CHECK(launch_amax(src, l.in_dt, n, b.amax, b.amax + 1, s));
-      float* trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part;
-      FUSP_CHECK(launch_scale_finalize(b.amax, b.qscale + part, trailer,
-                                       int64_t(l.slot_stride / 4), l.U, s));
-      p.src = src;
+      const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
+      FUSP_CHECK(launch_amax_blocks(src, block, l.nsc_local, b.amax, nullptr, s));
+      const float* scales = reinterpret_cast<const float*>(b.amax);
+      float* trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
+      FUSP_CHECK(launch_scatter_slot_scales(scales, trailer, int64_t(l.slot_stride / 4), l.B, l.H,
+                                            l.U, l.fp8_block ? 1 : 0, s));
+      p.src = src.x;
       p.dst = b.send_in + l.blk * 2 + part * l.blk;
       p.dst_dtype = FUSP_E4M3;
       p.dst_slot_stride = int64_t(l.slot_stride);
-      p.scale = b.qscale + part;
+      p.scale = scales;
+      p.scale_bh_stride = l.fp8_block ? 1 : 0;
       FUSP_CHECK(launch_pack(p, s));
     }
   }
@@ -318,8 +338,9 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       u.src = b.recv_in + l.blk * 2 + part * l.blk;
       u.src_dtype = FUSP_E4M3;
       u.src_slot_stride = int64_t(l.slot_stride);
-      u.scales = scales + part;
+      u.scales = scales + part * l.nsc_slot;
       u.scale_stride = int64_t(l.slot_stride / 4);
+      u.scale_bh_stride = l.fp8_block ? 1 : 0;
       u.dst = part == 0 ? b.Kr_w : b.Vr_w;
       u.dst_dtype = part == 0 ? l.qk_dt : FUSP_F16;
       FUSP_CHECK(launch_unpack(u, s));
@@ -328,8 +349,9 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       FUSP_CHECK(launch_unpack(u, s));
     }
     b.Ks = scales;
-    b.Vs = scales + 1;
+    b.Vs = scales + l.nsc_slot;
     b.s_stride = int64_t(l.slot_stride / 4);
+    b.bh_stride = l.fp8_block ? 1 : 0;
     b.seg_rows = l.SL;
   }
   return FUSP_OK;
@@ -389,7 +411,9 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
   const bool timing = !c->capturing && R <= fusp_ctx_s::kMaxSteps;
   c->timed_steps = timing ? R : 0;
   const size_t C2 = size_t(l.C) * 2;
-  const size_t part_bytes = l.fp8 ? size_t(l.C) + 4 : C2;  // reference: 4-byte scale + codes
+  // wire part per K and per V: codes + f32 scale(s) (the reference's 4-byte scale + codes)
+  const size_t part_bytes = l.fp8 ? size_t(l.C) + 4 * size_t(l.nsc_chunk) : C2;
+  const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : l.C;  // quantization block
   if (R == 1) {
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
     FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, true, out, lse_out, s));
@@ -397,25 +421,24 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     return FUSP_OK;
   }
   const bool usp_local = l.mode != Mode::kRing;
-  // Fill the FP8 send wire [codes][f32 scale] for one hop from the chunk we hold.
+  // Fill the FP8 send wire [codes][f32 scales] for one hop from the chunk we hold.
   auto quantize_hop = [&](int hop, int from_buf, cudaStream_t st) -> fusp_status {
     for (int p = 0; p < 2; ++p) {
       uint8_t* codes = reinterpret_cast<uint8_t*>(b.sw[p]);
-      float* scale = reinterpret_cast<float*>(b.sw[p] + l.C);
+      float* scales = reinterpret_cast<float*>(b.sw[p] + l.C);
+      Fp8Src src{};
       if (hop == 1 && !usp_local) {  // pure ring: quantize the caller's local chunk
-        const void* src = p == 0 ? k_src : v_src;
-        FUSP_CHECK(launch_amax(src, l.in_dt, l.C, b.amax + 2 * p, b.amax + 2 * p + 1, st));
-        FUSP_CHECK(launch_quantize(src, l.in_dt, l.C, b.amax + 2 * p, scale, codes, st));
+        src = Fp8Src{p == 0 ? k_src : v_src, l.in_dt, nullptr, 0, 0, l.D, l.span, l.span};
       } else if (hop == 1) {  // USP: exact f32 values of the (multi-scale) resharded chunk
-        FUSP_CHECK(launch_requantize_seg(p == 0 ? b.Kc : b.Vc, p == 0 ? b.Ks : b.Vs, b.s_stride,
-                                         l.D, l.span, b.seg_rows, l.C, b.amax + 2 * p, scale,
-                                         codes, st));
+        src = Fp8Src{p == 0 ? b.Kc : b.Vc, FUSP_E4M3, p == 0 ? b.Ks : b.Vs, b.s_stride,
+                     b.bh_stride, l.D, l.span, b.seg_rows};
       } else {  // forward: re-quantize the dequantized chunk just received (protocols.cpp:309-310)
         const char* w = b.rb[from_buf][p];
-        FUSP_CHECK(launch_requantize_seg(reinterpret_cast<const uint8_t*>(w),
-                                         reinterpret_cast<const float*>(w + l.C), 1, l.D, l.span,
-                                         l.span, l.C, b.amax + 2 * p, scale, codes, st));
+        src = Fp8Src{w, FUSP_E4M3, reinterpret_cast<const float*>(w + l.C), 0,
+                     l.fp8_block ? 1 : 0, l.D, l.span, l.span};
       }
+      FUSP_CHECK(launch_quantize_fp8(src, l.C, block, b.amax + p * (l.nsc_chunk + 1), scales,
+                                     codes, nullptr, st));
     }
     return FUSP_OK;
   };
@@ -448,10 +471,12 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     }
     const char* wk = b.rb[buf][0];
     const char* wv = b.rb[buf][1];
-    FUSP_CHECK(launch_dequantize(reinterpret_cast<const uint8_t*>(wk),
-                                 reinterpret_cast<const float*>(wk + l.C), l.C, b.Kd, l.qk_dt, st));
-    FUSP_CHECK(launch_dequantize(reinterpret_cast<const uint8_t*>(wv),
-                                 reinterpret_cast<const float*>(wv + l.C), l.C, b.Vd, FUSP_F16, st));
+    FUSP_CHECK(launch_dequantize_blocks(reinterpret_cast<const uint8_t*>(wk),
+                                        reinterpret_cast<const float*>(wk + l.C), block, l.C,
+                                        b.Kd, l.qk_dt, st));
+    FUSP_CHECK(launch_dequantize_blocks(reinterpret_cast<const uint8_t*>(wv),
+                                        reinterpret_cast<const float*>(wv + l.C), block, l.C,
+                                        b.Vd, FUSP_F16, st));
     *K = b.Kd;
     *V = b.Vd;
     return FUSP_OK;

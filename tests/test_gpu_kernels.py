@@ -93,6 +93,21 @@ def test_quantize_dequantize_match_restatement(cuda, fu, scale):
     assert np.array_equal(fu.dequantize(q).cpu().numpy(), R.dequantize(c, s))
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_quantize_blocks_equal_reference_per_slice(cuda, fu, dtype):
+    # per-block = uspsim::quantize applied to every (b,h) slab on its own (bit-exact)
+    t = R.round_bf16(R.rng_tensor(77, (2, 5, 96, 128), -3, 3))
+    t[1, 2] *= 50.0  # one slab with a very different range
+    codes, scales = fu.quantize_blocks(T(t, dtype), 96 * 128)
+    codes, scales = codes.cpu().numpy(), scales.cpu().numpy()
+    for b in range(2):
+        for h in range(5):
+            c, s = R.quantize(t[b:b + 1, h:h + 1])
+            assert np.array_equal(codes[b:b + 1, h:h + 1], c) and scales[b * 5 + h] == s
+    back = fu.dequantize_blocks(T(codes, torch.uint8), T(scales), 96 * 128).cpu().numpy()
+    assert np.array_equal(back, R.fake_quant(t, per_block=True))
+
+
 def test_quantize_rejects_non_finite_like_reference(cuda, fu):
     t = torch.zeros(1, 1, 2, 8, device="cuda")
     t[0, 0, 1, 3] = float("inf")

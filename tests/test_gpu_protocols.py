@@ -124,6 +124,36 @@ def test_usp_fp8_batch2_vs_restatement(cuda, fu):
     assert rel_l2(out, want) <= REL_L2_FP8
 
 
+@pytest.mark.parametrize("n,r", [(2, 1), (4, 2), (4, 4), (8, 2)])
+@pytest.mark.parametrize("b", [1, 2])
+def test_usp_fp8_per_block_vs_restatement(cuda, fu, n, r, b):
+    # BASELINE configs[3]: per-block FP8 all-to-all; parity = uspsim::quantize per (b,h) slab
+    q, k, v = qkv((b, 8, 32 * n, 128), (b, 8, 32 * n, 128), seeds=(51, 52, 53), lo=-3, hi=3)
+    k[:, 3] *= 40.0  # a head with a much larger range than the others
+    want = R.usp_attention(q, k, v, n, r, fp8=True, per_block=True)
+    out, rep = run_usp(fu, q, k, v, n, r, fp8_kv=True, fp8_block=1)
+    assert rel_l2(out, want) <= REL_L2_FP8
+    ser, _ = run_usp(fu, q, k, v, n, r, fp8_kv=True, fp8_block=1, pipelined_ring=False)
+    pip, _ = run_usp(fu, q, k, v, n, r, fp8_kv=True, fp8_block=1, pipelined_ring=True)
+    assert np.array_equal(ser, pip)
+    u = n // r
+    hp, sl = 8 // u, 32
+    blk = b * hp * sl * 128
+    a2a = (u - 1) * (4 * blk + 8 * b * hp) + (u - 1) * 4 * blk
+    assert [t[0] for t in rep.traffic] == [a2a] * n
+
+
+def test_fp8_per_block_beats_per_tensor_on_outlier_heads(cuda, fu):
+    # one loud head: per-tensor scales crush the quiet heads, per-block keeps them
+    q, k, v = qkv((1, 8, 256, 128), (1, 8, 256, 128), seeds=(61, 62, 63))
+    k[:, 0] *= 100.0
+    v[:, 0] *= 100.0
+    full, _ = R.attention_with_lse(q, k, v)
+    pt, _ = run_usp(fu, q, k, v, 4, 1, fp8_kv=True)
+    pb, _ = run_usp(fu, q, k, v, 4, 1, fp8_kv=True, fp8_block=1)
+    assert rel_l2(pb[:, 1:], full[:, 1:]) < 0.5 * rel_l2(pt[:, 1:], full[:, 1:])
+
+
 def test_flux_u8_on_one_gpu(cuda, fu):
     # FLUX layer (S=4608, H=24) as 8 Ulysses ranks sharing one B200, bf16 and fp8
     q, k, v = qkv((1, 24, 4608, 128), (1, 24, 4608, 128))
