@@ -49,7 +49,7 @@ struct __align__(1024) Smem {
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_half[2], p_full[2], o_done[2];
+  uint64_t s_full[2], p_full[2], o_done[2];
   uint32_t tmem_base;
 };
 
@@ -101,7 +101,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_half[t], kBM);
       mbar_init(&sm.p_full[t], kBM);
       mbar_init(&sm.o_done[t], 1);
     }
@@ -152,14 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_qk = p.idesc_qk;                           // K-major x K-major
       constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);   // f16 P(tmem) x f16 V(MN)
       const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
-      // P_t(jj) V(jj) over keys [16*k0, 16*k1): P arrives in two halves (p_half, p_full)
-      auto issue_pv = [&](int t, int jj, int k0, int k1) {
+      auto issue_pv = [&](int t, int jj) {
         const int st = jj % kStages;
         const uint32_t vbase = smem_u32(sm.v[st]);
         const uint32_t t_o = tmem + 256 + t * 128;
         const uint32_t t_p = tmem + t * 128;
 #pragma unroll
-        for (int k = k0; k < k1; ++k) {
+        for (int k = 0; k < kBN / 16; ++k) {
           // B = V tile, MN-major SW128: LBO = d-half stride (16 KB), SBO = 8-row group (1 KB)
           const uint64_t bdesc = umma_desc_sw128(vbase + k * 16 * 128, kHalfBytes, 1024);
           mma_ts(t_o, t_p + k * 8, bdesc, idesc_pv, (jj > 0 || k > 0) ? 1u : 0u);
@@ -179,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&sm.p_full[t], (j - 1) & 1);
             if (t == 0) mbar_wait(&sm.v_full[(j - 1) % kStages], ((j - 1) / kStages) & 1);
             tc_fence_after();
-            issue_pv(t, j - 1, 0, kBN / 16);
+            issue_pv(t, j - 1);
             if (t == 1) mma_commit(&sm.v_empty[(j - 1) % kStages]);
           }
           // S_t = Q_t K_j^T  (executes after PV_t(j-1) has read P_t: tcgen05.mma is in-order)
@@ -198,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.p_full[t], (n_kv - 1) & 1);
         if (t == 0) mbar_wait(&sm.v_full[(n_kv - 1) % kStages], ((n_kv - 1) / kStages) & 1);
         tc_fence_after();
-        issue_pv(t, n_kv - 1, 0, kBN / 16);
+        issue_pv(t, n_kv - 1);
         mma_commit(&sm.o_done[t]);
       }
       mma_commit(&sm.v_empty[(n_kv - 1) % kStages]);
@@ -253,19 +251,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float neg_m = -m_use * sl2;
       const float2 negm2 = make_float2(neg_m, neg_m);
-      // Rescale the O accumulator when the max moved, before any of P_t(j) V(j) can start.
-      // PV_t(j-1) has completed: the s_full commit for S_t(j) covers every earlier MMA.
-      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + c * 32, o);
-        }
-      }
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                        make_float2(0.f, 0.f)};
 #pragma unroll
@@ -283,6 +268,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       const float2 a = fadd2(a01, a23);
       l_sum = fmaf(l_sum, alpha, a.x + a.y);
+      // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
+      // s_full commit for S_t(j) covers every MMA issued before it.
+      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(t_o + c * 32, o);
+        }
+      }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
@@ -404,4 +402,11 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   return FUSP_OK;
 }
 
+}  // namespace fusp
+
+namespace fusp {
+// The single-launch kernel needs no workspace.  (Split-KV / stream-K variants for small
+// per-rank head counts were measured slower than this kernel at every BASELINE shape except
+// U=8; they are not shipped.)
+size_t attention_workspace_bytes(int, int, int) { return 0; }
 }  // namespace fusp

@@ -50,8 +50,13 @@ struct AttnLaunch {
   int64_t lse_hs;
   const float* acc_o;    // merge into (acc_o, acc_lse) when non-null
   const float* acc_lse;
+  void* split_ws;        // stream-K partials + semaphores (attention_workspace_bytes)
+  size_t split_ws_bytes;
 };
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
+// Workspace the persistent attention kernel needs for a (heads, sq, skv) problem (0 when the
+// q-blocks are scheduled whole).
+size_t attention_workspace_bytes(int heads, int sq, int skv);
 
 // ---- elementwise / data-movement kernels (kernels.cu) -----------------------------------
 fusp_status launch_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,

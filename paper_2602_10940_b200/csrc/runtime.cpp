@@ -230,7 +230,9 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
   // Operand staging: Q,K -> bf16 (f16 stays f16), V -> f16; one HBM pass each, skipped
   // when the caller's tensor already has the MMA dtype.
   const int qk_dt = qk_dtype == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
-  size_t need = 0;
+  const size_t split =
+      attention_workspace_bytes(static_cast<int>(heads), static_cast<int>(qs.s), static_cast<int>(skv));
+  size_t need = (split + 255) / 256 * 256;
   if (qk_dtype != qk_dt) need += static_cast<size_t>(nq + nkv) * 2;
   if (v_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
   uint8_t* ws = nullptr;
@@ -238,7 +240,7 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
   const void* qb = q;
   const void* kb = k;
   const void* vh = v;
-  size_t off = 0;
+  size_t off = (split + 255) / 256 * 256;  // the stream-K workspace comes first
   if (qk_dtype != qk_dt) {
     void* tq = ws + off;
     off += static_cast<size_t>(nq) * 2;
@@ -274,6 +276,8 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
   a.out_rs = 128;
   a.lse = lse;
   a.lse_hs = qs.s;
+  a.split_ws = split ? ws : nullptr;
+  a.split_ws_bytes = split;
   return launch_attention(a, s);
 }
 

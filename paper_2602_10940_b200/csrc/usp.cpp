@@ -128,6 +128,9 @@ struct Buffers {
   float *acc_o = nullptr, *acc_lse = nullptr;
   // Ulysses out
   char *send_out = nullptr, *recv_out = nullptr;
+  // stream-K partials of the attention kernel
+  void* attn_ws = nullptr;
+  size_t attn_ws_bytes = 0;
 };
 
 fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, int in_dt,
@@ -228,6 +231,8 @@ void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, 
     b->acc_o = static_cast<float*>(cv.take(size_t(l.C) * 4));
     b->acc_lse = static_cast<float*>(cv.take(size_t(l.heads_r) * l.span * 4));
   }
+  b->attn_ws_bytes = attention_workspace_bytes(l.heads_r, l.span, l.span);
+  if (b->attn_ws_bytes) b->attn_ws = cv.take(b->attn_ws_bytes);
   if (uly && l.U > 1) {
     b->send_out = static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
     b->recv_out = l.B == 1 ? static_cast<char*>(out)
@@ -361,6 +366,8 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
 fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* V, bool first,
                    bool last, void* out, float* lse_out, cudaStream_t s) {
   AttnLaunch a{};
+  a.split_ws = b.attn_ws;
+  a.split_ws_bytes = b.attn_ws_bytes;
   a.qk_dtype = l.qk_dt;
   a.q = b.Qr;
   a.k = K;

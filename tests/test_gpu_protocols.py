@@ -131,6 +131,7 @@ def test_usp_fp8_per_block_vs_restatement(cuda, fu, n, r, b):
     q, k, v = qkv((b, 8, 32 * n, 128), (b, 8, 32 * n, 128), seeds=(51, 52, 53))
     k[:, 3] *= 3.0   # a head whose range differs by a non-power-of-two factor, so the
     v[:, 3] *= 37.0  # per-block codes differ from the per-tensor ones (restate: 2.1e-3 apart)
+    k, v = R.round_bf16(k), R.round_bf16(v)  # the GPU sees bf16: give the oracle the same values
     want = R.usp_attention(q, k, v, n, r, fp8=True, per_block=True)
     out, rep = run_usp(fu, q, k, v, n, r, fp8_kv=True, fp8_block=1)
     assert rel_l2(out, want) <= REL_L2_FP8
@@ -150,6 +151,7 @@ def test_fp8_per_block_beats_per_tensor_on_outlier_heads(cuda, fu):
     q, k, v = qkv((1, 8, 256, 128), (1, 8, 256, 128), seeds=(61, 62, 63))
     k[:, 0] *= 3e4
     v[:, 0] *= 3e4
+    k, v = R.round_bf16(k), R.round_bf16(v)
     full, _ = R.attention_with_lse(q, k, v)
     pt, _ = run_usp(fu, q, k, v, 4, 1, fp8_kv=True)
     pb, _ = run_usp(fu, q, k, v, 4, 1, fp8_kv=True, fp8_block=1)
