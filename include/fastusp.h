@@ -127,6 +127,12 @@ int fusp_ctx_world(fusp_ctx ctx);
  * = TrafficLog::bytes_for("all_to_all"|"send", rank) (fabric.cpp:44-49). */
 fusp_status fusp_ctx_traffic(fusp_ctx ctx, uint64_t* all_to_all_bytes, uint64_t* send_bytes);
 fusp_status fusp_ctx_reset_traffic(fusp_ctx ctx);
+/* TrafficLog::to_json (fabric.cpp:72-87): [{"op","group","round","rank","bytes","msgs"}, ...]
+ * in (op, group, round, rank) order.  Writes at most cap bytes (NUL-terminated), *len = size. */
+fusp_status fusp_ctx_traffic_json(fusp_ctx ctx, char* buf, size_t cap, size_t* len);
+/* Timeline::to_json (fabric.cpp:115-125) of the last layer call, protocol event order, plus
+ * "t_ms": device time of the event from the first one (CUDA events on both streams). */
+fusp_status fusp_ctx_timeline_json(fusp_ctx ctx, char* buf, size_t cap, size_t* len);
 /* Per-step device timings of the last ring call (ms): compute[i], comm[i] for i < R. */
 fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms, float* comm_ms,
                                   int* steps);

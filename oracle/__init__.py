@@ -188,6 +188,19 @@ class ref:  # noqa: N801 -- namespace mirroring uspsim::
         return (out, a2a, snd) if traffic else out
 
     @staticmethod
+    def usp_report(q, k, v, n, r, fp8=False, pipelined=False):
+        """(TrafficLog JSON, Timeline JSON) of the reference's usp_attention run."""
+        import json
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        b, h, s, d = q.shape
+        tb = ctypes.create_string_buffer(1 << 20)
+        lb = ctypes.create_string_buffer(1 << 20)
+        _chk(_load().ref_usp_report(n, r, int(fp8), int(pipelined), _p(q), _p(k), _p(v), I64(b),
+                                    I64(h), I64(s), I64(d), tb, ctypes.c_size_t(1 << 20), lb,
+                                    ctypes.c_size_t(1 << 20)))
+        return json.loads(tb.value.decode()), json.loads(lb.value.decode())
+
+    @staticmethod
     def ulysses_attention(q, k, v, n, fp8=False):
         q, k, v = _f32(q), _f32(k), _f32(v)
         b, h, s, d = q.shape

@@ -239,6 +239,26 @@ int ref_usp_attention(int n, int r, int fp8, int pipelined, const float* q, cons
   });
 }
 
+// usp_attention returning the fabric's own report: TrafficLog::to_json and Timeline::to_json
+// (fabric.cpp:72-87, :115-125) as JSON text.
+int ref_usp_report(int n, int r, int fp8, int pipelined, const float* q, const float* k,
+                   const float* v, int64_t b, int64_t h, int64_t s, int64_t d, char* traffic,
+                   size_t traffic_cap, char* timeline, size_t timeline_cap) {
+  return guarded([&] {
+    Tensor4 Q = make(q, b, h, s, d), K = make(k, b, h, s, d), V = make(v, b, h, s, d);
+    auto qs = split_sequence(Q, n), ks = split_sequence(K, n), vs = split_sequence(V, n);
+    Mesh2D mesh = make_mesh(n, r);
+    CommOptions opts{fp8 != 0, pipelined != 0};
+    RunReport rep = run_protocol(n, [&](WorkerContext& ctx) {
+      const int rk = ctx.rank();
+      usp_attention(ctx, qs[rk], ks[rk], vs[rk], mesh, opts);
+    });
+    const std::string tj = rep.traffic.to_json().dump(), lj = rep.timeline.to_json().dump();
+    std::snprintf(traffic, traffic_cap, "%s", tj.c_str());
+    std::snprintf(timeline, timeline_cap, "%s", lj.c_str());
+  });
+}
+
 // Pure Ulysses over the world group (protocols.cpp:207-214).
 int ref_ulysses_attention(int n, int fp8, const float* q, const float* k, const float* v,
                           int64_t b, int64_t h, int64_t s, int64_t d, float* out_global) {

@@ -97,6 +97,8 @@ _SIGS = {
     "fusp_ctx_world": (ctypes.c_int, [_P]),
     "fusp_ctx_traffic": (ctypes.c_int, [_P, _P, _P]),
     "fusp_ctx_reset_traffic": (ctypes.c_int, [_P]),
+    "fusp_ctx_traffic_json": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P]),
+    "fusp_ctx_timeline_json": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P]),
     "fusp_ctx_ring_timings": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
     "fusp_usp_attention": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4, _P,
                                           ctypes.POINTER(CommOptions), _P]),

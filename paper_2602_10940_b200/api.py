@@ -335,6 +335,22 @@ class WorkerContext:
     def reset_traffic(self):
         check(lib().fusp_ctx_reset_traffic(self.handle))
 
+    def _json(self, fn):
+        import json
+        n = ctypes.c_size_t()
+        check(fn(self.handle, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check(fn(self.handle, buf, n.value + 1, ctypes.byref(n)))
+        return json.loads(buf.value.decode())
+
+    def traffic_log(self) -> list:
+        """TrafficLog::to_json entries of this rank (fabric.cpp:72-87)."""
+        return self._json(lib().fusp_ctx_traffic_json)
+
+    def timeline(self) -> list:
+        """Timeline::to_json of the last layer call, with device timestamps t_ms."""
+        return self._json(lib().fusp_ctx_timeline_json)
+
     def ring_timings(self, max_steps: int = 32):
         """Per ring step device times (ms) of the last call: (compute[], comm[])."""
         c = (ctypes.c_float * max_steps)()

@@ -11,7 +11,10 @@
 //   ulysses_output_reshard   :182-203  -> ulysses_out()  epilogue writes send slots -> all_to_all
 #include <cmath>
 #include <cstring>
+#include <algorithm>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -42,6 +45,19 @@ struct fusp_ctx_s {
   void* host_stage = nullptr;
   size_t host_stage_bytes = 0;
   uint64_t a2a_bytes = 0, send_bytes = 0;
+  // TrafficLog mirror (fabric.hpp:32-60): one entry per sender-side op, self traffic excluded
+  struct Traffic {
+    std::string op, group;
+    int round, rank;
+    uint64_t bytes, msgs;
+  };
+  std::vector<Traffic> traffic;
+  std::map<std::string, int> a2a_seq;  // per-group collective call index (fabric.cpp:211-213)
+  // schedule of the last ring call, for the Timeline mirror (fabric.hpp:62-93)
+  int tl_steps = 0;
+  bool tl_pipelined = false;
+  bool tl_valid = false;
+  int tl_next = -1;
 };
 
 struct fusp_graph_s {
@@ -63,6 +79,20 @@ std::string sstr(const fusp_shape4& s) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// TrafficLog entries as the reference's fabric records them (fabric.cpp:155-158, :343-351):
+// all_to_all: one per collective and member, bytes sent to the other members; send: one per
+// message, group "from->to", round = ring round.
+void log_a2a(fusp_ctx_s* c, const Group& g, uint64_t bytes) {
+  const std::string key = g.key();
+  const int round = c->a2a_seq[key]++;
+  c->traffic.push_back({"all_to_all", key, round, c->rank, bytes, uint64_t(g.size() - 1)});
+}
+void log_send(fusp_ctx_s* c, const Group& g, int round, uint64_t bytes) {
+  const int next = g.members[(g.pos + 1) % g.size()];
+  c->traffic.push_back(
+      {"send", std::to_string(c->rank) + "->" + std::to_string(next), round, c->rank, bytes, 1});
+}
 
 // Bump allocator over the context arena; the first (dry) pass only measures.
 struct Carve {
@@ -315,6 +345,7 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   }
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
+  log_a2a(c, l.ug, uint64_t(l.U - 1) * l.slot_bytes);
   // unpack: source j contributed our heads over its sequence shard (protocols.cpp:163-179)
   UnpackDesc u{};
   u.b = l.B;
@@ -467,6 +498,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     const size_t bytes[2] = {part_bytes, part_bytes};
     FUSP_CHECK(c->comm->ring_exchange(l.rg, snd, rcv, bytes, 2, st));
     c->send_bytes += 2 * part_bytes;
+    log_send(c, l.rg, hop, part_bytes);  // K (protocols.cpp:253)
+    log_send(c, l.rg, hop, part_bytes);  // V (protocols.cpp:254)
     return FUSP_OK;
   };
   auto operands = [&](int hop, cudaStream_t st, const void** K, const void** V) -> fusp_status {
@@ -547,6 +580,7 @@ fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, cu
   const size_t slot = size_t(l.blk) * l.wout;
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
   c->a2a_bytes += uint64_t(l.U - 1) * slot;
+  log_a2a(c, l.ug, uint64_t(l.U - 1) * slot);
   if (l.B > 1)  // concat_heads (protocols.cpp:196-202)
     FUSP_CHECK(launch_unpack_heads(b.recv_out, l.blk, out, l.out_dt, l.B, l.hp, l.SL, l.D, l.U, s));
   return FUSP_OK;
@@ -592,9 +626,16 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   cv = Carve{static_cast<char*>(c->arena), 0};
   b = Buffers{};
   carve(l, cv, &b, q, k, v, out);
+  const bool uly1 = l.mode != Mode::kRing && l.U == 1;  // the reference still runs a 1-member
+  if (uly1) log_a2a(c, l.ug, 0);                         // all_to_all (fabric.cpp:199-226)
   FUSP_CHECK(ulysses_in(c, l, b, q, k, v, s));
   FUSP_CHECK(ring(c, l, b, k, v, out, lse_out, s));
   FUSP_CHECK(ulysses_out(c, l, b, out, s));
+  if (uly1) log_a2a(c, l.ug, 0);
+  c->tl_steps = c->timed_steps;
+  c->tl_pipelined = l.pipelined && l.R > 1;
+  c->tl_valid = c->timed_steps > 0;
+  c->tl_next = l.rg.members[(l.rg.pos + 1) % l.rg.size()];
   return FUSP_OK;
 }
 
@@ -718,7 +759,94 @@ fusp_status fusp_ctx_traffic(fusp_ctx c, uint64_t* a2a, uint64_t* snd) {
 fusp_status fusp_ctx_reset_traffic(fusp_ctx c) {
   c->a2a_bytes = 0;
   c->send_bytes = 0;
+  c->traffic.clear();
+  c->a2a_seq.clear();
   return FUSP_OK;
+}
+
+static fusp_status put_json(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+    if (n < s.size()) return set_error(FUSP_ERR_INVALID_ARGUMENT, "json buffer too small");
+  }
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_traffic_json(fusp_ctx c, char* buf, size_t cap, size_t* len) {
+  clear_error();
+  // TrafficLog::to_json (fabric.cpp:72-87): entries in (op, group, round, rank) order
+  std::vector<fusp_ctx_s::Traffic> t = c->traffic;
+  std::stable_sort(t.begin(), t.end(), [](const auto& a, const auto& b) {
+    return std::tie(a.op, a.group, a.round, a.rank) < std::tie(b.op, b.group, b.round, b.rank);
+  });
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < t.size(); ++i) {
+    if (i) os << ",";
+    os << "{\"op\":\"" << t[i].op << "\",\"group\":\"" << t[i].group << "\",\"round\":"
+       << t[i].round << ",\"rank\":" << t[i].rank << ",\"bytes\":" << t[i].bytes
+       << ",\"msgs\":" << t[i].msgs << "}";
+  }
+  os << "]";
+  return put_json(os.str(), buf, cap, len);
+}
+
+fusp_status fusp_ctx_timeline_json(fusp_ctx c, char* buf, size_t cap, size_t* len) {
+  clear_error();
+  // Timeline::to_json (fabric.cpp:115-125) of the last layer, with device timestamps (ms from
+  // the first event).  Event order follows protocols.cpp:243-265 (serial) / :276-316 (pipelined);
+  // the merge is fused into the attention epilogue, so it carries compute_end's time.
+  if (!c->tl_valid) return put_json("[]", buf, cap, len);
+  FUSP_CUDA(cudaSetDevice(c->device));
+  const int R = c->tl_steps;
+  cudaEvent_t t0 = c->tc0[0];
+  if (R > 1 && c->tl_pipelined) t0 = c->tm0[1];
+  FUSP_CUDA(cudaEventSynchronize(c->tc1[R - 1]));
+  auto ms = [&](cudaEvent_t e) {
+    float v = 0.f;
+    cudaEventElapsedTime(&v, t0, e);
+    return v < 0.f ? 0.f : v;
+  };
+  struct Ev {
+    const char* kind;
+    const char* tag;
+    int round;
+    float t;
+  };
+  std::vector<Ev> ev;
+  if (c->tl_pipelined) {
+    ev.push_back({"recv_issue", "kv", 1, ms(c->tm0[1])});
+    ev.push_back({"send_issue", "kv", 1, ms(c->tm0[1])});
+  }
+  ev.push_back({"compute_begin", "attn", 0, ms(c->tc0[0])});
+  ev.push_back({"compute_end", "attn", 0, ms(c->tc1[0])});
+  for (int r = 1; r < R; ++r) {
+    if (!c->tl_pipelined) {
+      ev.push_back({"send_issue", "kv", r, ms(c->tm0[r])});
+      ev.push_back({"recv_issue", "kv", r, ms(c->tm0[r])});
+    }
+    ev.push_back({"transfer_complete", "kv", r, ms(c->tm1[r])});
+    if (c->tl_pipelined && r < R - 1) {
+      ev.push_back({"recv_issue", "kv", r + 1, ms(c->tm0[r + 1])});
+      ev.push_back({"send_issue", "kv", r + 1, ms(c->tm0[r + 1])});
+    }
+    ev.push_back({"compute_begin", "attn", r, ms(c->tc0[r])});
+    ev.push_back({"compute_end", "attn", r, ms(c->tc1[r])});
+    ev.push_back({"merge", "lse", r, ms(c->tc1[r])});
+  }
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < ev.size(); ++i) {
+    if (i) os << ",";
+    os << "{\"seq\":" << i << ",\"rank\":" << c->rank << ",\"kind\":\"" << ev[i].kind
+       << "\",\"tag\":\"" << ev[i].tag << "\",\"round\":" << ev[i].round << ",\"t_ms\":"
+       << ev[i].t << "}";
+  }
+  os << "]";
+  return put_json(os.str(), buf, cap, len);
 }
 
 fusp_status fusp_ctx_ring_timings(fusp_ctx c, int max_steps, float* compute_ms, float* comm_ms,

@@ -217,3 +217,43 @@ def test_graph_capture_matches_eager(cuda, fu):
     eager = fu.run_protocol(1, prog).results[0]
     for i in range(L):
         assert torch.equal(out[i], eager[i])
+
+
+@pytest.mark.parametrize("n,r,pipelined,fp8", [(4, 2, True, False), (4, 2, False, False),
+                                               (4, 4, True, True), (2, 1, False, False)])
+def test_traffic_and_timeline_mirror_reference(cuda, fu, n, r, pipelined, fp8):
+    # the reference's TrafficLog / Timeline (fabric.cpp:72-87, :115-125) for the same run:
+    # same entries (op, group, round, rank, msgs) and event sequence per rank; bytes at our
+    # wire widths (bf16/f16 Q,K,V; f32 output; FP8 codes + 4-byte scale per K and V part)
+    from oracle import ref, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    h, s = 8, 64
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128))
+    ref_t, ref_l = ref.usp_report(q, k, v, n, r, fp8=fp8, pipelined=pipelined)
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=pipelined)
+    rep = fu.run_protocol(n, lambda ctx: (fu.usp_attention(ctx, qs[ctx.rank()], ks[ctx.rank()],
+                                                           vs[ctx.rank()], mesh, opts),
+                                          ctx.traffic_log(), ctx.timeline()))
+    u = n // r
+    blk = (h // u) * (s // n) * 128
+    chunk = (h // u) * (s // r) * 128
+    for rank in range(n):
+        _, traffic, timeline = rep.results[rank]
+        want = [e for e in ref_t if e["rank"] == rank]
+        key = lambda e: (e["op"], e["group"], e["round"], e["msgs"])  # noqa: E731
+        assert sorted(map(key, traffic)) == sorted(map(key, want))
+        for e in traffic:
+            if e["op"] == "all_to_all":
+                per = (4 * blk + 8) if (fp8 and e["round"] == 0) else (6 * blk if e["round"] == 0 else 4 * blk)
+                assert e["bytes"] == (u - 1) * per
+            else:
+                assert e["bytes"] == ((chunk + 4) if fp8 else 2 * chunk)
+        seq = [(e["kind"], e["tag"], e["round"]) for e in timeline]
+        want_seq = [(e["kind"], e["tag"], e["round"]) for e in sorted(
+            (e for e in ref_l if e["rank"] == rank), key=lambda e: e["seq"])]
+        assert seq == want_seq
+        ts = [e["t_ms"] for e in timeline if e["kind"] in ("compute_begin", "compute_end")]
+        assert ts == sorted(ts)
