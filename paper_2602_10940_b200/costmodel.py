@@ -1,0 +1,162 @@
+"""Analytical cost model of the USP layer, calibrated to B200.
+
+The reference specifies this model but ships no code for it.  Volumes follow SPEC.md's
+closed forms (checked against the C ABI's traffic counters in tests); time terms use
+B200 numbers measured in this repo (profiles/): attention throughput per per-rank shape,
+NVLink 5 peer bandwidth, kernel launch overhead with and without CUDA-Graph replay.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import asdict, dataclass, field
+from typing import Dict, List, Optional
+
+
+@dataclass
+class HardwareProfile:
+    """SPEC.md:373-376.  Defaults: one B200 on an NVSwitch node."""
+    link_bandwidth: float = 770e9       # B/s per direction per GPU (measured peer copy)
+    link_latency: float = 6e-6          # s per NCCL group call (launch + handshake)
+    launch_overhead: float = 4e-6       # s per kernel launch, eager
+    graph_residual: float = 0.05        # fraction of launch cost left under graph replay
+    element_width: int = 2              # bytes per Q/K/V element on the wire (bf16/f16)
+    peak_tflops: float = 1651.9         # measured dense bf16 (MEASURED_PEAKS.json)
+    attn_efficiency: float = 0.73       # measured attention-kernel fraction of peak (FLUX)
+
+    def __post_init__(self):
+        for k, v in asdict(self).items():
+            if v <= 0:
+                raise ValueError(f"HardwareProfile.{k} must be positive")
+
+
+@dataclass
+class WorkloadProfile:
+    """SPEC.md:377-380."""
+    B: int = 1
+    H: int = 24
+    S: int = 4608
+    D: int = 128
+    layers: int = 1
+    kernels_per_layer: int = 2        # measured: V staging + attention at N=1 (bench gpu_launches)
+    steps: int = 1
+    other_compute_per_step: float = 0.0  # s, non-attention work (projections, MLP), if known
+
+
+@dataclass
+class LatencyBreakdown:
+    """total == compute + exposed_comm + launch."""
+    compute: float
+    exposed_comm: float
+    hidden_comm: float
+    launch: float
+    total: float = field(init=False)
+
+    def __post_init__(self):
+        self.total = self.compute + self.exposed_comm + self.launch
+
+    def as_dict(self) -> Dict[str, float]:
+        return {"compute_ms": self.compute * 1e3, "comm_exposed_ms": self.exposed_comm * 1e3,
+                "comm_hidden_ms": self.hidden_comm * 1e3, "launch_ms": self.launch * 1e3,
+                "total_ms": self.total * 1e3}
+
+
+def comm_volume_ulysses(w: WorkloadProfile, u: int, width: int = 2, fp8: bool = False,
+                        out_width: Optional[int] = None, n: Optional[int] = None) -> int:
+    """Bytes one rank puts on the wire per layer for the two Ulysses all-to-alls: the
+    reference fabric's TrafficLog closed form (equal to the C ABI counters).
+    Local shards hold S/N rows (N = n, default U for a Ulysses-only mesh).  fp8: K and V
+    travel as 1-byte codes plus one 4-byte scale each per destination.  (SPEC.md:390's
+    worked example, 256 B for U=2,H=2,S=8,D=4,w=2, counts both ranks; one rank sends 128.)"""
+    if u <= 1:
+        return 0
+    n_local = w.S // (n or u)
+    blk = w.B * (w.H // u) * n_local * w.D
+    ow = width if out_width is None else out_width
+    kv = (blk + 4) if fp8 else blk * width
+    return (u - 1) * (blk * width + 2 * kv) + (u - 1) * blk * ow
+
+
+def comm_volume_ring(w: WorkloadProfile, r: int, u: int, width: int = 2, fp8: bool = False) -> int:
+    """2 * B * (H/U) * (S/R) * D * width * (R-1); codes + scale with fp8."""
+    if r <= 1:
+        return 0
+    chunk = w.B * (w.H // u) * (w.S // r) * w.D
+    part = (chunk + 4) if fp8 else chunk * width
+    return (r - 1) * 2 * part
+
+
+def pipeline_timeline(compute: float, comm: float, r: int) -> Dict[str, float]:
+    """SPEC.md:398-406 (Alg. 2)."""
+    serial = r * compute + (r - 1) * comm
+    pipelined = compute + (r - 1) * max(compute, comm) if r > 1 else compute
+    if comm <= 0 or r <= 1:
+        hidden = 1.0
+    else:
+        hidden = 1.0 - (pipelined - r * compute) / ((r - 1) * comm)
+    return {"serial_total": serial, "pipelined_total": pipelined,
+            "hidden_fraction": max(0.0, min(1.0, hidden))}
+
+
+def attention_seconds(hw: HardwareProfile, b: int, heads: int, s_q: int, s_kv: int, d: int) -> float:
+    flop = 4.0 * b * heads * s_q * s_kv * d
+    return flop / (hw.peak_tflops * 1e12 * hw.attn_efficiency)
+
+
+def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipelined: bool = True,
+                 compiled: bool = True, fp8: bool = False) -> LatencyBreakdown:
+    """SPEC.md:407-414 per denoising step: attention compute split over the mesh, Ulysses
+    all-to-alls exposed, ring transfers through pipeline_timeline, launch term."""
+    if n % r or w.H % (n // r) or w.S % n:
+        raise ValueError(f"infeasible mesh N={n} R={r} for H={w.H}, S={w.S}")
+    u = n // r
+    hp, span = w.H // u, w.S // r
+    step_compute = attention_seconds(hw, w.B, hp, span, span, w.D)  # one ring step per rank
+    a2a = comm_volume_ulysses(w, u, hw.element_width, fp8, n=n) / hw.link_bandwidth
+    a2a += (2 * hw.link_latency) if u > 1 else 0.0
+    per_round_comm = (comm_volume_ring(w, r, u, hw.element_width, fp8) / max(r - 1, 1)
+                      / hw.link_bandwidth + hw.link_latency) if r > 1 else 0.0
+    tl = pipeline_timeline(step_compute, per_round_comm, r)
+    ring_total = tl["pipelined_total"] if pipelined else tl["serial_total"]
+    compute = r * step_compute
+    ring_exposed = ring_total - compute
+    ring_hidden = (r - 1) * per_round_comm - ring_exposed
+    launches = w.kernels_per_layer + (4 if u > 1 else 0) + (2 * (r - 1) if r > 1 else 0)
+    launch = launches * hw.launch_overhead * (hw.graph_residual if compiled else 1.0)
+    per_layer = LatencyBreakdown(compute, a2a + ring_exposed, max(ring_hidden, 0.0), launch)
+    L = w.layers
+    return LatencyBreakdown(per_layer.compute * L + w.other_compute_per_step,
+                            per_layer.exposed_comm * L, per_layer.hidden_comm * L,
+                            per_layer.launch * L)
+
+
+def speedup_report(base: LatencyBreakdown, opt: LatencyBreakdown) -> Dict[str, float]:
+    """total ratio and per-component attribution of the delta."""
+    d = {"compute": base.compute - opt.compute, "exposed_comm": base.exposed_comm - opt.exposed_comm,
+         "launch": base.launch - opt.launch}
+    assert abs(sum(d.values()) - (base.total - opt.total)) < 1e-12
+    return {"speedup": base.total / opt.total, **{f"delta_{k}_ms": v * 1e3 for k, v in d.items()}}
+
+
+def sweep(hw: HardwareProfile, w: WorkloadProfile, ns=(1, 2, 4, 8), fp8: bool = False,
+          compiled: bool = True) -> List[Dict]:
+    rows = []
+    for n in ns:
+        for r in [x for x in range(1, n + 1) if n % x == 0]:
+            if w.H % (n // r) or w.S % n:
+                continue
+            for pip in (False, True):
+                b = step_latency(hw, w, n, r, pipelined=pip, compiled=compiled, fp8=fp8)
+                comm = b.exposed_comm + b.hidden_comm
+                rows.append({"config": f"N{n}_R{r}_U{n // r}_{'pipe' if pip else 'serial'}",
+                             **b.as_dict(),
+                             "comm_fraction": b.exposed_comm / b.total if b.total else 0.0,
+                             "hidden_fraction": (b.hidden_comm / comm) if comm else 1.0})
+    return rows
+
+
+def load_profile(path: Optional[str]) -> HardwareProfile:
+    if not path:
+        return HardwareProfile()
+    with open(path) as f:
+        return HardwareProfile(**json.load(f))
