@@ -153,6 +153,29 @@ fusp_status fusp_ring_attention(fusp_ctx ctx, const void* q, const void* k, cons
                                 fusp_dtype in_dtype, fusp_shape4 local_shape, void* out,
                                 float* lse, const fusp_comm_options* opts, fusp_stream_t stream);
 
+/* Producer prologue fused into the Ulysses pack (B200 extension): the MMDiT
+ * joint-attention block's per-head RMSNorm of Q and K and rotary embedding, applied to the
+ * caller's projected rows on their way into the all-to-all slot, instead of as separate
+ * kernels before fusp_usp_attention.  Per row x of D = 128 elements at sequence position p:
+ *   y = x * rsqrt(mean(x^2) + eps) * w          (w = q_norm_weight / k_norm_weight; NULL = skip)
+ *   (y[2i], y[2i+1]) <- (y[2i] cos[p][i] - y[2i+1] sin[p][i], y[2i] sin[p][i] + y[2i+1] cos[p][i])
+ * RoPE (rope_cos/rope_sin NULL = skip) applies to Q and K.  All arrays f32 on the device.
+ * p = rope_pos0 + local row; rope_pos0 = -1 means rank * S_local (split_sequence order). */
+typedef struct {
+  const float* q_norm_weight; /* [D] */
+  const float* k_norm_weight; /* [D] */
+  float eps;
+  const float* rope_cos;      /* [rope_rows][D/2] */
+  const float* rope_sin;      /* [rope_rows][D/2] */
+  int64_t rope_rows;
+  int64_t rope_pos0;
+} fusp_qk_prologue;
+/* fusp_usp_attention with the fused prologue (prologue NULL = fusp_usp_attention). */
+fusp_status fusp_usp_attention_ex(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                                  const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                  void* out, const fusp_comm_options* opts,
+                                  const fusp_qk_prologue* prologue, fusp_stream_t stream);
+
 /* Host-buffer variant of fusp_usp_attention (the reference's calling convention: host
  * tensors in, host tensor out).  Copies H2D, runs, copies D2H, synchronizes. */
 fusp_status fusp_usp_attention_host(fusp_ctx ctx, int ring_dim, const void* q, const void* k,

@@ -282,6 +282,39 @@ def usp_attention(q, k, v, n: int, r: int, fp8: bool = False, attn=attention_wit
     return np.concatenate([final[i] for i in range(n)], axis=2)
 
 
+# ---- producer prologue (NOT in the reference) ---------------------------
+# The MMDiT block (FLUX) normalizes each Q/K head row with RMSNorm and applies
+# rotary embedding before attention.  The reference's uspsim takes Q/K/V after that point,
+# so there is no reference code to cite: this is the textbook definition the fused
+# fusp_qk_prologue kernel is checked against, in float64.
+def rms_norm(x, w, eps):
+    x = np.asarray(x, np.float64)
+    r = 1.0 / np.sqrt((x * x).mean(axis=-1, keepdims=True) + eps)
+    return x * r * np.asarray(w, np.float64)
+
+
+def rope_interleaved(x, cos, sin, pos0: int = 0):
+    """Rotate pairs (x[2i], x[2i+1]) of every row at sequence position pos0 + s."""
+    x = np.asarray(x, np.float64)
+    s = x.shape[-2]
+    c = np.asarray(cos, np.float64)[pos0:pos0 + s]
+    n = np.asarray(sin, np.float64)[pos0:pos0 + s]
+    x0, x1 = x[..., 0::2], x[..., 1::2]
+    y = np.empty_like(x)
+    y[..., 0::2] = x0 * c - x1 * n
+    y[..., 1::2] = x0 * n + x1 * c
+    return y
+
+
+def qk_prologue(x, w=None, eps=1e-6, cos=None, sin=None, pos0: int = 0):
+    y = np.asarray(x, np.float64)
+    if w is not None:
+        y = rms_norm(y, w, eps)
+    if cos is not None:
+        y = rope_interleaved(y, cos, sin, pos0)
+    return y
+
+
 def traffic_closed_form(b, h, s, d, n, r, fp8=False, w=4):
     """Per-rank bytes: all_to_all in+out, ring sends; self-slot free."""
     u = n // r

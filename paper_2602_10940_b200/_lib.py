@@ -59,6 +59,13 @@ class CommOptions(ctypes.Structure):
                 ("fp8_block", ctypes.c_int)]
 
 
+class QKPrologue(ctypes.Structure):
+    _fields_ = [("q_norm_weight", ctypes.c_void_p), ("k_norm_weight", ctypes.c_void_p),
+                ("eps", ctypes.c_float), ("rope_cos", ctypes.c_void_p),
+                ("rope_sin", ctypes.c_void_p), ("rope_rows", ctypes.c_int64),
+                ("rope_pos0", ctypes.c_int64)]
+
+
 def build(force: bool = False) -> str:
     """Compile libfastusp.so in-tree with nvcc for sm_100a (Makefile in this package)."""
     if force or not os.path.exists(LIB_PATH):
@@ -102,6 +109,9 @@ _SIGS = {
     "fusp_ctx_ring_timings": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
     "fusp_usp_attention": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4, _P,
                                           ctypes.POINTER(CommOptions), _P]),
+    "fusp_usp_attention_ex": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
+                                             _P, ctypes.POINTER(CommOptions),
+                                             ctypes.POINTER(QKPrologue), _P]),
     "fusp_ulysses_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P,
                                               ctypes.POINTER(CommOptions), _P]),
     "fusp_ring_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P, _P,

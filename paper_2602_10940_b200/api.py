@@ -446,17 +446,59 @@ def _inputs(q, k, v, where):
     return q, k, v
 
 
+@dataclass
+class QKPrologue:
+    """MMDiT QK RMSNorm + RoPE fused into the Ulysses pack (fusp_qk_prologue in fastusp.h).
+    Weights [D] and tables [rows][D/2] are f32 CUDA tensors; None skips that step.
+    rope_pos0 = -1: this rank's first row sits at position rank * S_local."""
+    q_norm_weight: Optional[torch.Tensor] = None
+    k_norm_weight: Optional[torch.Tensor] = None
+    eps: float = 1e-6
+    rope_cos: Optional[torch.Tensor] = None
+    rope_sin: Optional[torch.Tensor] = None
+    rope_pos0: int = -1
+
+    def _c(self) -> "_lib.QKPrologue":
+        def f32(t):
+            if t is None:
+                return None
+            if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                raise InvalidArgument(4, "QKPrologue tensors must be contiguous f32 CUDA tensors")
+            return t
+        qw, kw, c, s = (f32(t) for t in (self.q_norm_weight, self.k_norm_weight,
+                                         self.rope_cos, self.rope_sin))
+        rows = c.shape[0] if c is not None else 0
+        return _lib.QKPrologue(_ptr(qw), _ptr(kw), float(self.eps), _ptr(c), _ptr(s), rows,
+                               int(self.rope_pos0))
+
+
+def rope_tables(positions: int, d: int = 128, theta: float = 10000.0, device="cuda"):
+    """cos/sin [positions][d/2] f32 for frequencies theta^(-2i/d) (1-axis RoPE)."""
+    inv = theta ** (-torch.arange(0, d, 2, dtype=torch.float64) / d)
+    ang = torch.arange(positions, dtype=torch.float64)[:, None] * inv[None, :]
+    return (ang.cos().float().to(device).contiguous(), ang.sin().float().to(device).contiguous())
+
+
 def usp_attention(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
-                  opts: Optional[CommOptions] = None) -> torch.Tensor:
-    """usp_attention (protocols.cpp:321-340): local shards [B,H,S/N,D] -> [B,H,S/N,D]."""
+                  opts: Optional[CommOptions] = None,
+                  prologue: Optional[QKPrologue] = None) -> torch.Tensor:
+    """usp_attention (protocols.cpp:321-340): local shards [B,H,S/N,D] -> [B,H,S/N,D].
+    `prologue` (B200 extension): QK RMSNorm + RoPE applied inside the Ulysses pack."""
     opts = opts or CommOptions()
     if mesh.n != ctx.world_size():
         raise MeshError(2, f"mesh covers {mesh.n} workers but the fabric has {ctx.world_size()}")
     q, k, v = _inputs(q, k, v, "usp")
     out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
     co = opts._c()
-    check(lib().fusp_usp_attention(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
-                                   _shape4(q), _ptr(out), ctypes.byref(co), _stream()))
+    if prologue is None:
+        check(lib().fusp_usp_attention(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
+                                       _DT[q.dtype], _shape4(q), _ptr(out), ctypes.byref(co),
+                                       _stream()))
+    else:
+        pc = prologue._c()
+        check(lib().fusp_usp_attention_ex(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
+                                          _DT[q.dtype], _shape4(q), _ptr(out), ctypes.byref(co),
+                                          ctypes.byref(pc), _stream()))
     return out
 
 

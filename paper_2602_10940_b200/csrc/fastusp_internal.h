@@ -88,6 +88,12 @@ struct PackDesc {
   int64_t scale_bh_stride;  // 0: one tensor-wide scale; 1: one scale per (b,h) slab
 };
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
+// Fused QK RMSNorm (w != null) + interleaved RoPE (cosv != null, rows pos0 + s) + pack into
+// slot t = h / (H/u) at t * slot_stride elements (u = 1: plain [B][H][SL][D] output).
+fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
+                                  int64_t slot_stride, int b, int h, int sl, int d, int u,
+                                  const float* w, float eps, const float* cosv, const float* sinv,
+                                  int64_t pos0, cudaStream_t s);
 // Ulysses unpack: src slots [U][B][hp][SL][D] -> dst [B][hp][U*SL][D]; e4m3 src uses per-slot
 // scales scale[j] (device) -- value = decode(code) * scale[j] in f32, then cast to dst dtype.
 struct UnpackDesc {

@@ -1,0 +1,117 @@
+// The producer side of the layer fused into the Ulysses pack:
+// MMDiT joint attention applies RMSNorm to each Q and K head row and rotary position
+// embedding before attention (FLUX QK-norm + RoPE).  Instead of a norm
+// kernel, a RoPE kernel and the pack (three HBM round trips), one pass reads the
+// projected row, normalizes, rotates and writes it straight into its destination's
+// all-to-all slot (or into the attention operand when U = 1).
+//
+// One warp per (b, h, s) row of D = 128: each lane owns 4 consecutive elements = 2 RoPE
+// pairs.  RMSNorm in f32: y = x * rsqrt(mean(x^2) + eps) * w.  RoPE on interleaved pairs
+// (x0, x1) at position p: (x0 cos - x1 sin, x0 sin + x1 cos) with cos/sin[p][pair].
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "fastusp_internal.h"
+
+namespace fusp {
+namespace {
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ void load4(const void* p, int dt, int64_t i, float* f) {
+  if (dt == FUSP_F32) {
+    const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(p) + i);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  } else {
+    const uint2 w = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(p) + i);
+    if (dt == FUSP_BF16) {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
+      f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+    } else {
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+      f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void store4(void* p, int dt, int64_t i, const float* f) {
+  if (dt == FUSP_F32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p) + i) = make_float4(f[0], f[1], f[2], f[3]);
+  } else if (dt == FUSP_BF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
+    *reinterpret_cast<uint2*>(static_cast<uint16_t*>(p) + i) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  } else {
+    __half2 a = __floats2half2_rn(f[0], f[1]), b = __floats2half2_rn(f[2], f[3]);
+    *reinterpret_cast<uint2*>(static_cast<uint16_t*>(p) + i) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+// src [B][H][SL][D] -> dst slot t = h / hp: [B][hp][SL][D] at t * slot_stride (elements).
+__global__ void norm_rope_pack_kernel(const void* __restrict__ src, int sdt, void* __restrict__ dst,
+                                      int ddt, int64_t slot_stride, int b, int h, int sl, int u,
+                                      const float* __restrict__ w, float eps,
+                                      const float* __restrict__ cosv, const float* __restrict__ sinv,
+                                      int64_t pos0) {
+  constexpr int D = 128;
+  const int hp = h / u;
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = int64_t(b) * h * sl;
+  for (int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; row < rows;
+       row += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int s = static_cast<int>(row % sl);
+    const int64_t bh = row / sl;
+    const int hh = static_cast<int>(bh % h);
+    const int bb = static_cast<int>(bh / h);
+    float x[4];
+    load4(src, sdt, row * D + lane * 4, x);
+    if (w != nullptr) {  // RMSNorm over the head dim
+      float ss = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float r = rsqrtf(ss * (1.0f / D) + eps);
+      const float4 wv = *reinterpret_cast<const float4*>(w + lane * 4);
+      x[0] *= r * wv.x;
+      x[1] *= r * wv.y;
+      x[2] *= r * wv.z;
+      x[3] *= r * wv.w;
+    }
+    if (cosv != nullptr) {  // RoPE on the two interleaved pairs this lane owns
+      const int64_t pos = pos0 + s;
+      const float2 c = *reinterpret_cast<const float2*>(cosv + pos * (D / 2) + lane * 2);
+      const float2 n = *reinterpret_cast<const float2*>(sinv + pos * (D / 2) + lane * 2);
+      const float y0 = x[0] * c.x - x[1] * n.x, y1 = x[0] * n.x + x[1] * c.x;
+      const float y2 = x[2] * c.y - x[3] * n.y, y3 = x[2] * n.y + x[3] * c.y;
+      x[0] = y0; x[1] = y1; x[2] = y2; x[3] = y3;
+    }
+    const int t = hh / hp, hl = hh % hp;
+    const int64_t o = t * slot_stride + ((int64_t(bb) * hp + hl) * sl + s) * D + lane * 4;
+    store4(dst, ddt, o, x);
+  }
+}
+
+}  // namespace
+
+fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
+                                  int64_t slot_stride, int b, int h, int sl, int d, int u,
+                                  const float* w, float eps, const float* cosv, const float* sinv,
+                                  int64_t pos0, cudaStream_t s) {
+  if (d != 128) return set_error(FUSP_ERR_SHAPE, "qk prologue: head dim must be 128");
+  const int64_t rows = int64_t(b) * h * sl;
+  if (rows <= 0) return FUSP_OK;
+  int64_t grid = (rows * 32 + 255) / 256;
+  if (grid > kSMs * 16) grid = kSMs * 16;
+  norm_rope_pack_kernel<<<static_cast<int>(grid), 256, 0, s>>>(src, sdt, dst, ddt, slot_stride, b,
+                                                               h, sl, u, w, eps, cosv, sinv, pos0);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "norm_rope_pack_kernel");
+  return FUSP_OK;
+}
+
+}  // namespace fusp

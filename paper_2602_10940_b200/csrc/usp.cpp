@@ -135,6 +135,13 @@ struct Layer {
   int nsc_local = 1;  // scales of the caller's local K (or V): B*H per block
   int nsc_slot = 1;   // scales riding in one Ulysses slot: B*hp per block
   int nsc_chunk = 1;  // scales of a ring chunk: heads_r per block
+  // fused QK prologue (fusp_qk_prologue): Q goes through norm/rope on its way into the slot
+  // (or the attention operand); K likewise, except on the FP8 path, which normalizes K once
+  // into an f32 scratch copy (k_dt = F32) that the quantizers then read
+  const fusp_qk_prologue* pro = nullptr;
+  bool pro_q = false, pro_k = false, pro_k_pre = false;
+  int64_t pos0 = 0;
+  int k_dt = 0;  // dtype of the K source the FP8 quantizers read
 };
 
 struct Buffers {
@@ -158,6 +165,8 @@ struct Buffers {
   float *acc_o = nullptr, *acc_lse = nullptr;
   // Ulysses out
   char *send_out = nullptr, *recv_out = nullptr;
+  // FP8 path with a K prologue: normalized + rotated K in f32
+  float* Kpro = nullptr;
   // stream-K partials of the attention kernel
   void* attn_ws = nullptr;
   size_t attn_ws_bytes = 0;
@@ -198,6 +207,7 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   l.fp8 = o.fp8_kv != 0;
   l.pipelined = o.pipelined_ring != 0;
   l.in_dt = in_dt;
+  l.k_dt = in_dt;
   // FP8 K/V dequantize to decode(code)*scale (up to 28 significant bits): f16 keeps 2^-12 of
   // it where bf16 keeps 2^-9, so the FP8 path runs Q.K^T in f16 (Q converts exactly).
   l.qk_dt = (in_dt == FUSP_F16 || o.fp8_kv) ? FUSP_F16 : FUSP_BF16;
@@ -237,15 +247,16 @@ void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, 
     }
   } else {
     // U == 1: no transfer; operands are the caller's tensors when already in the MMA dtype.
-    if (l.in_dt == l.qk_dt) b->Qr = q; else b->Qr = b->Qr_w = cv.take(C2);
+    if (l.in_dt == l.qk_dt && !l.pro_q) b->Qr = q; else b->Qr = b->Qr_w = cv.take(C2);
     const bool fq = uly && l.fp8;  // Ulysses self slot still takes the FP8 round trip (D7)
-    if (l.in_dt == l.qk_dt && !fq) b->Kr = k; else b->Kr = b->Kr_w = cv.take(C2);
+    if (l.k_dt == l.qk_dt && !fq && !l.pro_k) b->Kr = k; else b->Kr = b->Kr_w = cv.take(C2);
     if (l.in_dt == FUSP_F16 && !fq) b->Vr = v; else b->Vr = b->Vr_w = cv.take(C2);
     if (fq) {
       b->Kc = static_cast<uint8_t*>(cv.take(l.C));
       b->Vc = static_cast<uint8_t*>(cv.take(l.C));
     }
   }
+  if (l.pro_k_pre) b->Kpro =static_cast<float*>(cv.take(size_t(l.C) * 4));
   const int nsc = l.nsc_local > l.nsc_chunk ? l.nsc_local : l.nsc_chunk;
   b->qscale = static_cast<float*>(cv.take(sizeof(float) * 2 * nsc));
   b->amax = static_cast<uint32_t*>(cv.take(sizeof(uint32_t) * 4 * (nsc + 1)));
@@ -274,15 +285,25 @@ void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, 
 fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q, const void* k,
                        const void* v, cudaStream_t s) {
   const bool uly = l.mode != Mode::kRing;
+  // norm/rope of Q (or K) written as `ddt` into slots of `stride` elements, u = 1: plain copy
+  auto prologue = [&](bool is_q, const void* src, void* dst, int ddt, int64_t stride,
+                      int u) -> fusp_status {
+    const fusp_qk_prologue& p = *l.pro;
+    return launch_norm_rope_pack(src, l.in_dt, dst, ddt, stride, l.B, l.H, l.SL, l.D, u,
+                                 is_q ? p.q_norm_weight : p.k_norm_weight, p.eps, p.rope_cos,
+                                 p.rope_sin, l.pos0, s);
+  };
   if (!uly || l.U == 1) {
     const int64_t n = l.C;
-    if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
+    if (l.pro_q) FUSP_CHECK(prologue(true, q, b.Qr_w, l.qk_dt, 0, 1));
+    else if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
     if (uly && l.fp8) {
       // quantize the whole local K and V (protocols.cpp:139-142; or per (b,h) slab), and the
       // self slot takes the dequantized values (:163-179)
       const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : n;
       for (int p = 0; p < 2; ++p) {
-        const Fp8Src src{p == 0 ? k : v, l.in_dt, nullptr, 0, 0, l.D, l.span, l.span};
+        const Fp8Src src{p == 0 ? k : v, p == 0 ? l.k_dt : l.in_dt, nullptr, 0, 0, l.D, l.span,
+                         l.span};
         uint8_t* codes = p == 0 ? b.Kc : b.Vc;
         float* sc = b.qscale + p * l.nsc_local;
         FUSP_CHECK(launch_quantize_fp8(src, n, block, b.amax, sc, codes, nullptr, s));
@@ -295,7 +316,8 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       b.bh_stride = l.fp8_block ? 1 : 0;
       b.seg_rows = l.span;
     } else {
-      if (b.Kr_w) FUSP_CHECK(launch_convert(k, l.in_dt, b.Kr_w, l.qk_dt, n, s));
+      if (l.pro_k) FUSP_CHECK(prologue(false, k, b.Kr_w, l.qk_dt, 0, 1));
+      else if (b.Kr_w) FUSP_CHECK(launch_convert(k, l.k_dt, b.Kr_w, l.qk_dt, n, s));
       if (b.Vr_w) FUSP_CHECK(launch_convert(v, l.in_dt, b.Vr_w, FUSP_F16, n, s));
     }
     return FUSP_OK;
@@ -313,11 +335,13 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   p.dst = b.send_in;
   p.dst_dtype = l.qk_dt;
   p.dst_slot_stride = se2;
-  FUSP_CHECK(launch_pack(p, s));
+  if (l.pro_q) FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
+  else FUSP_CHECK(launch_pack(p, s));
   if (!l.fp8) {
     p.src = k;
     p.dst = b.send_in + l.blk * 2;
-    FUSP_CHECK(launch_pack(p, s));
+    if (l.pro_k) FUSP_CHECK(prologue(false, k, p.dst, l.qk_dt, se2, l.U));
+    else FUSP_CHECK(launch_pack(p, s));
     p.src = v;
     p.dst = b.send_in + l.blk * 4;
     p.dst_dtype = FUSP_F16;
@@ -326,7 +350,8 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --
     // fused into the pack; every slot's trailer carries the scales of its heads
     for (int part = 0; part < 2; ++part) {
-      const Fp8Src src{part == 0 ? k : v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL};
+      const Fp8Src src{part == 0 ? k : v, part == 0 ? l.k_dt : l.in_dt, nullptr, 0, 0, l.D, l.SL,
+                       l.SL};
       const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
       const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
       FUSP_CHECK(launch_amax_blocks(src, block, l.nsc_local, b.amax, nullptr, s));
@@ -335,6 +360,7 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       FUSP_CHECK(launch_scatter_slot_scales(scales, trailer, int64_t(l.slot_stride / 4), l.B, l.H,
                                             l.U, l.fp8_block ? 1 : 0, s));
       p.src = src.x;
+      p.src_dtype = src.dt;
       p.dst = b.send_in + l.blk * 2 + part * l.blk;
       p.dst_dtype = FUSP_E4M3;
       p.dst_slot_stride = int64_t(l.slot_stride);
@@ -466,7 +492,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
       float* scales = reinterpret_cast<float*>(b.sw[p] + l.C);
       Fp8Src src{};
       if (hop == 1 && !usp_local) {  // pure ring: quantize the caller's local chunk
-        src = Fp8Src{p == 0 ? k_src : v_src, l.in_dt, nullptr, 0, 0, l.D, l.span, l.span};
+        src = Fp8Src{p == 0 ? k_src : v_src, p == 0 ? l.k_dt : l.in_dt, nullptr, 0, 0, l.D,
+                      l.span, l.span};
       } else if (hop == 1) {  // USP: exact f32 values of the (multi-scale) resharded chunk
         src = Fp8Src{p == 0 ? b.Kc : b.Vc, FUSP_E4M3, p == 0 ? b.Ks : b.Vs, b.s_stride,
                      b.bh_stride, l.D, l.span, b.seg_rows};
@@ -605,9 +632,35 @@ fusp_status check_inputs(fusp_ctx_s* c, Mode mode, const Layer& l, const void* q
   return FUSP_OK;
 }
 
+fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
+  Layer& l = *L;
+  if (!p) return FUSP_OK;
+  const bool rope = p->rope_cos != nullptr || p->rope_sin != nullptr;
+  if (rope && (p->rope_cos == nullptr || p->rope_sin == nullptr))
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: rope_cos and rope_sin go together");
+  if (!(p->eps >= 0.f))
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: eps must be >= 0");
+  l.pos0 = p->rope_pos0 < 0 ? int64_t(c->rank) * l.SL : p->rope_pos0;
+  if (rope && (p->rope_rows < l.pos0 + l.SL))
+    return set_error(FUSP_ERR_SHAPE, "qk prologue: rope table has " + std::to_string(p->rope_rows) +
+                                         " rows, positions up to " +
+                                         std::to_string(l.pos0 + l.SL) + " needed");
+  l.pro = p;
+  l.pro_q = rope || p->q_norm_weight != nullptr;
+  const bool pk = rope || p->k_norm_weight != nullptr;
+  if (pk && l.fp8) {  // quantizers read a normalized f32 copy of K
+    l.pro_k_pre = true;
+    l.k_dt = FUSP_F32;
+  } else {
+    l.pro_k = pk;
+  }
+  return FUSP_OK;
+}
+
 fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void* k,
                       const void* v, int in_dt, fusp_shape4 ls, void* out, float* lse_out,
-                      const fusp_comm_options* opts, cudaStream_t s, bool size_only = false) {
+                      const fusp_comm_options* opts, cudaStream_t s, bool size_only = false,
+                      const fusp_qk_prologue* pro = nullptr) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
   FUSP_CUDA(cudaSetDevice(c->device));
@@ -616,6 +669,7 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   if (opts) o = *opts;
   Layer l;
   FUSP_CHECK(plan_layer(c, mode, r, ls, in_dt, o, &l));
+  FUSP_CHECK(plan_prologue(c, pro, &l));
   if (c->nccl && l.U > 1 && l.R > 1) FUSP_CHECK(c->nccl->ensure_mesh(l.R));
   if (o.check_finite && !size_only) FUSP_CHECK(check_inputs(c, mode, l, q, k, v, s));
   Carve cv;
@@ -626,7 +680,13 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   cv = Carve{static_cast<char*>(c->arena), 0};
   b = Buffers{};
   carve(l, cv, &b, q, k, v, out);
-  const bool uly1 = l.mode != Mode::kRing && l.U == 1;  // the reference still runs a 1-member
+  if (l.pro_k_pre) {
+    FUSP_CHECK(launch_norm_rope_pack(k, l.in_dt, b.Kpro, FUSP_F32, 0, l.B, l.H, l.SL, l.D, 1,
+                                     pro->k_norm_weight, pro->eps, pro->rope_cos, pro->rope_sin,
+                                     l.pos0, s));
+    k = b.Kpro;
+  }
+  const bool uly1 =l.mode != Mode::kRing && l.U == 1;  // the reference still runs a 1-member
   if (uly1) log_a2a(c, l.ug, 0);                         // all_to_all (fabric.cpp:199-226)
   FUSP_CHECK(ulysses_in(c, l, b, q, k, v, s));
   FUSP_CHECK(ring(c, l, b, k, v, out, lse_out, s));
@@ -872,6 +932,14 @@ fusp_status fusp_usp_attention(fusp_ctx c, int ring_dim, const void* q, const vo
                                const fusp_comm_options* opts, fusp_stream_t stream) {
   return run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_usp_attention_ex(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                                  const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                  const fusp_comm_options* opts, const fusp_qk_prologue* prologue,
+                                  fusp_stream_t stream) {
+  return run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts,
+                   reinterpret_cast<cudaStream_t>(stream), false, prologue);
 }
 
 fusp_status fusp_ulysses_attention(fusp_ctx c, const void* q, const void* k, const void* v,

@@ -230,3 +230,23 @@ def test_reference_error_classes():
     with pytest.raises(Exception) as e:
         ref.usp_attention(bad, q, q, 1, 1)
     assert e.value.kind == "invalid_argument" and "non-finite" in e.value.msg
+
+
+def test_qk_prologue_restatement_properties():
+    """The prologue oracle (not in the reference): RMSNorm gives unit mean square with unit
+    weights; RoPE is an isometry on each pair and makes q.k depend only on the position gap."""
+    x = R.rng_tensor(3, (1, 2, 16, 128), -3, 3).astype(np.float64)
+    y = R.rms_norm(x, np.ones(128), 0.0)
+    assert np.allclose((y * y).mean(-1), 1.0, atol=1e-12)
+    inv = 10000.0 ** (-np.arange(0, 128, 2) / 128)
+    ang = np.arange(64)[:, None] * inv[None, :]
+    cos, sin = np.cos(ang), np.sin(ang)
+    z = R.rope_interleaved(x, cos, sin)
+    pair = lambda t: t[..., 0::2] ** 2 + t[..., 1::2] ** 2
+    assert np.allclose(pair(z), pair(x), rtol=1e-12)
+    assert np.array_equal(R.rope_interleaved(x, np.ones((16, 64)), np.zeros((16, 64))), x)
+    q, k = x[0, 0, :1], x[0, 1, :1]
+    d1 = R.rope_interleaved(q, cos, sin, 5) @ R.rope_interleaved(k, cos, sin, 2).T
+    d2 = R.rope_interleaved(q, cos, sin, 40) @ R.rope_interleaved(k, cos, sin, 37).T
+    assert np.allclose(d1, d2, rtol=1e-10)
+    assert np.array_equal(R.qk_prologue(x), x)
