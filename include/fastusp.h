@@ -60,6 +60,15 @@ const char* fusp_last_error(void);
 const char* fusp_version(void);
 /* Number of fastusp CUDA kernels launched so far by this process (all devices). */
 uint64_t fusp_kernel_launch_count(void);
+/* Tuning knob (no reference counterpart): attention work schedule, 0 = auto, 1 = whole
+ * 256-row q-blocks per CTA, 2 = stream-K split of (q-block x KV tile) units over the SMs;
+ * max_ctas caps the persistent grid (0 = every SM; leave SMs free for concurrent NCCL). */
+fusp_status fusp_attention_schedule(int mode, int max_ctas);
+/* Debug timeline (no reference counterpart): enable != 0 records per-CTA globaltimer events
+ * of subsequent attention launches; copies up to n u64 events of the last launch to host
+ * (layout: 72 per CTA = start, end, [8 segments][2 Q tiles][start, first S, O done, stored]).
+ * Returns the number copied. */
+int fusp_attention_trace(int enable, uint64_t* host, size_t n);
 
 /* ---- FP8 E4M3 codec (fp8.hpp:23-49) ---------------------------------------------------- */
 /* encode_e4m3 (fp8.cpp:45-68), elementwise: f32 -> code.  Bit-exact. */

@@ -11,6 +11,9 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libfastusp.so")
+# Kernel-variant experiments (tools/build_variants.sh) load an in-tree variant build instead.
+if os.environ.get("FUSP_VARIANT"):
+    LIB_PATH = os.path.join(PKG, "variants", os.environ["FUSP_VARIANT"], "libfastusp.so")
 
 F32, F16, BF16, E4M3 = 0, 1, 2, 3
 
@@ -81,6 +84,8 @@ _SIGS = {
     "fusp_last_error": (ctypes.c_char_p, []),
     "fusp_version": (ctypes.c_char_p, []),
     "fusp_kernel_launch_count": (ctypes.c_uint64, []),
+    "fusp_attention_schedule": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "fusp_attention_trace": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_size_t]),
     "fusp_encode_e4m3": (ctypes.c_int, [_P, _I64, _P, _P]),
     "fusp_decode_e4m3": (ctypes.c_int, [_P, _I64, _P, _P]),
     "fusp_quantize_e4m3": (ctypes.c_int, [_P, ctypes.c_int, _I64, _P, _P, ctypes.c_int, _P]),

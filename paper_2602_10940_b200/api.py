@@ -7,6 +7,7 @@ libfastusp.so's sm_100a kernels).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 from dataclasses import dataclass, field
@@ -171,6 +172,22 @@ def attention_with_lse(q, k, v, out_dtype=torch.float32) -> AttnResult:
                                            _shape4(q), int(k.shape[2]), _ptr(out), _DT[out_dtype],
                                            _ptr(lse), _stream()))
     return AttnResult(out, lse)
+
+
+_SCHEDULES = {"auto": 0, "whole": 1, "split": 2}
+
+
+@contextlib.contextmanager
+def attention_schedule(mode: str = "auto", max_ctas: int = 0):
+    """Pin the attention kernel's work schedule inside the block (tests, benchmarks):
+    "whole" = one 256-row q-block per CTA turn, "split" = stream-K over (q-block, KV tile)
+    units, "auto" = split only when whole q-blocks leave SMs idle; `max_ctas` caps the
+    persistent grid (0 = every SM)."""
+    check(lib().fusp_attention_schedule(_SCHEDULES[mode], int(max_ctas)))
+    try:
+        yield
+    finally:
+        check(lib().fusp_attention_schedule(0, 0))
 
 
 def attention_reference(q, k, v, out_dtype=torch.float32) -> torch.Tensor:

@@ -9,8 +9,21 @@
 // Non-causal, head dim D = 128.  Q/K are bf16, V is f16 (P.V runs in f16:
 // bf16 P cannot meet rel-L2 <= 1e-3 against the fp32 oracle).
 //
-// CTA = one head x 256 query rows as two 128-row tiles that ping-pong on the
-// tensor core; KV tiles of 128 rows stream through a 2-stage TMA ring.
+// Persistent kernel, one CTA per SM.  The work is (q-block of 256 rows) x (KV tile of 128
+// keys) units, q-block-major over heads.  Two schedules:
+//   whole  -- CTA c takes q-blocks c, c+G, c+2G, ... (used when the q-blocks fill the SMs
+//             in near-full waves);
+//   split  -- stream-K: CTA c takes the contiguous unit range [c*T/G, (c+1)*T/G), so a
+//             q-block may be cut into segments owned by consecutive CTAs.  Every segment but
+//             the last to finish writes its unnormalised (O, m, l) to a workspace slot; the
+//             last arriver (atomic ticket per q-block tile) merges them in segment order and
+//             runs the normal epilogue.  Nobody waits on a CTA that has not started, so the
+//             protocol is deadlock-free even when other kernels hold SMs.
+// This keeps every SM busy at the small per-rank head counts the USP meshes produce
+// (FLUX U=8: 3 heads = 54 q-blocks on 148 SMs).
+//
+// CTA = two 128-row Q tiles that ping-pong on the tensor core; KV tiles of 128 rows
+// stream through a 2-stage TMA ring.
 //   warp 0      TMA producer for Q and K
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warp 2      TMA producer for V
@@ -21,6 +34,9 @@
 // pairs) overwrites columns [0,64) of S_t after the softmax has read S_t.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -33,24 +49,57 @@ namespace {
 using namespace ptx;
 
 constexpr int kBM = 128;   // rows per Q tile (one softmax warpgroup)
+constexpr int kQB = 2 * kBM;  // rows per q-block (one CTA work item)
 constexpr int kBN = 128;   // keys per KV tile
 constexpr int kD = 128;    // head dim
 constexpr int kStages = 2; // KV ring depth
 constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: [2 halves][128 rows][128 B]
 constexpr uint32_t kHalfBytes = kTileBytes / 2;
+constexpr uint32_t kTmemS = 0;    // S_t / P_t at columns [128 t, 128 t + 128)
+constexpr uint32_t kTmemO = 256;  // O_t at columns [256 + 128 t, ...)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: lazy O rescale (P <= 2^8 in f16)
-constexpr int kEmuEvery = 4;               // 1 exp2 pair in 4 is emulated on the FMA pipe
+#ifndef FUSP_EMU_EVERY
+#define FUSP_EMU_EVERY 4
+#endif
+#ifndef FUSP_PRODUCER_REGS  // setmaxnreg split; the CTA pool is 168 x 384 registers, so
+#define FUSP_PRODUCER_REGS 56  // 128 * (168 - producer) >= 256 * (softmax - 168)
+#endif
+#ifndef FUSP_MMA_UNROLL  // unroll of the issuer's per-k MMA loops (code size vs issue cost)
+#define FUSP_MMA_UNROLL 8
+#endif
+#ifndef FUSP_SOFTMAX_REGS
+#define FUSP_SOFTMAX_REGS 224
+#endif
+static_assert(128 * (168 - FUSP_PRODUCER_REGS) >= 256 * (FUSP_SOFTMAX_REGS - 168),
+              "setmaxnreg split exceeds the CTA register pool");
+constexpr int kMmaUnroll = FUSP_MMA_UNROLL;
+constexpr int kEmuEvery = FUSP_EMU_EVERY;  // 1 exp2 pair in kEmuEvery runs on the FMA pipe
+// Stream-K partial slot for one 128-row tile: O as [32 column quads][128 rows][4] f32 (a
+// warp's float4 accesses to one quad are contiguous), then m[128], l[128].
+constexpr int kSlotTileFloats = kD * kBM + 2 * kBM;
+constexpr int kMaxGrid = 160;  // persistent grid cap (B200: 148 SMs)
+constexpr size_t kSlotBytes = size_t(2) * kSlotTileFloats * 4;  // both tiles of a q-block
 
 struct __align__(1024) Smem {
   uint8_t q[2][kTileBytes];
   uint8_t k[kStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
-  uint64_t q_full;
+  uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2], o_done[2];
   uint32_t tmem_base;
+  uint32_t ticket[2];
+};
+
+struct Sched {
+  int n_kv;         // KV tiles per q-block
+  int qb_per_head;  // q-blocks per head
+  int n_qb;         // heads * qb_per_head
+  int split;        // 1: stream-K unit ranges; 0: whole q-blocks, strided by gridDim.x
+  int total;        // n_qb * n_kv units (< 2^31)
+  int begin[kMaxGrid + 1];  // split: CTA c owns units [begin[c], begin[c+1]) = c*total/grid
 };
 
 struct Params {
@@ -65,7 +114,80 @@ struct Params {
   int64_t lse_hs;
   const float* acc_o;    // fp32 [heads][sq][D] running accumulator or null
   const float* acc_lse;  // [heads][sq]
+  Sched sc;
+  uint32_t* counters;    // split: [n_qb][2 tiles][arrive, written], zero between launches
+  float* slots;          // split: [gridDim.x][2 (first/last segment)][2 tiles][kSlotTileFloats]
+  unsigned long long* trace;  // optional per-CTA globaltimer events (attention_trace), or null
 };
+constexpr int kTraceSlots = 72;  // per CTA (SM cycles): start, end, then [8 segments][2 tiles][4 events]
+
+__device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (per-CTA deltas)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+#define FUSP_TRACE(p, slot)                                                        \
+  do {                                                                             \
+    if ((p).trace != nullptr) (p).trace[blockIdx.x * kTraceSlots + (slot)] = gtimer(); \
+  } while (0)
+
+// ---- schedule (identical in every role) -------------------------------------------------
+// The CTA whose unit range holds unit u: max c with begin[c] <= u (estimate, then correct).
+__device__ __forceinline__ int sk_cta_of(const Sched& s, int u) {
+  int c = static_cast<int>(static_cast<float>(u) * gridDim.x / static_cast<float>(s.total));
+  c = c < 0 ? 0 : (c >= static_cast<int>(gridDim.x) ? gridDim.x - 1 : c);
+  while (c > 0 && s.begin[c] > u) --c;
+  while (c + 1 < static_cast<int>(gridDim.x) && s.begin[c + 1] <= u) ++c;
+  return c;
+}
+struct Seg {
+  int qb, j0, j1;
+};
+struct SegIter {  // unit indices fit in 32 bits (the planner checks total < 2^31)
+  int u, end, qb;
+  __device__ explicit SegIter(const Sched& s) {
+    u = s.split ? s.begin[blockIdx.x] : 0;
+    end = s.split ? s.begin[blockIdx.x + 1] : 0;
+    qb = blockIdx.x;
+  }
+  __device__ bool next(const Sched& s, Seg& g) {
+    if (s.split) {
+      if (u >= end) return false;
+      g.qb = u / s.n_kv;
+      g.j0 = u - g.qb * s.n_kv;
+      const int left = end - u;
+      g.j1 = left < s.n_kv - g.j0 ? g.j0 + left : s.n_kv;
+      u += g.j1 - g.j0;
+      return true;
+    }
+    if (qb >= s.n_qb) return false;
+    g.qb = qb;
+    g.j0 = 0;
+    g.j1 = s.n_kv;
+    qb += gridDim.x;
+    return true;
+  }
+};
+// Workspace slot CTA c uses for its segment of q-block qb (0: its first segment, 1: last).
+__device__ __forceinline__ float* seg_slot(const Params& p, int c, int qb, int t) {
+  const int first_qb = p.sc.begin[c] / p.sc.n_kv;
+  const int which = qb == first_qb ? 0 : 1;
+  return p.slots + (static_cast<size_t>(c) * 2 + which) * (2 * kSlotTileFloats) +
+         static_cast<size_t>(t) * kSlotTileFloats;
+}
+
+// The 128 threads of softmax warpgroup t.  bar.sync counts a diverged warp once per divergent
+// arrival, so the warp reconverges first (callers often let lane 0 do a global op just before).
+__device__ __forceinline__ void wg_bar(int t) {
+  __syncwarp();
+  if (t == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+  else asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ float merge_coeffs(float l1, float l2, float& c1, float& c2) {
   // merge_lse per row (reference tensor.cpp:219-240), identity rows pass through.
@@ -85,274 +207,557 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5;
+  // shfl from lane 0: the compiler then knows the warp index (and every role branch on it)
+  // is warp-uniform, so schedule state and UMMA descriptors can live in uniform registers.
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int head = blockIdx.y;
-  const int row0 = blockIdx.x * (2 * kBM);
-  const int n_kv = (p.skv + kBN - 1) / kBN;
+  const Sched& sc = p.sc;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(&sm.q_full, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.q_full[t], 1);
+      mbar_init(&sm.q_empty[t], 1);
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], kBM);
+      mbar_init(&sm.o_done[t], 1);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], kBM);
-      mbar_init(&sm.o_done[t], 1);
-    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  __syncwarp();  // reconverge warp 0 (lane 0 initialised the barriers) before bar.sync
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  // 512 columns is the whole TMEM, so the allocation always starts at lane 0, column 0; the
+  // MMA and softmax roles use that constant base (uniform, foldable into the instructions).
+  if (tmem != 0u) __trap();
+  if (threadIdx.x == 0) FUSP_TRACE(p, 0);
   // Register split: the producer/MMA warpgroup gives registers to the softmax warpgroups.
   if (warp < 4) {
-  reg_dealloc<56>();
+  reg_dealloc<FUSP_PRODUCER_REGS>();  // warpgroup-collective: every warp of the group sets the same limit
   if (warp == 0) {
     // ---------------- TMA producer: Q tiles, then K tiles ----------------
     if (lane == 0) {
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
-      mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
-      for (int t = 0; t < 2; ++t)
-        for (int h = 0; h < 2; ++h)
-          tma_load_3d(sm.q[t] + h * kHalfBytes, &tm_q, &sm.q_full, h * 64, row0 + t * kBM, head);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        mbar_wait(&sm.k_empty[st], ph ^ 1);
-        mbar_expect_tx(&sm.k_full[st], kTileBytes);
-        for (int h = 0; h < 2; ++h)
-          tma_load_3d(sm.k[st] + h * kHalfBytes, &tm_k, &sm.k_full[st], h * 64, j * kBN, head);
+      SegIter si(sc);
+      Seg g;
+      uint32_t it = 0, ns = 0;
+      while (si.next(sc, g)) {
+        const int head = g.qb / sc.qb_per_head;
+        const int row0 = (g.qb - head * sc.qb_per_head) * kQB;
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&sm.q_empty[t], (ns & 1) ^ 1);
+          mbar_expect_tx(&sm.q_full[t], kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            tma_load_3d(sm.q[t] + h * kHalfBytes, &tm_q, &sm.q_full[t], h * 64, row0 + t * kBM, head);
+        }
+        for (int j = g.j0; j < g.j1; ++j, ++it) {
+          const int st = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&sm.k_empty[st], ph ^ 1);
+          mbar_expect_tx(&sm.k_full[st], kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            tma_load_3d(sm.k[st] + h * kHalfBytes, &tm_k, &sm.k_full[st], h * 64, j * kBN, head);
+        }
+        ++ns;
       }
     }
   } else if (warp == 2) {
     // ---------------- TMA producer: V tiles ----------------
     if (lane == 0) {
       prefetch_tmap(&tm_v);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        mbar_wait(&sm.v_empty[st], ph ^ 1);
-        mbar_expect_tx(&sm.v_full[st], kTileBytes);
-        for (int h = 0; h < 2; ++h)
-          tma_load_3d(sm.v[st] + h * kHalfBytes, &tm_v, &sm.v_full[st], h * 64, j * kBN, head);
+      SegIter si(sc);
+      Seg g;
+      uint32_t it = 0;
+      while (si.next(sc, g)) {
+        const int head = g.qb / sc.qb_per_head;
+        for (int j = g.j0; j < g.j1; ++j, ++it) {
+          const int st = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&sm.v_empty[st], ph ^ 1);
+          mbar_expect_tx(&sm.v_full[st], kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            tma_load_3d(sm.v[st] + h * kHalfBytes, &tm_v, &sm.v_full[st], h * 64, j * kBN, head);
+        }
       }
     }
   } else if (warp == 1) {
-    // ---------------- single-thread tcgen05.mma issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc_qk = p.idesc_qk;                           // K-major x K-major
-      constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);   // f16 P(tmem) x f16 V(MN)
-      const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
-      auto issue_pv = [&](int t, int jj) {
-        const int st = jj % kStages;
-        const uint32_t vbase = smem_u32(sm.v[st]);
-        const uint32_t t_o = tmem + 256 + t * 128;
-        const uint32_t t_p = tmem + t * 128;
-#pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          // B = V tile, MN-major SW128: LBO = d-half stride (16 KB), SBO = 8-row group (1 KB)
-          const uint64_t bdesc = umma_desc_sw128(vbase + k * 16 * 128, kHalfBytes, 1024);
-          mma_ts(t_o, t_p + k * 8, bdesc, idesc_pv, (jj > 0 || k > 0) ? 1u : 0u);
+    // ---------------- tcgen05.mma issuer ----------------
+    // The whole warp walks the schedule (so descriptors stay in uniform registers); lane 0
+    // issues every MMA and commit (tcgen05.commit tracks the issuing thread's MMAs).
+    const uint32_t idesc_qk = p.idesc_qk;                           // K-major x K-major
+    constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);   // f16 P(tmem) x f16 V(MN)
+    // Descriptors are built once per operand tile, outside the elected region, and advanced
+    // by adding the 16-byte-unit offset to the start-address field (smem < 256 KB: no carry).
+    // O_t (+)= P_t V(stage st); `first` starts the segment's accumulation.
+    auto issue_pv = [&](int t, int st, bool first) {
+      // B = V tile, MN-major SW128: LBO = d-half stride (16 KB), SBO = 8-row group (1 KB)
+      const uint64_t vdesc = umma_desc_sw128(smem_u32(sm.v[st]), kHalfBytes, 1024);
+      if (elect_one()) {
+#pragma unroll kMmaUnroll
+        for (int k = 0; k < kBN / 16; ++k)
+          mma_ts(kTmemO + t * 128, kTmemS + t * 128 + k * 8, vdesc + uint64_t(k * 16 * 128 / 16),
+                 idesc_pv, (!first || k > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    // S_t = Q_t K^T over D = 128 in 8 K-steps of 16 (two 64-element swizzle halves).
+    auto issue_qk = [&](int t, int st) {
+      const uint64_t qdesc = umma_desc_sw128(smem_u32(sm.q[t]), 16, 1024);
+      const uint64_t kdesc = umma_desc_sw128(smem_u32(sm.k[st]), 16, 1024);
+      if (elect_one()) {
+#pragma unroll kMmaUnroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint64_t off16 = ((k >> 2) * kHalfBytes + (k & 3) * 32) / 16;
+          mma_ss(kTmemS + t * 128, qdesc + off16, kdesc + off16, idesc_qk, k > 0 ? 1u : 0u);
         }
-      };
-      mbar_wait(&sm.q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {  // elect.sync picks the same lane as the MMAs
+      if (elect_one()) mma_commit(bar);
+      __syncwarp();
+    };
+    SegIter si(sc);
+    Seg g;
+    uint32_t it = 0, ns = 0;
+    while (si.next(sc, g)) {
+      for (int j = g.j0; j < g.j1; ++j, ++it) {
+        const int st = it % kStages;
+        const uint32_t ph = (it / kStages) & 1;
         mbar_wait(&sm.k_full[st], ph);
         tc_fence_after();
-        const uint32_t kbase = smem_u32(sm.k[st]);
         for (int t = 0; t < 2; ++t) {
-          if (j > 0) {
+          if (j > g.j0) {
             // O_t += P_t(j-1) V(j-1): needs the softmax to have published P_t(j-1)
-            mbar_wait(&sm.p_full[t], (j - 1) & 1);
-            if (t == 0) mbar_wait(&sm.v_full[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+            const uint32_t ip = it - 1;
+            mbar_wait(&sm.p_full[t], ip & 1);
+            if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
             tc_fence_after();
-            issue_pv(t, j - 1);
-            if (t == 1) mma_commit(&sm.v_empty[(j - 1) % kStages]);
+            issue_pv(t, ip % kStages, j - 1 == g.j0);
+            if (t == 1) commit(&sm.v_empty[ip % kStages]);
+          } else {
+            mbar_wait(&sm.q_full[t], ns & 1);
+            tc_fence_after();
           }
           // S_t = Q_t K_j^T  (executes after PV_t(j-1) has read P_t: tcgen05.mma is in-order)
-#pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
-            const uint64_t adesc = umma_desc_sw128(q_addr[t] + off, 16, 1024);
-            const uint64_t bdesc = umma_desc_sw128(kbase + off, 16, 1024);
-            mma_ss(tmem + t * 128, adesc, bdesc, idesc_qk, k > 0 ? 1u : 0u);
-          }
-          mma_commit(&sm.s_full[t]);
+          issue_qk(t, st);
+          commit(&sm.s_full[t]);
+          if (j == g.j1 - 1) commit(&sm.q_empty[t]);  // Q_t may be reloaded
         }
-        mma_commit(&sm.k_empty[st]);
+        commit(&sm.k_empty[st]);
       }
+      const uint32_t ip = it - 1;
       for (int t = 0; t < 2; ++t) {
-        mbar_wait(&sm.p_full[t], (n_kv - 1) & 1);
-        if (t == 0) mbar_wait(&sm.v_full[(n_kv - 1) % kStages], ((n_kv - 1) / kStages) & 1);
+        mbar_wait(&sm.p_full[t], ip & 1);
+        if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
         tc_fence_after();
-        issue_pv(t, n_kv - 1);
-        mma_commit(&sm.o_done[t]);
+        issue_pv(t, ip % kStages, g.j1 - 1 == g.j0);
+        commit(&sm.o_done[t]);
       }
-      mma_commit(&sm.v_empty[(n_kv - 1) % kStages]);
+      commit(&sm.v_empty[ip % kStages]);
+      ++ns;
     }
   }
   } else {
-    reg_alloc<224>();
+    reg_alloc<FUSP_SOFTMAX_REGS>();
     // ---------------- softmax warpgroups ----------------
     const int t = (warp - 4) >> 2;          // Q tile 0 / 1
     const int quad = warp & 3;              // TMEM lane quadrant of this warp
     const int r_in_tile = quad * 32 + lane; // row within the 128-row tile
-    const int row = row0 + t * kBM + r_in_tile;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + t * 128;
-    const uint32_t t_o = tmem + lane_off + 256 + t * 128;
+    const uint32_t t_s = kTmemS + lane_off + t * 128;
+    const uint32_t t_o = kTmemO + lane_off + t * 128;
     const float sl2 = p.scale_log2;
-
-    float m_use = -INFINITY;  // max used for the exponent (raw logit units)
-    float l_sum = 0.f;
     const float2 sl2x2 = make_float2(sl2, sl2);
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&sm.s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t s[128];
-      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
-      tmem_wait_ld();
-      const int valid = p.skv - j * kBN;  // keys in this tile (mask the tail)
-      if (valid < kBN) {
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c >= valid) s[c] = __float_as_uint(-INFINITY);
-      }
-      // row max with independent chains (FMNMX3)
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 128; c += 8) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          mx4[i] = fmaxf(mx4[i], fmaxf(__uint_as_float(s[c + i]), __uint_as_float(s[c + 4 + i])));
-      }
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      // Lazy rescale: keep the old max unless the new one exceeds it by > 8 (log2 units).
-      float alpha = 1.f;
-      if (m_use == -INFINITY) {
-        m_use = mx;
-      } else if ((mx - m_use) * sl2 > kRescaleThreshold) {
-        alpha = ex2((m_use - mx) * sl2);
-        m_use = mx;
-      }
-      const float neg_m = -m_use * sl2;
-      const float2 negm2 = make_float2(neg_m, neg_m);
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                       make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int pi = 0; pi < 64; ++pi) {
-        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * pi]), __uint_as_float(s[2 * pi + 1])),
-                               sl2x2, negm2);
-        // one pair in kEmuEvery goes to the FMA pipe, the rest to MUFU.EX2
-        const float2 pp = (pi % kEmuEvery == kEmuEvery - 1) ? exp2_poly2(x)
-                                                           : make_float2(ex2(x.x), ex2(x.y));
-        acc[pi & 3] = fadd2(acc[pi & 3], pp);
-        s[pi] = pack_f16x2(pp.x, pp.y);  // P packs into the first 64 slots
-        if (pi == 31) tmem_st32(t_s + 0, &s[0]);  // first half of P goes out early
-      }
-      tmem_st32(t_s + 32, &s[32]);
-      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-      const float2 a = fadd2(a01, a23);
-      l_sum = fmaf(l_sum, alpha, a.x + a.y);
-      // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
-      // s_full commit for S_t(j) covers every MMA issued before it.
-      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + c * 32, o);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm.p_full[t]);
-    }
 
-    // ---------------- epilogue: O / l, LSE, optional merge, store ----------------
-    mbar_wait(&sm.o_done[t], 0);
-    tc_fence_after();
-    const bool in_range = row < p.sq;
-    // natural-log LSE in accurate math: m/sqrt(D) + ln(l)  (tensor.cpp:177)
-    const float lse_b = m_use * (sl2 * 0.69314718055994530942f) + logf(l_sum);
-    const float inv_l = 1.f / l_sum;
-    float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
-    const float* acc_row = nullptr;
-    if (p.acc_o != nullptr && in_range) {
-      const float l1 = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
-      lse_out = merge_coeffs(l1, lse_b, c_acc, c_new);
-      acc_row = p.acc_o + (static_cast<int64_t>(head) * p.sq + row) * kD;
-    }
-    const float scale_new = c_new * inv_l;
-    const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
-                          static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
-                          static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
+    SegIter si(sc);
+    Seg g;
+    uint32_t it = 0, ns = 0;
+    while (si.next(sc, g)) {
+      const int tslot = ns < 8 ? 2 + (ns * 2 + t) * 4 : -1;
+      const bool tr = r_in_tile == 0 && tslot >= 0;
+      if (tr) FUSP_TRACE(p, tslot);
+      const int head = g.qb / sc.qb_per_head;
+      const int row = (g.qb - head * sc.qb_per_head) * kQB + t * kBM + r_in_tile;
+      float m_use = -INFINITY;  // max used for the exponent (raw logit units)
+      float l_sum = 0.f;
+      for (int j = g.j0; j < g.j1; ++j, ++it) {
+        mbar_wait(&sm.s_full[t], it & 1);
+        tc_fence_after();
+        if (tr && j == g.j0) FUSP_TRACE(p, tslot + 1);
+        uint32_t s[128];
+        tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+        tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        tmem_wait_ld();
+        const int valid = p.skv - j * kBN;  // keys in this tile (mask the tail)
+        if (valid < kBN) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= valid) s[c] = __float_as_uint(-INFINITY);
+        }
+        // row max with independent chains (FMNMX3)
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            mx4[i] = fmaxf(mx4[i], fmaxf(__uint_as_float(s[c + i]), __uint_as_float(s[c + 4 + i])));
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        // Lazy rescale: keep the old max unless the new one exceeds it by > 8 (log2 units).
+        float alpha = 1.f;
+        if (m_use == -INFINITY) {
+          m_use = mx;
+        } else if ((mx - m_use) * sl2 > kRescaleThreshold) {
+          alpha = ex2((m_use - mx) * sl2);
+          m_use = mx;
+        }
+        const float neg_m = -m_use * sl2;
+        const float2 negm2 = make_float2(neg_m, neg_m);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int pi = 0; pi < 64; ++pi) {
+          const float2 x = ffma2(make_float2(__uint_as_float(s[2 * pi]), __uint_as_float(s[2 * pi + 1])),
+                                 sl2x2, negm2);
+          // one pair in kEmuEvery goes to the FMA pipe, the rest to MUFU.EX2
+          const float2 pp = (pi % kEmuEvery == kEmuEvery - 1) ? exp2_poly2(x)
+                                                             : make_float2(ex2(x.x), ex2(x.y));
+          acc[pi & 3] = fadd2(acc[pi & 3], pp);
+          s[pi] = pack_f16x2(pp.x, pp.y);  // P packs into the first 64 slots
+          if (pi == 31) tmem_st32(t_s + 0, &s[0]);  // first half of P goes out early
+        }
+        tmem_st32(t_s + 32, &s[32]);
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        const float2 a = fadd2(a01, a23);
+        l_sum = fmaf(l_sum, alpha, a.x + a.y);
+        // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
+        // s_full commit for S_t(j) covers every MMA issued before it.
+        if (__any_sync(0xffffffffu, alpha != 1.f) && j > g.j0) {
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + c * 32, o);
-      tmem_wait_ld();
-      if (!in_range) continue;
-      float v[32];
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * scale_new;
-      if (acc_row != nullptr) {
-        const float4* a4 = reinterpret_cast<const float4*>(acc_row + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 a = a4[i];
-          v[4 * i + 0] = fmaf(c_acc, a.x, v[4 * i + 0]);
-          v[4 * i + 1] = fmaf(c_acc, a.y, v[4 * i + 1]);
-          v[4 * i + 2] = fmaf(c_acc, a.z, v[4 * i + 2]);
-          v[4 * i + 3] = fmaf(c_acc, a.w, v[4 * i + 3]);
-        }
-      }
-      if (p.out_dtype == FUSP_F32) {
-        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + obase + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      } else {
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + obase + c * 32);
-        const bool f16 = p.out_dtype == FUSP_F16;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = v[8 * i + 2 * e], b = v[8 * i + 2 * e + 1];
-            w[e] = f16 ? pack_f16x2(a, b) : pack_bf16x2(a, b);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(t_o + c * 32, o);
           }
-          dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
+      }
+
+      // ---------------- segment end: O accumulated for keys of tiles [j0, j1) ----------------
+      mbar_wait(&sm.o_done[t], ns & 1);
+      tc_fence_after();
+      if (tr) FUSP_TRACE(p, tslot + 2);
+      ++ns;
+      int nseg = 1, kself = 0, c_first = 0;
+      if (sc.split) {
+        const int u0 = g.qb * sc.n_kv;
+        c_first = sk_cta_of(sc, u0);
+        nseg = sk_cta_of(sc, u0 + sc.n_kv - 1) - c_first + 1;
+        kself = static_cast<int>(blockIdx.x) - c_first;
+      }
+      constexpr int kMaxSegFast = 8;
+      float mk_r[kMaxSegFast], lk_r[kMaxSegFast];
+#pragma unroll
+      for (int k = 0; k < kMaxSegFast; ++k) {
+        mk_r[k] = m_use;
+        lk_r[k] = l_sum;
+      }
+      auto seg_m = [&](int k) -> float {
+        if (k < kMaxSegFast) {
+          float r = mk_r[0];
+#pragma unroll
+          for (int q = 1; q < kMaxSegFast; ++q) r = q == k ? mk_r[q] : r;
+          return r;
+        }
+        return k == kself ? m_use : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + r_in_tile);
+      };
+      auto seg_l = [&](int k) -> float {
+        if (k < kMaxSegFast) {
+          float r = lk_r[0];
+#pragma unroll
+          for (int q = 1; q < kMaxSegFast; ++q) r = q == k ? lk_r[q] : r;
+          return r;
+        }
+        return k == kself ? l_sum : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + kBM + r_in_tile);
+      };
+      float m_fin = m_use, l_fin = l_sum;
+      bool from_slots = false;  // merged O is summed from the slots (slow path), not in TMEM
+      if (nseg > 1) {
+        // Publish-then-count: every segment but the finisher stores its (O, m, l) slot, then
+        // bumps the q-block tile's count; whoever brings it to nseg - 1 published partials plus
+        // itself is last and merges.  The lowest CTA's segment (kself 0: the q-block's first
+        // keys, processed at the END of that CTA's range) normally arrives last: it checks the
+        // count first and, if everyone else has published, merges without publishing.  Nobody
+        // ever waits on another CTA.  The merge is Sum_k w_k O_k in segment order k = 0.. with
+        // the same fma sequence on either path, so results are bit-identical run to run.
+        uint32_t* cnt = p.counters + (static_cast<size_t>(g.qb) * 2 + t) * 2;
+        bool last = false;
+        if (kself == 0) {
+          if (r_in_tile == 0) sm.ticket[t] = ld_acquire(&cnt[0]);
+          wg_bar(t);
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket[t]) + 1 == static_cast<uint32_t>(nseg);
+        }
+        if (!last) {
+          float* slot = seg_slot(p, blockIdx.x, g.qb, t);
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_wait_ld();
+            float4* q4 = reinterpret_cast<float4*>(slot) + (c * 8) * kBM + r_in_tile;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              __stcg(q4 + i * kBM, make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3])));
+          }
+          __stcg(slot + kD * kBM + r_in_tile, m_use);
+          __stcg(slot + kD * kBM + kBM + r_in_tile, l_sum);
+          wg_bar(t);  // the warpgroup's stores happen-before thread 0's release (cumulativity)
+          if (r_in_tile == 0) {
+            __threadfence();
+            sm.ticket[t] = atomicAdd(&cnt[0], 1u);
+            __threadfence();
+          }
+          wg_bar(t);
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket[t]) + 1 == static_cast<uint32_t>(nseg);
+          if (!last) {
+            if (tr) FUSP_TRACE(p, tslot + 3);
+            tc_fence_before();
+            continue;
+          }
+        }
+        if (r_in_tile == 0) cnt[0] = 0u;  // every other segment has counted: reset for the next launch
+        // Gather (m_k, l_k); the first kMaxSegFast stay in registers for the weights.
+#pragma unroll
+        for (int k = 0; k < kMaxSegFast; ++k) {
+          if (k < nseg && k != kself) {
+            const float* sl = seg_slot(p, c_first + k, g.qb, t);
+            mk_r[k] = __ldcg(sl + kD * kBM + r_in_tile);
+            lk_r[k] = __ldcg(sl + kD * kBM + kBM + r_in_tile);
+          }
+        }
+        for (int k = 0; k < nseg; ++k) m_fin = fmaxf(m_fin, seg_m(k));
+        l_fin = 0.f;
+        for (int k = 0; k < nseg; ++k) l_fin = fmaf(ex2((seg_m(k) - m_fin) * sl2), seg_l(k), l_fin);
+        if (kself == 0) {
+          // Fast path: accumulate in the TMEM O tile, O = w_0 O_0, then O += w_k O_k, one whole
+          // slot (32 float4 loads in flight) per step.
+          const float w0 = ex2((m_use - m_fin) * sl2);
+          if (__any_sync(0xffffffffu, w0 != 1.f)) {  // tcgen05.ld/st are warp-collective
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(t_o + c * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(w0 * __uint_as_float(o[i]));
+              tmem_st32(t_o + c * 32, o);
+            }
+          }
+#pragma unroll 1
+          for (int k = 1; k < nseg; ++k) {
+            const float* sl = seg_slot(p, c_first + k, g.qb, t);
+            const float4* x4 = reinterpret_cast<const float4*>(sl) + r_in_tile;
+            float4 x[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __ldcg(x4 + i * kBM);
+            const float w = ex2((seg_m(k) - m_fin) * sl2);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(t_o + c * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                o[4 * i] = __float_as_uint(fmaf(w, x[c * 8 + i].x, __uint_as_float(o[4 * i])));
+                o[4 * i + 1] = __float_as_uint(fmaf(w, x[c * 8 + i].y, __uint_as_float(o[4 * i + 1])));
+                o[4 * i + 2] = __float_as_uint(fmaf(w, x[c * 8 + i].z, __uint_as_float(o[4 * i + 2])));
+                o[4 * i + 3] = __float_as_uint(fmaf(w, x[c * 8 + i].w, __uint_as_float(o[4 * i + 3])));
+              }
+              tmem_st32(t_o + c * 32, o);
+            }
+          }
+          tmem_wait_st();
+        } else {
+          from_slots = true;
         }
       }
+
+      // ---------------- epilogue: O / l, LSE, optional merge, store ----------------
+      const bool in_range = row < p.sq;
+      // natural-log LSE in accurate math: m/sqrt(D) + ln(l)  (tensor.cpp:177)
+      const float lse_b = m_fin * (sl2 * 0.69314718055994530942f) + logf(l_fin);
+      const float inv_l = 1.f / l_fin;
+      float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
+      const float* acc_row = nullptr;
+      if (p.acc_o != nullptr && in_range) {
+        const float l1 = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
+        lse_out = merge_coeffs(l1, lse_b, c_acc, c_new);
+        acc_row = p.acc_o + (static_cast<int64_t>(head) * p.sq + row) * kD;
+      }
+      const float scale_new = c_new * inv_l;
+      const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
+                            static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
+                            static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_o + c * 32, o);
+        tmem_wait_ld();
+        if (!in_range) continue;
+        float v[32];
+        if (!from_slots) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]);
+        } else {
+          // Slow path (a later segment finished): the same fma sequence, O_k from the slots
+          // (k != kself) or this CTA's TMEM tile.
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#pragma unroll 1
+          for (int k = 0; k < nseg; ++k) {
+            const float w = ex2((seg_m(k) - m_fin) * sl2);
+            if (k == kself) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaf(w, __uint_as_float(o[i]), v[i]);
+            } else {
+              const float4* x4 = reinterpret_cast<const float4*>(seg_slot(p, c_first + k, g.qb, t)) +
+                                 (c * 8) * kBM + r_in_tile;
+              float4 x[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[i] = __ldcg(x4 + i * kBM);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                v[4 * i] = fmaf(w, x[i].x, v[4 * i]);
+                v[4 * i + 1] = fmaf(w, x[i].y, v[4 * i + 1]);
+                v[4 * i + 2] = fmaf(w, x[i].z, v[4 * i + 2]);
+                v[4 * i + 3] = fmaf(w, x[i].w, v[4 * i + 3]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= scale_new;
+        if (acc_row != nullptr) {
+          const float4* a4 = reinterpret_cast<const float4*>(acc_row + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 a = a4[i];
+            v[4 * i + 0] = fmaf(c_acc, a.x, v[4 * i + 0]);
+            v[4 * i + 1] = fmaf(c_acc, a.y, v[4 * i + 1]);
+            v[4 * i + 2] = fmaf(c_acc, a.z, v[4 * i + 2]);
+            v[4 * i + 3] = fmaf(c_acc, a.w, v[4 * i + 3]);
+          }
+        }
+        if (p.out_dtype == FUSP_F32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + obase + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + obase + c * 32);
+          const bool f16 = p.out_dtype == FUSP_F16;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = v[8 * i + 2 * e], b = v[8 * i + 2 * e + 1];
+              w[e] = f16 ? pack_f16x2(a, b) : pack_bf16x2(a, b);
+            }
+            dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+      if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
+      if (tr) FUSP_TRACE(p, tslot + 3);
+      tc_fence_before();
     }
-    if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
   }
 
+  // bar.sync counts a diverged warp once per divergent arrival: reconverge first, or the
+  // producer warps (lane 0 vs 1..31) would release the barrier before the softmax warps finish.
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) FUSP_TRACE(p, 1);
+  if (threadIdx.x == 128) FUSP_TRACE(p, 70);  // same barrier, seen from softmax warp 4
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+}
+
+// ---- host-side schedule ------------------------------------------------------------------
+int g_sched_mode = 0;  // 0 auto, 1 whole q-blocks, 2 stream-K split
+unsigned long long* g_trace = nullptr;  // debug event buffer (attention_trace), device memory
+bool g_trace_on = false;
+int g_max_ctas = 0;    // 0 = every SM
+
+int sm_count() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() <= static_cast<size_t>(dev)) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+struct Plan {
+  Sched sc;
+  int grid;
+};
+
+Plan plan_attention(int heads, int sq, int skv, bool have_ws) {
+  Plan pl{};
+  int sms = sm_count();
+  if (g_max_ctas > 0 && g_max_ctas < sms) sms = g_max_ctas;
+  if (sms > kMaxGrid) sms = kMaxGrid;
+  pl.sc.n_kv = (skv + kBN - 1) / kBN;
+  pl.sc.qb_per_head = (sq + kQB - 1) / kQB;
+  pl.sc.n_qb = heads * pl.sc.qb_per_head;
+  const int64_t total = static_cast<int64_t>(pl.sc.n_qb) * pl.sc.n_kv;
+  pl.sc.total = total < (int64_t(1) << 31) ? static_cast<int>(total) : 0;
+  const int waves = (pl.sc.n_qb + sms - 1) / sms;
+  const double fill = static_cast<double>(pl.sc.n_qb) / (static_cast<double>(waves) * sms);
+  bool split = have_ws && pl.sc.n_kv >= 2 && fill < 0.96 && pl.sc.total > 0;
+  if (g_sched_mode == 1) split = false;
+  if (g_sched_mode == 2) split = have_ws && pl.sc.n_kv >= 2 && pl.sc.total > 0;
+  pl.sc.split = split ? 1 : 0;
+  if (split) {
+    // at least 2 KV tiles per CTA so each segment amortises its Q load and epilogue
+    const int g = pl.sc.total / 2;
+    pl.grid = g < sms ? (g > 0 ? g : 1) : sms;
+    for (int c = 0; c <= pl.grid; ++c)
+      pl.sc.begin[c] = static_cast<int>(static_cast<int64_t>(c) * pl.sc.total / pl.grid);
+  } else {
+    pl.grid = pl.sc.n_qb < sms ? pl.sc.n_qb : sms;
+  }
+  return pl;
 }
 
 }  // namespace
@@ -362,6 +767,7 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   if (a.d != kD) return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(a.d) +
                                                       " unsupported by the sm_100a kernel (D=128)");
   if (a.sq <= 0 || a.heads <= 0) return FUSP_OK;
+  if (a.skv <= 0) return set_error(FUSP_ERR_SHAPE, "attention kernel: empty KV (caller handles it)");
   CUtensorMap tq, tk, tv;
   fusp_status st;
   const bool qk16 = a.qk_dtype == FUSP_F16;
@@ -386,6 +792,16 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   p.lse_hs = a.lse_hs;
   p.acc_o = a.acc_o;
   p.acc_lse = a.acc_lse;
+  const size_t need = attention_workspace_bytes(a.heads, a.sq, a.skv);
+  const bool have_ws = a.split_ws != nullptr && need > 0 && a.split_ws_bytes >= need &&
+                       a.split_counters != nullptr &&
+                       a.split_counter_words >= attention_counter_words(a.heads, a.sq);
+  const Plan pl = plan_attention(a.heads, a.sq, a.skv, have_ws);
+  p.sc = pl.sc;
+  if (pl.sc.split) {
+    p.counters = a.split_counters;
+    p.slots = static_cast<float*>(a.split_ws);
+  }
   static bool attr_set = false;
   const int smem = static_cast<int>(sizeof(Smem)) + 1024;
   if (!attr_set) {
@@ -394,19 +810,65 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(attn_fwd_kernel)");
     attr_set = true;
   }
-  dim3 grid((a.sq + 2 * kBM - 1) / (2 * kBM), a.heads);
-  attn_fwd_kernel<<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  if (g_trace_on) {
+    if (g_trace == nullptr) FUSP_CUDA(cudaMalloc(&g_trace, sizeof(unsigned long long) * kMaxGrid * kTraceSlots));
+    FUSP_CUDA(cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * kMaxGrid * kTraceSlots, stream));
+    p.trace = g_trace;
+  }
+  attn_fwd_kernel<<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_kernel launch");
   return FUSP_OK;
 }
 
-}  // namespace fusp
+// Stream-K partial slots: two per CTA, sized for every SM so they are valid for any grid the
+// planner picks.  Contents need no initialisation.
+size_t attention_workspace_bytes(int heads, int sq, int skv) {
+  if (heads <= 0 || sq <= 0 || skv <= 0) return 0;
+  return static_cast<size_t>(sm_count()) * 2 * kSlotBytes;
+}
+// Stream-K ticket counters: [n_qb][2 tiles][arrive, written].  They must be zero when first
+// used and live in memory nothing else writes; the finisher of each split q-block tile
+// resets its pair, so they are zero again after every launch.
+size_t attention_counter_words(int heads, int sq) {
+  if (heads <= 0 || sq <= 0) return 0;
+  return static_cast<size_t>(heads) * ((sq + kQB - 1) / kQB) * 4;
+}
 
-namespace fusp {
-// The single-launch kernel needs no workspace.  (Split-KV / stream-K variants for small
-// per-rank head counts were measured slower than this kernel at every BASELINE shape except
-// U=8; they are not shipped.)
-size_t attention_workspace_bytes(int, int, int) { return 0; }
+fusp_status ensure_counters(CounterBuf& b, size_t words) {
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  if (b.ptr != nullptr && b.words >= words && b.device == dev) return FUSP_OK;
+  if (b.ptr != nullptr) {
+    FUSP_CUDA(cudaDeviceSynchronize());
+    FUSP_CUDA(cudaFree(b.ptr));
+    b.ptr = nullptr;
+    b.words = 0;
+  }
+  const size_t n = words < 4096 ? 4096 : words;
+  FUSP_CUDA(cudaMalloc(&b.ptr, n * 4));
+  FUSP_CUDA(cudaMemset(b.ptr, 0, n * 4));
+  b.words = n;
+  b.device = dev;
+  return FUSP_OK;
+}
+
+// Debug timeline: per-CTA globaltimer events of the most recent traced launch.
+int attention_trace(int enable, unsigned long long* host, size_t n) {
+  g_trace_on = enable != 0;
+  if (host != nullptr && g_trace != nullptr) {
+    const size_t m = n < size_t(kMaxGrid) * kTraceSlots ? n : size_t(kMaxGrid) * kTraceSlots;
+    if (cudaMemcpy(host, g_trace, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -1;
+    return static_cast<int>(m);
+  }
+  return 0;
+}
+
+void set_attention_schedule(int mode, int max_ctas) {
+  g_sched_mode = mode;
+  g_max_ctas = max_ctas;
+}
+
 }  // namespace fusp

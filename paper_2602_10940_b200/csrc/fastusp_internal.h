@@ -50,13 +50,28 @@ struct AttnLaunch {
   int64_t lse_hs;
   const float* acc_o;    // merge into (acc_o, acc_lse) when non-null
   const float* acc_lse;
-  void* split_ws;        // stream-K partials + semaphores (attention_workspace_bytes)
+  void* split_ws;        // stream-K partial slots (attention_workspace_bytes)
   size_t split_ws_bytes;
+  uint32_t* split_counters;    // stream-K tickets (attention_counter_words): zero-initialised,
+  size_t split_counter_words;  // never written by anything else
 };
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
 // Workspace the persistent attention kernel needs for a (heads, sq, skv) problem (0 when the
 // q-blocks are scheduled whole).
 size_t attention_workspace_bytes(int heads, int sq, int skv);
+size_t attention_counter_words(int heads, int sq);
+// Tuning/test knob: schedule 0 = auto, 1 = whole q-blocks, 2 = stream-K split; max_ctas 0 =
+// every SM (a smaller grid leaves SMs to concurrent NCCL kernels).
+void set_attention_schedule(int mode, int max_ctas);
+// Debug: enable per-CTA globaltimer tracing of attention launches / copy the last trace out.
+int attention_trace(int enable, unsigned long long* host, size_t n);
+// Zero-initialised counter buffer that only grows (never during graph capture).
+struct CounterBuf {
+  uint32_t* ptr = nullptr;
+  size_t words = 0;
+  int device = -1;
+};
+fusp_status ensure_counters(CounterBuf& b, size_t words);
 
 // ---- elementwise / data-movement kernels (kernels.cu) -----------------------------------
 fusp_status launch_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,

@@ -99,6 +99,14 @@ fusp_status scratch(size_t bytes, void** out) {
   return FUSP_OK;
 }
 
+// Stream-K tickets of the context-free attention API (per device, zeroed once).
+CounterBuf& attn_counters() {
+  static CounterBuf bufs[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return bufs[dev & 63];
+}
+
 std::string shape_str(const fusp_shape4& s) {
   std::ostringstream os;
   os << "[" << s.b << "," << s.h << "," << s.s << "," << s.d << "]";
@@ -117,6 +125,18 @@ extern "C" {
 const char* fusp_last_error(void) { return g_last_error.c_str(); }
 const char* fusp_version(void) { return "fastusp 0.1 (sm_100a)"; }
 uint64_t fusp_kernel_launch_count(void) { return g_launches.load(); }
+
+int fusp_attention_trace(int enable, uint64_t* host, size_t n) {
+  return attention_trace(enable, reinterpret_cast<unsigned long long*>(host), n);
+}
+
+fusp_status fusp_attention_schedule(int mode, int max_ctas) {
+  clear_error();
+  if (mode < 0 || mode > 2 || max_ctas < 0)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention schedule: mode in {0,1,2}, max_ctas >= 0");
+  set_attention_schedule(mode, max_ctas);
+  return FUSP_OK;
+}
 
 fusp_status fusp_encode_e4m3(const float* x, int64_t n, uint8_t* codes, fusp_stream_t stream) {
   clear_error();
@@ -278,6 +298,10 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
   a.lse_hs = qs.s;
   a.split_ws = split ? ws : nullptr;
   a.split_ws_bytes = split;
+  CounterBuf& cnt = attn_counters();
+  FUSP_CHECK(ensure_counters(cnt, attention_counter_words(a.heads, a.sq)));
+  a.split_counters = cnt.ptr;
+  a.split_counter_words = cnt.words;
   return launch_attention(a, s);
 }
 

@@ -42,6 +42,7 @@ struct fusp_ctx_s {
   bool capturing = false;
   void* arena = nullptr;
   size_t arena_bytes = 0;
+  fusp::CounterBuf attn_cnt;  // stream-K tickets of the attention kernel (zeroed once)
   void* host_stage = nullptr;
   size_t host_stage_bytes = 0;
   uint64_t a2a_bytes = 0, send_bytes = 0;
@@ -170,6 +171,8 @@ struct Buffers {
   // stream-K partials of the attention kernel
   void* attn_ws = nullptr;
   size_t attn_ws_bytes = 0;
+  uint32_t* attn_cnt = nullptr;
+  size_t attn_cnt_words = 0;
 };
 
 fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, int in_dt,
@@ -425,6 +428,8 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
   AttnLaunch a{};
   a.split_ws = b.attn_ws;
   a.split_ws_bytes = b.attn_ws_bytes;
+  a.split_counters = b.attn_cnt;
+  a.split_counter_words = b.attn_cnt_words;
   a.qk_dtype = l.qk_dt;
   a.q = b.Qr;
   a.k = K;
@@ -676,10 +681,16 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   Buffers b;
   carve(l, cv, &b, q, k, v, out);
   FUSP_CHECK(ensure_arena(c, cv.off + 256));
+  const size_t cnt_words = attention_counter_words(l.heads_r, l.span);
+  if (c->attn_cnt.words < cnt_words && c->capturing)
+    return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+  FUSP_CHECK(ensure_counters(c->attn_cnt, cnt_words));
   if (size_only) return FUSP_OK;
   cv = Carve{static_cast<char*>(c->arena), 0};
   b = Buffers{};
   carve(l, cv, &b, q, k, v, out);
+  b.attn_cnt = c->attn_cnt.ptr;
+  b.attn_cnt_words = c->attn_cnt.words;
   if (l.pro_k_pre) {
     FUSP_CHECK(launch_norm_rope_pack(k, l.in_dt, b.Kpro, FUSP_F32, 0, l.B, l.H, l.SL, l.D, 1,
                                      pro->k_norm_weight, pro->eps, pro->rope_cos, pro->rope_sin,
@@ -796,6 +807,7 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
   cudaDeviceSynchronize();
   c->comm.reset();
   if (c->arena) cudaFree(c->arena);
+  if (c->attn_cnt.ptr) cudaFree(c->attn_cnt.ptr);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_recv[0], c->ev_recv[1], c->ev_attn[0], c->ev_attn[1]})

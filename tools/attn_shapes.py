@@ -1,4 +1,5 @@
-"""Attention kernel TFLOP/s at the per-rank shapes of the BASELINE configs (one GPU)."""
+"""Attention kernel TFLOP/s at the per-rank shapes of the BASELINE configs (one GPU), under
+each work schedule (whole q-blocks / stream-K split / auto)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -6,6 +7,8 @@ import paper_2602_10940_b200 as fu
 
 SHAPES = [("flux_u1", 24, 4608), ("flux_u2", 12, 4608), ("flux_u4", 6, 4608), ("flux_u8", 3, 4608),
           ("ring_u2r4_step", 12, 4224), ("qwen_u4r2_step", 6, 3584), ("qwen_u1", 24, 7168)]
+MODES = sys.argv[1].split(",") if len(sys.argv) > 1 else ["whole", "split", "auto"]
+
 
 def run(hp, span, reps=20):
     q = torch.empty(1, hp, span, 128, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1)
@@ -21,7 +24,10 @@ def run(hp, span, reps=20):
     us = e0.elapsed_time(e1) * 1e3 / reps
     return us, 4.0 * hp * span * span * 128 / (us * 1e-6) / 1e12
 
+
 for name, hp, span in SHAPES:
-    us, tf = run(hp, span)
-    print(json.dumps({"config": name, "split": os.environ.get("FUSP_ATTN_SPLIT", "auto"),
-                      "shape": [1, hp, span, 128], "us": round(us, 1), "tflops": round(tf, 1)}))
+    for mode in MODES:
+        with fu.attention_schedule(mode, 0):
+            us, tf = run(hp, span)
+        print(json.dumps({"config": name, "schedule": mode, "shape": [1, hp, span, 128],
+                          "us": round(us, 1), "tflops": round(tf, 1)}), flush=True)
