@@ -562,14 +562,21 @@ def ring_attention_pipelined(ctx, q, k, v, group=None, opts=None) -> AttnResult:
 
 
 def usp_attention_host(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
-                       opts: Optional[CommOptions] = None):
-    """usp_attention on HOST tensors (H2D, layer, D2H inside one C-ABI call)."""
+                       opts: Optional[CommOptions] = None, out=None):
+    """usp_attention on HOST tensors (H2D, layer, D2H inside one C-ABI call, pipelined over
+    head chunks).  Pinned q/k/v/out overlap the copies with the compute; `out` may be a
+    preallocated host tensor of the output dtype (default: a new pinned one)."""
     opts = opts or CommOptions()
     if q.is_cuda:
         raise InvalidArgument(4, "usp_attention_host expects host tensors")
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     _check_local(q, k, v, "usp")
-    out = torch.empty(q.shape, dtype=opts.out_dtype)
+    if out is None:
+        out = torch.empty(q.shape, dtype=opts.out_dtype, pin_memory=torch.cuda.is_available())
+    elif out.is_cuda or tuple(out.shape) != tuple(q.shape) or out.dtype != opts.out_dtype \
+            or not out.is_contiguous():
+        raise InvalidArgument(4, "usp_attention_host: out must be a contiguous host tensor "
+                                 f"{list(q.shape)} of {opts.out_dtype}")
     co = opts._c()
     check(lib().fusp_usp_attention_host(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
                                         _DT[q.dtype], _shape4(q), _ptr(out), ctypes.byref(co),

@@ -711,6 +711,7 @@ unsigned long long* g_trace = nullptr;  // debug event buffer (attention_trace),
 bool g_trace_on = false;
 int g_max_ctas = 0;    // 0 = every SM
 
+}  // namespace
 int sm_count() {
   static std::mutex mu;
   static std::vector<int> cache;
@@ -726,16 +727,18 @@ int sm_count() {
   }
   return cache[dev];
 }
+namespace {
 
 struct Plan {
   Sched sc;
   int grid;
 };
 
-Plan plan_attention(int heads, int sq, int skv, bool have_ws) {
+Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
   Plan pl{};
   int sms = sm_count();
   if (g_max_ctas > 0 && g_max_ctas < sms) sms = g_max_ctas;
+  if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
   if (sms > kMaxGrid) sms = kMaxGrid;
   pl.sc.n_kv = (skv + kBN - 1) / kBN;
   pl.sc.qb_per_head = (sq + kQB - 1) / kQB;
@@ -796,7 +799,7 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   const bool have_ws = a.split_ws != nullptr && need > 0 && a.split_ws_bytes >= need &&
                        a.split_counters != nullptr &&
                        a.split_counter_words >= attention_counter_words(a.heads, a.sq);
-  const Plan pl = plan_attention(a.heads, a.sq, a.skv, have_ws);
+  const Plan pl = plan_attention(a.heads, a.sq, a.skv, have_ws, a.max_ctas);
   p.sc = pl.sc;
   if (pl.sc.split) {
     p.counters = a.split_counters;

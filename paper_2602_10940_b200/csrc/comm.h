@@ -15,6 +15,7 @@
 //                  single B200.
 // All operations are stream-ordered: they enqueue on the given stream and return.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -50,6 +51,9 @@ class Comm {
   virtual fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                                     const size_t* bytes, int nparts, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;
+  // SMs a transfer in flight occupies (its kernels must find free SMs while the persistent
+  // attention kernel runs beside it): NCCL p2p kernels need some, copy engines none.
+  virtual int sms_in_flight() const { return 0; }
 };
 
 // ---- in-process fabric -------------------------------------------------------------------
@@ -112,6 +116,14 @@ class NcclComm : public Comm {
   fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                             const size_t* bytes, int nparts, cudaStream_t s) override;
   bool capturable() const override { return true; }
+  // FUSP_NCCL_SMS overrides; 8 covers the p2p channels NCCL uses for one send/recv pair.
+  int sms_in_flight() const override {
+    static const int n = [] {
+      const char* e = std::getenv("FUSP_NCCL_SMS");
+      return e ? std::atoi(e) : 8;
+    }();
+    return n;
+  }
   // Collective over the world: make sure sub-communicators for every group of the
   // (R,U) mesh exist (ncclCommSplit, color = ring / ulysses index).
   fusp_status ensure_mesh(int r);

@@ -54,12 +54,14 @@ struct AttnLaunch {
   size_t split_ws_bytes;
   uint32_t* split_counters;    // stream-K tickets (attention_counter_words): zero-initialised,
   size_t split_counter_words;  // never written by anything else
+  int max_ctas;  // persistent grid cap (0 = every SM): leaves SMs to a concurrent transfer
 };
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
 // Workspace the persistent attention kernel needs for a (heads, sq, skv) problem (0 when the
 // q-blocks are scheduled whole).
 size_t attention_workspace_bytes(int heads, int sq, int skv);
 size_t attention_counter_words(int heads, int sq);
+int sm_count();  // SMs of the current device (cached)
 // Tuning/test knob: schedule 0 = auto, 1 = whole q-blocks, 2 = stream-K split; max_ctas 0 =
 // every SM (a smaller grid leaves SMs to concurrent NCCL kernels).
 void set_attention_schedule(int mode, int max_ctas);

@@ -424,8 +424,9 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
 
 // ---------------------------------------------------------------- attention step
 fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* V, bool first,
-                   bool last, void* out, float* lse_out, cudaStream_t s) {
+                   bool last, void* out, float* lse_out, cudaStream_t s, int reserve_sms = 0) {
   AttnLaunch a{};
+  if (reserve_sms > 0) a.max_ctas = sm_count() - reserve_sms;
   a.split_ws = b.attn_ws;
   a.split_ws_bytes = b.attn_ws_bytes;
   a.split_counters = b.attn_cnt;
@@ -580,8 +581,10 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
   FUSP_CHECK(exchange(1, m));
   if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[1], m));
   FUSP_CUDA(cudaEventRecord(c->ev_recv[1], m));
+  // compute steps that run beside a transfer leave its SMs free (NCCL kernels need them)
+  const int reserve = c->comm->sms_in_flight();
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
-  FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s));
+  FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s, reserve));
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
   FUSP_CUDA(cudaEventRecord(c->ev_attn[0], s));
   for (int i = 1; i < R; ++i) {
@@ -597,7 +600,7 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     const void *K, *V;
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[i], s));
     FUSP_CHECK(operands(i, s, &K, &V));
-    FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s));
+    FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s, i < R - 1 ? reserve : 0));
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[i], s));
     FUSP_CUDA(cudaEventRecord(c->ev_attn[i % 2], s));
   }
@@ -975,29 +978,101 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
   FUSP_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int out_dt = opts ? opts->out_dtype : FUSP_F32;
-  const size_t n = size_t(ls.b * ls.h * ls.s * ls.d);
-  const size_t in_b = n * dtype_size(in_dtype), out_b = n * dtype_size(out_dt);
-  // device staging lives in its own allocation (the arena belongs to the layer)
-  static thread_local void* dstage = nullptr;
-  static thread_local size_t dstage_bytes = 0;
-  const size_t need = 3 * align_up(in_b, 256) + align_up(out_b, 256);
-  if (dstage_bytes < need) {
-    if (dstage) FUSP_CUDA(cudaFree(dstage));
-    FUSP_CUDA(cudaMalloc(&dstage, need));
-    dstage_bytes = need;
+  fusp_comm_options o{};
+  o.out_dtype = FUSP_F32;
+  if (opts) o = *opts;
+  const int out_dt = o.out_dtype;
+  // Validate the whole call first (shape / mesh errors as the unchunked layer reports them).
+  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, &o, s, true));
+  // Heads are independent through the whole layer, so the host path pipelines head chunks:
+  // H2D of chunk i+1 (copy stream) || layer on chunk i (caller's stream) || D2H of chunk i-1
+  // (second copy stream).  Chunks are a multiple of the Ulysses degree so every chunk is a
+  // valid USP layer; every rank picks the same chunking, so collectives stay matched.
+  const int U = c->world / (ring_dim > 0 ? ring_dim : 1);
+  int hc = static_cast<int>(ls.h);
+  for (int cand = U; cand <= ls.h; cand += U)
+    if (ls.h % cand == 0 && ls.h / cand <= 8) { hc = cand; break; }
+  const int nch = static_cast<int>(ls.h / hc);
+  const size_t esz_in = dtype_size(in_dtype), esz_out = dtype_size(out_dt);
+  const size_t head_elems = size_t(ls.s * ls.d);
+  const size_t chunk_in = size_t(ls.b) * hc * head_elems * esz_in;
+  const size_t chunk_out = size_t(ls.b) * hc * head_elems * esz_out;
+  // device staging (its own allocation: the arena belongs to the layer), two slots
+  struct Stage {
+    void* d = nullptr;
+    size_t bytes = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t in_ready[2], computed[2], out_done[2];
+    uint32_t* flag = nullptr;
+    int device = -1;
+  };
+  static thread_local Stage st;
+  if (st.device != c->device) {
+    st = Stage{};
+    FUSP_CUDA(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
+    FUSP_CUDA(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      FUSP_CUDA(cudaEventCreateWithFlags(&st.in_ready[i], cudaEventDisableTiming));
+      FUSP_CUDA(cudaEventCreateWithFlags(&st.computed[i], cudaEventDisableTiming));
+      FUSP_CUDA(cudaEventCreateWithFlags(&st.out_done[i], cudaEventDisableTiming));
+    }
+    FUSP_CUDA(cudaMalloc(&st.flag, 256));
+    st.device = c->device;
   }
-  char* d = static_cast<char*>(dstage);
-  void* dq = d;
-  void* dk = d + align_up(in_b, 256);
-  void* dv = d + 2 * align_up(in_b, 256);
-  void* dout = d + 3 * align_up(in_b, 256);
-  FUSP_CUDA(cudaMemcpyAsync(dq, q, in_b, cudaMemcpyHostToDevice, s));
-  FUSP_CUDA(cudaMemcpyAsync(dk, k, in_b, cudaMemcpyHostToDevice, s));
-  FUSP_CUDA(cudaMemcpyAsync(dv, v, in_b, cudaMemcpyHostToDevice, s));
-  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, dq, dk, dv, in_dtype, ls, dout, nullptr, opts, s));
-  FUSP_CUDA(cudaMemcpyAsync(out, dout, out_b, cudaMemcpyDeviceToHost, s));
+  const size_t slot = 3 * align_up(chunk_in, 256) + align_up(chunk_out, 256);
+  if (st.bytes < 2 * slot) {
+    if (st.d) FUSP_CUDA(cudaFree(st.d));
+    FUSP_CUDA(cudaMalloc(&st.d, 2 * slot));
+    st.bytes = 2 * slot;
+  }
+  const bool check = o.check_finite != 0;
+  o.check_finite = 0;  // checked per chunk on the device below, reported after the pipeline
+  if (check) FUSP_CUDA(cudaMemsetAsync(st.flag, 0, 4, s));
+  fusp_shape4 cs = ls;
+  cs.h = hc;
+  const size_t pitch_in = size_t(ls.h) * head_elems * esz_in, pitch_out = size_t(ls.h) * head_elems * esz_out;
+  FUSP_CUDA(cudaEventRecord(st.computed[0], s));  // order the copy streams after prior work
+  FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[0], 0));
+  for (int i = 0; i < nch; ++i) {
+    const int b = i % 2;
+    char* d = static_cast<char*>(st.d) + b * slot;
+    void* dq = d;
+    void* dk = d + align_up(chunk_in, 256);
+    void* dv = d + 2 * align_up(chunk_in, 256);
+    void* dout = d + 3 * align_up(chunk_in, 256);
+    const size_t off_in = size_t(i) * hc * head_elems * esz_in;
+    const size_t off_out = size_t(i) * hc * head_elems * esz_out;
+    // slot b's inputs were last read by the layer on chunk i-2
+    if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[b], 0));
+    const void* src[3] = {q, k, v};
+    void* dst[3] = {dq, dk, dv};
+    for (int t = 0; t < 3; ++t)
+      FUSP_CUDA(cudaMemcpy2DAsync(dst[t], chunk_in / ls.b, static_cast<const char*>(src[t]) + off_in,
+                                  pitch_in, chunk_in / ls.b, ls.b, cudaMemcpyHostToDevice, st.h2d));
+    FUSP_CUDA(cudaEventRecord(st.in_ready[b], st.h2d));
+    FUSP_CUDA(cudaStreamWaitEvent(s, st.in_ready[b], 0));
+    // slot b's output was last read by the D2H of chunk i-2
+    if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[b], 0));
+    if (check) {
+      const int64_t n = int64_t(ls.b) * hc * int64_t(head_elems);
+      FUSP_CHECK(launch_finite(dq, in_dtype, n, st.flag, s));
+      FUSP_CHECK(launch_finite(dk, in_dtype, n, st.flag, s));
+      FUSP_CHECK(launch_finite(dv, in_dtype, n, st.flag, s));
+    }
+    FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, dq, dk, dv, in_dtype, cs, dout, nullptr, &o, s));
+    FUSP_CUDA(cudaEventRecord(st.computed[b], s));
+    FUSP_CUDA(cudaStreamWaitEvent(st.d2h, st.computed[b], 0));
+    FUSP_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + off_out, pitch_out, dout, chunk_out / ls.b,
+                                chunk_out / ls.b, ls.b, cudaMemcpyDeviceToHost, st.d2h));
+    FUSP_CUDA(cudaEventRecord(st.out_done[b], st.d2h));
+  }
+  FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[(nch - 1) % 2], 0));
+  if (nch >= 2) FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[(nch - 2) % 2], 0));
+  uint32_t bad = 0;
+  if (check) FUSP_CUDA(cudaMemcpyAsync(&bad, st.flag, 4, cudaMemcpyDeviceToHost, s));
   FUSP_CUDA(cudaStreamSynchronize(s));
+  if (bad)  // check_local_qkv (protocols.cpp:102-104); the output is unspecified
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "usp: non-finite element in protocol input");
   return FUSP_OK;
 }
 
