@@ -33,10 +33,12 @@ def load(spec):
 
 variants = [load(s) for s in sys.argv[1:]]
 BF16, F16 = 2, 1
+VDT = BF16 if os.environ.get("VDT") == "bf16" else F16  # V dtype handed to the kernel
 for name, hp, s in SHAPES:
     q = torch.empty(1, hp, s, 128, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1)
     k = torch.empty_like(q).uniform_(-1, 1)
-    v = torch.empty(1, hp, s, 128, device="cuda", dtype=torch.float16).uniform_(-1, 1)
+    v = torch.empty(1, hp, s, 128, device="cuda",
+                    dtype=torch.bfloat16 if VDT == BF16 else torch.float16).uniform_(-1, 1)
     out = torch.empty(1, hp, s, 128, device="cuda", dtype=torch.float16)
     lse = torch.empty(1, hp, s, device="cuda", dtype=torch.float32)
     st = torch.cuda.current_stream().cuda_stream
@@ -44,7 +46,7 @@ for name, hp, s in SHAPES:
     times = {sp: [] for sp, _ in variants}
     for rnd in range(6):
         for sp, f in variants:
-            call = lambda: f(q.data_ptr(), k.data_ptr(), v.data_ptr(), BF16, F16, shp, s, out.data_ptr(),
+            call = lambda: f(q.data_ptr(), k.data_ptr(), v.data_ptr(), BF16, VDT, shp, s, out.data_ptr(),
                              F16, lse.data_ptr(), st)
             for _ in range(2):
                 assert call() == 0
