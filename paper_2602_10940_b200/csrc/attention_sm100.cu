@@ -119,7 +119,7 @@ struct Params {
   float* slots;          // split: [gridDim.x][2 (first/last segment)][2 tiles][kSlotTileFloats]
   unsigned long long* trace;  // optional per-CTA globaltimer events (attention_trace), or null
 };
-constexpr int kTraceSlots = 72;  // per CTA (SM cycles): start, end, then [8 segments][2 tiles][4 events]
+constexpr int kTraceSlots = 72;  // per CTA (SM cycles): start, end, [4 segments][2 tiles][8 events], 70: end (warp 4)
 
 __device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (per-CTA deltas)
   unsigned long long t;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Seg g;
     uint32_t it = 0, ns = 0;
     while (si.next(sc, g)) {
-      const int tslot = ns < 8 ? 2 + (ns * 2 + t) * 4 : -1;
+      const int tslot = ns < 4 ? 2 + (ns * 2 + t) * 8 : -1;
       const bool tr = r_in_tile == 0 && tslot >= 0;
       if (tr) FUSP_TRACE(p, tslot);
       const int head = g.qb / sc.qb_per_head;
@@ -472,43 +472,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         nseg = sk_cta_of(sc, u0 + sc.n_kv - 1) - c_first + 1;
         kself = static_cast<int>(blockIdx.x) - c_first;
       }
-      constexpr int kMaxSegFast = 8;
-      float mk_r[kMaxSegFast], lk_r[kMaxSegFast];
-#pragma unroll
-      for (int k = 0; k < kMaxSegFast; ++k) {
-        mk_r[k] = m_use;
-        lk_r[k] = l_sum;
-      }
-      auto seg_m = [&](int k) -> float {
-        if (k < kMaxSegFast) {
-          float r = mk_r[0];
-#pragma unroll
-          for (int q = 1; q < kMaxSegFast; ++q) r = q == k ? mk_r[q] : r;
-          return r;
-        }
-        return k == kself ? m_use : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + r_in_tile);
-      };
-      auto seg_l = [&](int k) -> float {
-        if (k < kMaxSegFast) {
-          float r = lk_r[0];
-#pragma unroll
-          for (int q = 1; q < kMaxSegFast; ++q) r = q == k ? lk_r[q] : r;
-          return r;
-        }
-        return k == kself ? l_sum : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + kBM + r_in_tile);
-      };
       float m_fin = m_use, l_fin = l_sum;
-      bool from_slots = false;  // merged O is summed from the slots (slow path), not in TMEM
       if (nseg > 1) {
         // Publish-then-count: every segment but the finisher stores its (O, m, l) slot, then
-        // bumps the q-block tile's count; whoever brings it to nseg - 1 published partials plus
-        // itself is last and merges.  The lowest CTA's segment (kself 0: the q-block's first
-        // keys, processed at the END of that CTA's range) normally arrives last: it checks the
-        // count first and, if everyone else has published, merges without publishing.  Nobody
-        // ever waits on another CTA.  The merge is Sum_k w_k O_k in segment order k = 0.. with
-        // the same fma sequence on either path, so results are bit-identical run to run.
+        // bumps the q-block tile's count; whoever brings it to nseg is last and merges.  The
+        // lowest CTA's segment (kself 0: the q-block's first keys, processed at the END of
+        // that CTA's range) checks the count first and, if every other segment has published,
+        // merges without publishing its own.  Nobody ever waits on another CTA.
+        // The merge accumulates in this tile's TMEM O: O = w_0 O_0, then O = fma(w_k, O_k, O)
+        // for k = 1.. in segment order -- the same fma sequence whichever CTA finishes, so
+        // results are bit-identical run to run.  Each step streams one whole 64 KB slot (32
+        // float4 loads per thread in flight) and does one TMEM read-modify-write.
         uint32_t* cnt = p.counters + (static_cast<size_t>(g.qb) * 2 + t) * 2;
-        bool last = false;
+        bool last = false, published = false;
         if (kself == 0) {
           if (r_in_tile == 0) sm.ticket[t] = ld_acquire(&cnt[0]);
           wg_bar(t);
@@ -529,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __stcg(slot + kD * kBM + r_in_tile, m_use);
           __stcg(slot + kD * kBM + kBM + r_in_tile, l_sum);
+          if (tr) FUSP_TRACE(p, tslot + 4);
           wg_bar(t);  // the warpgroup's stores happen-before thread 0's release (cumulativity)
           if (r_in_tile == 0) {
             __threadfence();
@@ -536,30 +513,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             __threadfence();
           }
           wg_bar(t);
+          published = true;
           last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket[t]) + 1 == static_cast<uint32_t>(nseg);
           if (!last) {
-            if (tr) FUSP_TRACE(p, tslot + 3);
+            if (tr) FUSP_TRACE(p, tslot + 7);
             tc_fence_before();
             continue;
           }
         }
-        if (r_in_tile == 0) cnt[0] = 0u;  // every other segment has counted: reset for the next launch
-        // Gather (m_k, l_k); the first kMaxSegFast stay in registers for the weights.
-#pragma unroll
-        for (int k = 0; k < kMaxSegFast; ++k) {
-          if (k < nseg && k != kself) {
-            const float* sl = seg_slot(p, c_first + k, g.qb, t);
-            mk_r[k] = __ldcg(sl + kD * kBM + r_in_tile);
-            lk_r[k] = __ldcg(sl + kD * kBM + kBM + r_in_tile);
-          }
+        if (tr) FUSP_TRACE(p, tslot + 3);
+        if (r_in_tile == 0) cnt[0] = 0u;  // every segment has counted: reset for the next launch
+        // (m_k, l_k) of every segment (own values for k == kself when unpublished)
+        m_fin = -INFINITY;
+        for (int k = 0; k < nseg; ++k) {
+          const float mk = (k == kself && !published) ? m_use
+                                                      : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + r_in_tile);
+          m_fin = fmaxf(m_fin, mk);
         }
-        for (int k = 0; k < nseg; ++k) m_fin = fmaxf(m_fin, seg_m(k));
         l_fin = 0.f;
-        for (int k = 0; k < nseg; ++k) l_fin = fmaf(ex2((seg_m(k) - m_fin) * sl2), seg_l(k), l_fin);
-        if (kself == 0) {
-          // Fast path: accumulate in the TMEM O tile, O = w_0 O_0, then O += w_k O_k, one whole
-          // slot (32 float4 loads in flight) per step.
-          const float w0 = ex2((m_use - m_fin) * sl2);
+        for (int k = 0; k < nseg; ++k) {
+          float mk = m_use, lk = l_sum;
+          if (k != kself || published) {
+            const float* sl = seg_slot(p, c_first + k, g.qb, t);
+            mk = __ldcg(sl + kD * kBM + r_in_tile);
+            lk = __ldcg(sl + kD * kBM + kBM + r_in_tile);
+          }
+          l_fin = fmaf(ex2((mk - m_fin) * sl2), lk, l_fin);
+        }
+        if (tr) FUSP_TRACE(p, tslot + 5);
+        // k = 0 term: own TMEM tile scaled in place (fast path), or slot 0 stored over it
+        const float w0 = ex2(((published ? __ldcg(seg_slot(p, c_first, g.qb, t) + kD * kBM + r_in_tile)
+                                         : m_use) - m_fin) * sl2);
+        if (!published) {
           if (__any_sync(0xffffffffu, w0 != 1.f)) {  // tcgen05.ld/st are warp-collective
 #pragma unroll 1
             for (int c = 0; c < 4; ++c) {
@@ -571,33 +556,50 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_st32(t_o + c * 32, o);
             }
           }
-#pragma unroll 1
-          for (int k = 1; k < nseg; ++k) {
-            const float* sl = seg_slot(p, c_first + k, g.qb, t);
-            const float4* x4 = reinterpret_cast<const float4*>(sl) + r_in_tile;
-            float4 x[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = __ldcg(x4 + i * kBM);
-            const float w = ex2((seg_m(k) - m_fin) * sl2);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t o[32];
-              tmem_ld32(t_o + c * 32, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                o[4 * i] = __float_as_uint(fmaf(w, x[c * 8 + i].x, __uint_as_float(o[4 * i])));
-                o[4 * i + 1] = __float_as_uint(fmaf(w, x[c * 8 + i].y, __uint_as_float(o[4 * i + 1])));
-                o[4 * i + 2] = __float_as_uint(fmaf(w, x[c * 8 + i].z, __uint_as_float(o[4 * i + 2])));
-                o[4 * i + 3] = __float_as_uint(fmaf(w, x[c * 8 + i].w, __uint_as_float(o[4 * i + 3])));
-              }
-              tmem_st32(t_o + c * 32, o);
-            }
-          }
-          tmem_wait_st();
         } else {
-          from_slots = true;
+          const float4* x4 = reinterpret_cast<const float4*>(seg_slot(p, c_first, g.qb, t)) + r_in_tile;
+          float4 x[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = __ldcg(x4 + i * kBM);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              o[4 * i] = __float_as_uint(w0 * x[c * 8 + i].x);
+              o[4 * i + 1] = __float_as_uint(w0 * x[c * 8 + i].y);
+              o[4 * i + 2] = __float_as_uint(w0 * x[c * 8 + i].z);
+              o[4 * i + 3] = __float_as_uint(w0 * x[c * 8 + i].w);
+            }
+            tmem_st32(t_o + c * 32, o);
+          }
         }
+        // k >= 1 terms from the slots
+#pragma unroll 1
+        for (int k = 1; k < nseg; ++k) {
+          const float* sl = seg_slot(p, c_first + k, g.qb, t);
+          const float4* x4 = reinterpret_cast<const float4*>(sl) + r_in_tile;
+          float4 x[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = __ldcg(x4 + i * kBM);
+          const float w = ex2((__ldcg(sl + kD * kBM + r_in_tile) - m_fin) * sl2);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              o[4 * i] = __float_as_uint(fmaf(w, x[c * 8 + i].x, __uint_as_float(o[4 * i])));
+              o[4 * i + 1] = __float_as_uint(fmaf(w, x[c * 8 + i].y, __uint_as_float(o[4 * i + 1])));
+              o[4 * i + 2] = __float_as_uint(fmaf(w, x[c * 8 + i].z, __uint_as_float(o[4 * i + 2])));
+              o[4 * i + 3] = __float_as_uint(fmaf(w, x[c * 8 + i].w, __uint_as_float(o[4 * i + 3])));
+            }
+            tmem_st32(t_o + c * 32, o);
+          }
+        }
+        tmem_wait_st();
+        if (tr) FUSP_TRACE(p, tslot + 6);
       }
 
       // ---------------- epilogue: O / l, LSE, optional merge, store ----------------
@@ -623,36 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_ld();
         if (!in_range) continue;
         float v[32];
-        if (!from_slots) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]);
-        } else {
-          // Slow path (a later segment finished): the same fma sequence, O_k from the slots
-          // (k != kself) or this CTA's TMEM tile.
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-#pragma unroll 1
-          for (int k = 0; k < nseg; ++k) {
-            const float w = ex2((seg_m(k) - m_fin) * sl2);
-            if (k == kself) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = fmaf(w, __uint_as_float(o[i]), v[i]);
-            } else {
-              const float4* x4 = reinterpret_cast<const float4*>(seg_slot(p, c_first + k, g.qb, t)) +
-                                 (c * 8) * kBM + r_in_tile;
-              float4 x[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) x[i] = __ldcg(x4 + i * kBM);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                v[4 * i] = fmaf(w, x[i].x, v[4 * i]);
-                v[4 * i + 1] = fmaf(w, x[i].y, v[4 * i + 1]);
-                v[4 * i + 2] = fmaf(w, x[i].z, v[4 * i + 2]);
-                v[4 * i + 3] = fmaf(w, x[i].w, v[4 * i + 3]);
-              }
-            }
-          }
-        }
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]);
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] *= scale_new;
         if (acc_row != nullptr) {
@@ -687,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
-      if (tr) FUSP_TRACE(p, tslot + 3);
+      if (tr) FUSP_TRACE(p, tslot + 7);
       tc_fence_before();
     }
   }

@@ -28,23 +28,28 @@ print(f"{len(ctas)} CTAs; longest CTA {us(max(max(tr[c,1], tr[c,70]) for c in ct
 # the later of the two end stamps (slot 70 = softmax warp 4 after the same barrier)
 ends = sorted(us(max(tr[c, 1], tr[c, 70])) for c in ctas)
 print(f"CTA end: min {ends[0]:.1f} median {ends[len(ends)//2]:.1f} max {ends[-1]:.1f}")
-agg = {"first_S": [], "compute": [], "epilogue": [], "gap": []}
+NAMES = ["start", "S", "O", "fin", "pub", "ml", "merged", "E"]
+agg = {k: [] for k in ("first_S", "compute", "publish", "fin_wait", "gather", "merge", "final_store")}
 for c in ctas[: int(os.environ.get("SHOW", "6"))]:
-    line = [f"cta{c:3d} start {us(tr[c,0]):6.1f}"]
-    for sgi in range(8):
+    line = [f"cta{c:3d}"]
+    for sgi in range(4):
         for t in range(2):
-            b = 2 + (sgi * 2 + t) * 4
-            if tr[c, b] == 0: continue
-            e = [us(x) for x in tr[c, b:b + 4]]
-            line.append(f"s{sgi}t{t}[{e[0]:.1f} S{e[1]:.1f} O{e[2]:.1f} E{e[3]:.1f}]")
-    line.append(f"end {us(tr[c,1]):.1f} end(w4) {us(tr[c,70]):.1f}")
+            b = 2 + (sgi * 2 + t) * 8
+            if tr[c, b] == 0 and sgi > 0: continue
+            e = tr[c, b:b + 8]
+            line.append(f"s{sgi}t{t}[" + " ".join(f"{n}{us(x):.1f}" for n, x in zip(NAMES, e) if x) + "]")
+    line.append(f"end {us(max(tr[c,1], tr[c,70])):.1f}")
     print(" ".join(line))
 for c in ctas:
-    prev_end = None
-    for sgi in range(8):
-        b = 2 + (sgi * 2) * 4
-        if tr[c, b] == 0: continue
-        e = tr[c, b:b + 4] / (GHZ * 1e3)
-        agg["first_S"].append(e[1] - e[0]); agg["compute"].append(e[2] - e[1]); agg["epilogue"].append(e[3] - e[2])
+    for sgi in range(4):
+        b = 2 + (sgi * 2) * 8
+        if tr[c, b + 2] == 0: continue
+        e = tr[c, b:b + 8] / (GHZ * 1e3)
+        agg["first_S"].append(e[1] - e[0]); agg["compute"].append(e[2] - e[1])
+        if e[4]: agg["publish"].append(e[4] - e[2])
+        if e[3]: agg["fin_wait"].append(e[3] - (e[4] if e[4] else e[2]))
+        if e[5] and e[3]: agg["gather"].append(e[5] - e[3])
+        if e[6] and e[5]: agg["merge"].append(e[6] - e[5])
+        agg["final_store"].append(e[7] - (e[6] if e[6] else e[2]))
 for k2, vals in agg.items():
-    if vals: print(f"{k2:9s} n={len(vals)} median {statistics.median(vals):.2f} us  max {max(vals):.2f} us  sum/CTA {sum(vals)/len(ctas):.2f} us")
+    if vals: print(f"{k2:11s} n={len(vals)} median {statistics.median(vals):.2f} us  max {max(vals):.2f} us")
