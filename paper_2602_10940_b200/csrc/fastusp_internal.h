@@ -105,8 +105,22 @@ struct PackDesc {
   int64_t scale_bh_stride;  // 0: one tensor-wide scale; 1: one scale per (b,h) slab
 };
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
+// Up to 6 packs / unpacks with one launch (same B, H, SL, D, U; else one launch each).
+fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s);
 // Fused QK RMSNorm (w != null) + interleaved RoPE (cosv != null, rows pos0 + s) + pack into
 // slot t = h / (H/u) at t * slot_stride elements (u = 1: plain [B][H][SL][D] output).
+// One operand of a batched prologue pack (w / cos / sin null = that step skipped).
+struct ProPack {
+  const void* src;
+  void* dst;
+  const float* w;
+  const float* cosv;
+  const float* sinv;
+  int sdt, ddt;
+};
+fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_stride, int b,
+                                        int h, int sl, int d, int u, float eps, int64_t pos0,
+                                        cudaStream_t s);
 fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
                                   int64_t slot_stride, int b, int h, int sl, int d, int u,
                                   const float* w, float eps, const float* cosv, const float* sinv,
@@ -125,6 +139,7 @@ struct UnpackDesc {
   int b, hp, sl, d, u;
 };
 fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s);
+fusp_status launch_unpack_multi(const UnpackDesc* us, int n, cudaStream_t s);
 // Output unpack for B>1: src slots [U][B][hp][SL][D] -> dst [B][H][SL][D].
 fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst, int dtype, int b,
                                 int hp, int sl, int d, int u, cudaStream_t s);
@@ -150,6 +165,10 @@ fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_e
 fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elems, uint32_t* work,
                                 float* scales, uint8_t* codes, uint32_t* nonfinite,
                                 cudaStream_t s);
+// K and V (parts = 2) quantized with one amax launch and one quantize launch.
+fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
+                                      uint32_t* const* work, float* const* scales,
+                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s);
 fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
                                      int64_t n, void* y, int ydt, cudaStream_t s);
 fusp_status launch_scatter_slot_scales(const float* scales, float* base, int64_t slot_stride_f,

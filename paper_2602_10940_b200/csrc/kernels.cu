@@ -17,7 +17,7 @@ namespace {
 constexpr int kSMs = 148;
 constexpr int kBlock = 256;
 
-inline int grid_for(int64_t work_items, int per_sm = 8) {
+inline int grid_for(int64_t work_items, int per_sm = 8) {  // grid-stride kernels
   int64_t g = (work_items + kBlock - 1) / kBlock;
   if (g > int64_t(kSMs) * per_sm) g = int64_t(kSMs) * per_sm;
   return g < 1 ? 1 : static_cast<int>(g);
@@ -428,6 +428,343 @@ __global__ void finite_kernel(const void* __restrict__ x, int dt, int64_t n, uin
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
+
+// ---- 16-byte-vector movers (the Ulysses pack / unpack and the FP8 passes) -----------------
+// One (b,h) slab of a [B][H][SL][D] tensor is SL*D contiguous elements in the source and in
+// its destination slot, so the copies are slab-to-slab: grid.y = slab, grid.z = tensor,
+// 32-bit offsets inside the slab, no per-element index arithmetic.  8 elements per step.
+struct Vec8 {
+  float f[8];
+};
+__device__ __forceinline__ Vec8 load8(const void* base, int dt, int64_t i) {
+  Vec8 v;
+  if (dt == FUSP_F32) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + i);
+    const float4 a = __ldg(p), b = __ldg(p + 1);
+    v.f[0] = a.x; v.f[1] = a.y; v.f[2] = a.z; v.f[3] = a.w;
+    v.f[4] = b.x; v.f[5] = b.y; v.f[6] = b.z; v.f[7] = b.w;
+  } else {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + i));
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 x;
+      if (dt == FUSP_F16) x = __half22float2(*reinterpret_cast<const __half2*>(&ww[e]));
+      else x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[e]));
+      v.f[2 * e] = x.x;
+      v.f[2 * e + 1] = x.y;
+    }
+  }
+  return v;
+}
+__device__ __forceinline__ void store8(void* base, int dt, int64_t i, const Vec8& v) {
+  if (dt == FUSP_F32) {
+    float4* p = reinterpret_cast<float4*>(static_cast<float*>(base) + i);
+    p[0] = make_float4(v.f[0], v.f[1], v.f[2], v.f[3]);
+    p[1] = make_float4(v.f[4], v.f[5], v.f[6], v.f[7]);
+    return;
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (dt == FUSP_F16) {
+      __half2 x = __floats2half2_rn(v.f[2 * e], v.f[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&x);
+    } else {
+      __nv_bfloat162 x = __floats2bfloat162_rn(v.f[2 * e], v.f[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&x);
+    }
+  }
+  *reinterpret_cast<uint4*>(static_cast<uint16_t*>(base) + i) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ uint32_t enc_pair(float a, float b) {  // (a -> low byte, b -> high)
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
+  uint32_t x = r;
+  if (isnan(a)) x = (x & 0xFF00u) | (signbit(a) ? 0xFFu : 0x7Fu);
+  if (isnan(b)) x = (x & 0x00FFu) | ((signbit(b) ? 0xFFu : 0x7Fu) << 8);
+  return x;
+}
+// RN(x / qs) as the E4M3 encoder sees it, bit-exact with IEEE division (fp8.cpp:121):
+// q = x * RN(1/qs) is within 2.5 f32 ulp of RN(x/qs), so it encodes identically unless
+// RN(x/qs) sits near an E4M3 rounding boundary -- the midpoint pattern 0x80000 in the low 20
+// mantissa bits (normal range), or anywhere in the E4M3 subnormal range (|q| < 2^-6).  Those
+// rare values take the exact division.  Above 448 everything saturates to 448 either way.
+__device__ __forceinline__ float qdiv(float x, float qs, float inv) {
+  const float q = x * inv;
+  const uint32_t b = __float_as_uint(q) & 0x7fffffffu;
+  if (b < 0x3c800000u || ((b & 0xFFFFFu) - 0x7FFF8u) < 16u) return __fdiv_rn(x, qs);
+  return q;
+}
+__device__ __forceinline__ uint2 encode8(const Vec8& v, float qs) {  // IEEE x / scale, RNE sat
+  const float inv = __frcp_rn(qs);
+  float q[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) q[e] = qdiv(v.f[e], qs, inv);
+  return make_uint2(enc_pair(q[0], q[1]) | (enc_pair(q[2], q[3]) << 16),
+                    enc_pair(q[4], q[5]) | (enc_pair(q[6], q[7]) << 16));
+}
+// Finite inputs only (the amax pass rejected non-finite ones): no NaN fix-ups.
+__device__ __forceinline__ uint32_t enc_pair_finite(float a, float b) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ uint2 encode8_finite(const Vec8& v, float qs, float inv) {
+  float q[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) q[e] = qdiv(v.f[e], qs, inv);
+  return make_uint2(enc_pair_finite(q[0], q[1]) | (enc_pair_finite(q[2], q[3]) << 16),
+                    enc_pair_finite(q[4], q[5]) | (enc_pair_finite(q[6], q[7]) << 16));
+}
+// 8 codes -> f32, exact: the hardware e4m3x2 -> f16x2 conversion is exact (every E4M3 value
+// is an f16; 0x7F / 0xFF -> NaN as in fp8.cpp:39-43), then f16 -> f32 and * scale (f32 RN).
+__device__ __forceinline__ void dec4(uint32_t w, float sc, float* f) {
+  uint32_t lo, hi;
+  asm("{\n\t.reg .b16 a, b;\n\tmov.b32 {a, b}, %2;\n\t"
+      "cvt.rn.f16x2.e4m3x2 %0, a;\n\tcvt.rn.f16x2.e4m3x2 %1, b;\n\t}"
+      : "=r"(lo), "=r"(hi) : "r"(w));
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&lo));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+  f[0] = __fmul_rn(a.x, sc);
+  f[1] = __fmul_rn(a.y, sc);
+  f[2] = __fmul_rn(b.x, sc);
+  f[3] = __fmul_rn(b.y, sc);
+}
+__device__ __forceinline__ Vec8 decode8(uint2 w, float sc) {
+  Vec8 v;
+  dec4(w.x, sc, v.f);
+  dec4(w.y, sc, v.f + 4);
+  return v;
+}
+
+constexpr int kMaxMoveOps = 6;  // tensors moved by one pack / unpack launch (grid.z)
+struct PackOp {
+  const void* src;
+  void* dst;
+  const float* scale;       // e4m3 destination: scale[slab * scale_bh_stride]
+  int64_t scale_bh_stride;
+  int64_t slot_stride;      // destination elements between slots
+  int sdt, ddt;
+};
+struct PackArgs {
+  PackOp op[kMaxMoveOps];
+  int h, hp, slab_vecs;  // slab_vecs = SL*D/8
+  int64_t slab_elems;
+};
+// Ulysses pack (protocols.cpp:143-153): slab (b, h) -> slot h / hp, position (b, h % hp).
+__global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ PackArgs a) {
+  const PackOp& o = a.op[blockIdx.z];
+  const int slab = blockIdx.y;
+  const int hh = slab % a.h, bb = slab / a.h;
+  const int t = hh / a.hp, hl = hh - t * a.hp;
+  const int64_t s0 = int64_t(slab) * a.slab_elems;
+  const int64_t d0 = int64_t(t) * o.slot_stride + (int64_t(bb) * a.hp + hl) * a.slab_elems;
+  const float qs = o.ddt == FUSP_E4M3 ? o.scale[slab * o.scale_bh_stride] : 1.f;
+  const int stride = gridDim.x * blockDim.x;
+  const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o.sdt == o.ddt && o.sdt != FUSP_F32) {  // same 16-bit type: 4 x 16 B in flight per thread
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(o.src) + s0);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o.dst) + d0);
+    for (int v = v0; v < a.slab_vecs; v += 4 * stride) {
+      uint4 x[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs) x[e] = __ldg(src + v + e * stride);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs) dst[v + e * stride] = x[e];
+    }
+    return;
+  }
+  for (int v = v0; v < a.slab_vecs; v += 4 * stride) {
+    Vec8 x[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (v + e * stride < a.slab_vecs) x[e] = load8(o.src, o.sdt, s0 + int64_t(v + e * stride) * 8);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (v + e * stride >= a.slab_vecs) break;
+      const int64_t i = int64_t(v + e * stride) * 8;
+      if (o.ddt == FUSP_E4M3)
+        *reinterpret_cast<uint2*>(static_cast<uint8_t*>(o.dst) + d0 + i) = encode8(x[e], qs);
+      else
+        store8(o.dst, o.ddt, d0 + i, x[e]);
+    }
+  }
+}
+
+struct UnpackOp {
+  const void* src;
+  void* dst;
+  const float* scales;  // e4m3 source: scales[j * scale_stride + bh * scale_bh_stride]
+  int64_t src_slot_stride, scale_stride, scale_bh_stride;
+  int sdt, ddt;
+};
+struct UnpackArgs {
+  UnpackOp op[kMaxMoveOps];
+  int bhp, sl, u, slab_vecs;  // bhp = B * hp
+  int64_t slab_elems;
+};
+// Ulysses unpack (protocols.cpp:163-179): slot j's slab bh -> rows [j*SL, (j+1)*SL) of slab bh.
+__global__ void __launch_bounds__(256) unpack_slab_kernel(const __grid_constant__ UnpackArgs a) {
+  const UnpackOp& o = a.op[blockIdx.z];
+  const int slab = blockIdx.y;
+  const int j = slab / a.bhp, bh = slab - j * a.bhp;
+  const int64_t s0 = int64_t(j) * o.src_slot_stride + int64_t(bh) * a.slab_elems;
+  const int64_t d0 = (int64_t(bh) * a.u + j) * a.slab_elems;
+  const float sc = o.sdt == FUSP_E4M3 ? o.scales[j * o.scale_stride + bh * o.scale_bh_stride] : 1.f;
+  const int stride = gridDim.x * blockDim.x;
+  const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o.sdt == o.ddt && (o.sdt == FUSP_F16 || o.sdt == FUSP_BF16)) {  // 4 x 16 B in flight
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(o.src) + s0);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o.dst) + d0);
+    for (int v = v0; v < a.slab_vecs; v += 4 * stride) {
+      uint4 x[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs) x[e] = __ldg(src + v + e * stride);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs) dst[v + e * stride] = x[e];
+    }
+    return;
+  }
+  if (o.sdt == FUSP_E4M3 && o.ddt != FUSP_E4M3) {  // dequantize: 4 x 8 codes in flight
+    for (int v = v0; v < a.slab_vecs; v += 4 * stride) {
+      uint2 c[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs)
+          c[e] = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(o.src) + s0 +
+                                                      int64_t(v + e * stride) * 8));
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (v + e * stride < a.slab_vecs) store8(o.dst, o.ddt, d0 + int64_t(v + e * stride) * 8, decode8(c[e], sc));
+    }
+    return;
+  }
+  for (int v = v0; v < a.slab_vecs; v += stride) {
+    const int64_t i = int64_t(v) * 8;
+    if (o.sdt == o.ddt) {
+      if (o.sdt == FUSP_E4M3)
+        *reinterpret_cast<uint2*>(static_cast<uint8_t*>(o.dst) + d0 + i) =
+            __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(o.src) + s0 + i));
+      else if (o.sdt == FUSP_F32)
+        store8(o.dst, FUSP_F32, d0 + i, load8(o.src, FUSP_F32, s0 + i));
+      else
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(o.dst) + d0 + i) =
+            __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(o.src) + s0 + i));
+      continue;
+    }
+    const Vec8 x = o.sdt == FUSP_E4M3
+                       ? decode8(__ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(o.src) + s0 + i)), sc)
+                       : load8(o.src, o.sdt, s0 + i);
+    store8(o.dst, o.ddt, d0 + i, x);
+  }
+}
+
+// Source value of 8 consecutive elements (one row segment) for the FP8 passes.
+__device__ __forceinline__ Vec8 src_vec8(const Fp8Src& s, int64_t i) {  // i < 2^31 (launcher)
+  if (s.dt != FUSP_E4M3) return load8(s.x, s.dt, i);
+  const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
+  const uint32_t bh = row / static_cast<uint32_t>(s.span);
+  const int r = static_cast<int>(row - bh * s.span);
+  const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
+  return decode8(__ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i)), sc);
+}
+
+// Pass 1 per block, 8 elements per step; grid.y = block, grid.z = tensor (K, V).
+struct AmaxArgs {
+  Fp8Src src[2];
+  uint32_t* amax[2];
+  int64_t block_vecs;
+  uint32_t* nonfinite;
+};
+__global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ AmaxArgs a) {
+  const Fp8Src& s = a.src[blockIdx.z];
+  const int64_t base = int64_t(blockIdx.y) * a.block_vecs;
+  float m = 0.f, nf = 0.f;
+  bool bad = false;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
+    Vec8 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + u * stride < a.block_vecs) x[u] = src_vec8(s, (base + v + u * stride) * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (v + u * stride >= a.block_vecs) break;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        nf = fmaf(x[u].f[e], 0.f, nf);  // stays 0 unless some element is inf / NaN
+        m = fmaxf(m, fabsf(x[u].f[e]));
+      }
+    }
+  }
+  bad = nf != 0.f;
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ float wm[kBlock / 32];
+  __shared__ int wb[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) {
+    wm[threadIdx.x >> 5] = m;
+    wb[threadIdx.x >> 5] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bm = 0.f;
+    int bb = 0;
+    for (int w = 0; w < kBlock / 32; ++w) {
+      bm = fmaxf(bm, wm[w]);
+      bb |= wb[w];
+    }
+    if (!(bm >= 0.f)) bm = 0.f;
+    atomicMax(&a.amax[blockIdx.z][blockIdx.y], __float_as_uint(bm));
+    if (bb && a.nonfinite) atomicOr(a.nonfinite, 1u);
+  }
+}
+
+// Pass 2: scale = amax/448 (1 if 0) per block, written by the block's first vector;
+// codes = encode(x / scale), IEEE division (fp8.cpp:119-121).
+struct QuantArgs {
+  Fp8Src src[2];
+  const uint32_t* amax[2];
+  float* scales[2];
+  uint8_t* codes[2];
+  int64_t block_vecs;
+};
+// grid.y = block, grid.z = part: the block's scale is computed once per CTA.
+__global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant__ QuantArgs a) {
+  const int z = blockIdx.z, blk = blockIdx.y;
+  const float am = __uint_as_float(a.amax[z][blk]);
+  const float qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;
+  const float inv = __frcp_rn(qs);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.scales[z]) a.scales[z][blk] = qs;
+  const int64_t base = int64_t(blk) * a.block_vecs;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
+    Vec8 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + u * stride < a.block_vecs) x[u] = src_vec8(a.src[z], (base + v + u * stride) * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + u * stride < a.block_vecs)
+        *reinterpret_cast<uint2*>(a.codes[z] + (base + v + u * stride) * 8) = encode8_finite(x[u], qs, inv);
+  }
+}
+
+__global__ void __launch_bounds__(256) dequantize_vec_kernel(const uint8_t* __restrict__ c,
+                                                             const float* __restrict__ scales,
+                                                             int64_t block_vecs, int64_t n_vecs,
+                                                             void* __restrict__ y, int ydt) {
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n_vecs;
+       v += int64_t(gridDim.x) * blockDim.x)
+    store8(y, ydt, v * 8, decode8(__ldg(reinterpret_cast<const uint2*>(c + v * 8)),
+                                  scales[static_cast<uint32_t>(v) / static_cast<uint32_t>(block_vecs)]));
+}
+
 }  // namespace
 
 size_t dtype_size(int dt) {
@@ -515,7 +852,91 @@ fusp_status launch_fill(void* p, int dt, int64_t n, float v, cudaStream_t s) {
   return FUSP_OK;
 }
 
-fusp_status launch_pack(const PackDesc& p, cudaStream_t s) {
+fusp_status launch_pack_generic(const PackDesc& p, cudaStream_t s);
+fusp_status launch_unpack_generic(const UnpackDesc& p, cudaStream_t s);
+namespace {
+bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+int slab_grid_x(int64_t slab_vecs, int64_t slabs) {
+  // enough CTAs per slab to cover it once with 4 vectors per thread, capped near 16
+  // resident CTAs per SM overall
+  int64_t gx = (slab_vecs + 4 * kBlock - 1) / (4 * kBlock);
+  const int64_t cap = (int64_t(kSMs) * 16 + slabs - 1) / slabs;
+  if (gx > cap) gx = cap;
+  return gx < 1 ? 1 : static_cast<int>(gx);
+}
+}  // namespace
+
+fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s) {
+  if (n <= 0) return FUSP_OK;
+  const PackDesc& p0 = ps[0];
+  const int64_t slab_elems = int64_t(p0.sl) * p0.d;
+  const int64_t slabs = int64_t(p0.b) * p0.h;
+  bool fast = n <= kMaxMoveOps && p0.d % 8 == 0 && p0.h % p0.u == 0 && slabs <= 65535 &&
+              slab_elems / 8 < (int64_t(1) << 31);
+  for (int i = 0; i < n && fast; ++i) {
+    const PackDesc& p = ps[i];
+    fast = p.b == p0.b && p.h == p0.h && p.sl == p0.sl && p.d == p0.d && p.u == p0.u &&
+           aligned16(p.src) && aligned16(p.dst) && (p.dst_dtype != FUSP_E4M3 || p.dst_slot_stride % 16 == 0) &&
+           (p.dst_dtype == FUSP_E4M3 || (p.dst_slot_stride * int64_t(dtype_size(p.dst_dtype))) % 16 == 0) &&
+           p.src_dtype != FUSP_E4M3;
+  }
+  if (!fast) {
+    for (int i = 0; i < n; ++i) FUSP_CHECK(launch_pack_generic(ps[i], s));
+    return FUSP_OK;
+  }
+  if (slabs == 0 || slab_elems == 0) return FUSP_OK;
+  PackArgs a{};
+  for (int i = 0; i < n; ++i) {
+    a.op[i] = PackOp{ps[i].src, ps[i].dst, ps[i].scale, ps[i].scale_bh_stride, ps[i].dst_slot_stride,
+                     ps[i].src_dtype, ps[i].dst_dtype};
+  }
+  a.h = p0.h;
+  a.hp = p0.h / p0.u;
+  a.slab_vecs = static_cast<int>(slab_elems / 8);
+  a.slab_elems = slab_elems;
+  pack_slab_kernel<<<dim3(slab_grid_x(a.slab_vecs, slabs * n), static_cast<unsigned>(slabs), n),
+                     kBlock, 0, s>>>(a);
+  FUSP_LAUNCHED("pack_slab_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_unpack_multi(const UnpackDesc* us, int n, cudaStream_t s) {
+  if (n <= 0) return FUSP_OK;
+  const UnpackDesc& u0 = us[0];
+  const int64_t slab_elems = int64_t(u0.sl) * u0.d;
+  const int64_t slabs = int64_t(u0.u) * u0.b * u0.hp;
+  bool fast = n <= kMaxMoveOps && u0.d % 8 == 0 && slabs <= 65535 && slab_elems / 8 < (int64_t(1) << 31);
+  for (int i = 0; i < n && fast; ++i) {
+    const UnpackDesc& u = us[i];
+    const int64_t esz = u.src_dtype == FUSP_E4M3 ? 1 : int64_t(dtype_size(u.src_dtype));
+    fast = u.b == u0.b && u.hp == u0.hp && u.sl == u0.sl && u.d == u0.d && u.u == u0.u &&
+           aligned16(u.src) && aligned16(u.dst) && (u.src_slot_stride * esz) % 16 == 0 &&
+           (u.dst_dtype != FUSP_E4M3 || u.src_dtype == FUSP_E4M3);
+  }
+  if (!fast) {
+    for (int i = 0; i < n; ++i) FUSP_CHECK(launch_unpack_generic(us[i], s));
+    return FUSP_OK;
+  }
+  if (slabs == 0 || slab_elems == 0) return FUSP_OK;
+  UnpackArgs a{};
+  for (int i = 0; i < n; ++i)
+    a.op[i] = UnpackOp{us[i].src, us[i].dst, us[i].scales, us[i].src_slot_stride, us[i].scale_stride,
+                       us[i].scale_bh_stride, us[i].src_dtype, us[i].dst_dtype};
+  a.bhp = u0.b * u0.hp;
+  a.sl = u0.sl;
+  a.u = u0.u;
+  a.slab_vecs = static_cast<int>(slab_elems / 8);
+  a.slab_elems = slab_elems;
+  unpack_slab_kernel<<<dim3(slab_grid_x(a.slab_vecs, slabs * n), static_cast<unsigned>(slabs), n),
+                       kBlock, 0, s>>>(a);
+  FUSP_LAUNCHED("unpack_slab_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_pack(const PackDesc& p, cudaStream_t s) { return launch_pack_multi(&p, 1, s); }
+fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s) { return launch_unpack_multi(&p, 1, s); }
+
+fusp_status launch_pack_generic(const PackDesc& p, cudaStream_t s) {
   const int64_t n = int64_t(p.b) * p.h * p.sl * p.d;
   if (n <= 0) return FUSP_OK;
   if (p.d % 8 != 0) return set_error(FUSP_ERR_SHAPE, "pack: head dim must be a multiple of 8");
@@ -526,7 +947,7 @@ fusp_status launch_pack(const PackDesc& p, cudaStream_t s) {
   return FUSP_OK;
 }
 
-fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s) {
+fusp_status launch_unpack_generic(const UnpackDesc& p, cudaStream_t s) {
   const int64_t n = int64_t(p.b) * p.hp * p.sl * p.d * p.u;
   if (n <= 0) return FUSP_OK;
   if (p.d % 8 != 0) return set_error(FUSP_ERR_SHAPE, "unpack: head dim must be a multiple of 8");
@@ -560,6 +981,23 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
   FUSP_CUDA(cudaMemsetAsync(amax, 0, sizeof(uint32_t) * nblocks, s));
   if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
   if (block_elems <= 0 || nblocks <= 0) return FUSP_OK;
+  if (block_elems % 8 == 0 && src.d % 8 == 0 && aligned16(src.x) && nblocks <= 65535 &&
+      block_elems * nblocks < (int64_t(1) << 31)) {
+    AmaxArgs a{};
+    a.src[0] = src;
+    a.amax[0] = amax;
+    a.block_vecs = block_elems / 8;
+    a.nonfinite = nonfinite;
+    int gx = grid_for(a.block_vecs, 8);
+    const int cap = (kSMs * 8 + nblocks - 1) / nblocks;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    amax_vec_kernel<<<dim3(gx, nblocks, 1), kBlock, 0, s>>>(a);
+    FUSP_LAUNCHED("amax_vec_kernel");
+    finalize_scales_kernel<<<(nblocks + kBlock - 1) / kBlock, kBlock, 0, s>>>(
+        amax, nblocks, reinterpret_cast<float*>(amax));
+    FUSP_LAUNCHED("finalize_scales_kernel");
+    return FUSP_OK;
+  }
   int gx = grid_for(block_elems, 4);
   const int cap = (kSMs * 8 + nblocks - 1) / nblocks;  // ~8 CTAs per SM in total
   if (gx > cap) gx = cap < 1 ? 1 : cap;
@@ -579,10 +1017,55 @@ fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_e
   return FUSP_OK;
 }
 
+namespace {
+bool fp8_vec_ok(const Fp8Src& src, int64_t n, int64_t block_elems, const void* codes) {
+  return n % 8 == 0 && block_elems % 8 == 0 && src.d % 8 == 0 && aligned16(src.x) &&
+         aligned16(codes);
+}
+}  // namespace
+
+fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
+                                      uint32_t* const* work, float* const* scales,
+                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s) {
+  const int nblocks = static_cast<int>((n + block_elems - 1) / block_elems);
+  bool fast = parts >= 1 && parts <= 2 && nblocks <= 65535 && n < (int64_t(1) << 31);
+  for (int p = 0; p < parts && fast; ++p) fast = fp8_vec_ok(src[p], n, block_elems, codes[p]);
+  if (!fast) {
+    for (int p = 0; p < parts; ++p)
+      FUSP_CHECK(launch_quantize_fp8(src[p], n, block_elems, work[p], scales[p], codes[p], nonfinite, s));
+    return FUSP_OK;
+  }
+  if (n <= 0) return FUSP_OK;
+  for (int p = 0; p < parts; ++p) FUSP_CUDA(cudaMemsetAsync(work[p], 0, sizeof(uint32_t) * nblocks, s));
+  if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
+  AmaxArgs a{};
+  QuantArgs q{};
+  for (int p = 0; p < parts; ++p) {
+    a.src[p] = q.src[p] = src[p];
+    a.amax[p] = work[p];
+    q.amax[p] = work[p];
+    q.scales[p] = scales[p];
+    q.codes[p] = codes[p];
+  }
+  a.block_vecs = block_elems / 8;
+  a.nonfinite = nonfinite;
+  int gx = grid_for(a.block_vecs, 8);
+  const int cap = (kSMs * 8 + nblocks * parts - 1) / (nblocks * parts);
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
+  FUSP_LAUNCHED("amax_vec_kernel");
+  q.block_vecs = block_elems / 8;
+  quantize_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(q);
+  FUSP_LAUNCHED("quantize_vec_kernel");
+  return FUSP_OK;
+}
+
 fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elems, uint32_t* work,
                                 float* scales, uint8_t* codes, uint32_t* nonfinite,
                                 cudaStream_t s) {
   const int nblocks = static_cast<int>((n + block_elems - 1) / block_elems);
+  if (fp8_vec_ok(src, n, block_elems, codes) && nblocks <= 65535)
+    return launch_quantize_fp8_multi(&src, 1, n, block_elems, &work, &scales, &codes, nonfinite, s);
   FUSP_CHECK(launch_amax_blocks(src, block_elems, nblocks, work, nonfinite, s));
   FUSP_CUDA(cudaMemcpyAsync(scales, work, sizeof(float) * nblocks, cudaMemcpyDeviceToDevice, s));
   return launch_quantize_blocks(src, n, block_elems, scales, codes, s);
@@ -591,6 +1074,12 @@ fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elem
 fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
                                      int64_t n, void* y, int ydt, cudaStream_t s) {
   if (n <= 0) return FUSP_OK;
+  if (n % 8 == 0 && block_elems % 8 == 0 && aligned16(c) && aligned16(y) && ydt != FUSP_E4M3 &&
+      n < (int64_t(1) << 31)) {
+    dequantize_vec_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(c, scales, block_elems / 8, n / 8, y, ydt);
+    FUSP_LAUNCHED("dequantize_vec_kernel");
+    return FUSP_OK;
+  }
   dequantize_blocks_kernel<<<grid_for(n), kBlock, 0, s>>>(c, scales, block_elems, n, y, ydt);
   FUSP_LAUNCHED("dequantize_blocks_kernel");
   return FUSP_OK;

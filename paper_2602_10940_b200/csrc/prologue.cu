@@ -52,66 +52,98 @@ __device__ __forceinline__ void store4(void* p, int dt, int64_t i, const float* 
   }
 }
 
-// src [B][H][SL][D] -> dst slot t = h / hp: [B][hp][SL][D] at t * slot_stride (elements).
-__global__ void norm_rope_pack_kernel(const void* __restrict__ src, int sdt, void* __restrict__ dst,
-                                      int ddt, int64_t slot_stride, int b, int h, int sl, int u,
-                                      const float* __restrict__ w, float eps,
-                                      const float* __restrict__ cosv, const float* __restrict__ sinv,
-                                      int64_t pos0) {
+struct ProOp {
+  const void* src;
+  void* dst;
+  const float* w;     // RMSNorm weight [D] or null
+  const float* cosv;  // RoPE tables [rows][D/2] or null (null: plain pack, e.g. V)
+  const float* sinv;
+  int sdt, ddt;
+};
+struct ProArgs {
+  ProOp op[3];
+  int64_t slot_stride;  // destination elements between slots
+  int h, hp, sl;
+  int rows;             // B * H * SL
+  float eps;
+  int64_t pos0;
+};
+
+// src [B][H][SL][D] -> dst slot t = h / hp: [B][hp][SL][D] at t * slot_stride (elements);
+// grid.y = operand (Q, K and, in the same launch, V as a plain pack).
+__global__ void __launch_bounds__(256) norm_rope_pack_kernel(const __grid_constant__ ProArgs a) {
   constexpr int D = 128;
-  const int hp = h / u;
+  const ProOp& o = a.op[blockIdx.y];
   const int lane = threadIdx.x & 31;
-  const int64_t rows = int64_t(b) * h * sl;
-  for (int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; row < rows;
-       row += (int64_t(gridDim.x) * blockDim.x) >> 5) {
-    const int s = static_cast<int>(row % sl);
-    const int64_t bh = row / sl;
-    const int hh = static_cast<int>(bh % h);
-    const int bb = static_cast<int>(bh / h);
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < a.rows;
+       row += (gridDim.x * blockDim.x) >> 5) {
+    const int bh = row / a.sl;
+    const int s = row - bh * a.sl;
+    const int bb = bh / a.h;
+    const int hh = bh - bb * a.h;
     float x[4];
-    load4(src, sdt, row * D + lane * 4, x);
-    if (w != nullptr) {  // RMSNorm over the head dim
+    load4(o.src, o.sdt, int64_t(row) * D + lane * 4, x);
+    if (o.w != nullptr) {  // RMSNorm over the head dim
       float ss = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      const float r = rsqrtf(ss * (1.0f / D) + eps);
-      const float4 wv = *reinterpret_cast<const float4*>(w + lane * 4);
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      const float r = rsqrtf(ss * (1.0f / D) + a.eps);
+      const float4 wv = *reinterpret_cast<const float4*>(o.w + lane * 4);
       x[0] *= r * wv.x;
       x[1] *= r * wv.y;
       x[2] *= r * wv.z;
       x[3] *= r * wv.w;
     }
-    if (cosv != nullptr) {  // RoPE on the two interleaved pairs this lane owns
-      const int64_t pos = pos0 + s;
-      const float2 c = *reinterpret_cast<const float2*>(cosv + pos * (D / 2) + lane * 2);
-      const float2 n = *reinterpret_cast<const float2*>(sinv + pos * (D / 2) + lane * 2);
+    if (o.cosv != nullptr) {  // RoPE on the two interleaved pairs this lane owns
+      const int64_t pos = a.pos0 + s;
+      const float2 c = *reinterpret_cast<const float2*>(o.cosv + pos * (D / 2) + lane * 2);
+      const float2 n = *reinterpret_cast<const float2*>(o.sinv + pos * (D / 2) + lane * 2);
       const float y0 = x[0] * c.x - x[1] * n.x, y1 = x[0] * n.x + x[1] * c.x;
       const float y2 = x[2] * c.y - x[3] * n.y, y3 = x[2] * n.y + x[3] * c.y;
       x[0] = y0; x[1] = y1; x[2] = y2; x[3] = y3;
     }
-    const int t = hh / hp, hl = hh % hp;
-    const int64_t o = t * slot_stride + ((int64_t(bb) * hp + hl) * sl + s) * D + lane * 4;
-    store4(dst, ddt, o, x);
+    const int t = hh / a.hp, hl = hh - t * a.hp;
+    const int64_t dst = t * a.slot_stride + ((int64_t(bb) * a.hp + hl) * a.sl + s) * D + lane * 4;
+    store4(o.dst, o.ddt, dst, x);
   }
 }
 
 }  // namespace
 
-fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
-                                  int64_t slot_stride, int b, int h, int sl, int d, int u,
-                                  const float* w, float eps, const float* cosv, const float* sinv,
-                                  int64_t pos0, cudaStream_t s) {
+fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_stride, int b,
+                                        int h, int sl, int d, int u, float eps, int64_t pos0,
+                                        cudaStream_t s) {
   if (d != 128) return set_error(FUSP_ERR_SHAPE, "qk prologue: head dim must be 128");
+  if (n < 1 || n > 3) return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: 1..3 operands");
   const int64_t rows = int64_t(b) * h * sl;
   if (rows <= 0) return FUSP_OK;
+  if (rows >= (int64_t(1) << 31)) return set_error(FUSP_ERR_SHAPE, "qk prologue: too many rows");
+  ProArgs a{};
+  for (int i = 0; i < n; ++i)
+    a.op[i] = ProOp{ops[i].src, ops[i].dst, ops[i].w, ops[i].cosv, ops[i].sinv, ops[i].sdt, ops[i].ddt};
+  a.slot_stride = slot_stride;
+  a.h = h;
+  a.hp = h / u;
+  a.sl = sl;
+  a.rows = static_cast<int>(rows);
+  a.eps = eps;
+  a.pos0 = pos0;
   int64_t grid = (rows * 32 + 255) / 256;
-  if (grid > kSMs * 16) grid = kSMs * 16;
-  norm_rope_pack_kernel<<<static_cast<int>(grid), 256, 0, s>>>(src, sdt, dst, ddt, slot_stride, b,
-                                                               h, sl, u, w, eps, cosv, sinv, pos0);
+  const int64_t cap = (int64_t(kSMs) * 16 + n - 1) / n;
+  if (grid > cap) grid = cap;
+  norm_rope_pack_kernel<<<dim3(static_cast<unsigned>(grid), n), 256, 0, s>>>(a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "norm_rope_pack_kernel");
   return FUSP_OK;
+}
+
+fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
+                                  int64_t slot_stride, int b, int h, int sl, int d, int u,
+                                  const float* w, float eps, const float* cosv, const float* sinv,
+                                  int64_t pos0, cudaStream_t s) {
+  const ProPack op{src, dst, w, cosv, sinv, sdt, ddt};
+  return launch_norm_rope_pack_multi(&op, 1, slot_stride, b, h, sl, d, u, eps, pos0, s);
 }
 
 }  // namespace fusp

@@ -338,18 +338,38 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   p.dst = b.send_in;
   p.dst_dtype = l.qk_dt;
   p.dst_slot_stride = se2;
-  if (l.pro_q) FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
-  else FUSP_CHECK(launch_pack(p, s));
-  if (!l.fp8) {
+  // Q, K, V (bf16 wire) leave in one pack launch -- with the fused QK prologue, one
+  // norm/RoPE/pack launch whose V operand is a plain pack.
+  PackDesc ops[3];
+  int nops = 0;
+  if (!l.fp8 && (l.pro_q || l.pro_k)) {
+    const fusp_qk_prologue& pr = *l.pro;
+    const ProPack pops[3] = {
+        {q, b.send_in, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
+         l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
+        {k, b.send_in + l.blk * 2, l.pro_k ? pr.k_norm_weight : nullptr,
+         l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
+        {v, b.send_in + l.blk * 4, nullptr, nullptr, nullptr, l.in_dt, FUSP_F16}};
+    FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, se2, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
+  } else if (l.pro_q) {
+    FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
+  } else {
+    ops[nops++] = p;
+  }
+  if (!l.fp8 && (l.pro_q || l.pro_k)) {
+    // packed above
+  } else if (!l.fp8) {
     p.src = k;
     p.dst = b.send_in + l.blk * 2;
     if (l.pro_k) FUSP_CHECK(prologue(false, k, p.dst, l.qk_dt, se2, l.U));
-    else FUSP_CHECK(launch_pack(p, s));
+    else ops[nops++] = p;
     p.src = v;
     p.dst = b.send_in + l.blk * 4;
     p.dst_dtype = FUSP_F16;
-    FUSP_CHECK(launch_pack(p, s));
+    ops[nops++] = p;
+    FUSP_CHECK(launch_pack_multi(ops, nops, s));
   } else {
+    FUSP_CHECK(launch_pack_multi(ops, nops, s));
     // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --
     // fused into the pack; every slot's trailer carries the scales of its heads
     for (int part = 0; part < 2; ++part) {
@@ -387,16 +407,20 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   u.src_slot_stride = se2;
   u.dst = b.Qr_w;
   u.dst_dtype = l.qk_dt;
-  FUSP_CHECK(launch_unpack(u, s));
+  // every operand of the attention leaves the receive slots in one unpack launch
+  UnpackDesc uops[5];
+  int nu = 0;
+  uops[nu++] = u;
   if (!l.fp8) {
     u.src = b.recv_in + l.blk * 2;
     u.dst = b.Kr_w;
-    FUSP_CHECK(launch_unpack(u, s));
+    uops[nu++] = u;
     u.src = b.recv_in + l.blk * 4;
     u.src_dtype = FUSP_F16;
     u.dst = b.Vr_w;
     u.dst_dtype = FUSP_F16;
-    FUSP_CHECK(launch_unpack(u, s));
+    uops[nu++] = u;
+    FUSP_CHECK(launch_unpack_multi(uops, nu, s));
   } else {
     const float* scales = reinterpret_cast<const float*>(b.recv_in + l.blk * 4);
     for (int part = 0; part < 2; ++part) {
@@ -408,11 +432,12 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       u.scale_bh_stride = l.fp8_block ? 1 : 0;
       u.dst = part == 0 ? b.Kr_w : b.Vr_w;
       u.dst_dtype = part == 0 ? l.qk_dt : FUSP_F16;
-      FUSP_CHECK(launch_unpack(u, s));
+      uops[nu++] = u;
       u.dst = part == 0 ? static_cast<void*>(b.Kc) : static_cast<void*>(b.Vc);
       u.dst_dtype = FUSP_E4M3;
-      FUSP_CHECK(launch_unpack(u, s));
+      uops[nu++] = u;
     }
+    FUSP_CHECK(launch_unpack_multi(uops, nu, s));
     b.Ks = scales;
     b.Vs = scales + l.nsc_slot;
     b.s_stride = int64_t(l.slot_stride / 4);
@@ -493,6 +518,10 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
   const bool usp_local = l.mode != Mode::kRing;
   // Fill the FP8 send wire [codes][f32 scales] for one hop from the chunk we hold.
   auto quantize_hop = [&](int hop, int from_buf, cudaStream_t st) -> fusp_status {
+    Fp8Src srcs[2];
+    uint32_t* works[2];
+    float* scs[2];
+    uint8_t* cds[2];
     for (int p = 0; p < 2; ++p) {
       uint8_t* codes = reinterpret_cast<uint8_t*>(b.sw[p]);
       float* scales = reinterpret_cast<float*>(b.sw[p] + l.C);
@@ -508,10 +537,12 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
         src = Fp8Src{w, FUSP_E4M3, reinterpret_cast<const float*>(w + l.C), 0,
                      l.fp8_block ? 1 : 0, l.D, l.span, l.span};
       }
-      FUSP_CHECK(launch_quantize_fp8(src, l.C, block, b.amax + p * (l.nsc_chunk + 1), scales,
-                                     codes, nullptr, st));
+      srcs[p] = src;
+      works[p] = b.amax + p * (l.nsc_chunk + 1);
+      scs[p] = scales;
+      cds[p] = codes;
     }
-    return FUSP_OK;
+    return launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, st);
   };
   auto exchange = [&](int hop, cudaStream_t st) -> fusp_status {
     const int into = hop % 2, from = (hop - 1) % 2;

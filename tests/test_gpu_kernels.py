@@ -247,3 +247,32 @@ def test_kernels_counted(cuda, fu):
     fu.attention_with_lse(q, q, q.half())
     torch.cuda.synchronize()
     assert fu.kernel_launch_count() > n0
+
+
+def test_quantize_near_rounding_boundaries_bit_exact(cuda, fu):
+    # x / scale landing within a few f32 ulps of every E4M3 rounding midpoint (normal and
+    # subnormal range, both signs): the vectorised quantizer must still encode exactly like
+    # the reference's IEEE division (fp8.cpp:121) -- its fast x * (1/scale) path has to defer
+    # to the exact division at every one of these.
+    mags = R.decode_e4m3(np.arange(0, 127, dtype=np.uint8))
+    mids = (np.float32(0.5) * (mags[:-1] + mags[1:])).astype(np.float32)
+    amax = np.float32(3.7)
+    scale = np.float32(amax / np.float32(448.0))
+    qs = []
+    for m in mids:
+        q = np.float32(m)
+        for _ in range(8):
+            q = np.nextafter(q, np.float32(0))
+        for _ in range(17):
+            qs.append(q)
+            q = np.nextafter(q, np.float32(np.inf))
+    q = np.array(qs, np.float32)
+    x = (q * scale).astype(np.float32)
+    x = np.concatenate([x, -x, np.array([amax], np.float32)])
+    x = np.concatenate([x, np.zeros((-x.size) % 128, np.float32)])
+    want, s = R.quantize(x)
+    codes, scales = fu.quantize_blocks(T(x), x.size)
+    assert scales.cpu().numpy()[0] == s
+    got = codes.cpu().numpy()
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, (bad[:5], x[bad[:5]], got[bad[:5]], want[bad[:5]])

@@ -1,0 +1,98 @@
+// Times the layer's HBM-bound movers (Ulysses pack / unpack, FP8 amax+quantize, dequantize)
+// at the BASELINE per-rank shapes with CUDA events: `hot` = back-to-back repetitions,
+// `cold` = a 256 MiB L2 flush before every repetition.  Algorithmic bytes = compulsory reads +
+// writes.  Links the library's internal launchers (exported C++ symbols of libfastusp.so).
+//   make -C tools/cpp && tools/cpp/movers_bench
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <vector>
+#include <functional>
+#include "../../paper_2602_10940_b200/csrc/fastusp_internal.h"
+
+using namespace fusp;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+#define FK(x) do { fusp_status st = (x); if (st != FUSP_OK) { printf("fusp error %d at %d\n", int(st), __LINE__); return 1; } } while (0)
+
+static void* flushbuf = nullptr;
+static double peak = 6548.5;
+
+static void report(const char* name, double bytes, const std::function<void()>& f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int i = 0; i < 3; ++i) f();
+  cudaDeviceSynchronize();
+  const int reps = 50;
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) f();
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float hot; cudaEventElapsedTime(&hot, a, b); hot /= reps;
+  float cold = 0;
+  for (int i = 0; i < 10; ++i) {
+    cudaMemsetAsync(flushbuf, i, 256u << 20);
+    cudaEventRecord(a); f(); cudaEventRecord(b); cudaEventSynchronize(b);
+    float t; cudaEventElapsedTime(&t, a, b); cold += t / 10;
+  }
+  printf("{\"kernel\": \"%s\", \"bytes\": %.0f, \"hot_us\": %.2f, \"hot_gbs\": %.0f, \"cold_us\": %.2f, \"cold_gbs\": %.0f, \"cold_frac_of_hbm\": %.3f}\n",
+         name, bytes, hot * 1e3, bytes / (hot * 1e-3) / 1e9, cold * 1e3, bytes / (cold * 1e-3) / 1e9,
+         bytes / (cold * 1e-3) / 1e9 / peak);
+}
+
+int main() {
+  CK(cudaMalloc(&flushbuf, 256u << 20));
+  struct Cfg { const char* name; int h, sl, u; };
+  const Cfg cfgs[] = {{"flux_u2", 24, 2304, 2}, {"flux_u8", 24, 576, 8}};
+  for (const Cfg& c : cfgs) {
+    const int64_t n = int64_t(c.h) * c.sl * 128;  // one local tensor [1,H,SL,128]
+    void *q, *k, *v, *slots, *dq, *dk, *dv;
+    CK(cudaMalloc(&q, n * 2)); CK(cudaMalloc(&k, n * 2)); CK(cudaMalloc(&v, n * 2));
+    CK(cudaMalloc(&slots, n * 6 + 4096)); CK(cudaMalloc(&dq, n * 2)); CK(cudaMalloc(&dk, n * 2)); CK(cudaMalloc(&dv, n * 2));
+    CK(cudaMemset(q, 0x3c, n * 2)); CK(cudaMemset(k, 0x3c, n * 2)); CK(cudaMemset(v, 0x3c, n * 2));
+    const int64_t blk = n / c.u;          // elements per (Q|K|V) slot piece
+    const int64_t se2 = 3 * blk;          // slot stride (16-bit elements): [Q][K][V]
+    PackDesc p[3];
+    for (int t = 0; t < 3; ++t) {
+      p[t] = PackDesc{};
+      p[t].src = t == 0 ? q : t == 1 ? k : v; p[t].src_dtype = FUSP_BF16;
+      p[t].dst = static_cast<uint16_t*>(slots) + t * blk; p[t].dst_dtype = t == 2 ? FUSP_F16 : FUSP_BF16;
+      p[t].dst_slot_stride = se2; p[t].b = 1; p[t].h = c.h; p[t].sl = c.sl; p[t].d = 128; p[t].u = c.u;
+    }
+    char nm[96];
+    snprintf(nm, sizeof nm, "%s pack Q,K,V bf16 -> slots (one launch)", c.name);
+    report(nm, 3.0 * n * 4, [&] { launch_pack_multi(p, 3, 0); });
+    UnpackDesc u[3];
+    for (int t = 0; t < 3; ++t) {
+      u[t] = UnpackDesc{};
+      u[t].src = static_cast<uint16_t*>(slots) + t * blk; u[t].src_dtype = t == 2 ? FUSP_F16 : FUSP_BF16;
+      u[t].src_slot_stride = se2; u[t].dst = t == 0 ? dq : t == 1 ? dk : dv; u[t].dst_dtype = u[t].src_dtype;
+      u[t].b = 1; u[t].hp = c.h / c.u; u[t].sl = c.sl; u[t].d = 128; u[t].u = c.u;
+    }
+    snprintf(nm, sizeof nm, "%s unpack Q,K,V slots -> operands (one launch)", c.name);
+    report(nm, 3.0 * n * 4, [&] { launch_unpack_multi(u, 3, 0); });
+    // FP8: K and V amax + quantize (per-tensor block), codes into a buffer
+    uint8_t *ck, *cv; float* sc; uint32_t* wk;
+    CK(cudaMalloc(&ck, n)); CK(cudaMalloc(&cv, n)); CK(cudaMalloc(&sc, 4096)); CK(cudaMalloc(&wk, 4096));
+    Fp8Src src[2] = {Fp8Src{k, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}, Fp8Src{v, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}};
+    uint32_t* works[2] = {wk, wk + 64};
+    float* scs[2] = {sc, sc + 64};
+    uint8_t* cds[2] = {ck, cv};
+    snprintf(nm, sizeof nm, "%s fp8 amax+quantize K,V (2 passes)", c.name);
+    report(nm, 2.0 * n * (2 + 2 + 1), [&] { launch_quantize_fp8_multi(src, 2, n, n, works, scs, cds, nullptr, 0); });
+    snprintf(nm, sizeof nm, "%s fp8 dequantize K -> bf16", c.name);
+    report(nm, double(n) * (1 + 2), [&] { launch_dequantize_blocks(ck, sc, n, n, dk, FUSP_BF16, 0); });
+    // ring hop: re-quantize an E4M3 chunk (per-segment scales) -- the FP8 ring forward
+    Fp8Src esrc[2] = {Fp8Src{ck, FUSP_E4M3, sc, 0, 0, 128, c.sl, c.sl}, Fp8Src{cv, FUSP_E4M3, sc + 64, 0, 0, 128, c.sl, c.sl}};
+    uint8_t *ck2, *cv2;
+    CK(cudaMalloc(&ck2, n)); CK(cudaMalloc(&cv2, n));
+    uint8_t* cds2[2] = {ck2, cv2};
+    snprintf(nm, sizeof nm, "%s fp8 ring hop re-quantize K,V from e4m3", c.name);
+    report(nm, 2.0 * n * (1 + 1 + 1), [&] { launch_quantize_fp8_multi(esrc, 2, n, n, works, scs, cds2, nullptr, 0); });
+    for (void* x : {q, k, v, slots, dq, dk, dv}) cudaFree(x);
+    for (void* x : std::vector<void*>{ck, cv, sc, wk, ck2, cv2}) cudaFree(x);
+  }
+  // reference: a plain device copy of 3 bf16 tensors (FLUX U=2 size)
+  const int64_t n = int64_t(24) * 2304 * 128 * 3;
+  void *a, *b;
+  CK(cudaMalloc(&a, n * 2)); CK(cudaMalloc(&b, n * 2));
+  report("reference cudaMemcpyAsync D2D (FLUX U=2 Q+K+V bytes)", 4.0 * n, [&] { cudaMemcpyAsync(b, a, n * 2, cudaMemcpyDeviceToDevice); });
+  return 0;
+}

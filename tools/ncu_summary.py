@@ -95,6 +95,45 @@ def launches(path, dest):
     print(dest)
 
 
+def hbm(path, dest, peak_gbs=None):
+    """Per-kernel achieved DRAM bandwidth from a launch list captured with
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum."""
+    if peak_gbs is None:
+        try:
+            peak_gbs = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+        except (OSError, ValueError, KeyError):
+            peak_gbs = 7700.0
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, mi, vi, ui = (hdr.index(c) for c in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    ii = hdr.index("ID")
+    per = defaultdict(dict)  # launch id -> metrics
+    names = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+             "msecond": 1e6}
+    for r in rows[1:]:
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+        per[r[ii]][r[mi]] = v
+        names[r[ii]] = re.sub(r"\(.*", "", r[ki])[:70]
+    agg = defaultdict(lambda: [0, 0.0, 0.0])
+    for lid, m in per.items():
+        a = agg[names[lid]]
+        a[0] += 1
+        a[1] += m.get("gpu__time_duration.sum", 0.0)
+        a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    lines = [f"# DRAM bandwidth per kernel (ncu launch list, --clock-control none): `{path}`", "",
+             f"Peak = {peak_gbs} GB/s (MEASURED_PEAKS.json hbm_gbs). Per-launch times are serialised "
+             "under ncu; tiny launches are latency-bound, compare the large ones.", "",
+             "| kernel | launches | avg us | avg DRAM MB | GB/s | of peak |", "|---|---|---|---|---|---|"]
+    for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        gbs = b / t if t else 0.0  # bytes / ns = GB/s
+        lines.append(f"| `{k}` | {n} | {t / n / 1e3:.2f} | {b / n / 1e6:.2f} | {gbs:.0f} | "
+                     f"{gbs / peak_gbs * 100:.0f}% |")
+    with open(dest, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print(dest)
+
+
 if __name__ == "__main__":
     mode, src, dst = sys.argv[1:4]
-    {"full": full, "launches": launches}[mode](src, dst)
+    {"full": full, "launches": launches, "hbm": hbm}[mode](src, dst)
