@@ -523,27 +523,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (tr) FUSP_TRACE(p, tslot + 3);
         if (r_in_tile == 0) cnt[0] = 0u;  // every segment has counted: reset for the next launch
-        // (m_k, l_k) of every segment (own values for k == kself when unpublished)
-        m_fin = -INFINITY;
-        for (int k = 0; k < nseg; ++k) {
-          const float mk = (k == kself && !published) ? m_use
-                                                      : __ldcg(seg_slot(p, c_first + k, g.qb, t) + kD * kBM + r_in_tile);
-          m_fin = fmaxf(m_fin, mk);
+        // (m_k, l_k) of every segment (own values for k == kself when unpublished): the loads of
+        // up to kMl segments are issued together (one L2 round trip), the rest stream after.
+        constexpr int kMl = 8;
+        float mk_r[kMl], lk_r[kMl];
+#pragma unroll
+        for (int k = 0; k < kMl; ++k) {
+          mk_r[k] = m_use;
+          lk_r[k] = l_sum;
+          if (k < nseg && (k != kself || published)) {
+            const float* sl = seg_slot(p, c_first + k, g.qb, t);
+            mk_r[k] = __ldcg(sl + kD * kBM + r_in_tile);
+            lk_r[k] = __ldcg(sl + kD * kBM + kBM + r_in_tile);
+          }
         }
-        l_fin = 0.f;
-        for (int k = 0; k < nseg; ++k) {
-          float mk = m_use, lk = l_sum;
+        auto seg_ml = [&](int k, float& mk, float& lk) {
+          if (k < kMl) {
+#pragma unroll
+            for (int q = 0; q < kMl; ++q)
+              if (q == k) { mk = mk_r[q]; lk = lk_r[q]; }
+            return;
+          }
+          mk = m_use;
+          lk = l_sum;
           if (k != kself || published) {
             const float* sl = seg_slot(p, c_first + k, g.qb, t);
             mk = __ldcg(sl + kD * kBM + r_in_tile);
             lk = __ldcg(sl + kD * kBM + kBM + r_in_tile);
           }
+        };
+        m_fin = -INFINITY;
+        for (int k = 0; k < nseg; ++k) {
+          float mk, lk;
+          seg_ml(k, mk, lk);
+          m_fin = fmaxf(m_fin, mk);
+        }
+        l_fin = 0.f;
+        for (int k = 0; k < nseg; ++k) {
+          float mk, lk;
+          seg_ml(k, mk, lk);
           l_fin = fmaf(ex2((mk - m_fin) * sl2), lk, l_fin);
         }
         if (tr) FUSP_TRACE(p, tslot + 5);
         // k = 0 term: own TMEM tile scaled in place (fast path), or slot 0 stored over it
-        const float w0 = ex2(((published ? __ldcg(seg_slot(p, c_first, g.qb, t) + kD * kBM + r_in_tile)
-                                         : m_use) - m_fin) * sl2);
+        float m0, l0;
+        seg_ml(0, m0, l0);
+        const float w0 = ex2((m0 - m_fin) * sl2);
         if (!published) {
           if (__any_sync(0xffffffffu, w0 != 1.f)) {  // tcgen05.ld/st are warp-collective
 #pragma unroll 1
@@ -582,7 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4 x[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = __ldcg(x4 + i * kBM);
-          const float w = ex2((__ldcg(sl + kD * kBM + r_in_tile) - m_fin) * sl2);
+          float mk, lk;
+          seg_ml(k, mk, lk);
+          const float w = ex2((mk - m_fin) * sl2);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
