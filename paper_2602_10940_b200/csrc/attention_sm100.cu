@@ -119,7 +119,9 @@ struct Params {
   float* slots;          // split: [gridDim.x][2 (first/last segment)][2 tiles][kSlotTileFloats]
   unsigned long long* trace;  // optional per-CTA globaltimer events (attention_trace), or null
 };
-constexpr int kTraceSlots = 72;  // per CTA (SM cycles): start, end, [4 segments][2 tiles][8 events], 70: end (warp 4)
+// per CTA (SM cycles): start, end, [4 segments][2 tiles][8 events], 70: end (warp 4); then
+// [2 tiles][64 KV steps of the first segment][S ready, P published]
+constexpr int kTraceSlots = 72 + 2 * 64 * 2;
 
 __device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (per-CTA deltas)
   unsigned long long t;
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.s_full[t], it & 1);
         tc_fence_after();
         if (tr && j == g.j0) FUSP_TRACE(p, tslot + 1);
+        if (tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0));
         uint32_t s[128];
         tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_st();
         tc_fence_before();
+        if (tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
         mbar_arrive(&sm.p_full[t]);
       }
 

@@ -13,10 +13,10 @@ with fu.attention_schedule(mode, 0):
     for _ in range(3): fu.attention_with_lse(q, k, v, out_dtype=torch.float16)
     L.fusp_attention_trace(1, None, 0)
     fu.attention_with_lse(q, k, v, out_dtype=torch.float16); torch.cuda.synchronize()
-    buf = np.zeros(160 * 72, np.uint64)
+    buf = np.zeros(160 * 328, np.uint64)
     L.fusp_attention_trace(0, buf.ctypes.data, buf.size)
 GHZ = float(os.environ.get("GHZ", "1.9"))  # events are SM cycles; per-CTA times from its own start
-tr = buf.reshape(160, 72).astype(np.int64)
+tr = buf.reshape(160, 328).astype(np.int64)
 ctas = [c for c in range(160) if tr[c, 0]]
 for c in ctas:
     base = tr[c, 0]
@@ -53,3 +53,17 @@ for c in ctas:
         agg["final_store"].append(e[7] - (e[6] if e[6] else e[2]))
 for k2, vals in agg.items():
     if vals: print(f"{k2:11s} n={len(vals)} median {statistics.median(vals):.2f} us  max {max(vals):.2f} us")
+
+# steady-state KV steps of the first segment: softmax time (S ready -> P published) and the
+# MMA chain (P published -> next S ready), per Q tile, medians over CTAs
+for t in range(2):
+    sm_t, chain = [], []
+    for c in ctas:
+        ev = tr[c, 72 + t * 128: 72 + t * 128 + 128].reshape(64, 2)
+        n = int((ev[:, 0] != 0).sum())
+        for j in range(2, n - 1):
+            sm_t.append((ev[j, 1] - ev[j, 0]) / (GHZ * 1e3))
+            chain.append((ev[j + 1, 0] - ev[j, 1]) / (GHZ * 1e3))
+    if sm_t:
+        print(f"tile {t}: softmax per KV step median {statistics.median(sm_t)*1e3:.0f} ns, "
+              f"P->next S median {statistics.median(chain)*1e3:.0f} ns  (steps {len(sm_t)})")
