@@ -674,6 +674,23 @@ __device__ __forceinline__ Vec8 src_vec8(const Fp8Src& s, int64_t i) {  // i < 2
   return decode8(__ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i)), sc);
 }
 
+// |value| maximum of 8 codes of an E4M3 source in one step: decode(c) * scale is monotone in
+// the code magnitude (sign-magnitude encoding, RN multiply), so the maximum is the decoded
+// largest magnitude -- a byte-SIMD max and one decode instead of eight.  A NaN code (0x7F)
+// is the largest magnitude and decodes to NaN, which the caller flags as non-finite.
+__device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, int64_t i) {
+  const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
+  const uint32_t bh = row / static_cast<uint32_t>(s.span);
+  const int r = static_cast<int>(row - bh * s.span);
+  const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
+  const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i));
+  uint32_t m = __vmaxu4(w.x & 0x7F7F7F7Fu, w.y & 0x7F7F7F7Fu);
+  m = max(max(m & 0xFFu, (m >> 8) & 0xFFu), max((m >> 16) & 0xFFu, m >> 24));
+  float f[4];
+  dec4(m, sc, f);
+  return f[0];
+}
+
 // Pass 1 per block, 8 elements per step; grid.y = block, grid.z = tensor (K, V).
 struct AmaxArgs {
   Fp8Src src[2];
@@ -687,6 +704,13 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
   float m = 0.f, nf = 0.f;
   bool bad = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (s.dt == FUSP_E4M3) {
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
+      const float x = e4m3_vec_absmax(s, (base + v) * 8);
+      nf = fmaf(x, 0.f, nf);
+      m = fmaxf(m, x);
+    }
+  } else
   for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
     Vec8 x[4];
 #pragma unroll
