@@ -257,3 +257,31 @@ def test_traffic_and_timeline_mirror_reference(cuda, fu, n, r, pipelined, fp8):
         assert seq == want_seq
         ts = [e["t_ms"] for e in timeline if e["kind"] in ("compute_begin", "compute_end")]
         assert ts == sorted(ts)
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_nccl_backend_world1(cuda, fu, fp8):
+    # the NCCL communicator path (ncclCommInitRank, sub-communicator splits, grouped
+    # send/recv) at world 1, eager and under CUDA-graph capture, against the oracle
+    q, k, v = qkv((1, 8, 512, 128), (1, 8, 512, 128), seeds=(61, 62, 63))
+    full, _ = R.attention_with_lse(q, k, v)
+    ctx = fu.WorkerContext.nccl(fu.WorkerContext.nccl_unique_id(), 1, 0, 0)
+    try:
+        mesh = fu.make_mesh(1, 1)
+        opts = fu.CommOptions(fp8_kv=fp8, out_dtype=torch.float32, check_finite=False)
+        tq, tk, tv = (torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v))
+        out = fu.usp_attention(ctx, tq, tk, tv, mesh, opts)
+        torch.cuda.synchronize()
+        want = full if not fp8 else None
+        if want is not None:
+            assert rel_l2(out.cpu().numpy(), want) <= REL_L2
+        o_graph = torch.empty(1, 1, 8, 512, 128, device="cuda", dtype=torch.float32)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):  # capture needs a non-legacy stream
+            g = fu.LayerGraph(ctx, tq[None], tk[None], tv[None], o_graph, mesh, opts, 1)
+            g.launch(st)
+        torch.cuda.synchronize()
+        assert torch.equal(o_graph[0], out)
+        g.close()
+    finally:
+        ctx.close()
