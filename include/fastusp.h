@@ -185,6 +185,23 @@ fusp_status fusp_usp_attention_ex(fusp_ctx ctx, int ring_dim, const void* q, con
                                   void* out, const fusp_comm_options* opts,
                                   const fusp_qk_prologue* prologue, fusp_stream_t stream);
 
+/* The joint-attention block's output projection, the layer's consumer (no reference
+ * counterpart): y[B][S][N] = O[B][H][S][128] (read as [B*S][H*128], the
+ * layout the output reshard delivers) x W[H*128][N].  O and W both bf16 or both f16; y f32,
+ * f16 or bf16; N a multiple of 64; 16-byte aligned pointers.  tcgen05 GEMM, stream-ordered. */
+fusp_status fusp_out_projection(const void* o, fusp_dtype o_dtype, fusp_shape4 o_shape,
+                                const void* w, int64_t n_out, void* y, fusp_dtype y_dtype,
+                                fusp_stream_t stream);
+
+/* fusp_usp_attention_ex followed by fusp_out_projection of its output on the same stream:
+ * attn_out [B,H,S/N,128] (opts->out_dtype bf16 or f16) -> y [B,S/N,n_out] = attn_out x w_out. */
+fusp_status fusp_usp_attention_proj(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                                    const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                    void* attn_out, const fusp_comm_options* opts,
+                                    const fusp_qk_prologue* prologue, const void* w_out,
+                                    int64_t n_out, void* y, fusp_dtype y_dtype,
+                                    fusp_stream_t stream);
+
 /* Host-buffer variant of fusp_usp_attention (the reference's calling convention: host
  * tensors in, host tensor out).  Copies H2D, runs, copies D2H, synchronizes. */
 fusp_status fusp_usp_attention_host(fusp_ctx ctx, int ring_dim, const void* q, const void* k,

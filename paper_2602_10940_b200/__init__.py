@@ -11,7 +11,8 @@ from .api import (AttnResult, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGr
                   encode_e4m3, quantize_blocks,
                   gather_output, kernel_launch_count, make_mesh, merge_lse, quantize,
                   ring_attention_pipelined, ring_attention_serial, run_protocol, split_sequence,
-                  ulysses_attention, usp_attention, usp_attention_host, kFp8Max, kFp8MaxCode,
+                  ulysses_attention, usp_attention, usp_attention_host, out_projection,
+                  usp_attention_proj, kFp8Max, kFp8MaxCode,
                   kFp8NanCode)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

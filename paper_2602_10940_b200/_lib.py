@@ -117,6 +117,11 @@ _SIGS = {
     "fusp_usp_attention_ex": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                              _P, ctypes.POINTER(CommOptions),
                                              ctypes.POINTER(QKPrologue), _P]),
+    "fusp_usp_attention_proj": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
+                                               _P, ctypes.POINTER(CommOptions),
+                                               ctypes.POINTER(QKPrologue), _P, _I64, _P,
+                                               ctypes.c_int, _P]),
+    "fusp_out_projection": (ctypes.c_int, [_P, ctypes.c_int, Shape4, _P, _I64, _P, ctypes.c_int, _P]),
     "fusp_ulysses_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P,
                                               ctypes.POINTER(CommOptions), _P]),
     "fusp_ring_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P, _P,

@@ -561,6 +561,41 @@ def ring_attention_pipelined(ctx, q, k, v, group=None, opts=None) -> AttnResult:
     return _ring(ctx, q, k, v, group, opts, True)
 
 
+def out_projection(o: torch.Tensor, w: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
+    """The joint-attention block's output projection on the tcgen05 GEMM (fusp_out_projection):
+    o [B,H,S,128] (bf16|f16, the layer's output layout) x w [H*128, N] -> y [B,S,N]."""
+    o, w = _dev(o), _dev(w)
+    b, h, s_, d = _shape4(o).b, o.shape[1], o.shape[2], o.shape[3]
+    if w.dim() != 2 or w.shape[0] != h * d:
+        raise ShapeError(1, f"out_projection: w must be [{h * d}, N], got {list(w.shape)}")
+    y = torch.empty(b, s_, w.shape[1], dtype=out_dtype, device=o.device)
+    check(lib().fusp_out_projection(_ptr(o), _DT[o.dtype], _shape4(o), _ptr(w), int(w.shape[1]),
+                                    _ptr(y), _DT[out_dtype], _stream()))
+    return y
+
+
+def usp_attention_proj(ctx: WorkerContext, q, k, v, mesh: Mesh2D, w_out: torch.Tensor,
+                       opts: Optional[CommOptions] = None, prologue: Optional[QKPrologue] = None,
+                       out_dtype=torch.bfloat16):
+    """usp_attention then the output projection in one C-ABI call (fusp_usp_attention_proj).
+    opts.out_dtype (bf16|f16) is the attention output that feeds the projection."""
+    opts = opts or CommOptions(out_dtype=torch.bfloat16)
+    if mesh.n != ctx.world_size():
+        raise MeshError(2, f"mesh covers {mesh.n} workers but the fabric has {ctx.world_size()}")
+    q, k, v = _inputs(q, k, v, "usp")
+    w_out = _dev(w_out)
+    attn = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    y = torch.empty(q.shape[0], q.shape[2], w_out.shape[1], dtype=out_dtype, device=q.device)
+    co = opts._c()
+    pc = prologue._c() if prologue is not None else None
+    check(lib().fusp_usp_attention_proj(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
+                                        _shape4(q), _ptr(attn), ctypes.byref(co),
+                                        ctypes.byref(pc) if pc is not None else None,
+                                        _ptr(w_out), int(w_out.shape[1]), _ptr(y), _DT[out_dtype],
+                                        _stream()))
+    return y
+
+
 def usp_attention_host(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
                        opts: Optional[CommOptions] = None, out=None):
     """usp_attention on HOST tensors (H2D, layer, D2H inside one C-ABI call, pipelined over

@@ -31,8 +31,16 @@ void count_launch(int n = 1);
 // ---- TMA descriptors ------------------------------------------------------------------
 // 3-D map over [heads][rows][128] 16-bit elements with a head stride of `head_stride`
 // elements (rows are 128 elements apart); box = 64 elements x 128 rows x 1 head, 128B swizzle.
+// Generic tiled tensor map (128B swizzle, L2 256B promotion, zero OOB fill).
+fusp_status encode_tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                        const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                        const cuuint32_t* elem_strides);
 fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int heads,
                            int rows, int64_t head_stride);
+
+// ---- output projection (proj_sm100.cu) ---------------------------------------------------
+fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, const void* w, int n,
+                            void* y, int y_dtype, cudaStream_t stream);
 
 // ---- attention kernel -----------------------------------------------------------------
 struct AttnLaunch {

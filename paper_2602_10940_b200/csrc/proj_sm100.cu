@@ -1,0 +1,262 @@
+// The consumer side of the layer (second half): the joint-attention
+// block's output projection y = O · W_o, read straight from the output all-to-all's result.
+//
+// O is the layer output in its native layout [B][H][S][D = 128] (heads-major, the order the
+// Ulysses output reshard delivers it), so the GEMM's K = H·D axis is walked as (head, d): a
+// 4-D TMA map {d, s, h, b} with 64 x 128 boxes loads the A tile [128 tokens][64 k] of one
+// head directly -- no transpose pass.  W_o is [H·D][N] row-major (N contiguous: MN-major B).
+// y is token-major [B][S][N].
+//
+// tcgen05 GEMM, persistent (one CTA per SM): tiles of 128 tokens x 256 outputs, K in blocks
+// of 64 through a 4-stage TMA ring (A 16 KB + B 32 KB per stage, 128B swizzle), one thread
+// issues 4 MMAs (M=128, N=256, K=16) per block into a TMEM accumulator; two accumulators
+// (2 x 256 columns) let the epilogue warpgroup drain tile i while tile i+1 accumulates.
+//   warp 0   TMA producer        warp 1   TMEM allocator + MMA issuer
+//   warps 4-7  epilogue (TMEM lane = token row): f32 -> y dtype, 16-byte stores
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "fastusp_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fusp {
+namespace {
+
+using namespace ptx;
+
+constexpr int kPM = 128;   // tokens per tile
+constexpr int kPNMax = 256;  // outputs per tile (256, or 128 when that fills the SMs better)
+constexpr int kPK = 64;    // K per stage (one 128-byte swizzle row of bf16)
+constexpr int kPStages = 4;
+constexpr int kPThreads = 256;
+constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
+constexpr uint32_t kBBytes = kPK * kPNMax * 2;  // up to 32 KB: chunks of [64 k][64 n]
+constexpr uint32_t kBChunk = kPK * 64 * 2;   // 8 KB
+
+struct __align__(1024) ProjSmem {
+  uint8_t a[kPStages][kABytes];
+  uint8_t b[kPStages][kBBytes];
+  uint64_t full[kPStages], empty[kPStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+struct ProjParams {
+  int m_tiles_per_b;  // ceil(S / 128)
+  int n_tiles;        // ceil(N / 256)
+  int tiles;          // B * m_tiles_per_b * n_tiles
+  int k_blocks;       // H * 2
+  int s, n;           // tokens per batch row, outputs
+  uint32_t idesc;
+  void* y;
+  int y_dtype;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <int kPN>
+__global__ void __launch_bounds__(kPThreads, 1)
+    out_proj_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const ProjParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  ProjSmem& sm = *reinterpret_cast<ProjSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.acc_full[b], 1);
+      mbar_init(&sm.acc_empty[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      prefetch_tmap(&tm_a);
+      prefetch_tmap(&tm_b);
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        const int nt = tile % p.n_tiles;
+        const int mt = tile / p.n_tiles;
+        const int bb = mt / p.m_tiles_per_b;
+        const int s0 = (mt - bb * p.m_tiles_per_b) * kPM;
+        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+          const int st = it % kPStages;
+          mbar_wait(&sm.empty[st], ((it / kPStages) & 1) ^ 1);
+          mbar_expect_tx(&sm.full[st], kABytes + kPK * kPN * 2);
+          // A: head kb/2, d-half kb%2, 128 tokens from s0
+          tma_load_4d(sm.a[st], &tm_a, &sm.full[st], (kb & 1) * 64, s0, kb >> 1, bb);
+          // B: rows k = kb*64 .. +64, four 64-wide n-chunks
+          for (int c = 0; c < kPN / 64; ++c)
+            tma_load_2d(sm.b[st] + c * kBChunk, &tm_b, &sm.full[st], nt * kPN + c * 64, kb * kPK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp walks, one lane issues) ----------------
+    uint32_t it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++lt) {
+      const int ab = lt & 1;
+      mbar_wait(&sm.acc_empty[ab], ((lt >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + ab * kPN;
+      for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        const int st = it % kPStages;
+        mbar_wait(&sm.full[st], (it / kPStages) & 1);
+        tc_fence_after();
+        const uint64_t adesc = umma_desc_sw128(smem_u32(sm.a[st]), 16, 1024);
+        // B MN-major SW128: LBO = stride between 64-wide n-chunks (8 KB), SBO = 8 k-rows (1 KB)
+        const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.b[st]), kBChunk, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kPK / 16; ++k)
+            mma_ss(d_tmem, adesc + uint64_t(k * 32 / 16), bdesc + uint64_t(k * 16 * 128 / 16), p.idesc,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&sm.empty[st]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(&sm.acc_full[ab]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    uint32_t lt = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++lt) {
+      const int ab = lt & 1;
+      const int nt = tile % p.n_tiles;
+      const int mt = tile / p.n_tiles;
+      const int bb = mt / p.m_tiles_per_b;
+      const int s = (mt - bb * p.m_tiles_per_b) * kPM + r;
+      mbar_wait(&sm.acc_full[ab], (lt >> 1) & 1);
+      tc_fence_after();
+      const bool in_range = s < p.s;
+      const int64_t ybase = (static_cast<int64_t>(bb) * p.s + s) * p.n + nt * kPN;
+#pragma unroll 1
+      for (int c = 0; c < kPN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + ab * kPN + c * 32, v);
+        tmem_wait_ld();
+        const int n0 = nt * kPN + c * 32;
+        if (!in_range || n0 >= p.n) continue;
+        if (p.y_dtype == FUSP_F32) {
+          float* y = static_cast<float*>(p.y) + ybase + c * 32;  // N % 64 == 0: whole chunks
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(y)[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        } else {
+          uint16_t* y = static_cast<uint16_t*>(p.y) + ybase + c * 32;
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            w[i] = p.y_dtype == FUSP_F16 ? pack_f16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]))
+                                         : pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<uint4*>(y)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.acc_empty[ab]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+// y[B][S][N] = O[B][H][S][128] (as [B*S][H*128]) x W[H*128][N].  O and W: both bf16 or both
+// f16; y: f32 / f16 / bf16.  N a multiple of 64 (TMA row pitch), pointers 16-byte aligned.
+fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, const void* w,
+                            int n, void* y, int y_dtype, cudaStream_t stream) {
+  if (b <= 0 || h <= 0 || s <= 0 || n <= 0) return FUSP_OK;
+  if (o_dtype != FUSP_BF16 && o_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "out projection: O must be bf16 or f16");
+  if (n % 64 != 0) return set_error(FUSP_ERR_SHAPE, "out projection: N must be a multiple of 64");
+  if ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y)) % 16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "out projection: pointers must be 16-byte aligned");
+  const CUtensorMapDataType dt =
+      o_dtype == FUSP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap ta, tb;
+  {
+    const cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(s), static_cast<cuuint64_t>(h),
+                                static_cast<cuuint64_t>(b)};
+    const cuuint64_t strides[3] = {128 * 2, static_cast<cuuint64_t>(s) * 128 * 2,
+                                   static_cast<cuuint64_t>(h) * s * 128 * 2};
+    const cuuint32_t box[4] = {64, kPM, 1, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    FUSP_CHECK(encode_tmap(&ta, dt, 4, o, dims, strides, box, es));
+  }
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(h) * 128};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * 2};
+    const cuuint32_t box[2] = {64, kPK};
+    const cuuint32_t es[2] = {1, 1};
+    FUSP_CHECK(encode_tmap(&tb, dt, 2, w, dims, strides, box, es));
+  }
+  ProjParams p{};
+  p.m_tiles_per_b = (s + kPM - 1) / kPM;
+  p.k_blocks = h * 2;
+  p.s = s;
+  p.n = n;
+  const uint32_t f = o_dtype == FUSP_BF16 ? 1u : 0u;
+  p.y = y;
+  p.y_dtype = y_dtype;
+  // 128 x 256 tiles unless 128 x 128 fills the SMs' waves clearly better (small token counts)
+  const int sms = sm_count();
+  auto fill = [&](int pn) {
+    const int t = b * p.m_tiles_per_b * ((n + pn - 1) / pn);
+    const int waves = (t + sms - 1) / sms;
+    return static_cast<double>(t) / (static_cast<double>(waves) * sms);
+  };
+  const int pn = fill(128) > 1.15 * fill(256) ? 128 : 256;
+  p.n_tiles = (n + pn - 1) / pn;
+  p.tiles = b * p.m_tiles_per_b * p.n_tiles;
+  p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
+  const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int grid = p.tiles < sms ? p.tiles : sms;
+  if (pn == 256) out_proj_kernel<256><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  else out_proj_kernel<128><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "out_proj_kernel launch");
+  return FUSP_OK;
+}
+
+}  // namespace fusp

@@ -52,6 +52,19 @@ EncodeTiledFn get_encode_fn() {
 }
 }  // namespace
 
+fusp_status encode_tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                        const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                        const cuuint32_t* elem_strides) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(FUSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUresult r = enc(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims, strides, box,
+                   elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(FUSP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return FUSP_OK;
+}
+
 fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int heads,
                            int rows, int64_t head_stride) {
   EncodeTiledFn enc = get_encode_fn();
@@ -128,6 +141,23 @@ uint64_t fusp_kernel_launch_count(void) { return g_launches.load(); }
 
 int fusp_attention_trace(int enable, uint64_t* host, size_t n) {
   return attention_trace(enable, reinterpret_cast<unsigned long long*>(host), n);
+}
+
+fusp_status fusp_out_projection(const void* o, fusp_dtype o_dtype, fusp_shape4 o_shape,
+                                const void* w, int64_t n_out, void* y, fusp_dtype y_dtype,
+                                fusp_stream_t stream) {
+  clear_error();
+  if (o_shape.d != 128)
+    return set_error(FUSP_ERR_SHAPE, "out projection: head dim D=" + std::to_string(o_shape.d) +
+                                         " unsupported (D=128)");
+  if (o_shape.b < 0 || o_shape.h < 0 || o_shape.s < 0 || n_out < 0 || o_shape.b * o_shape.s > (1 << 30) ||
+      n_out > (1 << 30))
+    return set_error(FUSP_ERR_SHAPE, "out projection: bad shape " + shape_str(o_shape));
+  if (!valid_float_dtype(y_dtype))
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "out projection: bad output dtype");
+  return launch_out_proj(o, o_dtype, static_cast<int>(o_shape.b), static_cast<int>(o_shape.h),
+                         static_cast<int>(o_shape.s), w, static_cast<int>(n_out), y, y_dtype,
+                         reinterpret_cast<cudaStream_t>(stream));
 }
 
 fusp_status fusp_attention_schedule(int mode, int max_ctas) {

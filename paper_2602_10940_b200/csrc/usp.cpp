@@ -988,6 +988,23 @@ fusp_status fusp_usp_attention_ex(fusp_ctx c, int ring_dim, const void* q, const
                    reinterpret_cast<cudaStream_t>(stream), false, prologue);
 }
 
+fusp_status fusp_usp_attention_proj(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                                    const void* v, fusp_dtype in_dtype, fusp_shape4 ls,
+                                    void* attn_out, const fusp_comm_options* opts,
+                                    const fusp_qk_prologue* prologue, const void* w_out,
+                                    int64_t n_out, void* y, fusp_dtype y_dtype,
+                                    fusp_stream_t stream) {
+  const int odt = opts ? opts->out_dtype : FUSP_F32;
+  if (odt != FUSP_BF16 && odt != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT,
+                     "usp_attention_proj: the attention output feeding the projection must be bf16 or f16");
+  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, attn_out, nullptr, opts,
+                       reinterpret_cast<cudaStream_t>(stream), false, prologue));
+  // the consumer, on the same stream straight after the output reshard (and inside any
+  // graph being captured)
+  return fusp_out_projection(attn_out, static_cast<fusp_dtype>(odt), ls, w_out, n_out, y, y_dtype, stream);
+}
+
 fusp_status fusp_ulysses_attention(fusp_ctx c, const void* q, const void* k, const void* v,
                                    fusp_dtype in_dtype, fusp_shape4 ls, void* out,
                                    const fusp_comm_options* opts, fusp_stream_t stream) {

@@ -1,0 +1,69 @@
+"""GPU parity of the layer's consumer: the joint-attention output projection (SURVEY.md §8(f)
+rank 1) on the tcgen05 GEMM, fed the attention output in its native [B,H,S,128] layout.
+
+Bar: against a float64 matmul of the same bf16-exact operands, rel-L2 <= 1e-5 with f32 output
+(only the f32 summation order differs) and <= 4e-3 with bf16 output (the output rounding)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import restate as R
+from oracle.make_golden import qkv
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def ref_proj(o, w):
+    b, h, s, d = o.shape
+    a = np.transpose(np.asarray(o, np.float64), (0, 2, 1, 3)).reshape(b, s, h * d)
+    return a @ np.asarray(w, np.float64)
+
+
+@pytest.mark.parametrize("b,h,s,n", [(1, 24, 4608, 3072), (2, 3, 300, 320), (1, 1, 128, 64),
+                                     (1, 6, 896, 3072)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_out_projection_matches_reference(cuda, fu, b, h, s, n, dtype):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(b * 1000 + h * 10 + s)
+    o = torch.empty(b, h, s, 128, device="cuda", dtype=dtype).uniform_(-1, 1, generator=g)
+    w = (torch.empty(h * 128, n, device="cuda", dtype=dtype).uniform_(-1, 1, generator=g) / (h * 128) ** 0.5).to(dtype)
+    want = ref_proj(o.float().cpu().numpy(), w.float().cpu().numpy())
+    y = fu.out_projection(o, w, out_dtype=torch.float32)
+    assert rel_l2(y.cpu().numpy(), want) <= 1e-5
+    yb = fu.out_projection(o, w, out_dtype=torch.bfloat16)
+    assert rel_l2(yb.float().cpu().numpy(), want) <= 4e-3
+
+
+def test_out_projection_rejects_bad_shapes(cuda, fu):
+    o = torch.zeros(1, 2, 64, 128, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(fu.ShapeError):
+        fu.out_projection(o, torch.zeros(256, 100, device="cuda", dtype=torch.bfloat16))
+    with pytest.raises(fu.ShapeError):
+        fu.out_projection(o, torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16))
+
+
+@pytest.mark.parametrize("n,r", [(1, 1), (2, 1), (4, 2)])
+def test_usp_attention_proj_end_to_end(cuda, fu, n, r):
+    # attention (oracle, fp64) then the projection, against the fused layer call per rank
+    h, s, nout = 8, 256 * n, 512
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(71, 72, 73))
+    att, _ = R.attention_with_lse(q, k, v)
+    gw = torch.Generator().manual_seed(5)
+    w = (torch.rand(h * 128, nout, generator=gw) * 2 - 1) / (h * 128) ** 0.5
+    w = w.bfloat16()
+    want = ref_proj(att, w.float().numpy())
+    qs, ks, vs = ([torch.from_numpy(np.ascontiguousarray(x)).cuda().bfloat16() for x in R.split_sequence(t, n)]
+                  for t in (q, k, v))
+    mesh = fu.make_mesh(n, r)
+    wd = w.cuda()
+    rep = fu.run_protocol(n, lambda ctx: fu.usp_attention_proj(
+        ctx, qs[ctx.rank()], ks[ctx.rank()], vs[ctx.rank()], mesh, wd,
+        fu.CommOptions(out_dtype=torch.bfloat16), out_dtype=torch.float32))
+    got = torch.cat(rep.results, dim=1).cpu().numpy()
+    # bf16 attention output (~1.7e-3) dominates the error budget
+    assert rel_l2(got, want) <= 4e-3
