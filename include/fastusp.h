@@ -202,6 +202,17 @@ fusp_status fusp_usp_attention_proj(fusp_ctx ctx, int ring_dim, const void* q, c
                                     int64_t n_out, void* y, fusp_dtype y_dtype,
                                     fusp_stream_t stream);
 
+/* The whole MMDiT joint-attention block on this rank's tokens: QKV projection (tcgen05 GEMM,
+ * x [batch][s_local][channels] x w_qkv [channels][3*heads*128], the QK RMSNorm + RoPE of
+ * `prologue` in its epilogue) -> the USP layer -> output projection (w_out [heads*128][n_out])
+ * -> y [batch][s_local][n_out].  x and both weights bf16 or f16 (the layer computes and
+ * hands its output over in that dtype); rope_pos0 < 0 means rank * s_local. */
+fusp_status fusp_usp_block(fusp_ctx ctx, int ring_dim, const void* x, fusp_dtype x_dtype,
+                           int64_t batch, int64_t s_local, int64_t channels, const void* w_qkv,
+                           int heads, const fusp_qk_prologue* prologue, const void* w_out,
+                           int64_t n_out, void* y, fusp_dtype y_dtype,
+                           const fusp_comm_options* opts, fusp_stream_t stream);
+
 /* Host-buffer variant of fusp_usp_attention (the reference's calling convention: host
  * tensors in, host tensor out).  Copies H2D, runs, copies D2H, synchronizes. */
 fusp_status fusp_usp_attention_host(fusp_ctx ctx, int ring_dim, const void* q, const void* k,

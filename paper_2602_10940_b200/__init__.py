@@ -12,7 +12,7 @@ from .api import (AttnResult, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGr
                   gather_output, kernel_launch_count, make_mesh, merge_lse, quantize,
                   ring_attention_pipelined, ring_attention_serial, run_protocol, split_sequence,
                   ulysses_attention, usp_attention, usp_attention_host, out_projection,
-                  usp_attention_proj, kFp8Max, kFp8MaxCode,
+                  usp_attention_proj, usp_block, kFp8Max, kFp8MaxCode,
                   kFp8NanCode)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

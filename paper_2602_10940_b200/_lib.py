@@ -122,6 +122,9 @@ _SIGS = {
                                                ctypes.POINTER(QKPrologue), _P, _I64, _P,
                                                ctypes.c_int, _P]),
     "fusp_out_projection": (ctypes.c_int, [_P, ctypes.c_int, Shape4, _P, _I64, _P, ctypes.c_int, _P]),
+    "fusp_usp_block": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _I64, _P,
+                                      ctypes.c_int, ctypes.POINTER(QKPrologue), _P, _I64, _P,
+                                      ctypes.c_int, ctypes.POINTER(CommOptions), _P]),
     "fusp_ulysses_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P,
                                               ctypes.POINTER(CommOptions), _P]),
     "fusp_ring_attention": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int, Shape4, _P, _P,

@@ -596,6 +596,32 @@ def usp_attention_proj(ctx: WorkerContext, q, k, v, mesh: Mesh2D, w_out: torch.T
     return y
 
 
+def usp_block(ctx: WorkerContext, x: torch.Tensor, w_qkv: torch.Tensor, heads: int,
+              w_out: torch.Tensor, mesh: Mesh2D, prologue: Optional[QKPrologue] = None,
+              opts: Optional[CommOptions] = None, out_dtype=torch.bfloat16) -> torch.Tensor:
+    """The MMDiT joint-attention block on this rank's tokens (fusp_usp_block): x [B,S/N,C]
+    -> QKV projection (+ QK RMSNorm / RoPE in its epilogue) -> USP layer -> output projection
+    -> y [B,S/N,N]."""
+    opts = opts or CommOptions(check_finite=False)
+    if mesh.n != ctx.world_size():
+        raise MeshError(2, f"mesh covers {mesh.n} workers but the fabric has {ctx.world_size()}")
+    x, w_qkv, w_out = _dev(x), _dev(w_qkv), _dev(w_out)
+    if x.dim() != 3:
+        raise ShapeError(1, f"usp_block: x must be [B, S, C], got {list(x.shape)}")
+    b, s_, c = x.shape
+    if tuple(w_qkv.shape) != (c, 3 * heads * 128) or w_out.dim() != 2 or w_out.shape[0] != heads * 128:
+        raise ShapeError(1, f"usp_block: w_qkv must be [{c}, {3 * heads * 128}] and w_out "
+                            f"[{heads * 128}, N]; got {list(w_qkv.shape)}, {list(w_out.shape)}")
+    y = torch.empty(b, s_, w_out.shape[1], dtype=out_dtype, device=x.device)
+    co = opts._c()
+    pc = prologue._c() if prologue is not None else None
+    check(lib().fusp_usp_block(ctx.handle, mesh.r, _ptr(x), _DT[x.dtype], b, s_, c, _ptr(w_qkv),
+                               heads, ctypes.byref(pc) if pc is not None else None, _ptr(w_out),
+                               int(w_out.shape[1]), _ptr(y), _DT[out_dtype], ctypes.byref(co),
+                               _stream()))
+    return y
+
+
 def usp_attention_host(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
                        opts: Optional[CommOptions] = None, out=None):
     """usp_attention on HOST tensors (H2D, layer, D2H inside one C-ABI call, pipelined over

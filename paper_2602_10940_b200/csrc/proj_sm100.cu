@@ -47,11 +47,21 @@ struct ProjParams {
   int m_tiles_per_b;  // ceil(S / 128)
   int n_tiles;        // ceil(N / 256)
   int tiles;          // B * m_tiles_per_b * n_tiles
-  int k_blocks;       // H * 2
+  int k_blocks;       // out-projection: H * 2; QKV projection: C / 64
   int s, n;           // tokens per batch row, outputs
   uint32_t idesc;
   void* y;
   int y_dtype;
+  // QKV projection epilogue (kQkv): columns [part][head][d] of N = 3 * H * 128; Q and K rows
+  // get RMSNorm (w != null) and interleaved RoPE (cos != null) and every part lands as
+  // [B][H][S][128] at qkv[part]
+  int heads;
+  void* qkv[3];
+  const float* norm_w[2];
+  float eps;
+  const float* cosv;
+  const float* sinv;
+  int64_t pos0;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
@@ -62,7 +72,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       : "memory");
 }
 
-template <int kPN>
+// kQkv = false: output projection, A = attention output [B][H][S][128] through a 4-D map.
+// kQkv = true:  QKV projection, A = x [B*S][C] token-major through a 2-D map, epilogue does
+//               the MMDiT QK RMSNorm + RoPE and writes Q, K, V head-major.
+template <int kPN, bool kQkv>
 __global__ void __launch_bounds__(kPThreads, 1)
     out_proj_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const ProjParams p) {
@@ -104,8 +117,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const int st = it % kPStages;
           mbar_wait(&sm.empty[st], ((it / kPStages) & 1) ^ 1);
           mbar_expect_tx(&sm.full[st], kABytes + kPK * kPN * 2);
-          // A: head kb/2, d-half kb%2, 128 tokens from s0
-          tma_load_4d(sm.a[st], &tm_a, &sm.full[st], (kb & 1) * 64, s0, kb >> 1, bb);
+          if (kQkv)  // A: x rows of batch bb, tokens s0.., channels kb*64..
+            tma_load_2d(sm.a[st], &tm_a, &sm.full[st], kb * kPK, bb * p.s + s0);
+          else       // A: head kb/2, d-half kb%2, 128 tokens from s0
+            tma_load_4d(sm.a[st], &tm_a, &sm.full[st], (kb & 1) * 64, s0, kb >> 1, bb);
           // B: rows k = kb*64 .. +64, four 64-wide n-chunks
           for (int c = 0; c < kPN / 64; ++c)
             tma_load_2d(sm.b[st] + c * kBChunk, &tm_b, &sm.full[st], nt * kPN + c * 64, kb * kPK);
@@ -154,6 +169,66 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_wait(&sm.acc_full[ab], (lt >> 1) & 1);
       tc_fence_after();
       const bool in_range = s < p.s;
+      if constexpr (kQkv) {
+        // two heads per 256-column tile (one per 128-column tile): RMSNorm needs the whole
+        // head row, so each head is read from TMEM twice (sum of squares, then scale + rotate)
+        const int hd = p.heads * 128;
+#pragma unroll 1
+        for (int hh = 0; hh < kPN / 128; ++hh) {
+          const int n0 = nt * kPN + hh * 128;
+          const int part = n0 / hd, head = (n0 - part * hd) / 128;
+          const uint32_t tcol = tmem + lane_off + ab * kPN + hh * 128;
+          const float* w = part < 2 ? p.norm_w[part] : nullptr;
+          const bool rope = part < 2 && p.cosv != nullptr;
+          float rinv = 1.f;
+          if (w != nullptr) {
+            float ss = 0.f;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t v[32];
+              tmem_ld32(tcol + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ss = fmaf(__uint_as_float(v[i]), __uint_as_float(v[i]), ss);
+            }
+            rinv = rsqrtf(ss * (1.0f / 128) + p.eps);
+          }
+          const int64_t pos = p.pos0 + s;
+          uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) +
+                          ((static_cast<int64_t>(bb) * p.heads + head) * p.s + s) * 128;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tcol + c * 32, v);
+            tmem_wait_ld();
+            if (!in_range) continue;
+            float x[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+            if (w != nullptr) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] *= rinv * __ldg(w + c * 32 + i);
+            }
+            if (rope) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float cs = __ldg(p.cosv + pos * 64 + c * 16 + i);
+                const float sn = __ldg(p.sinv + pos * 64 + c * 16 + i);
+                const float x0 = x[2 * i], x1 = x[2 * i + 1];
+                x[2 * i] = x0 * cs - x1 * sn;
+                x[2 * i + 1] = x0 * sn + x1 * cs;
+              }
+            }
+            uint32_t o16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              o16[i] = p.y_dtype == FUSP_F16 ? pack_f16x2(x[2 * i], x[2 * i + 1]) : pack_bf16x2(x[2 * i], x[2 * i + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(dst + c * 32)[i] = make_uint4(o16[4 * i], o16[4 * i + 1], o16[4 * i + 2], o16[4 * i + 3]);
+          }
+        }
+      } else {
       const int64_t ybase = (static_cast<int64_t>(bb) * p.s + s) * p.n + nt * kPN;
 #pragma unroll 1
       for (int c = 0; c < kPN / 32; ++c) {
@@ -179,6 +254,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int i = 0; i < 4; ++i)
             reinterpret_cast<uint4*>(y)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
+      }
       }
       tc_fence_before();
       mbar_arrive(&sm.acc_empty[ab]);
@@ -246,16 +322,95 @@ fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, con
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   const int grid = p.tiles < sms ? p.tiles : sms;
-  if (pn == 256) out_proj_kernel<256><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
-  else out_proj_kernel<128><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  if (pn == 256) out_proj_kernel<256, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  else out_proj_kernel<128, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "out_proj_kernel launch");
+  return FUSP_OK;
+}
+
+// Q, K, V [B][H][S][128] (dtype qkv_dtype: bf16 or f16) = x[B][S][C] . W[C][3*H*128], with
+// the QK prologue (RMSNorm weights wq / wk, interleaved RoPE tables [rows][64] at positions
+// pos0 + s; null = skipped) applied in the epilogue.  x and W both bf16 or both f16; C a
+// multiple of 64.
+fusp_status launch_qkv_proj(const void* x, int x_dtype, int b, int s, int c, const void* w, int heads,
+                            void* q, void* k, void* v, int qkv_dtype, const float* wq, const float* wk,
+                            float eps, const float* cosv, const float* sinv, int64_t pos0,
+                            cudaStream_t stream) {
+  if (b <= 0 || s <= 0 || c <= 0 || heads <= 0) return FUSP_OK;
+  if (x_dtype != FUSP_BF16 && x_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: x must be bf16 or f16");
+  if (qkv_dtype != FUSP_BF16 && qkv_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: Q/K/V must be bf16 or f16");
+  if (c % 64 != 0) return set_error(FUSP_ERR_SHAPE, "qkv projection: C must be a multiple of 64");
+  for (const void* ptr : {x, w, static_cast<const void*>(q), static_cast<const void*>(k), static_cast<const void*>(v)})
+    if (reinterpret_cast<uintptr_t>(ptr) % 16)
+      return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: pointers must be 16-byte aligned");
+  const CUtensorMapDataType dt =
+      x_dtype == FUSP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int n = 3 * heads * 128;
+  CUtensorMap ta, tb;
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(b) * s};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(c) * 2};
+    const cuuint32_t box[2] = {kPK, kPM};
+    const cuuint32_t es[2] = {1, 1};
+    FUSP_CHECK(encode_tmap(&ta, dt, 2, x, dims, strides, box, es));
+  }
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(c)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * 2};
+    const cuuint32_t box[2] = {64, kPK};
+    const cuuint32_t es[2] = {1, 1};
+    FUSP_CHECK(encode_tmap(&tb, dt, 2, w, dims, strides, box, es));
+  }
+  ProjParams p{};
+  p.m_tiles_per_b = (s + kPM - 1) / kPM;
+  p.k_blocks = c / kPK;
+  p.s = s;
+  p.n = n;
+  p.y_dtype = qkv_dtype;
+  p.heads = heads;
+  p.qkv[0] = q;
+  p.qkv[1] = k;
+  p.qkv[2] = v;
+  p.norm_w[0] = wq;
+  p.norm_w[1] = wk;
+  p.eps = eps;
+  p.cosv = cosv;
+  p.sinv = sinv;
+  p.pos0 = pos0;
+  const int sms = sm_count();
+  // 256-column tiles hold two whole heads, 128-column tiles one (heads never straddle tiles)
+  auto fill = [&](int pn) {
+    const int t = b * p.m_tiles_per_b * ((n + pn - 1) / pn);
+    const int waves = (t + sms - 1) / sms;
+    return static_cast<double>(t) / (static_cast<double>(waves) * sms);
+  };
+  const int pn = (n % 256 != 0 || fill(128) > 1.15 * fill(256)) ? 128 : 256;
+  p.n_tiles = n / pn;
+  p.tiles = b * p.m_tiles_per_b * p.n_tiles;
+  const uint32_t f = x_dtype == FUSP_BF16 ? 1u : 0u;
+  p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
+  const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int grid = p.tiles < sms ? p.tiles : sms;
+  if (pn == 256) out_proj_kernel<256, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  else out_proj_kernel<128, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "qkv_proj kernel launch");
   return FUSP_OK;
 }
 

@@ -43,6 +43,8 @@ struct fusp_ctx_s {
   void* arena = nullptr;
   size_t arena_bytes = 0;
   fusp::CounterBuf attn_cnt;  // stream-K tickets of the attention kernel (zeroed once)
+  void* block_ws = nullptr;   // Q, K, V and attention output of fusp_usp_block
+  size_t block_ws_bytes = 0;
   void* host_stage = nullptr;
   size_t host_stage_bytes = 0;
   uint64_t a2a_bytes = 0, send_bytes = 0;
@@ -842,6 +844,7 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
   c->comm.reset();
   if (c->arena) cudaFree(c->arena);
   if (c->attn_cnt.ptr) cudaFree(c->attn_cnt.ptr);
+  if (c->block_ws) cudaFree(c->block_ws);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_recv[0], c->ev_recv[1], c->ev_attn[0], c->ev_attn[1]})
@@ -1003,6 +1006,52 @@ fusp_status fusp_usp_attention_proj(fusp_ctx c, int ring_dim, const void* q, con
   // the consumer, on the same stream straight after the output reshard (and inside any
   // graph being captured)
   return fusp_out_projection(attn_out, static_cast<fusp_dtype>(odt), ls, w_out, n_out, y, y_dtype, stream);
+}
+
+fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x_dtype,
+                           int64_t batch, int64_t s_local, int64_t channels, const void* w_qkv,
+                           int heads, const fusp_qk_prologue* prologue, const void* w_out,
+                           int64_t n_out, void* y, fusp_dtype y_dtype,
+                           const fusp_comm_options* opts, fusp_stream_t stream) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (x_dtype != FUSP_BF16 && x_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "usp_block: x must be bf16 or f16");
+  if (batch <= 0 || s_local <= 0 || channels <= 0 || heads <= 0)
+    return set_error(FUSP_ERR_SHAPE, "usp_block: empty shape");
+  const int64_t pos0 = prologue && prologue->rope_pos0 >= 0 ? prologue->rope_pos0 : int64_t(c->rank) * s_local;
+  if (prologue && prologue->rope_cos && prologue->rope_rows < pos0 + s_local)
+    return set_error(FUSP_ERR_SHAPE, "qk prologue: rope table has " + std::to_string(prologue->rope_rows) +
+                                         " rows, positions up to " + std::to_string(pos0 + s_local) + " needed");
+  // Q, K, V and the attention output, one allocation per context (grown outside capture)
+  const size_t one = align_up(size_t(batch) * heads * s_local * 128 * 2, 256);
+  if (c->block_ws_bytes < 4 * one) {
+    if (c->capturing) return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+    FUSP_CUDA(cudaDeviceSynchronize());
+    if (c->block_ws) FUSP_CUDA(cudaFree(c->block_ws));
+    c->block_ws = nullptr;
+    c->block_ws_bytes = 0;
+    FUSP_CUDA(cudaMalloc(&c->block_ws, 4 * one));
+    c->block_ws_bytes = 4 * one;
+  }
+  char* ws = static_cast<char*>(c->block_ws);
+  void *q = ws, *k = ws + one, *v = ws + 2 * one, *attn = ws + 3 * one;
+  // producer: QKV projection with the QK RMSNorm + RoPE in its epilogue
+  FUSP_CHECK(launch_qkv_proj(x, x_dtype, int(batch), int(s_local), int(channels), w_qkv, heads, q, k, v,
+                             x_dtype, prologue ? prologue->q_norm_weight : nullptr,
+                             prologue ? prologue->k_norm_weight : nullptr, prologue ? prologue->eps : 0.f,
+                             prologue ? prologue->rope_cos : nullptr, prologue ? prologue->rope_sin : nullptr,
+                             pos0, st));
+  // the layer, its output in the projection's input dtype
+  fusp_comm_options o{};
+  if (opts) o = *opts;
+  o.out_dtype = x_dtype;
+  const fusp_shape4 ls{batch, heads, s_local, 128};
+  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st));
+  // consumer: output projection
+  return fusp_out_projection(attn, x_dtype, ls, w_out, n_out, y, y_dtype, stream);
 }
 
 fusp_status fusp_ulysses_attention(fusp_ctx c, const void* q, const void* k, const void* v,

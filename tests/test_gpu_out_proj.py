@@ -67,3 +67,48 @@ def test_usp_attention_proj_end_to_end(cuda, fu, n, r):
     got = torch.cat(rep.results, dim=1).cpu().numpy()
     # bf16 attention output (~1.7e-3) dominates the error budget
     assert rel_l2(got, want) <= 4e-3
+
+
+# ---- the producer side: QKV projection with the QK prologue in its epilogue ----------------
+def tables(s, d=128, theta=10000.0):
+    inv = theta ** (-np.arange(0, d, 2, dtype=np.float64) / d)
+    ang = np.arange(s, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def block_oracle(x, wqkv, wout, heads, wq, wk, cos, sin, n):
+    """fp64 MMDiT block: x @ Wqkv -> per-head RMSNorm + RoPE of Q, K -> bf16 operands ->
+    USP attention (restate, == full attention) -> bf16 output -> @ Wout."""
+    b, s, c = x.shape
+    p = np.asarray(x, np.float64) @ np.asarray(wqkv, np.float64)          # [b, s, 3*H*128]
+    p = p.reshape(b, s, 3, heads, 128).transpose(2, 0, 3, 1, 4)           # [3, b, H, s, 128]
+    q = R.qk_prologue(p[0], wq, 1e-6, cos, sin, 0)
+    k = R.qk_prologue(p[1], wk, 1e-6, cos, sin, 0)
+    q, k, v = (R.round_bf16(np.asarray(t, np.float32)) for t in (q, k, p[2]))
+    att, _ = R.attention_with_lse(q, k, v)
+    att = R.round_bf16(np.asarray(att, np.float32))
+    return ref_proj(att, wout)
+
+
+@pytest.mark.parametrize("n,r,heads,s", [(1, 1, 4, 512), (2, 1, 4, 512), (4, 2, 8, 1024)])
+def test_usp_block_end_to_end(cuda, fu, n, r, heads, s):
+    c, nout = 256, 256
+    rs = np.random.RandomState(11 + n)
+    x = R.round_bf16(rs.uniform(-1, 1, (1, s, c)).astype(np.float32))
+    wqkv = R.round_bf16((rs.uniform(-1, 1, (c, 3 * heads * 128)) / np.sqrt(c)).astype(np.float32))
+    wout = R.round_bf16((rs.uniform(-1, 1, (heads * 128, nout)) / np.sqrt(heads * 128)).astype(np.float32))
+    wq = rs.uniform(0.5, 1.5, 128).astype(np.float32)
+    wk = rs.uniform(0.5, 1.5, 128).astype(np.float32)
+    cos, sin = tables(s)
+    want = block_oracle(x, wqkv, wout, heads, wq, wk, cos, sin, n)
+    xs = [torch.from_numpy(np.ascontiguousarray(t)).cuda().bfloat16() for t in np.split(x, n, axis=1)]
+    pro = fu.QKPrologue(q_norm_weight=torch.from_numpy(wq).cuda(), k_norm_weight=torch.from_numpy(wk).cuda(),
+                        eps=1e-6, rope_cos=torch.from_numpy(cos).cuda(), rope_sin=torch.from_numpy(sin).cuda())
+    wq_d, wo_d = torch.from_numpy(wqkv).cuda().bfloat16(), torch.from_numpy(wout).cuda().bfloat16()
+    mesh = fu.make_mesh(n, r)
+    rep = fu.run_protocol(n, lambda ctx: fu.usp_block(ctx, xs[ctx.rank()], wq_d, heads, wo_d, mesh,
+                                                      prologue=pro, out_dtype=torch.float32))
+    got = torch.cat(rep.results, dim=1).cpu().numpy()
+    # Q/K/V rounded to bf16 from f32 accumulators (the oracle rounds fp64), bf16 attention
+    # output: the bf16 roundings dominate
+    assert rel_l2(got, want) <= 5e-3
