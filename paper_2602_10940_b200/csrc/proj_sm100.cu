@@ -12,7 +12,7 @@
 // issues 4 MMAs (M=128, N=256, K=16) per block into a TMEM accumulator; two accumulators
 // (2 x 256 columns) let the epilogue warpgroup drain tile i while tile i+1 accumulates.
 //   warp 0   TMA producer        warp 1   TMEM allocator + MMA issuer
-//   warps 4-7  epilogue (TMEM lane = token row): f32 -> y dtype, 16-byte stores
+//   warps 4-11 epilogue, two warpgroups splitting the tile's columns (TMEM lane = token row)
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -30,7 +30,7 @@ constexpr int kPM = 128;   // tokens per tile
 constexpr int kPNMax = 256;  // outputs per tile (256, or 128 when that fills the SMs better)
 constexpr int kPK = 64;    // K per stage (one 128-byte swizzle row of bf16)
 constexpr int kPStages = 4;
-constexpr int kPThreads = 256;
+constexpr int kPThreads = 384;  // producer / MMA warpgroup + 2 epilogue warpgroups
 constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kPK * kPNMax * 2;  // up to 32 KB: chunks of [64 k][64 n]
 constexpr uint32_t kBChunk = kPK * 64 * 2;   // 8 KB
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.acc_full[b], 1);
-      mbar_init(&sm.acc_empty[b], 128);
+      mbar_init(&sm.acc_empty[b], 256);
     }
     fence_mbar_init();
   }
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int quad = warp & 3;
+    const int eg = (warp - 4) >> 2;  // epilogue warpgroup: column half (QKV: head) of the tile
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     uint32_t lt = 0;
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // head row, so each head is read from TMEM twice (sum of squares, then scale + rotate)
         const int hd = p.heads * 128;
 #pragma unroll 1
-        for (int hh = 0; hh < kPN / 128; ++hh) {
+        for (int hh = eg; hh < kPN / 128; hh += 2) {
           const int n0 = nt * kPN + hh * 128;
           const int part = n0 / hd, head = (n0 - part * hd) / 128;
           const uint32_t tcol = tmem + lane_off + ab * kPN + hh * 128;
@@ -206,17 +207,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
             if (w != nullptr) {
+              const float4* w4 = reinterpret_cast<const float4*>(w + c * 32);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) x[i] *= rinv * __ldg(w + c * 32 + i);
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 wv = __ldg(w4 + q4);
+                x[4 * q4] *= rinv * wv.x;
+                x[4 * q4 + 1] *= rinv * wv.y;
+                x[4 * q4 + 2] *= rinv * wv.z;
+                x[4 * q4 + 3] *= rinv * wv.w;
+              }
             }
-            if (rope) {
+            if (rope) {  // this row's 16 (cos, sin) pairs of the chunk as float4 vectors
+              const float4* c4 = reinterpret_cast<const float4*>(p.cosv + pos * 64 + c * 16);
+              const float4* s4 = reinterpret_cast<const float4*>(p.sinv + pos * 64 + c * 16);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float cs = __ldg(p.cosv + pos * 64 + c * 16 + i);
-                const float sn = __ldg(p.sinv + pos * 64 + c * 16 + i);
-                const float x0 = x[2 * i], x1 = x[2 * i + 1];
-                x[2 * i] = x0 * cs - x1 * sn;
-                x[2 * i + 1] = x0 * sn + x1 * cs;
+              for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 cv = __ldg(c4 + q4), sv = __ldg(s4 + q4);
+                const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i = q4 * 4 + e;
+                  const float x0 = x[2 * i], x1 = x[2 * i + 1];
+                  x[2 * i] = x0 * cc[e] - x1 * ss[e];
+                  x[2 * i + 1] = x0 * ss[e] + x1 * cc[e];
+                }
               }
             }
             uint32_t o16[16];
@@ -231,7 +245,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       } else {
       const int64_t ybase = (static_cast<int64_t>(bb) * p.s + s) * p.n + nt * kPN;
 #pragma unroll 1
-      for (int c = 0; c < kPN / 32; ++c) {
+      for (int c = eg * (kPN / 64); c < (eg + 1) * (kPN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + lane_off + ab * kPN + c * 32, v);
         tmem_wait_ld();

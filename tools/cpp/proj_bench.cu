@@ -1,0 +1,32 @@
+// QKV projection (with / without the QK prologue epilogue) and output projection timings at
+// the FLUX shape, CUDA events over back-to-back launches.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include "../../paper_2602_10940_b200/csrc/fastusp_internal.h"
+using namespace fusp;
+int main() {
+  const int s = 4608, c = 3072, h = 24, n = 3 * h * 128;
+  void *x, *w, *q, *k, *v, *wo, *y;
+  float *wq, *cs;
+  cudaMalloc(&x, size_t(s) * c * 2); cudaMalloc(&w, size_t(c) * n * 2);
+  cudaMalloc(&q, size_t(s) * h * 128 * 2); cudaMalloc(&k, size_t(s) * h * 128 * 2); cudaMalloc(&v, size_t(s) * h * 128 * 2);
+  cudaMalloc(&wo, size_t(h) * 128 * c * 2); cudaMalloc(&y, size_t(s) * c * 2);
+  cudaMalloc(&wq, 128 * 4); cudaMalloc(&cs, size_t(s) * 64 * 4);
+  cudaMemset(x, 0x3c, size_t(s) * c * 2); cudaMemset(w, 0x1c, size_t(c) * n * 2); cudaMemset(wq, 0, 128 * 4); cudaMemset(cs, 0, size_t(s) * 64 * 4);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  auto run = [&](const char* name, double flop, auto f) {
+    for (int i = 0; i < 3; ++i) f();
+    cudaEventRecord(a);
+    for (int i = 0; i < 20; ++i) f();
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b); ms /= 20;
+    printf("{\"kernel\": \"%s\", \"us\": %.1f, \"tflops\": %.1f}\n", name, ms * 1e3, flop / (ms * 1e-3) / 1e12);
+  };
+  const double fq = 2.0 * s * c * n, fo = 2.0 * s * h * 128 * c;
+  run("qkv projection, plain epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, nullptr, nullptr, 0.f, nullptr, nullptr, 0, 0); });
+  run("qkv projection + RMSNorm + RoPE epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, wq, wq, 1e-6f, cs, cs, 0, 0); });
+  run("output projection", fo, [&] { launch_out_proj(q, FUSP_BF16, 1, h, s, wo, c, y, FUSP_BF16, 0); });
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("status %s\n", cudaGetErrorString(e));
+  return 0;
+}
