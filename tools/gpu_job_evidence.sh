@@ -13,3 +13,4 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn
 timeout 600 python tools/virtual_mesh_bench.py > gpurun_out/vmesh.jsonl 2> gpurun_out/vmesh.err
 timeout 120 python tools/attn_trace.py 3 4608 auto > gpurun_out/trace_u8.txt 2>&1
 tail -3 gpurun_out/gpu_tests.log; tail -3 gpurun_out/smoke.log; cat gpurun_out/bench.json; cut -c1-300 gpurun_out/bench_ref.json; ls -la gpurun_out/*.ncu-rep
+timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1
