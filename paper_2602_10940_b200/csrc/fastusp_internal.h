@@ -115,6 +115,9 @@ struct PackDesc {
   int b, h, sl, d, u;
   const float* scale;       // e4m3: quantization scale(s) (device)
   int64_t scale_bh_stride;  // 0: one tensor-wide scale; 1: one scale per (b,h) slab
+  const uint32_t* amax_bits = nullptr;  // e4m3: scales from amax words instead (amax/448)
+  float* trailer = nullptr;             // e4m3: write each slot's scales (slot t at t*trailer_stride)
+  int64_t trailer_stride = 0;           // floats
 };
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
 // Up to 6 packs / unpacks with one launch (same B, H, SL, D, U; else one launch each).
@@ -168,6 +171,12 @@ struct Fp8Src {
   int64_t seg_stride, bh_stride;
   int d, span, seg_rows;
 };
+// amax words of 1-2 sources (K, V) in one launch (zeroed first; no finalize: the pack reads
+// the words and computes amax/448 itself).
+fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems, int nblocks,
+                              uint32_t* const* amax, cudaStream_t s);
+fusp_status launch_amax_blocks_raw(const Fp8Src& src, int64_t block_elems, int nblocks,
+                                   uint32_t* amax, cudaStream_t s);
 // amax per block of `block_elems` (into work[0..nblocks)), then work[k] = scale bits.
 fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nblocks,
                                uint32_t* work, uint32_t* nonfinite, cudaStream_t s);

@@ -542,7 +542,10 @@ constexpr int kMaxMoveOps = 6;  // tensors moved by one pack / unpack launch (gr
 struct PackOp {
   const void* src;
   void* dst;
-  const float* scale;       // e4m3 destination: scale[slab * scale_bh_stride]
+  const float* scale;       // e4m3 destination: scale[slab * scale_bh_stride] ...
+  const uint32_t* amax;     // ... or, when set, scale = amax[slab * scale_bh_stride] / 448 (1 if 0)
+  float* trailer;           // e4m3: also write each slot's scales here (slot t at t * trailer_stride)
+  int64_t trailer_stride;
   int64_t scale_bh_stride;
   int64_t slot_stride;      // destination elements between slots
   int sdt, ddt;
@@ -560,7 +563,20 @@ __global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ 
   const int t = hh / a.hp, hl = hh - t * a.hp;
   const int64_t s0 = int64_t(slab) * a.slab_elems;
   const int64_t d0 = int64_t(t) * o.slot_stride + (int64_t(bb) * a.hp + hl) * a.slab_elems;
-  const float qs = o.ddt == FUSP_E4M3 ? o.scale[slab * o.scale_bh_stride] : 1.f;
+  float qs = 1.f;
+  if (o.ddt == FUSP_E4M3) {
+    if (o.amax != nullptr) {  // finalize fused in: scale = amax / 448, 1 for an all-zero block
+      const float am = __uint_as_float(o.amax[slab * o.scale_bh_stride]);
+      qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;
+    } else {
+      qs = o.scale[slab * o.scale_bh_stride];
+    }
+    // slot trailer (QuantizedTensor::slice_heads keeps the tensor-wide scale, fp8.cpp:100-105;
+    // per block: the scales of this slot's slabs in [b][hl] order)
+    if (o.trailer != nullptr && blockIdx.x == 0 && threadIdx.x == 0 &&
+        (o.scale_bh_stride != 0 || (bb == 0 && hl == 0)))
+      o.trailer[t * o.trailer_stride + (o.scale_bh_stride != 0 ? bb * a.hp + hl : 0)] = qs;
+  }
   const int stride = gridDim.x * blockDim.x;
   const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
   if (o.sdt == o.ddt && o.sdt != FUSP_F32) {  // same 16-bit type: 4 x 16 B in flight per thread
@@ -911,7 +927,8 @@ fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s) {
   if (slabs == 0 || slab_elems == 0) return FUSP_OK;
   PackArgs a{};
   for (int i = 0; i < n; ++i) {
-    a.op[i] = PackOp{ps[i].src, ps[i].dst, ps[i].scale, ps[i].scale_bh_stride, ps[i].dst_slot_stride,
+    a.op[i] = PackOp{ps[i].src, ps[i].dst, ps[i].scale, ps[i].amax_bits, ps[i].trailer,
+                     ps[i].trailer_stride, ps[i].scale_bh_stride, ps[i].dst_slot_stride,
                      ps[i].src_dtype, ps[i].dst_dtype};
   }
   a.h = p0.h;
@@ -964,9 +981,21 @@ fusp_status launch_pack_generic(const PackDesc& p, cudaStream_t s) {
   const int64_t n = int64_t(p.b) * p.h * p.sl * p.d;
   if (n <= 0) return FUSP_OK;
   if (p.d % 8 != 0) return set_error(FUSP_ERR_SHAPE, "pack: head dim must be a multiple of 8");
+  const float* scale = p.scale;
+  if (p.dst_dtype == FUSP_E4M3 && p.amax_bits != nullptr) {
+    // unfused form of the fast path's scale + trailer handling: amax words -> scales in place
+    const int nsc = p.scale_bh_stride != 0 ? p.b * p.h : 1;
+    uint32_t* w = const_cast<uint32_t*>(p.amax_bits);
+    finalize_scales_kernel<<<(nsc + kBlock - 1) / kBlock, kBlock, 0, s>>>(w, nsc, reinterpret_cast<float*>(w));
+    FUSP_LAUNCHED("finalize_scales_kernel");
+    scale = reinterpret_cast<const float*>(w);
+  }
+  if (p.dst_dtype == FUSP_E4M3 && p.trailer != nullptr)
+    FUSP_CHECK(launch_scatter_slot_scales(scale, p.trailer, p.trailer_stride, p.b, p.h, p.u,
+                                          p.scale_bh_stride != 0 ? 1 : 0, s));
   pack_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(p.src, p.src_dtype, p.dst, p.dst_dtype,
                                                   p.dst_slot_stride, p.b, p.h, p.sl, p.d, p.u,
-                                                  p.scale, p.scale_bh_stride);
+                                                  scale, p.scale_bh_stride);
   FUSP_LAUNCHED("pack_kernel");
   return FUSP_OK;
 }
@@ -999,6 +1028,17 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
 }  // namespace fusp
 
 namespace fusp {
+
+fusp_status launch_amax_blocks_raw(const Fp8Src& src, int64_t block_elems, int nblocks,
+                                   uint32_t* amax, cudaStream_t s) {  // amax zeroed by the caller
+  if (block_elems <= 0 || nblocks <= 0) return FUSP_OK;
+  int gx = grid_for(block_elems, 4);
+  const int cap = (kSMs * 8 + nblocks - 1) / nblocks;
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  amax_blocks_kernel<<<dim3(gx, nblocks), kBlock, 0, s>>>(src, block_elems, amax, nullptr);
+  FUSP_LAUNCHED("amax_blocks_kernel");
+  return FUSP_OK;
+}
 
 fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nblocks,
                                uint32_t* amax, uint32_t* nonfinite, cudaStream_t s) {
@@ -1047,6 +1087,37 @@ bool fp8_vec_ok(const Fp8Src& src, int64_t n, int64_t block_elems, const void* c
          aligned16(codes);
 }
 }  // namespace
+
+fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems, int nblocks,
+                              uint32_t* const* amax, cudaStream_t s) {
+  bool fast = parts >= 1 && parts <= 2 && nblocks <= 65535 && block_elems % 8 == 0 &&
+              block_elems * nblocks < (int64_t(1) << 31);
+  for (int p = 0; p < parts && fast; ++p) fast = src[p].d % 8 == 0 && aligned16(src[p].x);
+  if (!fast) {
+    for (int p = 0; p < parts; ++p) {
+      FUSP_CUDA(cudaMemsetAsync(amax[p], 0, sizeof(uint32_t) * nblocks, s));
+      FUSP_CHECK(launch_amax_blocks_raw(src[p], block_elems, nblocks, amax[p], s));
+    }
+    return FUSP_OK;
+  }
+  if (parts == 2 && amax[1] == amax[0] + nblocks) {
+    FUSP_CUDA(cudaMemsetAsync(amax[0], 0, sizeof(uint32_t) * 2 * nblocks, s));
+  } else {
+    for (int p = 0; p < parts; ++p) FUSP_CUDA(cudaMemsetAsync(amax[p], 0, sizeof(uint32_t) * nblocks, s));
+  }
+  AmaxArgs a{};
+  for (int p = 0; p < parts; ++p) {
+    a.src[p] = src[p];
+    a.amax[p] = amax[p];
+  }
+  a.block_vecs = block_elems / 8;
+  int gx = grid_for(a.block_vecs, 8);
+  const int cap = (kSMs * 8 + nblocks * parts - 1) / (nblocks * parts);
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
+  FUSP_LAUNCHED("amax_vec_kernel");
+  return FUSP_OK;
+}
 
 fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
                                       uint32_t* const* work, float* const* scales,

@@ -371,28 +371,29 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     ops[nops++] = p;
     FUSP_CHECK(launch_pack_multi(ops, nops, s));
   } else {
-    FUSP_CHECK(launch_pack_multi(ops, nops, s));
-    // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --
-    // fused into the pack; every slot's trailer carries the scales of its heads
+    // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --:
+    // one amax launch for K and V, then Q, K, V leave in one pack launch whose E4M3
+    // operands compute their scales from the amax words and write every slot's trailer
+    const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
+    const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
+    const Fp8Src srcs[2] = {Fp8Src{k, l.k_dt, nullptr, 0, 0, l.D, l.SL, l.SL},
+                            Fp8Src{v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL}};
+    uint32_t* am[2] = {b.amax, b.amax + l.nsc_local};
+    FUSP_CHECK(launch_amax_multi(srcs, 2, block, l.nsc_local, am, s));
     for (int part = 0; part < 2; ++part) {
-      const Fp8Src src{part == 0 ? k : v, part == 0 ? l.k_dt : l.in_dt, nullptr, 0, 0, l.D, l.SL,
-                       l.SL};
-      const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
-      const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
-      FUSP_CHECK(launch_amax_blocks(src, block, l.nsc_local, b.amax, nullptr, s));
-      const float* scales = reinterpret_cast<const float*>(b.amax);
-      float* trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
-      FUSP_CHECK(launch_scatter_slot_scales(scales, trailer, int64_t(l.slot_stride / 4), l.B, l.H,
-                                            l.U, l.fp8_block ? 1 : 0, s));
-      p.src = src.x;
-      p.src_dtype = src.dt;
+      p.src = srcs[part].x;
+      p.src_dtype = srcs[part].dt;
       p.dst = b.send_in + l.blk * 2 + part * l.blk;
       p.dst_dtype = FUSP_E4M3;
       p.dst_slot_stride = int64_t(l.slot_stride);
-      p.scale = scales;
+      p.scale = nullptr;
+      p.amax_bits = am[part];
       p.scale_bh_stride = l.fp8_block ? 1 : 0;
-      FUSP_CHECK(launch_pack(p, s));
+      p.trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
+      p.trailer_stride = int64_t(l.slot_stride / 4);
+      ops[nops++] = p;
     }
+    FUSP_CHECK(launch_pack_multi(ops, nops, s));
   }
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
