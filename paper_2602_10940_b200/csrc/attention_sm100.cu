@@ -52,7 +52,12 @@ constexpr int kBM = 128;   // rows per Q tile (one softmax warpgroup)
 constexpr int kQB = 2 * kBM;  // rows per q-block (one CTA work item)
 constexpr int kBN = 128;   // keys per KV tile
 constexpr int kD = 128;    // head dim
-constexpr int kStages = 2; // KV ring depth
+#ifndef FUSP_SPLIT_S  // 1: S_t(j+1) in two 64-key halves, the upper half issued while the
+#define FUSP_SPLIT_S 1   // softmax still works on S_t(j); P.V in two 64-key halves
+#endif
+constexpr bool kSplitS = FUSP_SPLIT_S != 0;
+constexpr int kStages = 2;  // V ring depth
+constexpr int kKStages = kSplitS ? 3 : 2;  // K ring depth (split S: K(j+1) is read one step early)
 constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: [2 halves][128 rows][128 B]
 constexpr uint32_t kHalfBytes = kTileBytes / 2;
@@ -83,12 +88,13 @@ constexpr size_t kSlotBytes = size_t(2) * kSlotTileFloats * 4;  // both tiles of
 
 struct __align__(1024) Smem {
   uint8_t q[2][kTileBytes];
-  uint8_t k[kStages][kTileBytes];
+  uint8_t k[kKStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
   uint64_t q_full[2], q_empty[2];
-  uint64_t k_full[kStages], k_empty[kStages];
+  uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2], o_done[2];
+  uint64_t s_read[2], p_half[2];  // split S: S_t loaded by the softmax / first half of P_t stored
   uint32_t tmem_base;
   uint32_t ticket[2];
 };
@@ -128,6 +134,12 @@ __device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (p
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
   return t;
 }
+#ifndef FUSP_TRACE_AT  // debug: which softmax point the per-step trace's 2nd event records
+#define FUSP_TRACE_AT 0  // (0 P published, 1 S loaded, 2 row max, 3 exp loop done)
+#endif
+#ifndef FUSP_TRACE_EPI  // debug: epilogue sub-steps into the (whole-mode unused) slots 3..6
+#define FUSP_TRACE_EPI 0
+#endif
 #define FUSP_TRACE(p, slot)                                                        \
   do {                                                                             \
     if ((p).trace != nullptr) (p).trace[blockIdx.x * kTraceSlots + (slot)] = gtimer(); \
@@ -221,11 +233,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_empty[t], 1);
       mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], kBM);
+      mbar_init(&sm.s_read[t], kBM);
+      mbar_init(&sm.p_half[t], kBM);
       mbar_init(&sm.o_done[t], 1);
     }
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
@@ -262,8 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_3d(sm.q[t] + h * kHalfBytes, &tm_q, &sm.q_full[t], h * 64, row0 + t * kBM, head);
         }
         for (int j = g.j0; j < g.j1; ++j, ++it) {
-          const int st = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
+          const int st = it % kKStages;
+          const uint32_t ph = (it / kKStages) & 1;
           mbar_wait(&sm.k_empty[st], ph ^ 1);
           mbar_expect_tx(&sm.k_full[st], kTileBytes);
           for (int h = 0; h < 2; ++h)
@@ -324,6 +340,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
+    // Split S: S_t[:, 64 half ..] = Q_t K[64 half ..]^T (N = 64) into S_t columns 64 half ..
+    const uint32_t idesc_qk_h = (idesc_qk & ~(0x3Fu << 17)) | ((64u >> 3) << 17);
+    auto issue_qk_half = [&](int t, int sk, int half) {
+      const uint64_t qdesc = umma_desc_sw128(smem_u32(sm.q[t]), 16, 1024);
+      const uint64_t kdesc = umma_desc_sw128(smem_u32(sm.k[sk]) + half * 64 * 128, 16, 1024);
+      if (elect_one()) {
+#pragma unroll kMmaUnroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint64_t off16 = ((k >> 2) * kHalfBytes + (k & 3) * 32) / 16;
+          mma_ss(kTmemS + t * 128 + half * 64, qdesc + off16, kdesc + off16, idesc_qk_h, k > 0 ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    };
+    // O_t (+)= P_t[:, keys 64 half ..] V[keys 64 half ..]
+    auto issue_pv_half = [&](int t, int st, int half, bool first) {
+      const uint64_t vdesc = umma_desc_sw128(smem_u32(sm.v[st]), kHalfBytes, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = half * 4; k < half * 4 + 4; ++k)
+          mma_ts(kTmemO + t * 128, kTmemS + t * 128 + k * 8, vdesc + uint64_t(k * 16 * 128 / 16),
+                 idesc_pv, (!first || k > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
     auto commit = [&](uint64_t* bar) {  // elect.sync picks the same lane as the MMAs
       if (elect_one()) mma_commit(bar);
       __syncwarp();
@@ -331,42 +372,95 @@ __global__ void __launch_bounds__(kThreads, 1)
     SegIter si(sc);
     Seg g;
     uint32_t it = 0, ns = 0;
-    while (si.next(sc, g)) {
-      for (int j = g.j0; j < g.j1; ++j, ++it) {
-        const int st = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
-        mbar_wait(&sm.k_full[st], ph);
-        tc_fence_after();
-        for (int t = 0; t < 2; ++t) {
-          if (j > g.j0) {
-            // O_t += P_t(j-1) V(j-1): needs the softmax to have published P_t(j-1)
-            const uint32_t ip = it - 1;
-            mbar_wait(&sm.p_full[t], ip & 1);
-            if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
-            tc_fence_after();
-            issue_pv(t, ip % kStages, j - 1 == g.j0);
-            if (t == 1) commit(&sm.v_empty[ip % kStages]);
-          } else {
+    if constexpr (kSplitS) {
+      // Per tile t and KV step j (it = global step):
+      //   [S_t(j+1) keys 64..127 -> columns 64..127]   once the softmax has loaded S_t(j)
+      //   O_t (+)= P_t(j)[keys 0..63] V                 once the first half of P_t(j) is out
+      //   O_t  += P_t(j)[keys 64..127] V                once all of P_t(j) is out
+      //   [S_t(j+1) keys 0..63 -> columns 0..63]        (P_t(j) lives there: after the P.V)
+      // so only 2 of the 4 64-key MMA groups sit between "P_t(j) published" and "S_t(j+1)
+      // complete" -- the dependency chain that bounds the kernel.
+      while (si.next(sc, g)) {
+        {
+          const int sk = it % kKStages;
+          mbar_wait(&sm.k_full[sk], (it / kKStages) & 1);
+          tc_fence_after();
+          for (int t = 0; t < 2; ++t) {
             mbar_wait(&sm.q_full[t], ns & 1);
             tc_fence_after();
+            issue_qk(t, sk);
+            commit(&sm.s_full[t]);
           }
-          // S_t = Q_t K_j^T  (executes after PV_t(j-1) has read P_t: tcgen05.mma is in-order)
-          issue_qk(t, st);
-          commit(&sm.s_full[t]);
-          if (j == g.j1 - 1) commit(&sm.q_empty[t]);  // Q_t may be reloaded
         }
-        commit(&sm.k_empty[st]);
+        for (int j = g.j0; j < g.j1; ++j, ++it) {
+          const bool nxt = j + 1 < g.j1;
+          const int st = it % kStages, sk = it % kKStages, sn = (it + 1) % kKStages;
+          if (nxt) {
+            mbar_wait(&sm.k_full[sn], ((it + 1) / kKStages) & 1);
+            tc_fence_after();
+          }
+          for (int t = 0; t < 2; ++t) {
+            if (nxt) {
+              mbar_wait(&sm.s_read[t], it & 1);
+              tc_fence_after();
+              issue_qk_half(t, sn, 1);
+            }
+            mbar_wait(&sm.p_half[t], it & 1);
+            if (t == 0) mbar_wait(&sm.v_full[st], (it / kStages) & 1);
+            tc_fence_after();
+            issue_pv_half(t, st, 0, j == g.j0);
+            mbar_wait(&sm.p_full[t], it & 1);
+            tc_fence_after();
+            issue_pv_half(t, st, 1, false);
+            if (nxt) {
+              issue_qk_half(t, sn, 0);
+              commit(&sm.s_full[t]);
+            } else {
+              commit(&sm.o_done[t]);  // (Q_t is released by the softmax warpgroup)
+            }
+          }
+          commit(&sm.k_empty[sk]);  // S(j) was issued in the previous step / segment start
+          commit(&sm.v_empty[st]);
+        }
+        ++ns;
       }
-      const uint32_t ip = it - 1;
-      for (int t = 0; t < 2; ++t) {
-        mbar_wait(&sm.p_full[t], ip & 1);
-        if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
-        tc_fence_after();
-        issue_pv(t, ip % kStages, g.j1 - 1 == g.j0);
-        commit(&sm.o_done[t]);
+    } else {
+      while (si.next(sc, g)) {
+        for (int j = g.j0; j < g.j1; ++j, ++it) {
+          const int st = it % kStages;
+          const int sk = it % kKStages;
+          mbar_wait(&sm.k_full[sk], (it / kKStages) & 1);
+          tc_fence_after();
+          for (int t = 0; t < 2; ++t) {
+            if (j > g.j0) {
+              // O_t += P_t(j-1) V(j-1): needs the softmax to have published P_t(j-1)
+              const uint32_t ip = it - 1;
+              mbar_wait(&sm.p_full[t], ip & 1);
+              if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
+              tc_fence_after();
+              issue_pv(t, ip % kStages, j - 1 == g.j0);
+              if (t == 1) commit(&sm.v_empty[ip % kStages]);
+            } else {
+              mbar_wait(&sm.q_full[t], ns & 1);
+              tc_fence_after();
+            }
+            // S_t = Q_t K_j^T  (executes after PV_t(j-1) has read P_t: tcgen05.mma is in-order)
+            issue_qk(t, sk);
+            commit(&sm.s_full[t]);
+          }
+          commit(&sm.k_empty[sk]);
+        }
+        const uint32_t ip = it - 1;
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&sm.p_full[t], ip & 1);
+          if (t == 0) mbar_wait(&sm.v_full[ip % kStages], (ip / kStages) & 1);
+          tc_fence_after();
+          issue_pv(t, ip % kStages, g.j1 - 1 == g.j0);
+          commit(&sm.o_done[t]);
+        }
+        commit(&sm.v_empty[ip % kStages]);
+        ++ns;
       }
-      commit(&sm.v_empty[ip % kStages]);
-      ++ns;
     }
   }
   } else {
@@ -403,6 +497,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
         tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
         tmem_wait_ld();
+        if (FUSP_TRACE_AT == 1 && tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
+        if constexpr (kSplitS) {  // S_t(j) is in registers: the MMA may overwrite columns 64..127
+          tc_fence_before();
+          mbar_arrive(&sm.s_read[t]);
+        }
         const int valid = p.skv - j * kBN;  // keys in this tile (mask the tail)
         if (valid < kBN) {
 #pragma unroll
@@ -418,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mx4[i] = fmaxf(mx4[i], fmaxf(__uint_as_float(s[c + i]), __uint_as_float(s[c + 4 + i])));
         }
         const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        if (FUSP_TRACE_AT == 2 && tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
         // Lazy rescale: keep the old max unless the new one exceeds it by > 8 (log2 units).
         float alpha = 1.f;
         if (m_use == -INFINITY) {
@@ -425,6 +525,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if ((mx - m_use) * sl2 > kRescaleThreshold) {
           alpha = ex2((m_use - mx) * sl2);
           m_use = mx;
+        }
+        if constexpr (kSplitS) {
+          // Rescale O before the first half of P is published (that half's P.V follows it).
+          // PV_t(j-1) has completed: the s_full commit for S_t(j) covers every MMA before it.
+          if (__any_sync(0xffffffffu, alpha != 1.f) && j > g.j0) {
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(t_o + c * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(t_o + c * 32, o);
+            }
+          }
         }
         const float neg_m = -m_use * sl2;
         const float2 negm2 = make_float2(neg_m, neg_m);
@@ -439,15 +554,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                              : make_float2(ex2(x.x), ex2(x.y));
           acc[pi & 3] = fadd2(acc[pi & 3], pp);
           s[pi] = pack_f16x2(pp.x, pp.y);  // P packs into the first 64 slots
-          if (pi == 31) tmem_st32(t_s + 0, &s[0]);  // first half of P goes out early
+          if (pi == 31) {  // first half of P goes out early
+            tmem_st32(t_s + 0, &s[0]);
+            if constexpr (kSplitS) {
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&sm.p_half[t]);
+            }
+          }
         }
+        if (FUSP_TRACE_AT == 3 && tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
         tmem_st32(t_s + 32, &s[32]);
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
         // Rescale the O accumulator when the max moved. PV_t(j-1) has completed: the
         // s_full commit for S_t(j) covers every MMA issued before it.
-        if (__any_sync(0xffffffffu, alpha != 1.f) && j > g.j0) {
+        if (!kSplitS && __any_sync(0xffffffffu, alpha != 1.f) && j > g.j0) {
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
@@ -460,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_st();
         tc_fence_before();
-        if (tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
+        if (FUSP_TRACE_AT == 0 && tr && ns == 0 && j - g.j0 < 64) FUSP_TRACE(p, 72 + t * 128 + 2 * (j - g.j0) + 1);
         mbar_arrive(&sm.p_full[t]);
       }
 
@@ -468,6 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&sm.o_done[t], ns & 1);
       tc_fence_after();
       if (tr) FUSP_TRACE(p, tslot + 2);
+      // Every MMA of the segment has completed: Q_t may be reloaded.
+      if (r_in_tile == 0) mbar_arrive(&sm.q_empty[t]);
       ++ns;
       int nseg = 1, kself = 0, c_first = 0;
       if (sc.split) {
@@ -649,12 +774,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
                             static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
                             static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
+      const bool o16 = p.out_dtype != FUSP_F32;  // (uniform) 16-bit O: transposed stores
+      // 16-bit O leaves through stores where 4 lanes write one row's 64 contiguous bytes of a
+      // 32-column chunk (8 rows per instruction instead of 32): row addresses of the 4-lane group
+      int64_t ob_g[4];
+      bool in_g[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ob_g[i] = __shfl_sync(0xffffffffu, obase, (lane & ~3) + i);
+        in_g[i] = row - (lane & 3) + i < p.sq;
+      }
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t o[32];
         tmem_ld32(t_o + c * 32, o);
         tmem_wait_ld();
-        if (!in_range) continue;
+        if (FUSP_TRACE_EPI && tr && c == 0) FUSP_TRACE(p, tslot + 3);
+        if (!in_range && !o16) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]);
@@ -671,26 +807,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * i + 3] = fmaf(c_acc, a.w, v[4 * i + 3]);
           }
         }
-        if (p.out_dtype == FUSP_F32) {
+        if (o16) {
+          const bool f16 = p.out_dtype == FUSP_F16;
+          uint32_t w[16];  // piece q (16 B) = words 4q..4q+3 = columns 32c + 8q ..
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            w[e] = f16 ? pack_f16x2(v[2 * e], v[2 * e + 1]) : pack_bf16x2(v[2 * e], v[2 * e + 1]);
+          // 4x4 transpose of 16-byte pieces inside each 4-lane group (butterfly, xor 2 then 1):
+          // afterwards lane 4G+e holds piece e of the group's rows 4G+0..3 in w[4i..4i+3]
+#pragma unroll
+          for (int m = 2; m >= 1; m >>= 1) {
+            const bool hi = (lane & m) != 0;
+#pragma unroll
+            for (int q0 = 0; q0 < 4; ++q0) {
+              if (q0 & m) continue;
+              const int q1 = q0 | m;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t y = __shfl_xor_sync(0xffffffffu, hi ? w[4 * q0 + k] : w[4 * q1 + k], m);
+                if (hi) w[4 * q0 + k] = y;
+                else w[4 * q1 + k] = y;
+              }
+            }
+          }
+          uint16_t* o16p = static_cast<uint16_t*>(p.out);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (in_g[i])
+              *reinterpret_cast<uint4*>(o16p + ob_g[i] + c * 32 + (lane & 3) * 8) =
+                  make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        } else {
           float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + obase + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + obase + c * 32);
-          const bool f16 = p.out_dtype == FUSP_F16;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a = v[8 * i + 2 * e], b = v[8 * i + 2 * e + 1];
-              w[e] = f16 ? pack_f16x2(a, b) : pack_bf16x2(a, b);
-            }
-            dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
         }
       }
+      if (FUSP_TRACE_EPI && tr) FUSP_TRACE(p, tslot + 4);
       if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
       if (tr) FUSP_TRACE(p, tslot + 7);
       tc_fence_before();
