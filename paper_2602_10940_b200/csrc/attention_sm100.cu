@@ -145,6 +145,29 @@ __device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (p
     if ((p).trace != nullptr) (p).trace[blockIdx.x * kTraceSlots + (slot)] = gtimer(); \
   } while (0)
 
+// 4x4 transpose of W-word pieces inside each 4-lane group (butterfly, xor 2 then 1): lane 4G+e
+// holding piece q of row 4G+e in w[W q ..] ends up holding piece e of row 4G+q there (and
+// back: the transpose is an involution).  Turns row-per-thread TMEM data into stores / loads
+// where 4 lanes cover one row's 4 W-word pieces -- 8 rows per instruction instead of 32.
+template <int W>
+__device__ __forceinline__ void xpose4(uint32_t (&w)[4 * W], int lane) {
+#pragma unroll
+  for (int m = 2; m >= 1; m >>= 1) {
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int q0 = 0; q0 < 4; ++q0) {
+      if (q0 & m) continue;
+      const int q1 = q0 | m;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, hi ? w[W * q0 + k] : w[W * q1 + k], m);
+        if (hi) w[W * q0 + k] = y;
+        else w[W * q1 + k] = y;
+      }
+    }
+  }
+}
+
 // ---- schedule (identical in every role) -------------------------------------------------
 // The CTA whose unit range holds unit u: max c with begin[c] <= u (estimate, then correct).
 __device__ __forceinline__ int sk_cta_of(const Sched& s, int u) {
@@ -764,83 +787,80 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float lse_b = m_fin * (sl2 * 0.69314718055994530942f) + logf(l_fin);
       const float inv_l = 1.f / l_fin;
       float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
-      const float* acc_row = nullptr;
       if (p.acc_o != nullptr && in_range) {
         const float l1 = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
         lse_out = merge_coeffs(l1, lse_b, c_acc, c_new);
-        acc_row = p.acc_o + (static_cast<int64_t>(head) * p.sq + row) * kD;
       }
       const float scale_new = c_new * inv_l;
       const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
                             static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
                             static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
-      const bool o16 = p.out_dtype != FUSP_F32;  // (uniform) 16-bit O: transposed stores
-      // 16-bit O leaves through stores where 4 lanes write one row's 64 contiguous bytes of a
-      // 32-column chunk (8 rows per instruction instead of 32): row addresses of the 4-lane group
+      // O leaves (and the ring accumulator comes in) through accesses where the 4 lanes of a
+      // group cover one row's contiguous 32-column chunk: row addresses of the group's 4 rows
+      const int e4 = lane & 3;
       int64_t ob_g[4];
       bool in_g[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         ob_g[i] = __shfl_sync(0xffffffffu, obase, (lane & ~3) + i);
-        in_g[i] = row - (lane & 3) + i < p.sq;
+        in_g[i] = row - e4 + i < p.sq;
       }
+      const float* acc_h = p.acc_o != nullptr ? p.acc_o + static_cast<int64_t>(head) * p.sq * kD : nullptr;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t o[32];
         tmem_ld32(t_o + c * 32, o);
         tmem_wait_ld();
         if (FUSP_TRACE_EPI && tr && c == 0) FUSP_TRACE(p, tslot + 3);
-        if (!in_range && !o16) continue;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]);
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * scale_new;
+        if (acc_h != nullptr) {  // merge_lse: O = c_acc * acc + c_new * O / l
+          uint32_t a[32];        // piece e (8 floats) of rows 4G+i, then transposed to own row
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= scale_new;
-        if (acc_row != nullptr) {
-          const float4* a4 = reinterpret_cast<const float4*>(acc_row + c * 32);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 a = a4[i];
-            v[4 * i + 0] = fmaf(c_acc, a.x, v[4 * i + 0]);
-            v[4 * i + 1] = fmaf(c_acc, a.y, v[4 * i + 1]);
-            v[4 * i + 2] = fmaf(c_acc, a.z, v[4 * i + 2]);
-            v[4 * i + 3] = fmaf(c_acc, a.w, v[4 * i + 3]);
+          for (int i = 0; i < 4; ++i) {
+            float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+            if (in_g[i]) {
+              const float4* src =
+                  reinterpret_cast<const float4*>(acc_h + static_cast<int64_t>(row - e4 + i) * kD + c * 32 + e4 * 8);
+              x0 = src[0];
+              x1 = src[1];
+            }
+            a[8 * i + 0] = __float_as_uint(x0.x); a[8 * i + 1] = __float_as_uint(x0.y);
+            a[8 * i + 2] = __float_as_uint(x0.z); a[8 * i + 3] = __float_as_uint(x0.w);
+            a[8 * i + 4] = __float_as_uint(x1.x); a[8 * i + 5] = __float_as_uint(x1.y);
+            a[8 * i + 6] = __float_as_uint(x1.z); a[8 * i + 7] = __float_as_uint(x1.w);
           }
+          xpose4<8>(a, lane);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaf(c_acc, __uint_as_float(a[i]), v[i]);
         }
-        if (o16) {
+        if (p.out_dtype != FUSP_F32) {
           const bool f16 = p.out_dtype == FUSP_F16;
           uint32_t w[16];  // piece q (16 B) = words 4q..4q+3 = columns 32c + 8q ..
 #pragma unroll
           for (int e = 0; e < 16; ++e)
             w[e] = f16 ? pack_f16x2(v[2 * e], v[2 * e + 1]) : pack_bf16x2(v[2 * e], v[2 * e + 1]);
-          // 4x4 transpose of 16-byte pieces inside each 4-lane group (butterfly, xor 2 then 1):
-          // afterwards lane 4G+e holds piece e of the group's rows 4G+0..3 in w[4i..4i+3]
-#pragma unroll
-          for (int m = 2; m >= 1; m >>= 1) {
-            const bool hi = (lane & m) != 0;
-#pragma unroll
-            for (int q0 = 0; q0 < 4; ++q0) {
-              if (q0 & m) continue;
-              const int q1 = q0 | m;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t y = __shfl_xor_sync(0xffffffffu, hi ? w[4 * q0 + k] : w[4 * q1 + k], m);
-                if (hi) w[4 * q0 + k] = y;
-                else w[4 * q1 + k] = y;
-              }
-            }
-          }
+          xpose4<4>(w, lane);
           uint16_t* o16p = static_cast<uint16_t*>(p.out);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             if (in_g[i])
-              *reinterpret_cast<uint4*>(o16p + ob_g[i] + c * 32 + (lane & 3) * 8) =
+              *reinterpret_cast<uint4*>(o16p + ob_g[i] + c * 32 + e4 * 8) =
                   make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         } else {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + obase + c * 32);
+          uint32_t w[32];  // piece q (32 B) = floats 8q..8q+7
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
+          xpose4<8>(w, lane);
+          float* o32p = static_cast<float*>(p.out);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (in_g[i]) {
+              uint4* dst = reinterpret_cast<uint4*>(o32p + ob_g[i] + c * 32 + e4 * 8);
+              dst[0] = make_uint4(w[8 * i], w[8 * i + 1], w[8 * i + 2], w[8 * i + 3]);
+              dst[1] = make_uint4(w[8 * i + 4], w[8 * i + 5], w[8 * i + 6], w[8 * i + 7]);
+            }
         }
       }
       if (FUSP_TRACE_EPI && tr) FUSP_TRACE(p, tslot + 4);
