@@ -67,7 +67,8 @@ fusp_status fusp_attention_schedule(int mode, int max_ctas);
 /* Debug timeline (no reference counterpart): enable != 0 records per-CTA globaltimer events
  * of subsequent attention launches; copies up to n u64 events of the last launch to host
  * (layout: 72 per CTA = start, end, [8 segments][2 Q tiles][start, first S, O done, stored]).
- * Returns the number copied. */
+ * Returns the number copied; -2 in the shipped library, where the tracing is compiled out (a
+ * debug build: nvcc -DFUSP_TRACE_BUILD=1, tools/build_variants.sh trace:-DFUSP_TRACE_BUILD=1). */
 int fusp_attention_trace(int enable, uint64_t* host, size_t n);
 
 /* ---- FP8 E4M3 codec (fp8.hpp:23-49) ---------------------------------------------------- */

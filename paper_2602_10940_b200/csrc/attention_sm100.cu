@@ -140,9 +140,13 @@ __device__ __forceinline__ unsigned long long gtimer() {  // SM cycle counter (p
 #ifndef FUSP_TRACE_EPI  // debug: epilogue sub-steps into the (whole-mode unused) slots 3..6
 #define FUSP_TRACE_EPI 0
 #endif
+#ifndef FUSP_TRACE_BUILD  // 1: per-CTA clock64 tracing compiled in (a debug build: the trace
+#define FUSP_TRACE_BUILD 0   // checks cost 1-2 % in the KV loop); 0: fusp_attention_trace returns -2
+#endif
 #define FUSP_TRACE(p, slot)                                                        \
   do {                                                                             \
-    if ((p).trace != nullptr) (p).trace[blockIdx.x * kTraceSlots + (slot)] = gtimer(); \
+    if (FUSP_TRACE_BUILD && (p).trace != nullptr)                                  \
+      (p).trace[blockIdx.x * kTraceSlots + (slot)] = gtimer();                     \
   } while (0)
 
 // 4x4 transpose of W-word pieces inside each 4-lane group (butterfly, xor 2 then 1): lane 4G+e
@@ -1037,6 +1041,7 @@ fusp_status ensure_counters(CounterBuf& b, size_t words) {
 
 // Debug timeline: per-CTA globaltimer events of the most recent traced launch.
 int attention_trace(int enable, unsigned long long* host, size_t n) {
+  if (!FUSP_TRACE_BUILD) return -2;  // tools/build_variants.sh trace:-DFUSP_TRACE_BUILD=1
   g_trace_on = enable != 0;
   if (host != nullptr && g_trace != nullptr) {
     const size_t m = n < size_t(kMaxGrid) * kTraceSlots ? n : size_t(kMaxGrid) * kTraceSlots;

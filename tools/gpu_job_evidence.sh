@@ -1,6 +1,7 @@
 # Round evidence: GPU tests, smoke, bench (both arms), ncu launch list, ncu --set full of the
 # attention kernel on the bench workload and on the FLUX U=8 per-rank shape (stream-K split),
 # virtual-mesh measurements. Outputs in gpurun_out/.
+# (build the traced variant first: bash tools/build_variants.sh trace:-DFUSP_TRACE_BUILD=1)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpuinfo.txt 2>&1
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
@@ -11,6 +12,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:attn_fwd -s 3 -c 1 -o gpurun_out/attn_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_full.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_fwd -s 3 -c 1 -o gpurun_out/attn_u8_split -f python tools/attn_once.py 3 4608 auto > gpurun_out/ncu_u8.log 2>&1
 timeout 600 python tools/virtual_mesh_bench.py > gpurun_out/vmesh.jsonl 2> gpurun_out/vmesh.err
-timeout 120 python tools/attn_trace.py 3 4608 auto > gpurun_out/trace_u8.txt 2>&1
+FUSP_VARIANT=trace timeout 120 python tools/attn_trace.py 3 4608 auto > gpurun_out/trace_u8.txt 2>&1
 tail -3 gpurun_out/gpu_tests.log; tail -3 gpurun_out/smoke.log; cat gpurun_out/bench.json; cut -c1-300 gpurun_out/bench_ref.json; ls -la gpurun_out/*.ncu-rep
 timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1
