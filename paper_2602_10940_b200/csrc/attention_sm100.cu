@@ -35,6 +35,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
+#include <array>
+#include <map>
 #include <mutex>
 #include <vector>
 #include <cuda_bf16.h>
@@ -981,7 +984,21 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   const bool have_ws = a.split_ws != nullptr && need > 0 && a.split_ws_bytes >= need &&
                        a.split_counters != nullptr &&
                        a.split_counter_words >= attention_counter_words(a.heads, a.sq);
-  const Plan pl = plan_attention(a.heads, a.sq, a.skv, have_ws, a.max_ctas);
+  // plans are pure functions of the shape and the knobs: cached (no per-launch host work)
+  Plan pl;
+  {
+    static std::mutex mu;
+    static std::map<std::array<int, 8>, Plan> cache;
+    const std::array<int, 8> key{a.heads, a.sq, a.skv, have_ws ? 1 : 0, a.max_ctas, g_sched_mode,
+                                 g_max_ctas, sm_count()};
+    std::lock_guard<std::mutex> lk(mu);
+    auto itp = cache.find(key);
+    if (itp == cache.end()) {
+      if (cache.size() > 256) cache.clear();
+      itp = cache.emplace(key, plan_attention(a.heads, a.sq, a.skv, have_ws, a.max_ctas)).first;
+    }
+    pl = itp->second;
+  }
   p.sc = pl.sc;
   if (pl.sc.split) {
     p.counters = a.split_counters;
