@@ -227,6 +227,13 @@ __device__ __forceinline__ void wg_bar(int t) {
   if (t == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
   else asm volatile("bar.sync 2, 128;" ::: "memory");
 }
+// Ticket: release orders this warpgroup's slot stores (seen through the preceding bar.sync)
+// before the count; acquire orders the last arriver's slot reads after it.
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -667,9 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tr) FUSP_TRACE(p, tslot + 4);
           wg_bar(t);  // the warpgroup's stores happen-before thread 0's release (cumulativity)
           if (r_in_tile == 0) {
-            __threadfence();
-            sm.ticket[t] = atomicAdd(&cnt[0], 1u);
-            __threadfence();
+            sm.ticket[t] = atom_add_acq_rel(&cnt[0], 1u);
           }
           wg_bar(t);
           published = true;
