@@ -1087,9 +1087,17 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   // (second copy stream).  Chunks are a multiple of the Ulysses degree so every chunk is a
   // valid USP layer; every rank picks the same chunking, so collectives stay matched.
   const int U = c->world / (ring_dim > 0 ? ring_dim : 1);
+  // At most 4 chunks (tuning knob FUSP_HOST_CHUNKS): PCIe moves larger copies faster (FLUX
+  // U=1: H2D per chunk ~50 GB/s at 4 chunks, ~45 GB/s at 8 with the D2H running alongside), and
+  // that outweighs the longer pipeline tail -- 1.88 ms per layer vs 2.10 ms at 8 chunks.
+  static const int max_chunks = [] {
+    const char* e = getenv("FUSP_HOST_CHUNKS");
+    const int n = e ? atoi(e) : 4;
+    return n > 0 ? n : 4;
+  }();
   int hc = static_cast<int>(ls.h);
   for (int cand = U; cand <= ls.h; cand += U)
-    if (ls.h % cand == 0 && ls.h / cand <= 8) { hc = cand; break; }
+    if (ls.h % cand == 0 && ls.h / cand <= max_chunks) { hc = cand; break; }
   const int nch = static_cast<int>(ls.h / hc);
   const size_t esz_in = dtype_size(in_dtype), esz_out = dtype_size(out_dt);
   const size_t head_elems = size_t(ls.s * ls.d);
@@ -1144,9 +1152,14 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
     if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[b], 0));
     const void* src[3] = {q, k, v};
     void* dst[3] = {dq, dk, dv};
-    for (int t = 0; t < 3; ++t)
-      FUSP_CUDA(cudaMemcpy2DAsync(dst[t], chunk_in / ls.b, static_cast<const char*>(src[t]) + off_in,
-                                  pitch_in, chunk_in / ls.b, ls.b, cudaMemcpyHostToDevice, st.h2d));
+    for (int t = 0; t < 3; ++t) {
+      if (ls.b == 1)
+        FUSP_CUDA(cudaMemcpyAsync(dst[t], static_cast<const char*>(src[t]) + off_in, chunk_in,
+                                  cudaMemcpyHostToDevice, st.h2d));
+      else
+        FUSP_CUDA(cudaMemcpy2DAsync(dst[t], chunk_in / ls.b, static_cast<const char*>(src[t]) + off_in,
+                                    pitch_in, chunk_in / ls.b, ls.b, cudaMemcpyHostToDevice, st.h2d));
+    }
     FUSP_CUDA(cudaEventRecord(st.in_ready[b], st.h2d));
     FUSP_CUDA(cudaStreamWaitEvent(s, st.in_ready[b], 0));
     // slot b's output was last read by the D2H of chunk i-2
@@ -1160,8 +1173,12 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
     FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, dq, dk, dv, in_dtype, cs, dout, nullptr, &o, s));
     FUSP_CUDA(cudaEventRecord(st.computed[b], s));
     FUSP_CUDA(cudaStreamWaitEvent(st.d2h, st.computed[b], 0));
-    FUSP_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + off_out, pitch_out, dout, chunk_out / ls.b,
-                                chunk_out / ls.b, ls.b, cudaMemcpyDeviceToHost, st.d2h));
+    if (ls.b == 1)
+      FUSP_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + off_out, dout, chunk_out, cudaMemcpyDeviceToHost,
+                                st.d2h));
+    else
+      FUSP_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + off_out, pitch_out, dout, chunk_out / ls.b,
+                                  chunk_out / ls.b, ls.b, cudaMemcpyDeviceToHost, st.d2h));
     FUSP_CUDA(cudaEventRecord(st.out_done[b], st.d2h));
   }
   FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[(nch - 1) % 2], 0));
