@@ -783,6 +783,24 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.scales[z]) a.scales[z][blk] = qs;
   const int64_t base = int64_t(blk) * a.block_vecs;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const Fp8Src& s = a.src[z];
+  if (s.dt == FUSP_E4M3) {
+    // Ring hop (protocols.cpp:113-115): codes = encode(RN(decode(c) * s_src) / s_new).  When
+    // s_new == s_src the result is c itself: RN(RN(d * s) / s) = d (1 + e), |e| <= 2^-23, and
+    // every E4M3 neighbour of d is >= 2^-4 away relatively (2^-9 absolutely near 0; 448 is
+    // the saturation value), so the nearest code is d's own -- the vector is copied.  After the
+    // first hop every segment of a chunk shares the chunk's scale, so later hops are copies.
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
+      const int64_t i = (base + v) * 8;
+      const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
+      const uint32_t bh = row / static_cast<uint32_t>(s.span);
+      const int r = static_cast<int>(row - bh * s.span);
+      const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i));
+      *reinterpret_cast<uint2*>(a.codes[z] + i) = sc == qs ? w : encode8_finite(decode8(w, sc), qs, inv);
+    }
+    return;
+  }
   for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
     Vec8 x[4];
 #pragma unroll
