@@ -89,6 +89,13 @@ fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n
 fusp_status fusp_dequantize_e4m3_blocks(const uint8_t* codes, const float* scales_dev, int64_t n,
                                         int64_t block, void* y, fusp_dtype dtype,
                                         fusp_stream_t stream);
+/* Ring-hop re-quantization (protocols.cpp:113-115, 309-310): quantize(dequantize(chunk)) where
+ * every run of `seg` consecutive codes carries its own scale seg_scales_dev[i / seg] (the
+ * resharded chunk holds rows from several senders) -> one scale *scale_dev and codes_out.
+ * Bit-exact with uspsim::quantize of the dequantized f32 values; seg % 8 == 0, n % seg == 0. */
+fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_dev, int64_t n,
+                                 int64_t seg, uint8_t* codes_out, float* scale_dev,
+                                 fusp_stream_t stream);
 /* dequantize (fp8.cpp:125-130): y = decode(code) * (*scale_dev), written as `dtype`. */
 fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, int64_t n, void* y,
                                  fusp_dtype dtype, fusp_stream_t stream);

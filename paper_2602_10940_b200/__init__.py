@@ -8,7 +8,7 @@ from ._lib import (BF16, E4M3, F16, F32, FabricError, FuspError, InvalidArgument
 from .api import (AttnResult, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGroup,
                   QKPrologue, QuantizedTensor, rope_tables, RunReport, WorkerContext, attention_reference,
                   attention_schedule, attention_with_lse, build_mesh, decode_e4m3, dequantize, dequantize_blocks,
-                  encode_e4m3, quantize_blocks,
+                  encode_e4m3, quantize_blocks, requantize,
                   gather_output, kernel_launch_count, make_mesh, merge_lse, quantize,
                   ring_attention_pipelined, ring_attention_serial, run_protocol, split_sequence,
                   ulysses_attention, usp_attention, usp_attention_host, out_projection,

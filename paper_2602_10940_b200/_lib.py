@@ -90,6 +90,7 @@ _SIGS = {
     "fusp_decode_e4m3": (ctypes.c_int, [_P, _I64, _P, _P]),
     "fusp_quantize_e4m3": (ctypes.c_int, [_P, ctypes.c_int, _I64, _P, _P, ctypes.c_int, _P]),
     "fusp_dequantize_e4m3": (ctypes.c_int, [_P, _P, _I64, _P, ctypes.c_int, _P]),
+    "fusp_requantize_e4m3": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
     "fusp_quantize_e4m3_blocks": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, _P, _P]),
     "fusp_dequantize_e4m3_blocks": (ctypes.c_int, [_P, _P, _I64, _I64, _P, ctypes.c_int, _P]),
     "fusp_attention_with_lse": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, Shape4, _I64, _P,

@@ -116,6 +116,17 @@ def dequantize_blocks(codes: torch.Tensor, scales: torch.Tensor, block: int,
     return out
 
 
+def requantize(codes: torch.Tensor, seg_scales: torch.Tensor, seg: int) -> QuantizedTensor:
+    """Ring-hop re-quantization (protocols.cpp:113-115, 309-310): quantize(dequantize(chunk))
+    where every run of `seg` codes carries its own scale seg_scales[i // seg].  Bit-exact."""
+    codes, seg_scales = _dev(codes), _dev(seg_scales).float().contiguous()
+    out = torch.empty(codes.shape, dtype=torch.uint8, device=codes.device)
+    scale = torch.empty(1, dtype=torch.float32, device=codes.device)
+    check(lib().fusp_requantize_e4m3(_ptr(codes), _ptr(seg_scales), codes.numel(), seg, _ptr(out),
+                                     _ptr(scale), _stream()))
+    return QuantizedTensor(out, scale)
+
+
 def dequantize(q: QuantizedTensor, dtype=torch.float32) -> torch.Tensor:
     """dequantize (fp8.cpp:125-130): decode(code) * scale."""
     out = torch.empty(q.codes.shape, dtype=dtype, device=q.codes.device)

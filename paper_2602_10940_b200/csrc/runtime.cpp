@@ -238,6 +238,24 @@ fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n
                              reinterpret_cast<cudaStream_t>(stream));
 }
 
+fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_dev, int64_t n,
+                                 int64_t seg, uint8_t* codes_out, float* scale_dev,
+                                 fusp_stream_t stream) {
+  clear_error();
+  if (seg <= 0 || seg % 8 != 0 || n % seg != 0 || n / 8 >= (int64_t(1) << 31))
+    return set_error(FUSP_ERR_SHAPE, "requantize: segment " + std::to_string(seg) +
+                                         " must be a multiple of 8 dividing " + std::to_string(n));
+  if (n == 0) return FUSP_OK;
+  void* ws = nullptr;
+  FUSP_CHECK(scratch(256, &ws));
+  // the ring-hop source: rows of 8 codes, one bh, a scale per `seg / 8` rows
+  const Fp8Src src{codes, FUSP_E4M3, seg_scales_dev, 1, 0, 8, static_cast<int>(n / 8),
+                   static_cast<int>(seg / 8)};
+  uint32_t* work = static_cast<uint32_t*>(ws);
+  return launch_quantize_fp8_multi(&src, 1, n, n, &work, &scale_dev, &codes_out, nullptr,
+                                   reinterpret_cast<cudaStream_t>(stream));
+}
+
 fusp_status fusp_dequantize_e4m3_blocks(const uint8_t* codes, const float* scales_dev, int64_t n,
                                         int64_t block, void* y, fusp_dtype dtype,
                                         fusp_stream_t stream) {

@@ -276,3 +276,35 @@ def test_quantize_near_rounding_boundaries_bit_exact(cuda, fu):
     got = codes.cpu().numpy()
     bad = np.flatnonzero(got != want)
     assert bad.size == 0, (bad[:5], x[bad[:5]], got[bad[:5]], want[bad[:5]])
+
+
+@pytest.mark.parametrize("seg_scales", [
+    [0.01, 0.01, 0.01, 0.01],          # uniform: a later ring hop, every vector copied
+    [0.01, 0.0371, 0.002, 0.0371],     # the resharded first hop: senders' scales differ
+    [1.0, 1.0],                        # an all-zero chunk re-quantizes to scale 1
+    [3.3e-3, 1.7e-5, 2.9, 0.125, 0.125, 7.0e-2],
+])
+def test_requantize_ring_hop_bit_exact(cuda, fu, seg_scales):
+    # quantize(dequantize(chunk)) of the ring forward (protocols.cpp:113-115, 309-310) on a
+    # chunk whose segments carry different scales: codes and scale bit-exact vs the oracle,
+    # including the copy path taken when a segment's scale equals the new one.
+    rng = np.random.default_rng(len(seg_scales))
+    seg = 1024
+    codes = rng.integers(0, 256, size=seg * len(seg_scales), dtype=np.uint8)
+    codes[(codes & 0x7F) == 0x7F] = 0x7E   # no NaN codes (the reference throws on them)
+    for i in range(len(seg_scales)):       # each sender's chunk reached 448 (its own amax)
+        codes[i * seg + 5] = 0x7E
+    if seg_scales == [1.0, 1.0]:
+        codes[:] = rng.choice(np.array([0x00, 0x80], np.uint8), size=codes.size)
+    sc = np.array(seg_scales, np.float32)
+    x = np.concatenate([R.dequantize(codes[i * seg:(i + 1) * seg], sc[i]) for i in range(len(sc))])
+    want, ws = R.quantize(x)
+    q = fu.requantize(T(codes, torch.uint8), T(sc, torch.float32), seg)
+    assert q.scale == ws
+    got = q.codes.cpu().numpy()
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], want[bad[:5]])
+    # the hop after: same values, one scale -> the codes come back unchanged
+    q2 = fu.requantize(q.codes, q.scale_dev, q.codes.numel())
+    want2, ws2 = R.quantize(R.dequantize(got, np.float32(q.scale)))
+    assert q2.scale == ws2 and np.array_equal(q2.codes.cpu().numpy(), want2)
