@@ -41,6 +41,15 @@ fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType
 // ---- output projection (proj_sm100.cu) ---------------------------------------------------
 fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, const void* w, int n,
                             void* y, int y_dtype, cudaStream_t stream);
+struct QkvDst {  // where the QKV projection writes: plain [B][H][S][128] (u = 1) or Ulysses slots
+  void *q, *k, *v;
+  int qk_dtype, v_dtype;
+  int u;
+  int64_t slot_stride;  // elements between slots
+};
+fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, const void* w, int heads,
+                               const QkvDst& dst, const float* wq, const float* wk, float eps,
+                               const float* cosv, const float* sinv, int64_t pos0, cudaStream_t stream);
 fusp_status launch_qkv_proj(const void* x, int x_dtype, int b, int s, int c, const void* w, int heads,
                             void* q, void* k, void* v, int qkv_dtype, const float* wq, const float* wk,
                             float eps, const float* cosv, const float* sinv, int64_t pos0,

@@ -57,6 +57,9 @@ struct ProjParams {
   // [B][H][S][128] at qkv[part]
   int heads;
   void* qkv[3];
+  int part_dt[3];       // Q, K, V output dtypes (bf16 / f16)
+  int u;                // Ulysses slots: head h -> slot h / (heads / u), position h % (heads / u)
+  int64_t slot_stride;  // elements between slots (u = 1: unused)
   const float* norm_w[2];
   float eps;
   const float* cosv;
@@ -195,8 +198,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
             rinv = rsqrtf(ss * (1.0f / 128) + p.eps);
           }
           const int64_t pos = p.pos0 + s;
-          uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) +
-                          ((static_cast<int64_t>(bb) * p.heads + head) * p.s + s) * 128;
+          const int hp = p.heads / p.u, slot = head / hp, hl = head - slot * hp;
+          uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) + slot * p.slot_stride +
+                          ((static_cast<int64_t>(bb) * hp + hl) * p.s + s) * 128;
+          const bool o_f16 = p.part_dt[part] == FUSP_F16;
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t v[32];
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             uint32_t o16[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              o16[i] = p.y_dtype == FUSP_F16 ? pack_f16x2(x[2 * i], x[2 * i + 1]) : pack_bf16x2(x[2 * i], x[2 * i + 1]);
+              o16[i] = o_f16 ? pack_f16x2(x[2 * i], x[2 * i + 1]) : pack_bf16x2(x[2 * i], x[2 * i + 1]);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               reinterpret_cast<uint4*>(dst + c * 32)[i] = make_uint4(o16[4 * i], o16[4 * i + 1], o16[4 * i + 2], o16[4 * i + 3]);
@@ -357,11 +362,25 @@ fusp_status launch_qkv_proj(const void* x, int x_dtype, int b, int s, int c, con
                             void* q, void* k, void* v, int qkv_dtype, const float* wq, const float* wk,
                             float eps, const float* cosv, const float* sinv, int64_t pos0,
                             cudaStream_t stream) {
+  const QkvDst dst{q, k, v, qkv_dtype, qkv_dtype, 1, 0};
+  return launch_qkv_proj_to(x, x_dtype, b, s, c, w, heads, dst, wq, wk, eps, cosv, sinv, pos0, stream);
+}
+
+// Same, writing Q, K, V straight into the layer's Ulysses send slots (dst.u > 1): head h of
+// part P lands at P's base + (h / hp) * slot_stride + ((b * hp + h % hp) * S + s) * 128.
+fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, const void* w, int heads,
+                               const QkvDst& dst, const float* wq, const float* wk, float eps,
+                               const float* cosv, const float* sinv, int64_t pos0, cudaStream_t stream) {
+  void *q = dst.q, *k = dst.k, *v = dst.v;
+  const int qkv_dtype = dst.qk_dtype;
   if (b <= 0 || s <= 0 || c <= 0 || heads <= 0) return FUSP_OK;
   if (x_dtype != FUSP_BF16 && x_dtype != FUSP_F16)
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: x must be bf16 or f16");
-  if (qkv_dtype != FUSP_BF16 && qkv_dtype != FUSP_F16)
-    return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: Q/K/V must be bf16 or f16");
+  for (int dt : {dst.qk_dtype, dst.v_dtype})
+    if (dt != FUSP_BF16 && dt != FUSP_F16)
+      return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: Q/K/V must be bf16 or f16");
+  if (dst.u < 1 || heads % dst.u != 0 || (dst.u > 1 && dst.slot_stride % 8 != 0))
+    return set_error(FUSP_ERR_SHAPE, "qkv projection: heads must split evenly over the slots");
   if (c % 64 != 0) return set_error(FUSP_ERR_SHAPE, "qkv projection: C must be a multiple of 64");
   for (const void* ptr : {x, w, static_cast<const void*>(q), static_cast<const void*>(k), static_cast<const void*>(v)})
     if (reinterpret_cast<uintptr_t>(ptr) % 16)
@@ -394,6 +413,10 @@ fusp_status launch_qkv_proj(const void* x, int x_dtype, int b, int s, int c, con
   p.qkv[0] = q;
   p.qkv[1] = k;
   p.qkv[2] = v;
+  p.part_dt[0] = p.part_dt[1] = qkv_dtype;
+  p.part_dt[2] = dst.v_dtype;
+  p.u = dst.u;
+  p.slot_stride = dst.slot_stride;
   p.norm_w[0] = wq;
   p.norm_w[1] = wk;
   p.eps = eps;

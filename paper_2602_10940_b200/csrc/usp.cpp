@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -145,6 +146,9 @@ struct Layer {
   bool pro_q = false, pro_k = false, pro_k_pre = false;
   int64_t pos0 = 0;
   int k_dt = 0;  // dtype of the K source the FP8 quantizers read
+  // Q, K, V were written into the layer's own buffers by a producer (fusp_usp_block's QKV
+  // projection): the Ulysses pack (U > 1) or the operand conversion (U = 1) is skipped
+  bool prepacked = false;
 };
 
 struct Buffers {
@@ -299,6 +303,7 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
                                  p.rope_sin, l.pos0, s);
   };
   if (!uly || l.U == 1) {
+    if (l.prepacked) return FUSP_OK;
     const int64_t n = l.C;
     if (l.pro_q) FUSP_CHECK(prologue(true, q, b.Qr_w, l.qk_dt, 0, 1));
     else if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
@@ -327,73 +332,75 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     }
     return FUSP_OK;
   }
-  // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153)
   const int64_t se2 = int64_t(l.slot_stride) / 2;  // slot stride in 16-bit elements
-  PackDesc p{};
-  p.b = l.B;
-  p.h = l.H;
-  p.sl = l.SL;
-  p.d = l.D;
-  p.u = l.U;
-  p.src = q;
-  p.src_dtype = l.in_dt;
-  p.dst = b.send_in;
-  p.dst_dtype = l.qk_dt;
-  p.dst_slot_stride = se2;
-  // Q, K, V (bf16 wire) leave in one pack launch -- with the fused QK prologue, one
-  // norm/RoPE/pack launch whose V operand is a plain pack.
-  PackDesc ops[3];
-  int nops = 0;
-  if (!l.fp8 && (l.pro_q || l.pro_k)) {
-    const fusp_qk_prologue& pr = *l.pro;
-    const ProPack pops[3] = {
-        {q, b.send_in, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
-         l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
-        {k, b.send_in + l.blk * 2, l.pro_k ? pr.k_norm_weight : nullptr,
-         l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
-        {v, b.send_in + l.blk * 4, nullptr, nullptr, nullptr, l.in_dt, FUSP_F16}};
-    FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, se2, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
-  } else if (l.pro_q) {
-    FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
-  } else {
-    ops[nops++] = p;
-  }
-  if (!l.fp8 && (l.pro_q || l.pro_k)) {
-    // packed above
-  } else if (!l.fp8) {
-    p.src = k;
-    p.dst = b.send_in + l.blk * 2;
-    if (l.pro_k) FUSP_CHECK(prologue(false, k, p.dst, l.qk_dt, se2, l.U));
-    else ops[nops++] = p;
-    p.src = v;
-    p.dst = b.send_in + l.blk * 4;
-    p.dst_dtype = FUSP_F16;
-    ops[nops++] = p;
-    FUSP_CHECK(launch_pack_multi(ops, nops, s));
-  } else {
-    // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --:
-    // one amax launch for K and V, then Q, K, V leave in one pack launch whose E4M3
-    // operands compute their scales from the amax words and write every slot's trailer
-    const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
-    const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
-    const Fp8Src srcs[2] = {Fp8Src{k, l.k_dt, nullptr, 0, 0, l.D, l.SL, l.SL},
-                            Fp8Src{v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL}};
-    uint32_t* am[2] = {b.amax, b.amax + l.nsc_local};
-    FUSP_CHECK(launch_amax_multi(srcs, 2, block, l.nsc_local, am, s));
-    for (int part = 0; part < 2; ++part) {
-      p.src = srcs[part].x;
-      p.src_dtype = srcs[part].dt;
-      p.dst = b.send_in + l.blk * 2 + part * l.blk;
-      p.dst_dtype = FUSP_E4M3;
-      p.dst_slot_stride = int64_t(l.slot_stride);
-      p.scale = nullptr;
-      p.amax_bits = am[part];
-      p.scale_bh_stride = l.fp8_block ? 1 : 0;
-      p.trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
-      p.trailer_stride = int64_t(l.slot_stride / 4);
+  if (!l.prepacked) {
+    // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153)
+    PackDesc p{};
+    p.b = l.B;
+    p.h = l.H;
+    p.sl = l.SL;
+    p.d = l.D;
+    p.u = l.U;
+    p.src = q;
+    p.src_dtype = l.in_dt;
+    p.dst = b.send_in;
+    p.dst_dtype = l.qk_dt;
+    p.dst_slot_stride = se2;
+    // Q, K, V (bf16 wire) leave in one pack launch -- with the fused QK prologue, one
+    // norm/RoPE/pack launch whose V operand is a plain pack.
+    PackDesc ops[3];
+    int nops = 0;
+    if (!l.fp8 && (l.pro_q || l.pro_k)) {
+      const fusp_qk_prologue& pr = *l.pro;
+      const ProPack pops[3] = {
+          {q, b.send_in, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
+           l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
+          {k, b.send_in + l.blk * 2, l.pro_k ? pr.k_norm_weight : nullptr,
+           l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
+          {v, b.send_in + l.blk * 4, nullptr, nullptr, nullptr, l.in_dt, FUSP_F16}};
+      FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, se2, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
+    } else if (l.pro_q) {
+      FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
+    } else {
       ops[nops++] = p;
     }
-    FUSP_CHECK(launch_pack_multi(ops, nops, s));
+    if (!l.fp8 && (l.pro_q || l.pro_k)) {
+      // packed above
+    } else if (!l.fp8) {
+      p.src = k;
+      p.dst = b.send_in + l.blk * 2;
+      if (l.pro_k) FUSP_CHECK(prologue(false, k, p.dst, l.qk_dt, se2, l.U));
+      else ops[nops++] = p;
+      p.src = v;
+      p.dst = b.send_in + l.blk * 4;
+      p.dst_dtype = FUSP_F16;
+      ops[nops++] = p;
+      FUSP_CHECK(launch_pack_multi(ops, nops, s));
+    } else {
+      // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --:
+      // one amax launch for K and V, then Q, K, V leave in one pack launch whose E4M3
+      // operands compute their scales from the amax words and write every slot's trailer
+      const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
+      const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
+      const Fp8Src srcs[2] = {Fp8Src{k, l.k_dt, nullptr, 0, 0, l.D, l.SL, l.SL},
+                              Fp8Src{v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL}};
+      uint32_t* am[2] = {b.amax, b.amax + l.nsc_local};
+      FUSP_CHECK(launch_amax_multi(srcs, 2, block, l.nsc_local, am, s));
+      for (int part = 0; part < 2; ++part) {
+        p.src = srcs[part].x;
+        p.src_dtype = srcs[part].dt;
+        p.dst = b.send_in + l.blk * 2 + part * l.blk;
+        p.dst_dtype = FUSP_E4M3;
+        p.dst_slot_stride = int64_t(l.slot_stride);
+        p.scale = nullptr;
+        p.amax_bits = am[part];
+        p.scale_bh_stride = l.fp8_block ? 1 : 0;
+        p.trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
+        p.trailer_stride = int64_t(l.slot_stride / 4);
+        ops[nops++] = p;
+      }
+      FUSP_CHECK(launch_pack_multi(ops, nops, s));
+    }
   }
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
@@ -699,10 +706,13 @@ fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
   return FUSP_OK;
 }
 
+// Producer of the layer's Q, K, V, called with the layer's own operand buffers (slots).
+using Produce = std::function<fusp_status(const QkvDst&)>;
+
 fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void* k,
                       const void* v, int in_dt, fusp_shape4 ls, void* out, float* lse_out,
                       const fusp_comm_options* opts, cudaStream_t s, bool size_only = false,
-                      const fusp_qk_prologue* pro = nullptr) {
+                      const fusp_qk_prologue* pro = nullptr, const Produce* produce = nullptr) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
   FUSP_CUDA(cudaSetDevice(c->device));
@@ -733,6 +743,20 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
                                      pro->k_norm_weight, pro->eps, pro->rope_cos, pro->rope_sin,
                                      l.pos0, s));
     k = b.Kpro;
+  }
+  if (produce != nullptr) {
+    if (l.fp8 || l.pro != nullptr || l.mode == Mode::kRing || o.check_finite)
+      return set_error(FUSP_ERR_UNSUPPORTED, "operand producer: bf16/f16 wire, no prologue, no check");
+    QkvDst d{};
+    if (l.U > 1) {  // straight into the Ulysses send slots: [Q blk][K blk][V f16 blk] per slot
+      d = QkvDst{b.send_in, b.send_in + l.blk * 2, b.send_in + l.blk * 4, l.qk_dt, FUSP_F16, l.U,
+                 int64_t(l.slot_stride) / 2};
+    } else {        // the attention operands themselves (V as the f16 the P.V MMA reads)
+      d = QkvDst{b.Qr_w ? b.Qr_w : const_cast<void*>(q), b.Kr_w ? b.Kr_w : const_cast<void*>(k),
+                 b.Vr_w ? b.Vr_w : const_cast<void*>(v), l.qk_dt, FUSP_F16, 1, 0};
+    }
+    FUSP_CHECK((*produce)(d));
+    l.prepacked = true;
   }
   const bool uly1 =l.mode != Mode::kRing && l.U == 1;  // the reference still runs a 1-member
   if (uly1) log_a2a(c, l.ug, 0);                         // all_to_all (fabric.cpp:199-226)
@@ -1039,18 +1063,28 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
   }
   char* ws = static_cast<char*>(c->block_ws);
   void *q = ws, *k = ws + one, *v = ws + 2 * one, *attn = ws + 3 * one;
-  // producer: QKV projection with the QK RMSNorm + RoPE in its epilogue
-  FUSP_CHECK(launch_qkv_proj(x, x_dtype, int(batch), int(s_local), int(channels), w_qkv, heads, q, k, v,
-                             x_dtype, prologue ? prologue->q_norm_weight : nullptr,
-                             prologue ? prologue->k_norm_weight : nullptr, prologue ? prologue->eps : 0.f,
-                             prologue ? prologue->rope_cos : nullptr, prologue ? prologue->rope_sin : nullptr,
-                             pos0, st));
-  // the layer, its output in the projection's input dtype
   fusp_comm_options o{};
   if (opts) o = *opts;
-  o.out_dtype = x_dtype;
+  o.out_dtype = x_dtype;  // the layer's output in the projection's input dtype
   const fusp_shape4 ls{batch, heads, s_local, 128};
-  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st));
+  // producer: QKV projection with the QK RMSNorm + RoPE in its epilogue
+  auto qkv = [&](const QkvDst& d) {
+    return launch_qkv_proj_to(x, x_dtype, int(batch), int(s_local), int(channels), w_qkv, heads, d,
+                              prologue ? prologue->q_norm_weight : nullptr,
+                              prologue ? prologue->k_norm_weight : nullptr, prologue ? prologue->eps : 0.f,
+                              prologue ? prologue->rope_cos : nullptr, prologue ? prologue->rope_sin : nullptr,
+                              pos0, st);
+  };
+  if (!o.fp8_kv && !o.check_finite) {
+    // the projection writes Q, K, V straight into the layer's Ulysses send slots (U = 1: the
+    // attention operands, V already f16), so neither the pack nor the V conversion runs
+    const Produce produce = qkv;
+    FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st, false,
+                         nullptr, &produce));
+  } else {
+    FUSP_CHECK(qkv(QkvDst{q, k, v, x_dtype, x_dtype, 1, 0}));
+    FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st));
+  }
   // consumer: output projection
   return fusp_out_projection(attn, x_dtype, ls, w_out, n_out, y, y_dtype, stream);
 }

@@ -90,8 +90,12 @@ def block_oracle(x, wqkv, wout, heads, wq, wk, cos, sin, n):
     return ref_proj(att, wout)
 
 
-@pytest.mark.parametrize("n,r,heads,s", [(1, 1, 4, 512), (2, 1, 4, 512), (4, 2, 8, 1024)])
-def test_usp_block_end_to_end(cuda, fu, n, r, heads, s):
+@pytest.mark.parametrize("path", ["slots", "staged"])
+@pytest.mark.parametrize("n,r,heads,s", [(1, 1, 4, 512), (2, 1, 4, 512), (4, 2, 8, 1024), (8, 1, 8, 1024)])
+def test_usp_block_end_to_end(cuda, fu, n, r, heads, s, path):
+    # "slots": the QKV projection writes straight into the layer's Ulysses send slots (U = 1:
+    # the attention operands, V as f16); "staged" (check_finite forces it): Q, K, V land in
+    # a scratch tensor first and the layer packs / converts them as for a caller's input
     c, nout = 256, 256
     rs = np.random.RandomState(11 + n)
     x = R.round_bf16(rs.uniform(-1, 1, (1, s, c)).astype(np.float32))
@@ -106,8 +110,9 @@ def test_usp_block_end_to_end(cuda, fu, n, r, heads, s):
                         eps=1e-6, rope_cos=torch.from_numpy(cos).cuda(), rope_sin=torch.from_numpy(sin).cuda())
     wq_d, wo_d = torch.from_numpy(wqkv).cuda().bfloat16(), torch.from_numpy(wout).cuda().bfloat16()
     mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(check_finite=(path == "staged"))
     rep = fu.run_protocol(n, lambda ctx: fu.usp_block(ctx, xs[ctx.rank()], wq_d, heads, wo_d, mesh,
-                                                      prologue=pro, out_dtype=torch.float32))
+                                                      prologue=pro, opts=opts, out_dtype=torch.float32))
     got = torch.cat(rep.results, dim=1).cpu().numpy()
     # Q/K/V rounded to bf16 from f32 accumulators (the oracle rounds fp64), bf16 attention
     # output: the bf16 roundings dominate
