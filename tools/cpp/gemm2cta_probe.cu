@@ -61,6 +61,13 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -201,6 +208,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// 1-CTA comparison: the same pipeline with cta_group::1, 128 x 256 per CTA, full B per CTA
+constexpr int kStages1 = 4;
+struct __align__(1024) Smem1 {
+  uint8_t a[kStages1][kABytes];
+  uint8_t b[kStages1][2 * kBBytes];
+  uint64_t full[kStages1], empty[kStages1];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm1(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, const Args p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem1& sm = *reinterpret_cast<Smem1*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int tiles = p.m_tiles * p.n_tiles;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages1; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.acc_full[b], 1);
+      mbar_init(&sm.acc_empty[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int nt = t % p.n_tiles, mt = t / p.n_tiles;
+        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+          const int st = it % kStages1;
+          mbar_wait(&sm.empty[st], ((it / kStages1) & 1) ^ 1);
+          mbar_expect_tx(&sm.full[st], kABytes + 2 * kBBytes);
+          tma_load_2d(sm.a[st], &tm_a, &sm.full[st], kb * kK, mt * kM);
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d(sm.b[st] + c * kBChunk, &tm_b, &sm.full[st], nt * kN + c * 64, kb * kK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t it = 0, lt = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const int ab = lt & 1;
+      mbar_wait(&sm.acc_empty[ab], ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        const int st = it % kStages1;
+        mbar_wait(&sm.full[st], (it / kStages1) & 1);
+        tc_fence_after();
+        const uint64_t adesc = umma_desc_sw128(smem_u32(sm.a[st]), 16, 1024);
+        const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.b[st]), kBChunk, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kK / 16; ++k)
+            mma_ss(tmem + ab * kN, adesc + uint64_t(k * 32 / 16), bdesc + uint64_t(k * 16 * 128 / 16), p.idesc,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&sm.empty[st]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(&sm.acc_full[ab]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int quad = warp & 3, eg = (warp - 4) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const int ab = lt & 1, nt = t % p.n_tiles, mt = t / p.n_tiles;
+      mbar_wait(&sm.acc_full[ab], (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * kM + r;
+      for (int c = eg * 4; c < eg * 4 + 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + ab * kN + c * 32, v);
+        tmem_wait_ld();
+        if (!p.nostore && row < p.m) {
+          float* y = p.c + static_cast<int64_t>(row) * p.n + nt * kN + c * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(y)[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (threadIdx.x == 128) mbar_arrive(&sm.acc_empty[ab]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 __global__ void ref_gemm(const __nv_bfloat16* a, const __nv_bfloat16* b, float* c, int m, int n, int k) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (j >= n) return;
@@ -254,8 +370,10 @@ int main(int argc, char** argv) {
   p.idesc = idesc_f16(1, 1, 0, 1, 256, kN);
   p.nostore = getenv("NOSTORE") != nullptr;
   p.c = c;
-  const int smem = sizeof(Smem) + 1024;
-  CK(cudaFuncSetAttribute(gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const bool one = getenv("ONE") != nullptr;
+  const int smem = one ? int(sizeof(Smem1)) + 1024 : int(sizeof(Smem)) + 1024;
+  CK(cudaFuncSetAttribute(gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(Smem)) + 1024));
+  CK(cudaFuncSetAttribute(gemm1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(Smem1)) + 1024));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int pairs = ((p.m_tiles + 1) / 2) * p.n_tiles;
@@ -265,6 +383,7 @@ int main(int argc, char** argv) {
     cfg.gridDim = dim3((sms / 2) * 2);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = sizeof(Smem) + 1024;
     CK(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2, &cfg));
   }
   int grid = (sms / 2) * 2;
@@ -272,7 +391,12 @@ int main(int argc, char** argv) {
   else if (max_clusters > 0 && 2 * max_clusters < grid) grid = 2 * max_clusters;
   fprintf(stderr, "max active clusters %d, grid %d\n", max_clusters, grid);
   if (pairs * 2 < grid) grid = pairs * 2;
-  gemm2<<<grid, kThreads, smem>>>(ta, tb, p);
+  if (one) p.idesc = idesc_f16(1, 1, 0, 1, 128, kN);
+  auto launch = [&] {
+    if (one) gemm1<<<sms, kThreads, smem>>>(ta, tb, p);
+    else gemm2<<<grid, kThreads, smem>>>(ta, tb, p);
+  };
+  launch();
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   ref_gemm<<<dim3((n + 255) / 256, m), 256>>>(a, b, cr, m, n, k);
@@ -288,15 +412,15 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int i = 0; i < 3; ++i) gemm2<<<grid, kThreads, smem>>>(ta, tb, p);
+  for (int i = 0; i < 3; ++i) launch();
   cudaEventRecord(e0);
-  for (int i = 0; i < 20; ++i) gemm2<<<grid, kThreads, smem>>>(ta, tb, p);
+  for (int i = 0; i < 20; ++i) launch();
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double us = ms * 1e3 / 20, tf = 2.0 * m * n * k / (us * 1e-6) / 1e12;
-  printf("{\"probe\": \"gemm 2-CTA 256x256\", \"m\": %d, \"n\": %d, \"k\": %d, \"rel_l2\": %.3e, \"us\": %.1f, \"tflops\": %.1f}\n",
-         m, n, k, std::sqrt(num / den), us, tf);
+  printf("{\"probe\": \"%s\", \"m\": %d, \"n\": %d, \"k\": %d, \"rel_l2\": %.3e, \"us\": %.1f, \"tflops\": %.1f}\n",
+         one ? "gemm 1-CTA 128x256" : "gemm 2-CTA 256x256", m, n, k, std::sqrt(num / den), us, tf);
   return 0;
 }
