@@ -45,6 +45,16 @@ def test_version(fu):
     assert b"sm_100a" in lib().fusp_version()
 
 
+def test_attention_trace_compiled_out(fu):
+    # the per-CTA trace instrumentation costs 1-2 % in the KV loop, so the shipped library
+    # compiles it out and says so (tools/build_variants.sh builds the traced debug variant)
+    import os
+    from paper_2602_10940_b200._lib import lib
+    if os.environ.get("FUSP_VARIANT"):
+        pytest.skip("a variant build is loaded")
+    assert lib().fusp_attention_trace(1, None, 0) == -2
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 6, 8])
 @pytest.mark.parametrize("max_ring", [1, 2, 4, 8])
 @pytest.mark.parametrize("heads", [1, 3, 8, 24])
