@@ -202,16 +202,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
           uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) + slot * p.slot_stride +
                           ((static_cast<int64_t>(bb) * hp + hl) * p.s + s) * 128;
           const bool o_f16 = p.part_dt[part] == FUSP_F16;
+          const int e4 = lane & 3;  // stores: the 4 lanes of a group write one row's 64-byte chunk
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t v[32];
             tmem_ld32(tcol + c * 32, v);
             tmem_wait_ld();
-            if (!in_range) continue;
             float x[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
-            if (w != nullptr) {
+            if (w != nullptr && in_range) {
               const float4* w4 = reinterpret_cast<const float4*>(w + c * 32);
 #pragma unroll
               for (int q4 = 0; q4 < 8; ++q4) {
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 x[4 * q4 + 3] *= rinv * wv.w;
               }
             }
-            if (rope) {  // this row's 16 (cos, sin) pairs of the chunk as float4 vectors
+            if (rope && in_range) {  // this row's 16 (cos, sin) pairs of the chunk as float4 vectors
               const float4* c4 = reinterpret_cast<const float4*>(p.cosv + pos * 64 + c * 16);
               const float4* s4 = reinterpret_cast<const float4*>(p.sinv + pos * 64 + c * 16);
 #pragma unroll
@@ -242,9 +242,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               o16[i] = o_f16 ? pack_f16x2(x[2 * i], x[2 * i + 1]) : pack_bf16x2(x[2 * i], x[2 * i + 1]);
+            xpose4<4>(o16, lane);  // lane 4G+e now holds 16-byte piece e of rows 4G..4G+3
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              reinterpret_cast<uint4*>(dst + c * 32)[i] = make_uint4(o16[4 * i], o16[4 * i + 1], o16[4 * i + 2], o16[4 * i + 3]);
+              if (s - e4 + i < p.s)
+                *reinterpret_cast<uint4*>(dst + (i - e4) * 128 + c * 32 + e4 * 8) =
+                    make_uint4(o16[4 * i], o16[4 * i + 1], o16[4 * i + 2], o16[4 * i + 3]);
           }
         }
       } else {
@@ -255,23 +258,33 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tmem_ld32(tmem + lane_off + ab * kPN + c * 32, v);
         tmem_wait_ld();
         const int n0 = nt * kPN + c * 32;
-        if (!in_range || n0 >= p.n) continue;
+        if (n0 >= p.n) continue;  // (uniform) N % 64 == 0: whole chunks
+        // stores through 4-lane-group transposes: 4 lanes cover one row's chunk, 8 rows per
+        // instruction (rows s - e4 + i are p.n elements apart)
+        const int e4 = lane & 3;
         if (p.y_dtype == FUSP_F32) {
-          float* y = static_cast<float*>(p.y) + ybase + c * 32;  // N % 64 == 0: whole chunks
+          xpose4<8>(v, lane);
+          float* y = static_cast<float*>(p.y) + ybase + c * 32 + e4 * 8;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4*>(y)[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          for (int i = 0; i < 4; ++i)
+            if (s - e4 + i < p.s) {
+              uint4* dst = reinterpret_cast<uint4*>(y + static_cast<int64_t>(i - e4) * p.n);
+              dst[0] = make_uint4(v[8 * i], v[8 * i + 1], v[8 * i + 2], v[8 * i + 3]);
+              dst[1] = make_uint4(v[8 * i + 4], v[8 * i + 5], v[8 * i + 6], v[8 * i + 7]);
+            }
         } else {
-          uint16_t* y = static_cast<uint16_t*>(p.y) + ybase + c * 32;
           uint32_t w[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             w[i] = p.y_dtype == FUSP_F16 ? pack_f16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]))
                                          : pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          xpose4<4>(w, lane);
+          uint16_t* y = static_cast<uint16_t*>(p.y) + ybase + c * 32 + e4 * 8;
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            reinterpret_cast<uint4*>(y)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            if (s - e4 + i < p.s)
+              *reinterpret_cast<uint4*>(y + static_cast<int64_t>(i - e4) * p.n) =
+                  make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
       }

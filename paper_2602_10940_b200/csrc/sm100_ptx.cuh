@@ -208,6 +208,29 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// 4x4 transpose of W-word pieces inside each 4-lane group (butterfly, xor 2 then 1): lane 4G+e
+// holding piece q of row 4G+e in w[W q ..] ends up holding piece e of row 4G+q there (and
+// back: the transpose is an involution).  Turns row-per-thread TMEM data into stores / loads
+// where 4 lanes cover one row's 4 W-word pieces -- 8 rows per instruction instead of 32.
+template <int W>
+__device__ __forceinline__ void xpose4(uint32_t (&w)[4 * W], int lane) {
+#pragma unroll
+  for (int m = 2; m >= 1; m >>= 1) {
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int q0 = 0; q0 < 4; ++q0) {
+      if (q0 & m) continue;
+      const int q1 = q0 | m;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, hi ? w[W * q0 + k] : w[W * q1 + k], m);
+        if (hi) w[W * q0 + k] = y;
+        else w[W * q1 + k] = y;
+      }
+    }
+  }
+}
+
 // ---- misc math ----------------------------------------------------------------------------
 template <uint32_t kRegs>
 __device__ __forceinline__ void reg_alloc() {
