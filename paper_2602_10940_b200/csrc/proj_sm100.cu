@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "fastusp_internal.h"
 #include "sm100_ptx.cuh"
@@ -47,6 +48,8 @@ struct ProjParams {
   int m_tiles_per_b;  // ceil(S / 128)
   int n_tiles;        // ceil(N / 256)
   int tiles;          // B * m_tiles_per_b * n_tiles
+  int m_tiles;        // B * m_tiles_per_b
+  int m_fast;         // tile order: 1 = m-tiles fastest (consecutive CTAs share a B tile)
   int k_blocks;       // out-projection: H * 2; QKV projection: C / 64
   int s, n;           // tokens per batch row, outputs
   uint32_t idesc;
@@ -73,6 +76,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// Tile raster: walk the m-tiles fastest when B (the weights) is the larger operand, so the
+// CTAs in flight share a few B column blocks and stream A; otherwise n fastest.  Keeps the
+// working set in L2 (QKV projection, W 56.6 MB vs x 28 MB at FLUX: 207 -> 179 us).
+// FUSP_PROJ_MFAST=0/1 overrides.
+bool proj_m_fast(int64_t a_bytes, int64_t b_bytes) {
+  static const int v = [] {
+    const char* e = getenv("FUSP_PROJ_MFAST");
+    return e == nullptr ? -1 : atoi(e);
+  }();
+  return v < 0 ? b_bytes > a_bytes : v != 0;
 }
 
 // kQkv = false: output projection, A = attention output [B][H][S][128] through a 4-D map.
@@ -112,8 +127,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       prefetch_tmap(&tm_b);
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-        const int nt = tile % p.n_tiles;
-        const int mt = tile / p.n_tiles;
+        const int nt = p.m_fast ? tile / p.m_tiles : tile % p.n_tiles;
+        const int mt = p.m_fast ? tile % p.m_tiles : tile / p.n_tiles;
         const int bb = mt / p.m_tiles_per_b;
         const int s0 = (mt - bb * p.m_tiles_per_b) * kPM;
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
@@ -166,8 +181,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++lt) {
       const int ab = lt & 1;
-      const int nt = tile % p.n_tiles;
-      const int mt = tile / p.n_tiles;
+      const int nt = p.m_fast ? tile / p.m_tiles : tile % p.n_tiles;
+      const int mt = p.m_fast ? tile % p.m_tiles : tile / p.n_tiles;
       const int bb = mt / p.m_tiles_per_b;
       const int s = (mt - bb * p.m_tiles_per_b) * kPM + r;
       mbar_wait(&sm.acc_full[ab], (lt >> 1) & 1);
@@ -350,6 +365,8 @@ fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, con
   const int pn = fill(128) > 1.15 * fill(256) ? 128 : 256;
   p.n_tiles = (n + pn - 1) / pn;
   p.tiles = b * p.m_tiles_per_b * p.n_tiles;
+  p.m_tiles = b * p.m_tiles_per_b;
+  p.m_fast = proj_m_fast(int64_t(b) * s * h * 128 * 2, int64_t(h) * 128 * n * 2) ? 1 : 0;
   p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   static bool attr = false;
@@ -446,6 +463,8 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   const int pn = (n % 256 != 0 || fill(128) > 1.15 * fill(256)) ? 128 : 256;
   p.n_tiles = n / pn;
   p.tiles = b * p.m_tiles_per_b * p.n_tiles;
+  p.m_tiles = b * p.m_tiles_per_b;
+  p.m_fast = proj_m_fast(int64_t(b) * s * c * 2, int64_t(c) * n * 2) ? 1 : 0;
   const uint32_t f = x_dtype == FUSP_BF16 ? 1u : 0u;
   p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
