@@ -115,6 +115,13 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
                                        fusp_dtype qk_dtype, fusp_dtype v_dtype,
                                        fusp_shape4 q_shape, int64_t skv, void* out,
                                        fusp_dtype out_dtype, float* lse, fusp_stream_t stream);
+/* Range-guarded f16 staging of a tensor-core operand (B200 extension; what every
+ * fusp_attention* / protocol call does to f32, bf16 and FP8-decoded operands internally):
+ * x [heads][rows][128] (F32/BF16/F16) -> y f16 = x * 2^-exps[h], exps[heads] int32 out, with
+ * exps[h] = 0 while max|x[h]| lies in [2^-6, 2^15), else the power of two that brings it into
+ * [2^14, 2^15) (see fastusp_internal.h).  Exact power-of-two scaling: no inf, no f16 subnormal. */
+fusp_status fusp_stage_f16(const void* x, fusp_dtype dtype, int64_t heads, int64_t rows, void* y,
+                           int* exps, fusp_stream_t stream);
 /* merge_lse (tensor.cpp:204-243): f32 o1,o2 [B,H,S,D], l1,l2 [B,H,S] -> out, lse (may alias o1/l1). */
 fusp_status fusp_merge_lse(const float* o1, const float* l1, const float* o2, const float* l2,
                            fusp_shape4 shape, float* out, float* lse, fusp_stream_t stream);
@@ -138,6 +145,12 @@ fusp_status fusp_nccl_unique_id(uint8_t uid[128]);
 fusp_status fusp_ctx_create_nccl(const uint8_t uid[128], int world, int rank, int device,
                                  fusp_ctx* out);
 fusp_status fusp_ctx_destroy(fusp_ctx ctx);
+/* Wait for `stream` on the host, bounded: the NCCL backend polls ncclCommGetAsyncError while
+ * the stream drains, and a peer that failed or never joined its collective (or timeout_s
+ * elapsing; <= 0: FUSP_TIMEOUT_S, default 120) aborts every communicator of the context and
+ * returns FUSP_ERR_DEADLOCK ("deadlock: rank R ...", DeadlockError, fabric.hpp:106-126)
+ * instead of hanging.  Later collectives on an aborted context return FUSP_ERR_COMM. */
+fusp_status fusp_ctx_synchronize(fusp_ctx ctx, fusp_stream_t stream, double timeout_s);
 int fusp_ctx_rank(fusp_ctx ctx);
 int fusp_ctx_world(fusp_ctx ctx);
 /* Bytes this rank put on the wire since creation, self-traffic excluded, per op:
@@ -169,6 +182,50 @@ fusp_status fusp_ulysses_attention(fusp_ctx ctx, const void* q, const void* k, c
 fusp_status fusp_ring_attention(fusp_ctx ctx, const void* q, const void* k, const void* v,
                                 fusp_dtype in_dtype, fusp_shape4 local_shape, void* out,
                                 float* lse, const fusp_comm_options* opts, fusp_stream_t stream);
+
+/* usp_attention (protocols.cpp:321-340) that also returns the rows' natural-log LSE:
+ * lse [B,H,S/N] f32 (nullable).  The reference drops it (protocols.cpp:339); here it rides a
+ * second, small all-to-all back with the output ([B][H/U][S/N] f32 per member). */
+fusp_status fusp_usp_attention_lse(fusp_ctx ctx, int ring_dim, const void* q, const void* k,
+                                   const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                   void* out, float* lse, const fusp_comm_options* opts,
+                                   fusp_stream_t stream);
+
+/* ---- process groups (uspsim::ProcessGroup, fabric.hpp:20-28) ----------------------------- */
+typedef struct fusp_group_s* fusp_group;
+/* A group of world ranks members[0..n) in group order (position = index).  Collective over the
+ * WORLD for NCCL contexts (one ncclCommSplit): every rank calls it, with the group it belongs
+ * to (the groups of one call must be disjoint) or n = 0 to take part without a group (*out =
+ * NULL).  Errors as validate_group (fabric.cpp:316-324) / all_to_all (:204-205): FUSP_ERR_COMM
+ * "group member X out of range [0,N)", "duplicate member X in group K", "rank R not in group K". */
+fusp_status fusp_group_create(fusp_ctx ctx, const int* members, int n, fusp_group* out);
+fusp_status fusp_group_destroy(fusp_group group);
+int fusp_group_size(fusp_group group);
+int fusp_group_position(fusp_group group);
+/* ulysses_attention(ctx, q, k, v, group, opts) (protocols.hpp:47-48, protocols.cpp:207-214)
+ * over `group` (NULL = the world); lse [B,H,S/U,D...] -> [B,H,S/U] f32, nullable. */
+fusp_status fusp_ulysses_attention_group(fusp_ctx ctx, fusp_group group, const void* q,
+                                         const void* k, const void* v, fusp_dtype in_dtype,
+                                         fusp_shape4 local_shape, void* out, float* lse,
+                                         const fusp_comm_options* opts, fusp_stream_t stream);
+/* ring_attention_{serial,pipelined}(ctx, q, k, v, group, opts) (protocols.hpp:54-65) over
+ * `group` (NULL = the world): out and lse [B,H,S/R] (lse nullable); opts->pipelined_ring. */
+fusp_status fusp_ring_attention_group(fusp_ctx ctx, fusp_group group, const void* q, const void* k,
+                                      const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                      void* out, float* lse, const fusp_comm_options* opts,
+                                      fusp_stream_t stream);
+/* detail::ulysses_input_reshard (protocols.hpp:81-83, protocols.cpp:125-180): local q, k, v
+ * [B,H,S_l,D] -> q_out, k_out, v_out [B,H/U,U*S_l,D] in out_dtype (F32 = the reference's
+ * Resharded; with opts->fp8_kv, K and V are the exact dequantized values decode(code)*scale). */
+fusp_status fusp_ulysses_input_reshard(fusp_ctx ctx, fusp_group group, const void* q, const void* k,
+                                       const void* v, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                       void* q_out, void* k_out, void* v_out, fusp_dtype out_dtype,
+                                       const fusp_comm_options* opts, fusp_stream_t stream);
+/* detail::ulysses_output_reshard (protocols.hpp:85-86, protocols.cpp:182-203):
+ * o [B,H/U,S,D] (o_shape) -> out [B,H,S/U,D], same dtype. */
+fusp_status fusp_ulysses_output_reshard(fusp_ctx ctx, fusp_group group, const void* o,
+                                        fusp_dtype dtype, fusp_shape4 o_shape, void* out,
+                                        fusp_stream_t stream);
 
 /* Producer prologue fused into the Ulysses pack (B200 extension): the MMDiT
  * joint-attention block's per-head RMSNorm of Q and K and rotary embedding, applied to the

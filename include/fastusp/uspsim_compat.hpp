@@ -92,6 +92,16 @@ struct Tensor4T {
   }
   T& at(int64_t b, int64_t h, int64_t s, int64_t d) { return data[index(b, h, s, d)]; }
   const T& at(int64_t b, int64_t h, int64_t s, int64_t d) const { return data[index(b, h, s, d)]; }
+  Tensor4T slice_heads(int64_t h0, int64_t count) const {  // tensor.cpp:35-46
+    if (h0 < 0 || count < 0 || h0 + count > shape.h)
+      throw ShapeError("head slice [" + std::to_string(h0) + "," + std::to_string(h0 + count) +
+                       ") out of range for H=" + std::to_string(shape.h));
+    Tensor4T r(Shape4{shape.b, count, shape.s, shape.d});
+    for (int64_t b = 0; b < shape.b; ++b)
+      for (int64_t h = 0; h < count; ++h)
+        std::memcpy(&r.at(b, h, 0, 0), &at(b, h0 + h, 0, 0), sizeof(T) * shape.s * shape.d);
+    return r;
+  }
   Tensor4T slice_seq(int64_t s0, int64_t count) const {
     if (s0 < 0 || count < 0 || s0 + count > shape.s)
       throw ShapeError("sequence slice [" + std::to_string(s0) + "," + std::to_string(s0 + count) +
@@ -147,6 +157,13 @@ struct QuantizedTensor {
   CodeTensor codes;
   float scale = 1.0f;
   const Shape4& shape() const { return codes.shape; }
+  // fp8.cpp:100-105: a head slice keeps the tensor-wide scale
+  QuantizedTensor slice_heads(int64_t h0, int64_t count) const {
+    QuantizedTensor r;
+    r.scale = scale;
+    r.codes = codes.slice_heads(h0, count);
+    return r;
+  }
 };
 
 inline QuantizedTensor quantize(const Tensor4& x) {
@@ -216,10 +233,48 @@ inline AttnResult attention_with_lse(const Tensor4& q, const Tensor4& k, const T
   return r;
 }
 
+// attention_reference (tensor.cpp:185-191): attention_with_lse without the LSE
+inline Tensor4 attention_reference(const Tensor4& q, const Tensor4& k, const Tensor4& v) {
+  return attention_with_lse(q, k, v).out;
+}
+
+// merge_lse (tensor.cpp:204-243) on the device merge kernel
+inline AttnResult merge_lse(const AttnResult& a, const AttnResult& b) {
+  if (!(a.out.shape == b.out.shape))
+    throw ShapeError("merge_lse: output shapes differ, " + a.out.shape.str() + " vs " + b.out.shape.str());
+  if (a.lse.size() != b.lse.size())
+    throw ShapeError("merge_lse: lse lengths differ, " + std::to_string(a.lse.size()) + " vs " +
+                     std::to_string(b.lse.size()));
+  const size_t n = a.out.data.size(), m = a.lse.size();
+  detail::DevBuf o1(n * 4), o2(n * 4), l1(m * 4), l2(m * 4), ro(n * 4), rl(m * 4);
+  detail::h2d(o1.p, a.out.data.data(), n * 4);
+  detail::h2d(o2.p, b.out.data.data(), n * 4);
+  detail::h2d(l1.p, a.lse.data(), m * 4);
+  detail::h2d(l2.p, b.lse.data(), m * 4);
+  check(fusp_merge_lse(o1.as<float>(), l1.as<float>(), o2.as<float>(), l2.as<float>(), a.out.shape.c(),
+                       ro.as<float>(), rl.as<float>(), nullptr));
+  AttnResult r;
+  r.out = Tensor4(a.out.shape);
+  r.lse.resize(m);
+  detail::d2h(r.out.data.data(), ro.p, n * 4);
+  detail::d2h(r.lse.data(), rl.p, m * 4);
+  return r;
+}
+
 // ---- mesh (mesh.hpp:22-50) ---------------------------------------------------------------------
 struct ProcessGroup {
   std::vector<int> members;
   int size() const { return static_cast<int>(members.size()); }
+  int position_of(int rank) const {
+    for (size_t i = 0; i < members.size(); ++i)
+      if (members[i] == rank) return static_cast<int>(i);
+    return -1;
+  }
+  std::string key() const {
+    std::string k;
+    for (size_t i = 0; i < members.size(); ++i) k += (i ? "," : "") + std::to_string(members[i]);
+    return k;
+  }
 };
 
 struct Mesh2D {
@@ -260,12 +315,31 @@ struct CommOptions {
 class WorkerContext {
  public:
   WorkerContext(fusp_ctx c) : c_(c) {}
+  ~WorkerContext() {
+    for (auto& g : groups_) fusp_group_destroy(g.second);
+  }
+  WorkerContext(const WorkerContext&) = delete;
+  WorkerContext& operator=(const WorkerContext&) = delete;
   int rank() const { return fusp_ctx_rank(c_); }
   int world_size() const { return fusp_ctx_world(c_); }
   fusp_ctx handle() const { return c_; }
+  // The fastusp handle of a ProcessGroup on this rank (created on first use; run_protocol's
+  // in-process fabric needs no collective setup).  The world in rank order is NULL.
+  fusp_group group(const ProcessGroup& g) {
+    bool world = g.size() == world_size();
+    for (int i = 0; i < g.size() && world; ++i) world = g.members[i] == i;
+    if (world) return nullptr;
+    for (auto& e : groups_)
+      if (e.first == g.members) return e.second;
+    fusp_group h = nullptr;
+    check(fusp_group_create(c_, g.members.data(), g.size(), &h));
+    groups_.emplace_back(g.members, h);
+    return h;
+  }
 
  private:
   fusp_ctx c_;
+  std::vector<std::pair<std::vector<int>, fusp_group>> groups_;
 };
 
 using WorkerProgram = std::function<void(WorkerContext&)>;
@@ -327,6 +401,159 @@ inline Tensor4 gather_output(const std::vector<Tensor4>& shards) {
   }
   return r;
 }
+
+// ShardSpec / gather_shards (protocols.hpp:17-35, protocols.cpp:25-50): reassembly with
+// explicit coverage checking (host-side, like the reference).
+struct ShardSpec {
+  enum class Axis { kSequence, kHead };
+  Axis axis = Axis::kSequence;
+  int index = 0;
+  int count = 1;
+};
+
+inline Tensor4 gather_shards(const std::vector<std::pair<ShardSpec, Tensor4>>& shards) {
+  if (shards.empty()) throw ShapeError("gather_shards: no shards");
+  const int count = shards.front().first.count;
+  std::vector<const Tensor4*> ordered(static_cast<size_t>(count > 0 ? count : 0), nullptr);
+  for (const auto& [spec, t] : shards) {
+    if (spec.axis != ShardSpec::Axis::kSequence)
+      throw ShapeError("gather_shards: only sequence-axis shards are gathered");
+    if (spec.count != count)
+      throw ShapeError("gather_shards: inconsistent shard counts " + std::to_string(spec.count) +
+                       " vs " + std::to_string(count));
+    if (spec.index < 0 || spec.index >= count)
+      throw ShapeError("gather_shards: shard index " + std::to_string(spec.index) + " outside [0," +
+                       std::to_string(count) + ")");
+    auto& slot = ordered[static_cast<size_t>(spec.index)];
+    if (slot != nullptr)
+      throw ShapeError("gather_shards: shard index " + std::to_string(spec.index) + " covered twice");
+    slot = &t;
+  }
+  std::vector<Tensor4> parts;
+  for (int i = 0; i < count; ++i) {
+    if (!ordered[static_cast<size_t>(i)])
+      throw ShapeError("gather_shards: gap in coverage at shard index " + std::to_string(i));
+    parts.push_back(*ordered[static_cast<size_t>(i)]);
+  }
+  return gather_output(parts);
+}
+
+namespace detail {
+inline fusp_comm_options c_opts(const CommOptions& opts) {
+  fusp_comm_options o{};
+  o.fp8_kv = opts.fp8_kv;
+  o.pipelined_ring = opts.pipelined_ring;
+  o.out_dtype = FUSP_F32;
+  o.check_finite = 1;
+  return o;
+}
+inline void check_local(const Tensor4& q, const Tensor4& k, const Tensor4& v, const char* where) {
+  if (!(q.shape == k.shape) || !(q.shape == v.shape))
+    throw ShapeError(std::string(where) + ": local Q/K/V shapes differ: Q=" + q.shape.str() +
+                     " K=" + k.shape.str() + " V=" + v.shape.str());
+}
+// Host tensors staged to the device around one collective call (the reference's convention).
+struct Staged {
+  DevBuf q, k, v;
+  explicit Staged(const Tensor4& tq, const Tensor4& tk, const Tensor4& tv)
+      : q(tq.data.size() * 4), k(tk.data.size() * 4), v(tv.data.size() * 4) {
+    h2d(q.p, tq.data.data(), tq.data.size() * 4);
+    h2d(k.p, tk.data.data(), tk.data.size() * 4);
+    h2d(v.p, tv.data.data(), tv.data.size() * 4);
+  }
+};
+}  // namespace detail
+
+// ulysses_attention (protocols.hpp:47-48, protocols.cpp:207-214) over `group`
+inline Tensor4 ulysses_attention(WorkerContext& ctx, const Tensor4& q, const Tensor4& k,
+                                 const Tensor4& v, const ProcessGroup& group,
+                                 const CommOptions& opts) {
+  detail::check_local(q, k, v, "ulysses");
+  const fusp_comm_options o = detail::c_opts(opts);
+  detail::Staged d(q, k, v);
+  detail::DevBuf out(q.data.size() * 4);
+  check(fusp_ulysses_attention_group(ctx.handle(), ctx.group(group), d.q.p, d.k.p, d.v.p, FUSP_F32,
+                                     q.shape.c(), out.p, nullptr, &o, nullptr));
+  Tensor4 r(q.shape);
+  detail::d2h(r.data.data(), out.p, q.data.size() * 4);
+  return r;
+}
+
+namespace detail {
+inline AttnResult ring(WorkerContext& ctx, const Tensor4& q, const Tensor4& k, const Tensor4& v,
+                       const ProcessGroup& group, const CommOptions& opts, bool pipelined) {
+  check_local(q, k, v, "ring");
+  fusp_comm_options o = c_opts(opts);
+  o.pipelined_ring = pipelined;
+  Staged d(q, k, v);
+  const size_t rows = static_cast<size_t>(q.shape.b * q.shape.h * q.shape.s);
+  DevBuf out(q.data.size() * 4), lse(rows * 4);
+  check(fusp_ring_attention_group(ctx.handle(), ctx.group(group), d.q.p, d.k.p, d.v.p, FUSP_F32,
+                                  q.shape.c(), out.p, lse.as<float>(), &o, nullptr));
+  AttnResult r;
+  r.out = Tensor4(q.shape);
+  r.lse.resize(rows);
+  d2h(r.out.data.data(), out.p, q.data.size() * 4);
+  d2h(r.lse.data(), lse.p, rows * 4);
+  return r;
+}
+}  // namespace detail
+
+// ring_attention_serial / _pipelined (protocols.hpp:54-65, protocols.cpp:237-319)
+inline AttnResult ring_attention_serial(WorkerContext& ctx, const Tensor4& q, const Tensor4& k,
+                                        const Tensor4& v, const ProcessGroup& group,
+                                        const CommOptions& opts) {
+  return detail::ring(ctx, q, k, v, group, opts, false);
+}
+inline AttnResult ring_attention_pipelined(WorkerContext& ctx, const Tensor4& q, const Tensor4& k,
+                                           const Tensor4& v, const ProcessGroup& group,
+                                           const CommOptions& opts) {
+  return detail::ring(ctx, q, k, v, group, opts, true);
+}
+
+namespace detail {
+// detail::Resharded / ulysses_input_reshard / ulysses_output_reshard (protocols.hpp:73-86)
+struct Resharded {
+  Tensor4 q, k, v;  // [B, H/U, S_span, D]
+};
+
+inline Resharded ulysses_input_reshard(WorkerContext& ctx, const Tensor4& q, const Tensor4& k,
+                                       const Tensor4& v, const ProcessGroup& group,
+                                       const CommOptions& opts) {
+  check_local(q, k, v, "ulysses");
+  const int u = group.size();
+  if (u < 1 || q.shape.h % u != 0)
+    throw ShapeError("ulysses: head count H=" + std::to_string(q.shape.h) +
+                     " not divisible by ulysses dimension U=" + std::to_string(u));
+  const fusp_comm_options o = c_opts(opts);
+  Staged d(q, k, v);
+  const Shape4 rs{q.shape.b, q.shape.h / u, q.shape.s * u, q.shape.d};
+  const size_t n = static_cast<size_t>(rs.count()) * 4;
+  DevBuf rq(n), rk(n), rv(n);
+  check(fusp_ulysses_input_reshard(ctx.handle(), ctx.group(group), d.q.p, d.k.p, d.v.p, FUSP_F32,
+                                   q.shape.c(), rq.p, rk.p, rv.p, FUSP_F32, &o, nullptr));
+  Resharded r{Tensor4(rs), Tensor4(rs), Tensor4(rs)};
+  d2h(r.q.data.data(), rq.p, n);
+  d2h(r.k.data.data(), rk.p, n);
+  d2h(r.v.data.data(), rv.p, n);
+  return r;
+}
+
+inline Tensor4 ulysses_output_reshard(WorkerContext& ctx, const Tensor4& out, const ProcessGroup& group) {
+  const int u = group.size();
+  if (u < 1 || out.shape.s % u != 0)
+    throw ShapeError("ulysses: gathered sequence length S=" + std::to_string(out.shape.s) +
+                     " not divisible by ulysses dimension U=" + std::to_string(u));
+  const size_t n = out.data.size() * 4;
+  DevBuf o(n), res(n);
+  h2d(o.p, out.data.data(), n);
+  check(fusp_ulysses_output_reshard(ctx.handle(), ctx.group(group), o.p, FUSP_F32, out.shape.c(),
+                                    res.p, nullptr));
+  Tensor4 r(Shape4{out.shape.b, out.shape.h * u, out.shape.s / u, out.shape.d});
+  d2h(r.data.data(), res.p, n);
+  return r;
+}
+}  // namespace detail
 
 inline Tensor4 usp_attention(WorkerContext& ctx, const Tensor4& q, const Tensor4& k,
                              const Tensor4& v, const Mesh2D& mesh, const CommOptions& opts) {

@@ -48,7 +48,11 @@ class InvalidArgument(FuspError, ValueError):
     pass
 
 
-_EXC = {1: ShapeError, 2: MeshError, 3: FabricError, 4: InvalidArgument}
+class DeadlockError(FuspError):
+    """= uspsim::DeadlockError (fabric.hpp:112-116): a stalled or failed peer."""
+
+
+_EXC = {1: ShapeError, 2: MeshError, 3: FabricError, 4: InvalidArgument, 5: DeadlockError}
 
 
 class Shape4(ctypes.Structure):
@@ -97,6 +101,7 @@ _SIGS = {
                                                ctypes.c_int, _P, _P]),
     "fusp_attention_with_lse_ex": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int, Shape4,
                                                   _I64, _P, ctypes.c_int, _P, _P]),
+    "fusp_stage_f16": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, _P, _P]),
     "fusp_merge_lse": (ctypes.c_int, [_P, _P, _P, _P, Shape4, _P, _P, _P]),
     "fusp_mesh_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
     "fusp_mesh_make": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P]),
@@ -132,6 +137,21 @@ _SIGS = {
                                            ctypes.POINTER(CommOptions), _P]),
     "fusp_usp_attention_host": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                                _P, ctypes.POINTER(CommOptions), _P]),
+    "fusp_usp_attention_lse": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
+                                              _P, _P, ctypes.POINTER(CommOptions), _P]),
+    "fusp_ctx_synchronize": (ctypes.c_int, [_P, _P, ctypes.c_double]),
+    "fusp_group_create": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
+    "fusp_group_destroy": (ctypes.c_int, [_P]),
+    "fusp_group_size": (ctypes.c_int, [_P]),
+    "fusp_group_position": (ctypes.c_int, [_P]),
+    "fusp_ulysses_attention_group": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_int, Shape4, _P,
+                                                    _P, ctypes.POINTER(CommOptions), _P]),
+    "fusp_ring_attention_group": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_int, Shape4, _P, _P,
+                                                 ctypes.POINTER(CommOptions), _P]),
+    "fusp_ulysses_input_reshard": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_int, Shape4, _P, _P,
+                                                  _P, ctypes.c_int, ctypes.POINTER(CommOptions),
+                                                  _P]),
+    "fusp_ulysses_output_reshard": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, Shape4, _P, _P]),
     "fusp_graph_capture_usp": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                               _P, ctypes.POINTER(CommOptions), ctypes.c_int, _I64,
                                               _I64, _P, _P]),

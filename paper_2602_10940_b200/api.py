@@ -185,6 +185,20 @@ def attention_with_lse(q, k, v, out_dtype=torch.float32) -> AttnResult:
     return AttnResult(out, lse)
 
 
+def stage_f16(x: torch.Tensor):
+    """Range-guarded f16 staging (fusp_stage_f16): x [..., rows, 128] viewed as [heads][rows][128]
+    -> (y f16, exps int32 [heads]) with x = y * 2^exps exactly (fastusp_internal.h)."""
+    x = _dev(x)
+    if x.dtype not in _DT:
+        x = x.float()
+    heads = x.numel() // (x.shape[-2] * x.shape[-1])
+    y = torch.empty(x.shape, dtype=torch.float16, device=x.device)
+    exps = torch.empty(heads, dtype=torch.int32, device=x.device)
+    check(lib().fusp_stage_f16(_ptr(x), _DT[x.dtype], heads, x.shape[-2], _ptr(y), _ptr(exps),
+                               _stream()))
+    return y, exps
+
+
 _SCHEDULES = {"auto": 0, "whole": 1, "split": 2}
 
 
@@ -351,6 +365,20 @@ class WorkerContext:
     def rank(self) -> int:
         return lib().fusp_ctx_rank(self.handle)
 
+    def create_group(self, members) -> ctypes.c_void_p:
+        """fusp_group_create: a ProcessGroup handle on this context, cached by member list.
+        Collective over the world for NCCL contexts (every rank calls, members=[] to opt out)."""
+        key = tuple(int(m) for m in members)
+        cache = self.__dict__.setdefault("_groups", {})
+        if key in cache:
+            return cache[key]
+        arr = (ctypes.c_int * max(len(key), 1))(*key)
+        h = ctypes.c_void_p()
+        check(lib().fusp_group_create(self.handle, arr, len(key), ctypes.byref(h)))
+        if key:
+            cache[key] = h
+        return h
+
     def world_size(self) -> int:
         return lib().fusp_ctx_world(self.handle)
 
@@ -379,6 +407,11 @@ class WorkerContext:
         """Timeline::to_json of the last layer call, with device timestamps t_ms."""
         return self._json(lib().fusp_ctx_timeline_json)
 
+    def synchronize(self, stream=None, timeout_s: float = 0.0):
+        """fusp_ctx_synchronize: bounded host wait; a stalled / failed peer raises
+        DeadlockError (the NCCL communicators are aborted) instead of hanging."""
+        check(lib().fusp_ctx_synchronize(self.handle, _stream(stream), float(timeout_s)))
+
     def ring_timings(self, max_steps: int = 32):
         """Per ring step device times (ms) of the last call: (compute[], comm[])."""
         c = (ctypes.c_float * max_steps)()
@@ -389,6 +422,8 @@ class WorkerContext:
 
     def close(self):
         if self.handle:
+            for h in self.__dict__.pop("_groups", {}).values():
+                lib().fusp_group_destroy(h)
             lib().fusp_ctx_destroy(self.handle)
             self.handle = None
 
@@ -530,46 +565,116 @@ def usp_attention(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
     return out
 
 
-def _world_group(ctx, group: Optional[ProcessGroup]):
-    if group is not None and list(group.members) != list(range(ctx.world_size())):
-        raise FabricError(3, "fastusp runs ulysses/ring protocols on the world group; "
-                             "use usp_attention with a Mesh2D for sub-groups")
+def usp_attention_with_lse(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
+                           opts: Optional[CommOptions] = None) -> AttnResult:
+    """usp_attention that also returns the rows' natural-log LSE [B,H,S/N] (fusp_usp_attention_lse;
+    the reference drops it, protocols.cpp:339)."""
+    opts = opts or CommOptions()
+    if mesh.n != ctx.world_size():
+        raise MeshError(2, f"mesh covers {mesh.n} workers but the fabric has {ctx.world_size()}")
+    q, k, v = _inputs(q, k, v, "usp")
+    out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    co = opts._c()
+    check(lib().fusp_usp_attention_lse(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
+                                       _shape4(q), _ptr(out), _ptr(lse), ctypes.byref(co),
+                                       _stream()))
+    return AttnResult(out, lse)
+
+
+def _group_handle(ctx: WorkerContext, group: Optional[ProcessGroup]):
+    """The fusp_group of `group` on this context (NULL for the world in rank order).  Created on
+    first use -- for NCCL contexts group creation is collective over the world, so create
+    those groups up front on every rank with ctx.create_group(members)."""
+    if group is None or list(group.members) == list(range(ctx.world_size())):
+        return ctypes.c_void_p(0)
+    return ctx.create_group(group.members)
 
 
 def ulysses_attention(ctx: WorkerContext, q, k, v, group: Optional[ProcessGroup] = None,
-                      opts: Optional[CommOptions] = None) -> torch.Tensor:
-    """ulysses_attention (protocols.cpp:207-214) over the world group."""
+                      opts: Optional[CommOptions] = None, return_lse: bool = False):
+    """ulysses_attention(ctx, q, k, v, group, opts) (protocols.cpp:207-214); group None = world.
+    return_lse: an AttnResult with the rows' LSE (B200 extension)."""
     opts = opts or CommOptions()
-    _world_group(ctx, group)
     q, k, v = _inputs(q, k, v, "ulysses")
     out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device) if return_lse else None
     co = opts._c()
-    check(lib().fusp_ulysses_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
-                                       _shape4(q), _ptr(out), ctypes.byref(co), _stream()))
-    return out
+    check(lib().fusp_ulysses_attention_group(ctx.handle, _group_handle(ctx, group), _ptr(q), _ptr(k),
+                                             _ptr(v), _DT[q.dtype], _shape4(q), _ptr(out), _ptr(lse),
+                                             ctypes.byref(co), _stream()))
+    return AttnResult(out, lse) if return_lse else out
 
 
 def _ring(ctx, q, k, v, group, opts, pipelined):
     opts = opts or CommOptions()
-    _world_group(ctx, group)
     q, k, v = _inputs(q, k, v, "ring")
     out = torch.empty(q.shape, dtype=opts.out_dtype, device=q.device)
     lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
     co = opts._c()
     co.pipelined_ring = int(pipelined)
-    check(lib().fusp_ring_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _DT[q.dtype],
-                                    _shape4(q), _ptr(out), _ptr(lse), ctypes.byref(co), _stream()))
+    check(lib().fusp_ring_attention_group(ctx.handle, _group_handle(ctx, group), _ptr(q), _ptr(k),
+                                          _ptr(v), _DT[q.dtype], _shape4(q), _ptr(out), _ptr(lse),
+                                          ctypes.byref(co), _stream()))
     return AttnResult(out, lse)
 
 
 def ring_attention_serial(ctx, q, k, v, group=None, opts=None) -> AttnResult:
-    """ring_attention_serial (protocols.cpp:237-268) over the world group."""
+    """ring_attention_serial (protocols.cpp:237-268) over `group` (None = world)."""
     return _ring(ctx, q, k, v, group, opts, False)
 
 
 def ring_attention_pipelined(ctx, q, k, v, group=None, opts=None) -> AttnResult:
     """ring_attention_pipelined (protocols.cpp:270-319): double-buffered on a side stream."""
     return _ring(ctx, q, k, v, group, opts, True)
+
+
+@dataclass
+class Resharded:
+    """= uspsim::detail::Resharded (protocols.hpp:77-79): [B, H/U, U*S_local, D]."""
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+
+
+class detail:  # noqa: N801 -- namespace mirroring uspsim::detail (protocols.hpp:73-95)
+    @staticmethod
+    def ulysses_input_reshard(ctx: WorkerContext, q, k, v, group: Optional[ProcessGroup] = None,
+                              opts: Optional[CommOptions] = None,
+                              out_dtype=torch.float32) -> Resharded:
+        """detail::ulysses_input_reshard (protocols.cpp:125-180) on the GPU path: pack ->
+        all_to_all -> unpack; FP8 K/V come back as the exact dequantized values."""
+        opts = opts or CommOptions()
+        q, k, v = _inputs(q, k, v, "ulysses")
+        gh = _group_handle(ctx, group)
+        u = len(group.members) if group is not None else ctx.world_size()
+        b, h, s, d = q.shape
+        if h % u:
+            raise ShapeError(1, f"ulysses: head count H={h} not divisible by ulysses dimension U={u}")
+        shp = (b, h // u, s * u, d)
+        outs = [torch.empty(shp, dtype=out_dtype, device=q.device) for _ in range(3)]
+        co = opts._c()
+        check(lib().fusp_ulysses_input_reshard(ctx.handle, gh, _ptr(q), _ptr(k), _ptr(v),
+                                               _DT[q.dtype], _shape4(q), _ptr(outs[0]),
+                                               _ptr(outs[1]), _ptr(outs[2]), _DT[out_dtype],
+                                               ctypes.byref(co), _stream()))
+        return Resharded(*outs)
+
+    @staticmethod
+    def ulysses_output_reshard(ctx: WorkerContext, out, group: Optional[ProcessGroup] = None):
+        """detail::ulysses_output_reshard (protocols.cpp:182-203): [B,H/U,S,D] -> [B,H,S/U,D]."""
+        o = _dev(out)
+        if o.dtype not in _DT:
+            o = o.float()
+        u = len(group.members) if group is not None else ctx.world_size()
+        b, hp, s, d = o.shape
+        if s % u:
+            raise ShapeError(1, f"ulysses: gathered sequence length S={s} not divisible by ulysses "
+                                f"dimension U={u}")
+        res = torch.empty((b, hp * u, s // u, d), dtype=o.dtype, device=o.device)
+        check(lib().fusp_ulysses_output_reshard(ctx.handle, _group_handle(ctx, group), _ptr(o),
+                                                _DT[o.dtype], _shape4(o), _ptr(res), _stream()))
+        return res
 
 
 def out_projection(o: torch.Tensor, w: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
@@ -668,6 +773,7 @@ class LayerGraph:
         per_out = out[0].numel() * out.element_size()
         h = ctypes.c_void_p()
         self._keep = (q, k, v, out)
+        self._ctx = ctx  # the graph replays the context's communicators: keep it alive
         check(lib().fusp_graph_capture_usp(ctx.handle, mesh.r, _ptr(q), _ptr(k), _ptr(v),
                                            _DT[q.dtype], _shape4(q[0]), _ptr(out),
                                            ctypes.byref(co), layers, per_in, per_out, _stream(),

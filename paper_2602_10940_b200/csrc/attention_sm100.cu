@@ -121,8 +121,12 @@ struct Params {
   int64_t out_hs, out_cs, out_rs;  // element strides: head, chunk, row
   float* lse;        // [heads][lse_hs] natural-log LSE or null
   int64_t lse_hs;
+  int64_t lse_cs;    // floats between output chunks (the output all-to-all slots), like out_cs
   const float* acc_o;    // fp32 [heads][sq][D] running accumulator or null
   const float* acc_lse;  // [heads][sq]
+  const int* q_exp;      // per-head f16 range-guard exponents of the operands (null = 0)
+  const int* k_exp;
+  const int* v_exp;
   Sched sc;
   uint32_t* counters;    // split: [n_qb][2 tiles][arrive, written], zero between launches
   float* slots;          // split: [gridDim.x][2 (first/last segment)][2 tiles][kSlotTileFloats]
@@ -486,8 +490,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t t_s = kTmemS + lane_off + t * 128;
     const uint32_t t_o = kTmemO + lane_off + t * 128;
-    const float sl2 = p.scale_log2;
-    const float2 sl2x2 = make_float2(sl2, sl2);
 
     SegIter si(sc);
     Seg g;
@@ -497,6 +499,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool tr = r_in_tile == 0 && tslot >= 0;
       if (tr) FUSP_TRACE(p, tslot);
       const int head = g.qb / sc.qb_per_head;
+      // f16 range guard (fastusp_internal.h): Q, K, V of this head were staged as x * 2^-e;
+      // 2^(eq + ek) folds into the softmax scale, 2^ev into the output
+      const int e_qk = (p.q_exp != nullptr ? p.q_exp[head] : 0) + (p.k_exp != nullptr ? p.k_exp[head] : 0);
+      const float sl2 = p.scale_log2 * __int_as_float((127 + e_qk) << 23);
+      const float v_scale = p.v_exp != nullptr ? __int_as_float((127 + p.v_exp[head]) << 23) : 1.f;
+      const float2 sl2x2 = make_float2(sl2, sl2);
       const int row = (g.qb - head * sc.qb_per_head) * kQB + t * kBM + r_in_tile;
       float m_use = -INFINITY;  // max used for the exponent (raw logit units)
       float l_sum = 0.f;
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float l1 = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
         lse_out = merge_coeffs(l1, lse_b, c_acc, c_new);
       }
-      const float scale_new = c_new * inv_l;
+      const float scale_new = c_new * inv_l * v_scale;
       const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
                             static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
                             static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
@@ -853,7 +861,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (FUSP_TRACE_EPI && tr) FUSP_TRACE(p, tslot + 4);
-      if (in_range && p.lse != nullptr) p.lse[static_cast<int64_t>(head) * p.lse_hs + row] = lse_out;
+      if (in_range && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(head) * p.lse_hs + static_cast<int64_t>(row / p.out_chunk) * p.lse_cs +
+              row % p.out_chunk] = lse_out;
       if (tr) FUSP_TRACE(p, tslot + 7);
       tc_fence_before();
     }
@@ -960,8 +970,12 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   p.out_rs = a.out_rs;
   p.lse = a.lse;
   p.lse_hs = a.lse_hs;
+  p.lse_cs = a.lse_cs;
   p.acc_o = a.acc_o;
   p.acc_lse = a.acc_lse;
+  p.q_exp = a.q_exp;
+  p.k_exp = a.k_exp;
+  p.v_exp = a.v_exp;
   const size_t need = attention_workspace_bytes(a.heads, a.sq, a.skv);
   const bool have_ws = a.split_ws != nullptr && need > 0 && a.split_ws_bytes >= need &&
                        a.split_counters != nullptr &&
@@ -986,14 +1000,8 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
     p.counters = a.split_counters;
     p.slots = static_cast<float*>(a.split_ws);
   }
-  static bool attr_set = false;
   const int smem = static_cast<int>(sizeof(Smem)) + 1024;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(attn_fwd_kernel)");
-    attr_set = true;
-  }
+  FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem, "attn_fwd_kernel"));
   if (g_trace_on) {
     if (g_trace == nullptr) FUSP_CUDA(cudaMalloc(&g_trace, sizeof(unsigned long long) * kMaxGrid * kTraceSlots));
     FUSP_CUDA(cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * kMaxGrid * kTraceSlots, stream));

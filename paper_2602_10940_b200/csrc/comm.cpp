@@ -1,8 +1,10 @@
 // LocalComm (threads-as-ranks fabric with copy-engine pulls) and NcclComm.
 #include "comm.h"
 
+#include <algorithm>
 #include <chrono>
 #include <sstream>
+#include <thread>
 
 namespace fusp {
 
@@ -24,6 +26,11 @@ fusp_status nccl_error(ncclResult_t r, const std::string& where) {
     ncclResult_t _r = (expr);                             \
     if (_r != ncclSuccess) return nccl_error(_r, #expr);  \
   } while (0)
+
+fusp_status Comm::wait(cudaStream_t s, double, const char*) {
+  FUSP_CUDA(cudaStreamSynchronize(s));  // in-process fabric: its rendezvous carries the timeout
+  return FUSP_OK;
+}
 
 // ---- LocalComm ----------------------------------------------------------------------------
 LocalComm::LocalComm(LocalFabric* f, int rank, int device) : fabric_(f), rank_(rank), device_(device) {
@@ -131,8 +138,54 @@ NcclComm::NcclComm(ncclComm_t world, int rank, int nranks)
     : world_(world), rank_(rank), nranks_(nranks) {}
 
 NcclComm::~NcclComm() {
+  if (aborted_) return;  // ncclCommAbort already released them
   for (auto& kv : subs_) ncclCommDestroy(kv.second);
   if (world_) ncclCommDestroy(world_);
+}
+
+fusp_status NcclComm::fail(const std::string& why) {
+  if (!aborted_) {
+    for (auto& kv : subs_) ncclCommAbort(kv.second);
+    if (world_) ncclCommAbort(world_);
+    subs_.clear();
+    world_ = nullptr;
+    aborted_ = true;
+  }
+  return set_error(FUSP_ERR_DEADLOCK, "deadlock: rank " + std::to_string(rank_) + " " + why);
+}
+
+fusp_status NcclComm::check_async(const char* op, const Group& g) {
+  std::vector<ncclComm_t> all{world_};
+  for (auto& kv : subs_) all.push_back(kv.second);
+  for (ncclComm_t c : all) {
+    ncclResult_t r = ncclSuccess;
+    if (c == nullptr || ncclCommGetAsyncError(c, &r) != ncclSuccess) continue;
+    if (r != ncclSuccess && r != ncclInProgress)
+      return fail(std::string("stalled in ") + op + "(group=" + g.key() + "): NCCL " +
+                  ncclGetErrorString(r) + "; communicators aborted");
+  }
+  return FUSP_OK;
+}
+
+fusp_status NcclComm::wait(cudaStream_t s, double timeout_s, const char* what) {
+  if (aborted_) return set_error(FUSP_ERR_COMM, "NCCL communicators were aborted after a failure");
+  const auto t0 = std::chrono::steady_clock::now();
+  Group world;
+  for (int i = 0; i < nranks_; ++i) world.members.push_back(i);
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return FUSP_OK;
+    if (q != cudaErrorNotReady) return set_cuda_error(q, "cudaStreamQuery");
+    FUSP_CHECK(check_async(what, world));
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > timeout_s) {
+      std::ostringstream os;
+      os << "timed out after " << timeout_s << " s waiting in " << what
+         << " (a peer never joined its collective); communicators aborted";
+      return fail(os.str());
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
 }
 
 fusp_status NcclComm::ensure_mesh(int r) {
@@ -157,8 +210,25 @@ fusp_status NcclComm::ensure_mesh(int r) {
   return FUSP_OK;
 }
 
+fusp_status NcclComm::split_group(const Group& g) {
+  // Collective over the world: members pass color = their group's smallest member (disjoint
+  // groups of one call get distinct colors) and key = position; others opt out.
+  const bool in = g.size() > 0 && g.pos >= 0;
+  int color = NCCL_SPLIT_NOCOLOR;
+  if (in) color = *std::min_element(g.members.begin(), g.members.end());
+  ncclComm_t c = nullptr;
+  FUSP_NCCL(ncclCommSplit(world_, color, in ? g.pos : 0, &c, nullptr));
+  if (!in) return FUSP_OK;
+  auto it = subs_.find(g.key());
+  if (it != subs_.end()) ncclCommDestroy(it->second);
+  subs_[g.key()] = c;
+  return FUSP_OK;
+}
+
 fusp_status NcclComm::sub(const Group& g, ncclComm_t* out) {
-  if (g.size() == nranks_) {
+  bool identity = g.size() == nranks_;
+  for (int i = 0; i < g.size() && identity; ++i) identity = g.members[i] == i;
+  if (identity) {  // the world communicator's ranks are the group positions
     *out = world_;
     return FUSP_OK;
   }
@@ -178,6 +248,7 @@ fusp_status NcclComm::all_to_all(const Group& g, const void* send, void* recv, s
     FUSP_CUDA(cudaMemcpyAsync(rp + g.pos * stride, sp + g.pos * stride, bytes,
                               cudaMemcpyDeviceToDevice, s));
   if (n == 1 || bytes == 0) return FUSP_OK;
+  if (aborted_) return set_error(FUSP_ERR_COMM, "NCCL communicators were aborted after a failure");
   ncclComm_t c;
   FUSP_CHECK(sub(g, &c));
   FUSP_NCCL(ncclGroupStart());
@@ -187,7 +258,7 @@ fusp_status NcclComm::all_to_all(const Group& g, const void* send, void* recv, s
     FUSP_NCCL(ncclRecv(rp + j * stride, bytes, ncclUint8, j, c, s));
   }
   FUSP_NCCL(ncclGroupEnd());
-  return FUSP_OK;
+  return check_async("all_to_all", g);
 }
 
 fusp_status NcclComm::ring_exchange(const Group& g, const void* const* send, void* const* recv,
@@ -199,6 +270,7 @@ fusp_status NcclComm::ring_exchange(const Group& g, const void* const* send, voi
         FUSP_CUDA(cudaMemcpyAsync(recv[i], send[i], bytes[i], cudaMemcpyDeviceToDevice, s));
     return FUSP_OK;
   }
+  if (aborted_) return set_error(FUSP_ERR_COMM, "NCCL communicators were aborted after a failure");
   ncclComm_t c;
   FUSP_CHECK(sub(g, &c));
   FUSP_NCCL(ncclGroupStart());
@@ -207,7 +279,7 @@ fusp_status NcclComm::ring_exchange(const Group& g, const void* const* send, voi
     FUSP_NCCL(ncclRecv(recv[i], bytes[i], ncclUint8, (g.pos - 1 + n) % n, c, s));
   }
   FUSP_NCCL(ncclGroupEnd());
-  return FUSP_OK;
+  return check_async("send", g);
 }
 
 }  // namespace fusp

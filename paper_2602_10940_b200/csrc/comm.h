@@ -51,6 +51,9 @@ class Comm {
   virtual fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                                     const size_t* bytes, int nparts, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;
+  // Host wait until `s` drained, bounded by timeout_s: a stalled or failed peer becomes
+  // FUSP_ERR_DEADLOCK (the reference's DeadlockError, fabric.hpp:112-116) instead of a hang.
+  virtual fusp_status wait(cudaStream_t s, double timeout_s, const char* what);
   // SMs a transfer in flight occupies (its kernels must find free SMs while the persistent
   // attention kernel runs beside it): NCCL p2p kernels need some, copy engines none.
   virtual int sms_in_flight() const { return 0; }
@@ -127,9 +130,20 @@ class NcclComm : public Comm {
   // Collective over the world: make sure sub-communicators for every group of the
   // (R,U) mesh exist (ncclCommSplit, color = ring / ulysses index).
   fusp_status ensure_mesh(int r);
+  // Collective over the world (fusp_group_create): a sub-communicator for `g` (g.pos < 0 or an
+  // empty group: this rank joins the split call without a group).
+  fusp_status split_group(const Group& g);
+  // Polls ncclCommGetAsyncError on every communicator while the stream drains; on an error or
+  // the timeout, ncclCommAbort on all of them (fabric.hpp:106-126 semantics).
+  fusp_status wait(cudaStream_t s, double timeout_s, const char* what) override;
 
  private:
   fusp_status sub(const Group& g, ncclComm_t* out);
+  // After an enqueue: a communicator that already reports an asynchronous error (a peer that
+  // failed or never arrived) aborts the world -> FUSP_ERR_DEADLOCK naming the operation.
+  fusp_status check_async(const char* op, const Group& g);
+  fusp_status fail(const std::string& why);
+  bool aborted_ = false;
   ncclComm_t world_;
   int rank_, nranks_;
   std::map<std::string, ncclComm_t> subs_;

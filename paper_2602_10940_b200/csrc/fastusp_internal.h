@@ -27,6 +27,9 @@ void clear_error();
   } while (0)
 
 void count_launch(int n = 1);
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) attribute: set it
+// once per (kernel, device), thread-safely, before the first launch on that device.
+fusp_status ensure_smem_attr(const void* kernel, int bytes, const char* name);
 
 // ---- TMA descriptors ------------------------------------------------------------------
 // 3-D map over [heads][rows][128] 16-bit elements with a head stride of `head_stride`
@@ -69,6 +72,7 @@ struct AttnLaunch {
   int64_t out_hs, out_cs, out_rs;
   float* lse;
   int64_t lse_hs;
+  int64_t lse_cs = 0;  // floats between output chunks (LSE riding the output all-to-all)
   const float* acc_o;    // merge into (acc_o, acc_lse) when non-null
   const float* acc_lse;
   void* split_ws;        // stream-K partial slots (attention_workspace_bytes)
@@ -76,6 +80,9 @@ struct AttnLaunch {
   uint32_t* split_counters;    // stream-K tickets (attention_counter_words): zero-initialised,
   size_t split_counter_words;  // never written by anything else
   int max_ctas;  // persistent grid cap (0 = every SM): leaves SMs to a concurrent transfer
+  const int* q_exp = nullptr;  // per-head range-guard exponents (StageOp.exps) or null
+  const int* k_exp = nullptr;
+  const int* v_exp = nullptr;
 };
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
 // Workspace the persistent attention kernel needs for a (heads, sq, skv) problem (0 when the
@@ -169,6 +176,44 @@ fusp_status launch_unpack_heads(const void* src, int64_t slot_stride, void* dst,
                                 int hp, int sl, int d, int u, cudaStream_t s);
 
 size_t dtype_size(int dt);
+
+// ---- operand staging (kernels.cu) --------------------------------------------------------
+// The tensor-core operands of the attention kernel are bf16 (Q, K of bf16 inputs) or f16.  f16
+// has 5 exponent bits, so every staging pass INTO f16 from a wider-range source (f32, bf16, or
+// decode(code) * scale of an FP8 chunk) is range-guarded: it records max|x| per head, and a
+// head whose maximum falls outside [2^-6, 2^15) is stored as x * 2^-e with the power of two
+// e = exps[head] chosen so that max|x| * 2^-e lies in [2^14, 2^15) -- exact scaling, no
+// overflow to inf, no loss to f16 subnormals.  The attention kernel folds 2^(eq + ek) into
+// its softmax scale and 2^ev into the output, so results are the unscaled ones.  The decision
+// needs the whole head's maximum: the staging kernel converts with e = 0 and folds max|x| into
+// a per-(op, head) word (one relaxed atomic per warp); a small per-head kernel then sets
+// exps[head], resets the word and, only when e != 0, rewrites that head (the rare path; one
+// CTA per affected head, heads in parallel).
+//
+// Layout (the Ulysses unpack; u = 1 is plain staging of a [bhp][sl][d] tensor): slab (j, bh)
+// of the source, at src + j * src_slot_stride + bh * sl * d, lands at rows [j*sl, (j+1)*sl)
+// of operand slab bh: dst + (bh * u + j) * sl * d.
+constexpr int kGuardExpMin = -40, kGuardExpMax = 60;  // clamp (eq + ek, ev stay normal f32)
+struct StageOp {
+  const void* src;
+  int sdt;                  // F32 / BF16 / F16 / E4M3
+  int64_t src_slot_stride;  // source elements (bytes for e4m3) between slots j
+  const float* scales;      // e4m3: value = decode(c) * scales[j * scale_stride + bh * scale_bh_stride]
+  int64_t scale_stride, scale_bh_stride;
+  void* dst;                // operand in ddt (F16 / BF16 / F32), or null (raw only)
+  int ddt;
+  void* raw;                // optional: the source bytes unchanged, in operand layout
+  int* exps;                // non-null: guarded f16 destination, per-bh exponent out
+  uint32_t* words;          // guarded: bhp zero-initialised words (max|x| bits), left zeroed
+  // Layout overrides (elements; 0 = the unpack layout above): slab (j, bh) reads
+  // src + j * src_slot_stride + bh * src_bh_stride and writes dst/raw + j * dst_slot_stride +
+  // bh * dst_bh_stride.  The inverse mapping (operand rows -> slots) is the output-reshard pack.
+  int64_t src_bh_stride = 0, dst_slot_stride = 0, dst_bh_stride = 0;
+};
+constexpr int kMaxStageOps = 6;
+fusp_status launch_stage(const StageOp* ops, int n, int bhp, int sl, int d, int u, cudaStream_t s);
+// zeroed words one guarded StageOp needs
+inline size_t stage_words(int bhp) { return 2 * static_cast<size_t>(bhp); }
 
 // FP8 helpers for the protocols (blocked quantizer; one block = per-tensor reference mode).
 // Source of the values to quantize: a float tensor (dt = F32/F16/BF16), or an E4M3 chunk

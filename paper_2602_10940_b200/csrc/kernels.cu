@@ -14,12 +14,11 @@
 namespace fusp {
 namespace {
 
-constexpr int kSMs = 148;
 constexpr int kBlock = 256;
 
 inline int grid_for(int64_t work_items, int per_sm = 8) {  // grid-stride kernels
   int64_t g = (work_items + kBlock - 1) / kBlock;
-  if (g > int64_t(kSMs) * per_sm) g = int64_t(kSMs) * per_sm;
+  if (g > int64_t(sm_count()) * per_sm) g = int64_t(sm_count()) * per_sm;
   return g < 1 ? 1 : static_cast<int>(g);
 }
 
@@ -680,6 +679,204 @@ __global__ void __launch_bounds__(256) unpack_slab_kernel(const __grid_constant_
   }
 }
 
+// ---- operand staging with the f16 range guard (fastusp_internal.h, StageOp) ---------------
+struct Raw8 {  // 8 source elements as loaded: f32 = a,b; 16-bit = a; e4m3 = a.x, a.y
+  uint4 a, b;
+};
+__device__ __forceinline__ Raw8 load_raw8(const void* base, int sdt, int64_t i) {
+  Raw8 r;
+  if (sdt == FUSP_F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const float*>(base) + i);
+    r.a = __ldg(p);
+    r.b = __ldg(p + 1);
+  } else if (sdt == FUSP_E4M3) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(base) + i));
+    r.a = make_uint4(w.x, w.y, 0u, 0u);
+  } else {
+    r.a = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + i));
+  }
+  return r;
+}
+__device__ __forceinline__ void store_raw8(void* base, int sdt, int64_t i, const Raw8& r) {
+  if (sdt == FUSP_F32) {
+    uint4* p = reinterpret_cast<uint4*>(static_cast<float*>(base) + i);
+    p[0] = r.a;
+    p[1] = r.b;
+  } else if (sdt == FUSP_E4M3) {
+    *reinterpret_cast<uint2*>(static_cast<uint8_t*>(base) + i) = make_uint2(r.a.x, r.a.y);
+  } else {
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(base) + i) = r.a;
+  }
+}
+__device__ __forceinline__ Vec8 raw_to_f32(const Raw8& r, int sdt, float sc) {
+  Vec8 v;
+  if (sdt == FUSP_F32) {
+    v.f[0] = __uint_as_float(r.a.x); v.f[1] = __uint_as_float(r.a.y);
+    v.f[2] = __uint_as_float(r.a.z); v.f[3] = __uint_as_float(r.a.w);
+    v.f[4] = __uint_as_float(r.b.x); v.f[5] = __uint_as_float(r.b.y);
+    v.f[6] = __uint_as_float(r.b.z); v.f[7] = __uint_as_float(r.b.w);
+  } else if (sdt == FUSP_E4M3) {
+    v = decode8(make_uint2(r.a.x, r.a.y), sc);
+  } else {
+    const uint32_t ww[4] = {r.a.x, r.a.y, r.a.z, r.a.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 x;
+      if (sdt == FUSP_F16) x = __half22float2(*reinterpret_cast<const __half2*>(&ww[e]));
+      else x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[e]));
+      v.f[2 * e] = x.x;
+      v.f[2 * e + 1] = x.y;
+    }
+  }
+  return v;
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+// Exponent of the f16 range guard: 0 while max|x| is in [2^-6, 2^15) (or zero / non-finite),
+// else e with max|x| * 2^-e in [2^14, 2^15), clamped to [kGuardExpMin, kGuardExpMax].
+__device__ __forceinline__ int guard_exp(float amax) {
+  if (!(amax > 0.f) || !isfinite(amax)) return 0;
+  if (amax >= 0x1p-6f && amax < 0x1p15f) return 0;
+  const int e = static_cast<int>((__float_as_uint(amax) >> 23) & 0xFFu) - 127 - 14;
+  return e < kGuardExpMin ? kGuardExpMin : (e > kGuardExpMax ? kGuardExpMax : e);
+}
+
+#ifndef FUSP_STAGE_MINB   // resident CTAs per SM the staging kernel is compiled for
+#define FUSP_STAGE_MINB 4
+#endif
+#ifndef FUSP_STAGE_NV     // 16-byte vectors in flight per thread (f32 sources: half as many 32-byte)
+#define FUSP_STAGE_NV 4
+#endif
+#ifndef FUSP_STAGE_WAVES  // grid cap: CTAs per SM (one resident wave at FUSP_STAGE_MINB)
+#define FUSP_STAGE_WAVES FUSP_STAGE_MINB
+#endif
+struct StageArgs {
+  StageOp op[kMaxStageOps];
+  int bhp, u, slab_vecs;
+  int64_t slab_elems;
+};
+// Main pass of one staging op, everything per element known at compile time: the source
+// dtype, the destination mode (DDT = -1: copy of the source bytes), the range guard (max|x|)
+// and the optional raw copy.  Pointers and offsets are hoisted out of the loop.  Registers:
+// the f32 source keeps half as many (32-byte) vectors in flight per thread.
+template <int SDT, int DDT, bool GUARD, bool RAW>
+__device__ __forceinline__ float stage_main(const void* __restrict__ src, void* __restrict__ dst,
+                                            void* __restrict__ raw, int slab_vecs, float sc) {
+  constexpr int NV = SDT == FUSP_F32 ? (FUSP_STAGE_NV + 1) / 2 : FUSP_STAGE_NV;
+  const int stride = gridDim.x * blockDim.x;
+  float m = 0.f;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < slab_vecs; v += NV * stride) {
+    Raw8 r[NV];
+#pragma unroll
+    for (int e = 0; e < NV; ++e)
+      if (v + e * stride < slab_vecs) r[e] = load_raw8(src, SDT, int64_t(v + e * stride) * 8);
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      if (v + e * stride >= slab_vecs) break;
+      const int64_t i = int64_t(v + e * stride) * 8;
+      if (RAW) store_raw8(raw, SDT, i, r[e]);
+      if (DDT < 0) {
+        store_raw8(dst, SDT, i, r[e]);
+      } else {
+        const Vec8 x = raw_to_f32(r[e], SDT, sc);
+        if (GUARD) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(x.f[k]));
+        }
+        store8(dst, DDT, i, x);
+      }
+    }
+  }
+  return m;
+}
+
+template <int SDT>
+__device__ __forceinline__ float stage_dispatch(const StageOp& o, const char* src, char* dst,
+                                                char* raw, int slab_vecs, float sc) {
+  const bool guard = o.exps != nullptr;
+  if (o.dst == nullptr) return stage_main<SDT, -1, false, false>(src, raw, nullptr, slab_vecs, sc);
+  if (o.ddt == SDT && !guard) return stage_main<SDT, -1, false, false>(src, dst, nullptr, slab_vecs, sc);
+  if (guard) {
+    if (raw != nullptr) return stage_main<SDT, FUSP_F16, true, true>(src, dst, raw, slab_vecs, sc);
+    return stage_main<SDT, FUSP_F16, true, false>(src, dst, nullptr, slab_vecs, sc);
+  }
+  switch (o.ddt) {
+    case FUSP_F16: return stage_main<SDT, FUSP_F16, false, false>(src, dst, nullptr, slab_vecs, sc);
+    case FUSP_BF16: return stage_main<SDT, FUSP_BF16, false, false>(src, dst, nullptr, slab_vecs, sc);
+    default: return stage_main<SDT, FUSP_F32, false, false>(src, dst, nullptr, slab_vecs, sc);
+  }
+}
+
+// grid (x: part of a slab, y: slab (j, bh), z: op).  Plain copies, conversions, e4m3 decodes;
+// guarded f16 destinations fold max|x| into their per-head word (fastusp_internal.h).
+__global__ void __launch_bounds__(256, FUSP_STAGE_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");  // let stage_decide_kernel get scheduled
+  const StageOp& o = a.op[blockIdx.z];
+  const int slab = blockIdx.y;
+  const int j = slab / a.bhp, bh = slab - j * a.bhp;
+  const int64_t s0 = int64_t(j) * o.src_slot_stride + int64_t(bh) * o.src_bh_stride;
+  const int64_t d0 = int64_t(j) * o.dst_slot_stride + int64_t(bh) * o.dst_bh_stride;
+  const int sdt = o.sdt;
+  const float sc = sdt == FUSP_E4M3 ? o.scales[j * o.scale_stride + bh * o.scale_bh_stride] : 1.f;
+  const bool guard = o.exps != nullptr;
+  const int64_t ssz = sdt == FUSP_F32 ? 4 : sdt == FUSP_E4M3 ? 1 : 2;
+  const int64_t dsz = o.dst == nullptr ? ssz : (o.ddt == FUSP_F32 ? 4 : 2);
+  const char* src = static_cast<const char*>(o.src) + s0 * ssz;
+  char* dst = o.dst != nullptr ? static_cast<char*>(o.dst) + d0 * dsz : nullptr;
+  char* raw = o.raw != nullptr ? static_cast<char*>(o.raw) + d0 * ssz : nullptr;
+  float m;
+  switch (sdt) {
+    case FUSP_F32: m = stage_dispatch<FUSP_F32>(o, src, dst, raw, a.slab_vecs, sc); break;
+    case FUSP_F16: m = stage_dispatch<FUSP_F16>(o, src, dst, raw, a.slab_vecs, sc); break;
+    case FUSP_BF16: m = stage_dispatch<FUSP_BF16>(o, src, dst, raw, a.slab_vecs, sc); break;
+    default: m = stage_dispatch<FUSP_E4M3>(o, src, dst, raw, a.slab_vecs, sc); break;
+  }
+  if (!guard) return;
+  // per-warp max -> one relaxed atomic per warp; no CTA barrier, no fence: the per-head
+  // decision runs in stage_decide_kernel, ordered after this kernel by the stream
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(&o.words[bh], __float_as_uint(m));
+}
+
+// Per (head, guarded op), kFixParts CTAs: each derives e from the head's max|x| word; part 0
+// publishes exps[bh]; the last part to count (relaxed ticket, words[bhp + bh]) resets both
+// words for the next call.  A head outside [2^-6, 2^15) is rewritten as x * 2^-e, its slabs'
+// vectors split over the parts -- the rare path; the common one exits after one load.
+constexpr int kFixParts = 8;
+__global__ void __launch_bounds__(256) stage_decide_kernel(const __grid_constant__ StageArgs a) {
+  const StageOp& o = a.op[blockIdx.y];
+  if (o.exps == nullptr) return;
+  const int bh = blockIdx.x, part = blockIdx.z;
+  // launched as a programmatic dependent of stage_kernel: resident early, and this waits for
+  // the staging grid's completion and memory (griddepcontrol.wait)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ int s_e;
+  if (threadIdx.x == 0) {
+    const int e = guard_exp(__uint_as_float(__ldcg(&o.words[bh])));
+    if (part == 0) o.exps[bh] = e;
+    __threadfence();  // our read of the word before our ticket
+    if (atomicAdd(&o.words[a.bhp + bh], 1u) + 1 == kFixParts) {
+      o.words[bh] = 0u;
+      o.words[a.bhp + bh] = 0u;
+    }
+    s_e = e;
+  }
+  __syncthreads();
+  if (s_e == 0) return;
+  const bool e4 = o.sdt == FUSP_E4M3;
+  const float f = pow2f(-s_e);
+  for (int jj = 0; jj < a.u; ++jj) {
+    const int64_t sj = int64_t(jj) * o.src_slot_stride + int64_t(bh) * o.src_bh_stride;
+    const int64_t dj = int64_t(jj) * o.dst_slot_stride + int64_t(bh) * o.dst_bh_stride;
+    const float scj = e4 ? o.scales[jj * o.scale_stride + bh * o.scale_bh_stride] : 1.f;
+    for (int v = part * blockDim.x + threadIdx.x; v < a.slab_vecs; v += kFixParts * blockDim.x) {
+      Vec8 x = raw_to_f32(load_raw8(o.src, o.sdt, sj + int64_t(v) * 8), o.sdt, scj);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x.f[k] *= f;
+      store8(o.dst, o.ddt, dj + int64_t(v) * 8, x);
+    }
+  }
+}
+
 // Source value of 8 consecutive elements (one row segment) for the FP8 passes.
 __device__ __forceinline__ Vec8 src_vec8(const Fp8Src& s, int64_t i) {  // i < 2^31 (launcher)
   if (s.dt != FUSP_E4M3) return load8(s.x, s.dt, i);
@@ -918,7 +1115,7 @@ int slab_grid_x(int64_t slab_vecs, int64_t slabs) {
   // enough CTAs per slab to cover it once with 4 vectors per thread, capped near 16
   // resident CTAs per SM overall
   int64_t gx = (slab_vecs + 4 * kBlock - 1) / (4 * kBlock);
-  const int64_t cap = (int64_t(kSMs) * 16 + slabs - 1) / slabs;
+  const int64_t cap = (int64_t(sm_count()) * 16 + slabs - 1) / slabs;
   if (gx > cap) gx = cap;
   return gx < 1 ? 1 : static_cast<int>(gx);
 }
@@ -992,6 +1189,65 @@ fusp_status launch_unpack_multi(const UnpackDesc* us, int n, cudaStream_t s) {
   return FUSP_OK;
 }
 
+fusp_status launch_stage(const StageOp* ops, int n, int bhp, int sl, int d, int u, cudaStream_t s) {
+  if (n <= 0 || bhp <= 0 || sl <= 0 || u <= 0) return FUSP_OK;
+  if (n > kMaxStageOps) return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: too many operands");
+  const int64_t slab_elems = int64_t(sl) * d;
+  const int64_t slabs = int64_t(u) * bhp;
+  if (d % 8 != 0 || slabs > 65535 || slab_elems / 8 >= (int64_t(1) << 31))
+    return set_error(FUSP_ERR_SHAPE, "stage: unsupported operand shape");
+  StageArgs a{};
+  for (int i = 0; i < n; ++i) {
+    const StageOp& o = ops[i];
+    const int64_t esz = int64_t(dtype_size(o.sdt));
+    const bool ok = aligned16(o.src) && (o.src_slot_stride * esz) % 16 == 0 &&
+                    (o.dst == nullptr || aligned16(o.dst)) && (o.raw == nullptr || aligned16(o.raw)) &&
+                    (o.sdt != FUSP_E4M3 || o.scales != nullptr) &&
+                    (o.exps == nullptr || (o.words != nullptr && o.dst != nullptr && o.ddt == FUSP_F16)) &&
+                    (o.dst == nullptr || o.ddt != FUSP_E4M3);
+    if (!ok) return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: operand not 16-byte aligned or malformed");
+    a.op[i] = o;
+    StageOp& x = a.op[i];
+    if (x.src_bh_stride == 0) x.src_bh_stride = slab_elems;
+    if (x.dst_slot_stride == 0) x.dst_slot_stride = slab_elems;
+    if (x.dst_bh_stride == 0) x.dst_bh_stride = int64_t(u) * slab_elems;
+    const int64_t dsz = x.dst != nullptr ? int64_t(dtype_size(x.ddt)) : esz;
+    if ((x.src_bh_stride * esz) % 16 != 0 || (x.dst_slot_stride * dsz) % 16 != 0 ||
+        (x.dst_bh_stride * dsz) % 16 != 0)
+      return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: strides not 16-byte granular");
+  }
+  a.bhp = bhp;
+  a.u = u;
+  a.slab_vecs = static_cast<int>(slab_elems / 8);
+  a.slab_elems = slab_elems;
+  // one resident wave (4 CTAs per SM): each CTA loops over its slab part, so the per-CTA
+  // ticket of the range guard is paid once per CTA, not once per 16 KB
+  int64_t gx = (a.slab_vecs + 4 * kBlock - 1) / (4 * kBlock);
+  const int64_t cap = (int64_t(sm_count()) * FUSP_STAGE_WAVES + slabs * n - 1) / (slabs * n);
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  stage_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(slabs), n), kBlock, 0, s>>>(a);
+  FUSP_LAUNCHED("stage_kernel");
+  bool guarded = false;
+  for (int i = 0; i < n; ++i) guarded = guarded || a.op[i].exps != nullptr;
+  if (guarded) {
+    // programmatic dependent launch: the decision kernel's launch latency hides under the
+    // staging grid instead of following it
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(bhp), n, kFixParts);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FUSP_CUDA(cudaLaunchKernelEx(&cfg, stage_decide_kernel, a));
+    FUSP_LAUNCHED("stage_decide_kernel");
+  }
+  return FUSP_OK;
+}
+
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s) { return launch_pack_multi(&p, 1, s); }
 fusp_status launch_unpack(const UnpackDesc& p, cudaStream_t s) { return launch_unpack_multi(&p, 1, s); }
 
@@ -1051,7 +1307,7 @@ fusp_status launch_amax_blocks_raw(const Fp8Src& src, int64_t block_elems, int n
                                    uint32_t* amax, cudaStream_t s) {  // amax zeroed by the caller
   if (block_elems <= 0 || nblocks <= 0) return FUSP_OK;
   int gx = grid_for(block_elems, 4);
-  const int cap = (kSMs * 8 + nblocks - 1) / nblocks;
+  const int cap = (sm_count() * 8 + nblocks - 1) / nblocks;
   if (gx > cap) gx = cap < 1 ? 1 : cap;
   amax_blocks_kernel<<<dim3(gx, nblocks), kBlock, 0, s>>>(src, block_elems, amax, nullptr);
   FUSP_LAUNCHED("amax_blocks_kernel");
@@ -1071,7 +1327,7 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
     a.block_vecs = block_elems / 8;
     a.nonfinite = nonfinite;
     int gx = grid_for(a.block_vecs, 8);
-    const int cap = (kSMs * 8 + nblocks - 1) / nblocks;
+    const int cap = (sm_count() * 8 + nblocks - 1) / nblocks;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
     amax_vec_kernel<<<dim3(gx, nblocks, 1), kBlock, 0, s>>>(a);
     FUSP_LAUNCHED("amax_vec_kernel");
@@ -1081,7 +1337,7 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
     return FUSP_OK;
   }
   int gx = grid_for(block_elems, 4);
-  const int cap = (kSMs * 8 + nblocks - 1) / nblocks;  // ~8 CTAs per SM in total
+  const int cap = (sm_count() * 8 + nblocks - 1) / nblocks;  // ~8 CTAs per SM in total
   if (gx > cap) gx = cap < 1 ? 1 : cap;
   amax_blocks_kernel<<<dim3(gx, nblocks), kBlock, 0, s>>>(src, block_elems, amax, nonfinite);
   FUSP_LAUNCHED("amax_blocks_kernel");
@@ -1130,7 +1386,7 @@ fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems,
   }
   a.block_vecs = block_elems / 8;
   int gx = grid_for(a.block_vecs, 8);
-  const int cap = (kSMs * 8 + nblocks * parts - 1) / (nblocks * parts);
+  const int cap = (sm_count() * 8 + nblocks * parts - 1) / (nblocks * parts);
   if (gx > cap) gx = cap < 1 ? 1 : cap;
   amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("amax_vec_kernel");
@@ -1163,7 +1419,7 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
   a.block_vecs = block_elems / 8;
   a.nonfinite = nonfinite;
   int gx = grid_for(a.block_vecs, 8);
-  const int cap = (kSMs * 8 + nblocks * parts - 1) / (nblocks * parts);
+  const int cap = (sm_count() * 8 + nblocks * parts - 1) / (nblocks * parts);
   if (gx > cap) gx = cap < 1 ? 1 : cap;
   amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("amax_vec_kernel");

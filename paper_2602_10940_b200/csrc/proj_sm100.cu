@@ -369,12 +369,8 @@ fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, con
   p.m_fast = proj_m_fast(int64_t(b) * s * h * 128 * 2, int64_t(h) * 128 * n * 2) ? 1 : 0;
   p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, false>), smem, "out_proj_kernel<256>"));
+  FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, false>), smem, "out_proj_kernel<128>"));
   const int grid = p.tiles < sms ? p.tiles : sms;
   if (pn == 256) out_proj_kernel<256, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
   else out_proj_kernel<128, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
@@ -468,12 +464,8 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   const uint32_t f = x_dtype == FUSP_BF16 ? 1u : 0u;
   p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FUSP_CUDA(cudaFuncSetAttribute(out_proj_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, true>), smem, "out_proj_kernel<256>"));
+  FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, true>), smem, "out_proj_kernel<128>"));
   const int grid = p.tiles < sms ? p.tiles : sms;
   if (pn == 256) out_proj_kernel<256, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
   else out_proj_kernel<128, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);

@@ -18,7 +18,6 @@
 namespace fusp {
 namespace {
 
-constexpr int kSMs = 148;
 
 __device__ __forceinline__ void load4(const void* p, int dt, int64_t i, float* f) {
   if (dt == FUSP_F32) {
@@ -129,7 +128,7 @@ fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_
   a.eps = eps;
   a.pos0 = pos0;
   int64_t grid = (rows * 32 + 255) / 256;
-  const int64_t cap = (int64_t(kSMs) * 16 + n - 1) / n;
+  const int64_t cap = (int64_t(sm_count()) * 16 + n - 1) / n;
   if (grid > cap) grid = cap;
   norm_rope_pack_kernel<<<dim3(static_cast<unsigned>(grid), n), 256, 0, s>>>(a);
   count_launch();

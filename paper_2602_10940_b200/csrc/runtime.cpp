@@ -3,8 +3,12 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <set>
 #include <sstream>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -31,6 +35,20 @@ fusp_status set_cuda_error(cudaError_t e, const std::string& where) {
 void clear_error() { g_last_error.clear(); }
 
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+fusp_status ensure_smem_attr(const void* kernel, int bytes, const char* name) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;  // (kernel, device, bytes)
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kernel, dev, bytes);
+  if (done.count(key)) return FUSP_OK;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return set_cuda_error(e, std::string("cudaFuncSetAttribute(") + name + ")");
+  done.insert(key);
+  return FUSP_OK;
+}
 
 // ---- TMA ------------------------------------------------------------------------------
 namespace {
@@ -83,41 +101,62 @@ fusp_status make_tmap_rows(CUtensorMap* m, const void* base, CUtensorMapDataType
   return FUSP_OK;
 }
 
-// ---- per-device scratch used by the context-free single-GPU API -------------------------
+// ---- per-(device, stream) workspace of the context-free single-GPU API -------------------
+// Every use of a workspace is ordered on its stream, and a call holds the workspace's mutex
+// from handing out its pointers until its kernels are enqueued, so two host threads (or two
+// streams) never share scratch words, and a buffer is only freed after its stream drained.
 namespace {
-struct Scratch {
+struct StreamWs {
+  std::mutex mu;
   void* ptr = nullptr;
   size_t bytes = 0;
+  CounterBuf cnt;  // zero-initialised words (stream-K tickets, staging amax / tickets)
 };
-std::mutex g_scratch_mu;
-std::vector<Scratch> g_scratch;  // indexed by device
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, std::unique_ptr<StreamWs>> g_ws;
 
-fusp_status scratch(size_t bytes, void** out) {
+fusp_status stream_ws(cudaStream_t s, StreamWs** out) {
   int dev = 0;
   FUSP_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(g_scratch_mu);
-  if (g_scratch.size() <= static_cast<size_t>(dev)) g_scratch.resize(dev + 1);
-  Scratch& s = g_scratch[dev];
-  if (s.bytes < bytes) {
-    if (s.ptr) {
-      FUSP_CUDA(cudaDeviceSynchronize());
-      FUSP_CUDA(cudaFree(s.ptr));
-      s.ptr = nullptr;
-      s.bytes = 0;
-    }
-    FUSP_CUDA(cudaMalloc(&s.ptr, bytes));
-    s.bytes = bytes;
-  }
-  *out = s.ptr;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& w = g_ws[{dev, s}];
+  if (!w) w = std::make_unique<StreamWs>();
+  *out = w.get();
   return FUSP_OK;
 }
 
-// Stream-K tickets of the context-free attention API (per device, zeroed once).
-CounterBuf& attn_counters() {
-  static CounterBuf bufs[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return bufs[dev & 63];
+// Call with w->mu held.
+fusp_status ws_scratch(StreamWs* w, cudaStream_t s, size_t bytes, void** out) {
+  if (w->bytes < bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+    if (w->ptr) {
+      FUSP_CUDA(cudaStreamSynchronize(s));  // the old buffer's last users ran on `s`
+      FUSP_CUDA(cudaFree(w->ptr));
+      w->ptr = nullptr;
+      w->bytes = 0;
+    }
+    const size_t n = bytes < (size_t(1) << 20) ? (size_t(1) << 20) : bytes;
+    FUSP_CUDA(cudaMalloc(&w->ptr, n));
+    w->bytes = n;
+  }
+  *out = w->ptr;
+  return FUSP_OK;
+}
+
+fusp_status ws_words(StreamWs* w, cudaStream_t s, size_t words, uint32_t** out) {
+  if (w->cnt.words < words || w->cnt.ptr == nullptr) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+    if (w->cnt.ptr) FUSP_CUDA(cudaStreamSynchronize(s));
+  }
+  FUSP_CHECK(ensure_counters(w->cnt, words));
+  *out = w->cnt.ptr;
+  return FUSP_OK;
 }
 
 std::string shape_str(const fusp_shape4& s) {
@@ -183,8 +222,11 @@ fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8
   clear_error();
   if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: bad dtype");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
   void* ws = nullptr;
-  FUSP_CHECK(scratch(256, &ws));
+  FUSP_CHECK(ws_scratch(w, s, 256, &ws));
   uint32_t* amax = static_cast<uint32_t*>(ws);
   uint32_t* bad = amax + 1;
   FUSP_CHECK(launch_amax(x, dtype, n, amax, bad, s));
@@ -231,11 +273,14 @@ fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n
     return set_error(FUSP_ERR_SHAPE, "quantize: block " + std::to_string(block) +
                                          " does not divide " + std::to_string(n) + " elements");
   const int64_t nblocks = n / block;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
   void* ws = nullptr;
-  FUSP_CHECK(scratch(static_cast<size_t>(nblocks) * 4 + 256, &ws));
+  FUSP_CHECK(ws_scratch(w, s, static_cast<size_t>(nblocks) * 4 + 256, &ws));
   const Fp8Src src{x, dtype, nullptr, 0, 0, 1, 1, 1};
-  return launch_quantize_fp8(src, n, block, static_cast<uint32_t*>(ws), scales_dev, codes, nullptr,
-                             reinterpret_cast<cudaStream_t>(stream));
+  return launch_quantize_fp8(src, n, block, static_cast<uint32_t*>(ws), scales_dev, codes, nullptr, s);
 }
 
 fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_dev, int64_t n,
@@ -246,14 +291,17 @@ fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_d
     return set_error(FUSP_ERR_SHAPE, "requantize: segment " + std::to_string(seg) +
                                          " must be a multiple of 8 dividing " + std::to_string(n));
   if (n == 0) return FUSP_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
   void* ws = nullptr;
-  FUSP_CHECK(scratch(256, &ws));
+  FUSP_CHECK(ws_scratch(w, s, 256, &ws));
   // the ring-hop source: rows of 8 codes, one bh, a scale per `seg / 8` rows
   const Fp8Src src{codes, FUSP_E4M3, seg_scales_dev, 1, 0, 8, static_cast<int>(n / 8),
                    static_cast<int>(seg / 8)};
   uint32_t* work = static_cast<uint32_t*>(ws);
-  return launch_quantize_fp8_multi(&src, 1, n, n, &work, &scale_dev, &codes_out, nullptr,
-                                   reinterpret_cast<cudaStream_t>(stream));
+  return launch_quantize_fp8_multi(&src, 1, n, n, &work, &scale_dev, &codes_out, nullptr, s);
 }
 
 fusp_status fusp_dequantize_e4m3_blocks(const uint8_t* codes, const float* scales_dev, int64_t n,
@@ -295,44 +343,79 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
     return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(qs.d) +
                                          " unsupported by the sm_100a kernel (D=128)");
   const int64_t nkv = heads * skv * qs.d;
-  // Operand staging: Q,K -> bf16 (f16 stays f16), V -> f16; one HBM pass each, skipped
-  // when the caller's tensor already has the MMA dtype.
-  const int qk_dt = qk_dtype == FUSP_F16 ? FUSP_F16 : FUSP_BF16;
+  if (heads > 65535 / 1 || qs.s > (int64_t(1) << 30) || skv > (int64_t(1) << 30))
+    return set_error(FUSP_ERR_SHAPE, "attention: shape too large " + shape_str(qs));
+  // Operand staging: bf16 Q, K feed the bf16 MMA as they are; f16 operands too.  f32 Q, K run
+  // the f16 MMA and any non-f16 V the f16 P.V MMA: one range-guarded staging pass each
+  // (fastusp_internal.h), with per-head power-of-two exponents the kernel folds back in.
+  const int qk_dt = qk_dtype == FUSP_BF16 ? FUSP_BF16 : FUSP_F16;
+  const bool stage_qk = qk_dtype != qk_dt;
+  const bool stage_v = v_dtype != FUSP_F16;
+  const int nh = static_cast<int>(heads);
   const size_t split =
-      attention_workspace_bytes(static_cast<int>(heads), static_cast<int>(qs.s), static_cast<int>(skv));
-  size_t need = (split + 255) / 256 * 256;
-  if (qk_dtype != qk_dt) need += static_cast<size_t>(nq + nkv) * 2;
-  if (v_dtype != FUSP_F16) need += static_cast<size_t>(nkv) * 2;
+      attention_workspace_bytes(nh, static_cast<int>(qs.s), static_cast<int>(skv));
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t need = up(split) + up(sizeof(int) * 3 * heads);
+  if (stage_qk) need += up(static_cast<size_t>(nq) * 2) + up(static_cast<size_t>(nkv) * 2);
+  if (stage_v) need += up(static_cast<size_t>(nkv) * 2);
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
   uint8_t* ws = nullptr;
-  if (need) FUSP_CHECK(scratch(need + 256, reinterpret_cast<void**>(&ws)));
+  FUSP_CHECK(ws_scratch(w, s, need, reinterpret_cast<void**>(&ws)));
+  const size_t cnt_words = attention_counter_words(nh, static_cast<int>(qs.s));
+  uint32_t* words = nullptr;
+  FUSP_CHECK(ws_words(w, s, cnt_words + 3 * stage_words(nh), &words));
+  size_t off = up(split);  // the stream-K workspace comes first
+  int* exps = reinterpret_cast<int*>(ws + off);
+  off += up(sizeof(int) * 3 * heads);
   const void* qb = q;
   const void* kb = k;
   const void* vh = v;
-  size_t off = (split + 255) / 256 * 256;  // the stream-K workspace comes first
-  if (qk_dtype != qk_dt) {
+  uint32_t* sw = words + cnt_words;
+  auto guarded = [&](const void* src, int sdt, void* dst, int part) {
+    StageOp o{};
+    o.src = src;
+    o.sdt = sdt;
+    o.dst = dst;
+    o.ddt = FUSP_F16;
+    o.exps = exps + part * heads;
+    o.words = sw + part * stage_words(nh);
+    return o;
+  };
+  StageOp kv[2];
+  int nkv_ops = 0;
+  if (stage_qk) {
     void* tq = ws + off;
-    off += static_cast<size_t>(nq) * 2;
+    off += up(static_cast<size_t>(nq) * 2);
     void* tk = ws + off;
-    off += static_cast<size_t>(nkv) * 2;
-    FUSP_CHECK(launch_convert(q, qk_dtype, tq, qk_dt, nq, s));
-    FUSP_CHECK(launch_convert(k, qk_dtype, tk, qk_dt, nkv, s));
+    off += up(static_cast<size_t>(nkv) * 2);
+    const StageOp oq = guarded(q, qk_dtype, tq, 0);
+    FUSP_CHECK(launch_stage(&oq, 1, nh, static_cast<int>(qs.s), 128, 1, s));
+    kv[nkv_ops++] = guarded(k, qk_dtype, tk, 1);
     qb = tq;
     kb = tk;
   }
-  if (v_dtype != FUSP_F16) {
+  if (stage_v) {
     void* tv = ws + off;
-    FUSP_CHECK(launch_convert(v, v_dtype, tv, FUSP_F16, nkv, s));
+    kv[nkv_ops++] = guarded(v, v_dtype, tv, 2);
     vh = tv;
   }
+  FUSP_CHECK(launch_stage(kv, nkv_ops, nh, static_cast<int>(skv), 128, 1, s));
   AttnLaunch a{};
   a.q = qb;
   a.k = kb;
   a.v = vh;
   a.qk_dtype = qk_dt;
+  if (stage_qk) {
+    a.q_exp = exps;
+    a.k_exp = exps + heads;
+  }
+  if (stage_v) a.v_exp = exps + 2 * heads;
   a.q_hs = qs.s * 128;
   a.k_hs = skv * 128;
   a.v_hs = skv * 128;
-  a.heads = static_cast<int>(heads);
+  a.heads = nh;
   a.sq = static_cast<int>(qs.s);
   a.skv = static_cast<int>(skv);
   a.d = static_cast<int>(qs.d);
@@ -346,11 +429,32 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
   a.lse_hs = qs.s;
   a.split_ws = split ? ws : nullptr;
   a.split_ws_bytes = split;
-  CounterBuf& cnt = attn_counters();
-  FUSP_CHECK(ensure_counters(cnt, attention_counter_words(a.heads, a.sq)));
-  a.split_counters = cnt.ptr;
-  a.split_counter_words = cnt.words;
+  a.split_counters = words;
+  a.split_counter_words = cnt_words;
   return launch_attention(a, s);
+}
+
+fusp_status fusp_stage_f16(const void* x, fusp_dtype dtype, int64_t heads, int64_t rows, void* y,
+                           int* exps, fusp_stream_t stream) {
+  clear_error();
+  if (!valid_float_dtype(dtype)) return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: bad dtype");
+  if (heads < 0 || rows < 0 || heads > 65535 || rows > (int64_t(1) << 30))
+    return set_error(FUSP_ERR_SHAPE, "stage: bad shape");
+  if (heads == 0 || rows == 0) return FUSP_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
+  uint32_t* words = nullptr;
+  FUSP_CHECK(ws_words(w, s, stage_words(static_cast<int>(heads)), &words));
+  StageOp o{};
+  o.src = x;
+  o.sdt = dtype;
+  o.dst = y;
+  o.ddt = FUSP_F16;
+  o.exps = exps;
+  o.words = words;
+  return launch_stage(&o, 1, static_cast<int>(heads), static_cast<int>(rows), 128, 1, s);
 }
 
 fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,

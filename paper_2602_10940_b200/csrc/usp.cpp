@@ -30,6 +30,43 @@ struct fusp_fabric_s {
   LocalFabric fabric;
 };
 
+// Device workspace of a layer: the arena (wire slots, operands, ring buffers, accumulators)
+// and zero-initialised words (attention stream-K tickets, staging amax / tickets) that every
+// kernel leaves zeroed.  A context owns one for eager calls; every captured graph owns its
+// own, so eager calls may regrow the context's without touching memory a graph replays.
+struct Workspace {
+  void* arena = nullptr;
+  size_t bytes = 0;
+  fusp::CounterBuf words;
+  void release() {
+    if (arena) cudaFree(arena);
+    if (words.ptr) cudaFree(words.ptr);
+    arena = nullptr;
+    bytes = 0;
+    words = fusp::CounterBuf{};
+  }
+};
+
+// Device staging of the host-buffer path: two slots of Q, K, V and output chunks, and the
+// copy streams / events of its H2D || layer || D2H pipeline.  Owned by the context.
+struct HostStage {
+  void* d = nullptr;
+  size_t bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t in_ready[2] = {nullptr, nullptr}, computed[2] = {nullptr, nullptr},
+              out_done[2] = {nullptr, nullptr};
+  uint32_t* flag = nullptr;
+  ~HostStage() {
+    if (d) cudaFree(d);
+    if (flag) cudaFree(flag);
+    for (cudaStream_t x : {h2d, d2h})
+      if (x) cudaStreamDestroy(x);
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {in_ready[i], computed[i], out_done[i]})
+        if (e) cudaEventDestroy(e);
+  }
+};
+
 struct fusp_ctx_s {
   int rank = 0, world = 1, device = 0;
   std::unique_ptr<Comm> comm;
@@ -41,13 +78,12 @@ struct fusp_ctx_s {
   cudaEvent_t tc0[kMaxSteps], tc1[kMaxSteps], tm0[kMaxSteps], tm1[kMaxSteps];
   int timed_steps = 0;
   bool capturing = false;
-  void* arena = nullptr;
-  size_t arena_bytes = 0;
-  fusp::CounterBuf attn_cnt;  // stream-K tickets of the attention kernel (zeroed once)
-  void* block_ws = nullptr;   // Q, K, V and attention output of fusp_usp_block
+  Workspace own;             // eager calls
+  Workspace* ws = &own;      // the workspace in use (a graph's while it is being captured)
+  int live_graphs = 0;       // graphs captured on this context and not yet destroyed
+  void* block_ws = nullptr;  // Q, K, V and attention output of fusp_usp_block
   size_t block_ws_bytes = 0;
-  void* host_stage = nullptr;
-  size_t host_stage_bytes = 0;
+  std::unique_ptr<HostStage> host;  // fusp_usp_attention_host's staging (created on first use)
   uint64_t a2a_bytes = 0, send_bytes = 0;
   // TrafficLog mirror (fabric.hpp:32-60): one entry per sender-side op, self traffic excluded
   struct Traffic {
@@ -64,10 +100,17 @@ struct fusp_ctx_s {
   int tl_next = -1;
 };
 
+struct fusp_group_s {  // = uspsim::ProcessGroup (fabric.hpp:20-28) seen from one rank
+  fusp::Group g;
+  fusp_ctx_s* ctx = nullptr;
+};
+
 struct fusp_graph_s {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int device = 0;
+  fusp_ctx_s* ctx = nullptr;  // its communicators are replayed: the context must outlive it
+  Workspace ws;               // the arena and words the captured kernels address
 };
 
 namespace {
@@ -83,6 +126,17 @@ std::string sstr(const fusp_shape4& s) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bound of every host wait on collectives (FUSP_TIMEOUT_S, default 120 s like the in-process
+// fabric's rendezvous): past it a stalled peer is reported as DeadlockError.
+double sync_timeout_s() {
+  static const double t = [] {
+    const char* e = std::getenv("FUSP_TIMEOUT_S");
+    const double v = e ? std::atof(e) : 120.0;
+    return v > 0 ? v : 120.0;
+  }();
+  return t;
+}
 
 // TrafficLog entries as the reference's fabric records them (fabric.cpp:155-158, :343-351):
 // all_to_all: one per collective and member, bytes sent to the other members; send: one per
@@ -111,17 +165,36 @@ struct Carve {
 };
 
 fusp_status ensure_arena(fusp_ctx_s* c, size_t bytes) {
-  if (c->arena_bytes >= bytes) return FUSP_OK;
+  Workspace& w = *c->ws;
+  if (w.bytes >= bytes) return FUSP_OK;
   if (c->capturing)
     return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
   FUSP_CUDA(cudaDeviceSynchronize());
-  if (c->arena) FUSP_CUDA(cudaFree(c->arena));
-  c->arena = nullptr;
-  c->arena_bytes = 0;
-  FUSP_CUDA(cudaMalloc(&c->arena, bytes));
-  c->arena_bytes = bytes;
+  if (w.arena) FUSP_CUDA(cudaFree(w.arena));
+  w.arena = nullptr;
+  w.bytes = 0;
+  FUSP_CUDA(cudaMalloc(&w.arena, bytes));
+  w.bytes = bytes;
   return FUSP_OK;
 }
+
+fusp_status ensure_words(fusp_ctx_s* c, size_t words) {
+  if (c->ws->words.ptr != nullptr && c->ws->words.words >= words) return FUSP_OK;
+  if (c->capturing)
+    return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+  return ensure_counters(c->ws->words, words);
+}
+
+// Bump allocator over the zero-initialised words.
+struct CarveWords {
+  uint32_t* base = nullptr;
+  size_t off = 0;
+  uint32_t* take(size_t n) {
+    uint32_t* p = base ? base + off : nullptr;
+    off += (n + 31) / 32 * 32;
+    return p;
+  }
+};
 
 struct Layer {
   Mode mode;
@@ -129,10 +202,16 @@ struct Layer {
   int64_t blk, C;  // elements per (Q|K|V) slot piece, elements per ring chunk (= U*blk)
   bool fp8, pipelined;
   int in_dt, out_dt;
-  int qk_dt;  // MMA dtype of Q and K: bf16, or f16 for f16 inputs and the FP8 path
+  // MMA dtype of Q and K: bf16 for bf16 inputs (exact), f16 otherwise -- f32 inputs keep 11
+  // significant bits instead of bf16's 8, and the FP8 path's decode(code)*scale values too.
+  // Every staging into f16 from a wider-range source is range-guarded (fastusp_internal.h).
+  int qk_dt;
+  size_t w_in;  // bytes per element of the caller's dtype = of the wire (non-FP8 Q/K/V, FP8 Q)
   size_t wout;
   Group ug, rg;
-  // Ulysses wire slot: [Q blk][K bf16|e4m3 blk][V f16|e4m3 blk]{[k scales][v scales]}
+  // Ulysses wire slot: [Q blk][K blk][V blk] in the caller's dtype (the reference's f32 wire
+  // for f32 inputs), or, FP8, [Q blk][K codes][V codes][k scales][v scales]; byte offsets
+  size_t off_k = 0, off_v = 0, off_tr = 0;
   size_t slot_bytes, slot_stride;
   // FP8 scale counts: per-tensor (reference) = 1; per block = one per (b,h) slab
   bool fp8_block = false;
@@ -149,14 +228,29 @@ struct Layer {
   // Q, K, V were written into the layer's own buffers by a producer (fusp_usp_block's QKV
   // projection): the Ulysses pack (U > 1) or the operand conversion (U = 1) is skipped
   bool prepacked = false;
+  // detail::ulysses_input_reshard (fusp_ulysses_input_reshard): the wire path runs even for a
+  // one-member group and the unpack writes the caller's buffers in `reshard_dt`, unstaged
+  bool force_wire = false;
+  void *reshard_q = nullptr, *reshard_k = nullptr, *reshard_v = nullptr;
+  int reshard_dt = FUSP_F32;
+  bool wire() const { return mode != Mode::kRing && (U > 1 || force_wire); }
 };
 
 struct Buffers {
   // Ulysses in
   char *send_in = nullptr, *recv_in = nullptr;
-  // attention operands of the local chunk
+  // attention operands of the local chunk, and their buffers when staged
   const void *Qr = nullptr, *Kr = nullptr, *Vr = nullptr;
   void *Qr_w = nullptr, *Kr_w = nullptr, *Vr_w = nullptr;
+  // range-guard exponents of the local operands (null: not staged from a wider range)
+  const int *q_exp = nullptr, *k_exp = nullptr, *v_exp = nullptr;
+  int* exps = nullptr;  // [7][heads_r]: q, k, v, then K / V of ring buffer 0 and 1
+  // sources of the U = 1 staging: Q / K as they come (caller, prologue or producer output)
+  const void *Qs = nullptr, *Ks_src = nullptr, *Vs_src = nullptr;
+  int qs_dt = 0, ks_dt = 0;
+  void *Qtmp = nullptr, *Ktmp = nullptr, *Vtmp = nullptr;  // f32 prologue / producer outputs
+  // the local K / V chunk in the wire dtype (first ring hop, non-FP8)
+  const void *Kw = nullptr, *Vw = nullptr;
   // fp8 exact local chunk: codes [heads_r][span][D] + per-segment scales
   uint8_t *Kc = nullptr, *Vc = nullptr;
   const float *Ks = nullptr, *Vs = nullptr;
@@ -168,10 +262,12 @@ struct Buffers {
   // ring
   char* rb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buf][K|V] wire parts
   char* sw[2] = {nullptr, nullptr};                           // fp8 send wire parts
-  void *Kd = nullptr, *Vd = nullptr;                          // fp8 dequantized operands
+  void* Kd[2] = {nullptr, nullptr};                           // staged ring operands per buffer
+  void* Vd[2] = {nullptr, nullptr};
   float *acc_o = nullptr, *acc_lse = nullptr;
-  // Ulysses out
+  // Ulysses out (LSE rides a second all-to-all when the caller asks for it)
   char *send_out = nullptr, *recv_out = nullptr;
+  float *lse_send = nullptr, *lse_recv = nullptr;
   // FP8 path with a K prologue: normalized + rotated K in f32
   float* Kpro = nullptr;
   // stream-K partials of the attention kernel
@@ -179,12 +275,19 @@ struct Buffers {
   size_t attn_ws_bytes = 0;
   uint32_t* attn_cnt = nullptr;
   size_t attn_cnt_words = 0;
+  // zero-initialised staging words: local operands (3), ring buffer x K/V
+  uint32_t* stage_w[3] = {nullptr, nullptr, nullptr};
+  uint32_t* ring_w[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 };
 
 fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, int in_dt,
-                       const fusp_comm_options& o, Layer* L) {
+                       const fusp_comm_options& o, Layer* L, const Group* grp = nullptr) {
   if (mode != Mode::kUsp) r = mode == Mode::kRing ? c->world : 1;
-  if (r < 1 || c->world % r != 0)
+  if (grp != nullptr) {  // ulysses / ring over a caller's ProcessGroup (protocols.hpp:47-65)
+    if (grp->pos < 0)
+      return set_error(FUSP_ERR_COMM, "rank " + std::to_string(c->rank) + " not in group " + grp->key());
+    r = mode == Mode::kRing ? grp->size() : 1;
+  } else if (r < 1 || c->world % r != 0)
     return set_error(FUSP_ERR_MESH, "ring dimension " + std::to_string(r) +
                                         " does not divide worker count " + std::to_string(c->world));
   if (ls.b < 1 || ls.h < 1 || ls.s < 1 || ls.d < 1)
@@ -200,7 +303,7 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   l.SL = static_cast<int>(ls.s);
   l.D = static_cast<int>(ls.d);
   l.R = r;
-  l.U = mode == Mode::kRing ? 1 : c->world / r;
+  l.U = mode == Mode::kRing ? 1 : (grp != nullptr ? grp->size() : c->world / r);
   if (l.H % l.U != 0)
     return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": head count H=" +
                                          std::to_string(l.H) + " not divisible by ulysses dimension U=" +
@@ -217,34 +320,52 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   l.pipelined = o.pipelined_ring != 0;
   l.in_dt = in_dt;
   l.k_dt = in_dt;
-  // FP8 K/V dequantize to decode(code)*scale (up to 28 significant bits): f16 keeps 2^-12 of
-  // it where bf16 keeps 2^-9, so the FP8 path runs Q.K^T in f16 (Q converts exactly).
-  l.qk_dt = (in_dt == FUSP_F16 || o.fp8_kv) ? FUSP_F16 : FUSP_BF16;
+  l.qk_dt = (in_dt == FUSP_BF16 && !l.fp8) ? FUSP_BF16 : FUSP_F16;
+  l.w_in = dtype_size(in_dt);
   l.out_dt = o.out_dtype;
   l.wout = dtype_size(o.out_dtype);
-  // mesh groups (mesh.cpp:44-53): rank = ring_idx * U + uly_idx
-  const int ri = c->rank / l.U, ui = c->rank % l.U;
-  for (int j = 0; j < l.U; ++j) l.ug.members.push_back(ri * l.U + j);
-  for (int i = 0; i < l.R; ++i) l.rg.members.push_back(i * l.U + ui);
-  l.ug.pos = ui;
-  l.rg.pos = ri;
+  if (grp != nullptr) {  // the caller's group on one axis, this rank alone on the other
+    Group self;
+    self.members = {c->rank};
+    self.pos = 0;
+    l.ug = mode == Mode::kRing ? self : *grp;
+    l.rg = mode == Mode::kRing ? *grp : self;
+  } else {
+    // mesh groups (mesh.cpp:44-53): rank = ring_idx * U + uly_idx
+    const int ri = c->rank / l.U, ui = c->rank % l.U;
+    for (int j = 0; j < l.U; ++j) l.ug.members.push_back(ri * l.U + j);
+    for (int i = 0; i < l.R; ++i) l.rg.members.push_back(i * l.U + ui);
+    l.ug.pos = ui;
+    l.rg.pos = ri;
+  }
   l.fp8_block = l.fp8 && o.fp8_block != 0;
   if (l.fp8_block) {
     l.nsc_local = l.B * l.H;
     l.nsc_slot = l.B * l.hp;
     l.nsc_chunk = l.heads_r;
   }
-  l.slot_bytes = l.fp8 ? size_t(l.blk) * 4 + 8 * size_t(l.nsc_slot) : size_t(l.blk) * 6;
+  l.off_k = size_t(l.blk) * l.w_in;
+  l.off_v = l.off_k + size_t(l.blk) * (l.fp8 ? 1 : l.w_in);
+  l.off_tr = l.off_v + size_t(l.blk) * (l.fp8 ? 1 : l.w_in);
+  l.slot_bytes = l.fp8 ? l.off_tr + 8 * size_t(l.nsc_slot) : l.off_tr;
   l.slot_stride = align_up(l.slot_bytes, 256);
   return FUSP_OK;
 }
 
-// Assign workspace for a layer. `user_*` are the caller's tensors (zero-copy when possible).
-void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, const void* v,
-           void* out) {
-  const size_t C2 = size_t(l.C) * 2;
+// Assign workspace for a layer. `q`, `k`, `v` are the caller's tensors (zero-copy when the
+// attention can read them as they are).
+void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q, const void* k,
+           const void* v, void* out) {
+  const size_t C2 = size_t(l.C) * 2;  // one 16-bit operand chunk
+  const size_t C4 = size_t(l.C) * 4;
   const bool uly = l.mode != Mode::kRing;
-  if (uly && l.U > 1) {
+  const int hr = l.heads_r;
+  const bool wire = l.wire();
+  b->exps = static_cast<int*>(cv.take(sizeof(int) * 7 * size_t(hr)));
+  for (int i = 0; i < 3; ++i) b->stage_w[i] = cw.take(stage_words(hr));
+  for (int i = 0; i < 2; ++i)
+    for (int p = 0; p < 2; ++p) b->ring_w[i][p] = cw.take(stage_words(hr));
+  if (wire) {
     b->send_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
     b->recv_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
     b->Qr = b->Qr_w = cv.take(C2);
@@ -253,47 +374,115 @@ void carve(const Layer& l, Carve& cv, Buffers* b, const void* q, const void* k, 
     if (l.fp8) {
       b->Kc = static_cast<uint8_t*>(cv.take(l.C));
       b->Vc = static_cast<uint8_t*>(cv.take(l.C));
+    } else if (l.R > 1) {  // the ring forwards the chunk in the wire dtype
+      b->Kw = l.in_dt == l.qk_dt ? b->Kr : cv.take(size_t(l.C) * l.w_in);
+      b->Vw = l.in_dt == FUSP_F16 ? b->Vr : cv.take(size_t(l.C) * l.w_in);
     }
   } else {
-    // U == 1: no transfer; operands are the caller's tensors when already in the MMA dtype.
-    if (l.in_dt == l.qk_dt && !l.pro_q) b->Qr = q; else b->Qr = b->Qr_w = cv.take(C2);
+    // U == 1: no transfer; the operands are the caller's tensors when already in the MMA dtype.
     const bool fq = uly && l.fp8;  // Ulysses self slot still takes the FP8 round trip (D7)
-    if (l.k_dt == l.qk_dt && !fq && !l.pro_k) b->Kr = k; else b->Kr = b->Kr_w = cv.take(C2);
-    if (l.in_dt == FUSP_F16 && !fq) b->Vr = v; else b->Vr = b->Vr_w = cv.take(C2);
+    // Q source: the caller's q, or the prologue's output -- straight into the operand in the
+    // MMA dtype when that is the caller's dtype, else an f32 copy that is staged
+    if (l.pro_q || l.prepacked) {
+      if (l.in_dt == l.qk_dt) {
+        b->Qr = b->Qr_w = cv.take(C2);
+        b->Qs = b->Qr;
+        b->qs_dt = l.qk_dt;
+      } else {
+        b->Qs = b->Qtmp = cv.take(C4);
+        b->qs_dt = FUSP_F32;
+      }
+    } else {
+      b->Qs = q;
+      b->qs_dt = l.in_dt;
+    }
+    if (b->Qr == nullptr) {
+      if (b->qs_dt == l.qk_dt) b->Qr = b->Qs;
+      else b->Qr = b->Qr_w = cv.take(C2);
+    }
+    // K source likewise (the FP8 path with a K prologue reads the f32 Kpro copy instead)
+    if (l.pro_k || l.prepacked) {
+      if (l.in_dt == l.qk_dt) {
+        b->Kr = b->Kr_w = cv.take(C2);
+        b->Ks_src = b->Kr;
+        b->ks_dt = l.qk_dt;
+      } else {
+        b->Ks_src = b->Ktmp = cv.take(C4);
+        b->ks_dt = FUSP_F32;
+      }
+    } else {
+      b->Ks_src = k;  // (or Kpro, set by run_layer)
+      b->ks_dt = l.k_dt;
+    }
+    if (b->Kr == nullptr) {
+      if (b->ks_dt == l.qk_dt && !fq) b->Kr = b->Ks_src;
+      else b->Kr = b->Kr_w = cv.take(C2);
+    }
+    if (l.prepacked && l.in_dt != FUSP_F16) {
+      b->Vs_src = b->Vtmp = cv.take(size_t(l.C) * l.w_in);
+    } else if (l.prepacked) {
+      b->Vs_src = b->Vr = b->Vr_w = cv.take(C2);
+    } else {
+      b->Vs_src = v;
+    }
+    if (b->Vr == nullptr) {
+      if (l.in_dt == FUSP_F16 && !fq) b->Vr = b->Vs_src;
+      else b->Vr = b->Vr_w = cv.take(C2);
+    }
+    b->Kw = b->Ks_src;
+    b->Vw = b->Vs_src;
     if (fq) {
       b->Kc = static_cast<uint8_t*>(cv.take(l.C));
       b->Vc = static_cast<uint8_t*>(cv.take(l.C));
     }
   }
-  if (l.pro_k_pre) b->Kpro =static_cast<float*>(cv.take(size_t(l.C) * 4));
+  if (l.pro_k_pre) b->Kpro = static_cast<float*>(cv.take(C4));
   const int nsc = l.nsc_local > l.nsc_chunk ? l.nsc_local : l.nsc_chunk;
   b->qscale = static_cast<float*>(cv.take(sizeof(float) * 2 * nsc));
   b->amax = static_cast<uint32_t*>(cv.take(sizeof(uint32_t) * 4 * (nsc + 1)));
   if (l.R > 1) {
-    const size_t part = l.fp8 ? align_up(size_t(l.C) + 4 * size_t(l.nsc_chunk), 256) : C2;
+    const size_t part = l.fp8 ? align_up(size_t(l.C) + 4 * size_t(l.nsc_chunk), 256)
+                              : size_t(l.C) * l.w_in;
     for (int i = 0; i < 2; ++i)
       for (int p = 0; p < 2; ++p) b->rb[i][p] = static_cast<char*>(cv.take(part));
-    if (l.fp8) {
+    if (l.fp8)
       for (int p = 0; p < 2; ++p) b->sw[p] = static_cast<char*>(cv.take(part));
-      b->Kd = cv.take(C2);
-      b->Vd = cv.take(C2);
+    for (int i = 0; i < 2; ++i) {
+      if (l.fp8 || l.in_dt != l.qk_dt) b->Kd[i] = cv.take(C2);
+      if (l.fp8 || l.in_dt != FUSP_F16) b->Vd[i] = cv.take(C2);
     }
-    b->acc_o = static_cast<float*>(cv.take(size_t(l.C) * 4));
+    b->acc_o = static_cast<float*>(cv.take(C4));
     b->acc_lse = static_cast<float*>(cv.take(size_t(l.heads_r) * l.span * 4));
   }
   b->attn_ws_bytes = attention_workspace_bytes(l.heads_r, l.span, l.span);
   if (b->attn_ws_bytes) b->attn_ws = cv.take(b->attn_ws_bytes);
-  if (uly && l.U > 1) {
+  if (wire) {
     b->send_out = static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
     b->recv_out = l.B == 1 ? static_cast<char*>(out)
                            : static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
+    const size_t lb = size_t(l.blk / l.D) * 4 * l.U;  // [U][B][hp][SL] f32
+    b->lse_send = static_cast<float*>(cv.take(lb));
+    b->lse_recv = static_cast<float*>(cv.take(lb));
   }
+}
+
+// A range-guarded f16 staging op (fastusp_internal.h).
+StageOp guarded_op(const void* src, int sdt, void* dst, int* exps, uint32_t* words) {
+  StageOp o{};
+  o.src = src;
+  o.sdt = sdt;
+  o.dst = dst;
+  o.ddt = FUSP_F16;
+  o.exps = exps;
+  o.words = words;
+  return o;
 }
 
 // ---------------------------------------------------------------- Ulysses input reshard
 fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q, const void* k,
                        const void* v, cudaStream_t s) {
   const bool uly = l.mode != Mode::kRing;
+  const int hr = l.heads_r;
   // norm/rope of Q (or K) written as `ddt` into slots of `stride` elements, u = 1: plain copy
   auto prologue = [&](bool is_q, const void* src, void* dst, int ddt, int64_t stride,
                       int u) -> fusp_status {
@@ -302,39 +491,58 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
                                  is_q ? p.q_norm_weight : p.k_norm_weight, p.eps, p.rope_cos,
                                  p.rope_sin, l.pos0, s);
   };
-  if (!uly || l.U == 1) {
-    if (l.prepacked) return FUSP_OK;
-    const int64_t n = l.C;
-    if (l.pro_q) FUSP_CHECK(prologue(true, q, b.Qr_w, l.qk_dt, 0, 1));
-    else if (b.Qr_w) FUSP_CHECK(launch_convert(q, l.in_dt, b.Qr_w, l.qk_dt, n, s));
+  if (!l.wire()) {
+    // (the producer path wrote Qs / Ks_src / Vs_src itself)
+    if (l.pro_q && !l.prepacked)
+      FUSP_CHECK(prologue(true, q, const_cast<void*>(b.Qs), b.qs_dt, 0, 1));
+    if (l.pro_k && !l.prepacked)
+      FUSP_CHECK(prologue(false, k, const_cast<void*>(b.Ks_src), b.ks_dt, 0, 1));
+    StageOp ops[3];
+    int n = 0;
+    if (b.Qr_w != nullptr && b.Qr != b.Qs) {
+      ops[n++] = guarded_op(b.Qs, b.qs_dt, b.Qr_w, b.exps, b.stage_w[0]);
+      b.q_exp = b.exps;
+    }
     if (uly && l.fp8) {
       // quantize the whole local K and V (protocols.cpp:139-142; or per (b,h) slab), and the
       // self slot takes the dequantized values (:163-179)
-      const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : n;
+      const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : l.C;
+      const Fp8Src srcs[2] = {Fp8Src{b.Ks_src, b.ks_dt, nullptr, 0, 0, l.D, l.span, l.span},
+                              Fp8Src{b.Vs_src, l.in_dt, nullptr, 0, 0, l.D, l.span, l.span}};
+      uint32_t* works[2] = {b.amax, b.amax + (l.nsc_local + 1)};
+      float* scs[2] = {b.qscale, b.qscale + l.nsc_local};
+      uint8_t* cds[2] = {b.Kc, b.Vc};
+      FUSP_CHECK(launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, s));
       for (int p = 0; p < 2; ++p) {
-        const Fp8Src src{p == 0 ? k : v, p == 0 ? l.k_dt : l.in_dt, nullptr, 0, 0, l.D, l.span,
-                         l.span};
-        uint8_t* codes = p == 0 ? b.Kc : b.Vc;
-        float* sc = b.qscale + p * l.nsc_local;
-        FUSP_CHECK(launch_quantize_fp8(src, n, block, b.amax, sc, codes, nullptr, s));
-        FUSP_CHECK(launch_dequantize_blocks(codes, sc, block, n, p == 0 ? b.Kr_w : b.Vr_w,
-                                            p == 0 ? l.qk_dt : FUSP_F16, s));
+        StageOp o = guarded_op(cds[p], FUSP_E4M3, p == 0 ? b.Kr_w : b.Vr_w, b.exps + (1 + p) * hr,
+                               b.stage_w[1 + p]);
+        o.scales = scs[p];
+        o.scale_bh_stride = l.fp8_block ? 1 : 0;
+        ops[n++] = o;
       }
+      b.k_exp = b.exps + hr;
+      b.v_exp = b.exps + 2 * hr;
       b.Ks = b.qscale;
       b.Vs = b.qscale + l.nsc_local;
       b.s_stride = 0;
       b.bh_stride = l.fp8_block ? 1 : 0;
       b.seg_rows = l.span;
     } else {
-      if (l.pro_k) FUSP_CHECK(prologue(false, k, b.Kr_w, l.qk_dt, 0, 1));
-      else if (b.Kr_w) FUSP_CHECK(launch_convert(k, l.k_dt, b.Kr_w, l.qk_dt, n, s));
-      if (b.Vr_w) FUSP_CHECK(launch_convert(v, l.in_dt, b.Vr_w, FUSP_F16, n, s));
+      if (b.Kr_w != nullptr && b.Kr != b.Ks_src) {
+        ops[n++] = guarded_op(b.Ks_src, b.ks_dt, b.Kr_w, b.exps + hr, b.stage_w[1]);
+        b.k_exp = b.exps + hr;
+      }
+      if (b.Vr_w != nullptr && b.Vr != b.Vs_src) {
+        ops[n++] = guarded_op(b.Vs_src, l.in_dt, b.Vr_w, b.exps + 2 * hr, b.stage_w[2]);
+        b.v_exp = b.exps + 2 * hr;
+      }
     }
-    return FUSP_OK;
+    return launch_stage(ops, n, hr, l.span, l.D, 1, s);
   }
-  const int64_t se2 = int64_t(l.slot_stride) / 2;  // slot stride in 16-bit elements
+  const int64_t sew = int64_t(l.slot_stride / l.w_in);  // slot stride in wire elements
   if (!l.prepacked) {
-    // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153)
+    // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153); Q, K, V
+    // keep the caller's dtype on the wire (the receiver stages them for the tensor cores)
     PackDesc p{};
     p.b = l.B;
     p.h = l.H;
@@ -344,39 +552,32 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     p.src = q;
     p.src_dtype = l.in_dt;
     p.dst = b.send_in;
-    p.dst_dtype = l.qk_dt;
-    p.dst_slot_stride = se2;
-    // Q, K, V (bf16 wire) leave in one pack launch -- with the fused QK prologue, one
-    // norm/RoPE/pack launch whose V operand is a plain pack.
+    p.dst_dtype = l.in_dt;
+    p.dst_slot_stride = sew;
     PackDesc ops[3];
     int nops = 0;
     if (!l.fp8 && (l.pro_q || l.pro_k)) {
+      // one norm/RoPE/pack launch whose V operand is a plain pack
       const fusp_qk_prologue& pr = *l.pro;
       const ProPack pops[3] = {
           {q, b.send_in, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
-           l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
-          {k, b.send_in + l.blk * 2, l.pro_k ? pr.k_norm_weight : nullptr,
-           l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.qk_dt},
-          {v, b.send_in + l.blk * 4, nullptr, nullptr, nullptr, l.in_dt, FUSP_F16}};
-      FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, se2, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
-    } else if (l.pro_q) {
-      FUSP_CHECK(prologue(true, q, b.send_in, l.qk_dt, se2, l.U));
-    } else {
-      ops[nops++] = p;
-    }
-    if (!l.fp8 && (l.pro_q || l.pro_k)) {
-      // packed above
+           l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.in_dt},
+          {k, b.send_in + l.off_k, l.pro_k ? pr.k_norm_weight : nullptr,
+           l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.in_dt},
+          {v, b.send_in + l.off_v, nullptr, nullptr, nullptr, l.in_dt, l.in_dt}};
+      FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, sew, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
     } else if (!l.fp8) {
+      ops[nops++] = p;
       p.src = k;
-      p.dst = b.send_in + l.blk * 2;
-      if (l.pro_k) FUSP_CHECK(prologue(false, k, p.dst, l.qk_dt, se2, l.U));
-      else ops[nops++] = p;
+      p.dst = b.send_in + l.off_k;
+      ops[nops++] = p;
       p.src = v;
-      p.dst = b.send_in + l.blk * 4;
-      p.dst_dtype = FUSP_F16;
+      p.dst = b.send_in + l.off_v;
       ops[nops++] = p;
       FUSP_CHECK(launch_pack_multi(ops, nops, s));
     } else {
+      if (l.pro_q) FUSP_CHECK(prologue(true, q, b.send_in, l.in_dt, sew, l.U));
+      else ops[nops++] = p;
       // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --:
       // one amax launch for K and V, then Q, K, V leave in one pack launch whose E4M3
       // operands compute their scales from the amax words and write every slot's trailer
@@ -389,13 +590,13 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       for (int part = 0; part < 2; ++part) {
         p.src = srcs[part].x;
         p.src_dtype = srcs[part].dt;
-        p.dst = b.send_in + l.blk * 2 + part * l.blk;
+        p.dst = b.send_in + (part == 0 ? l.off_k : l.off_v);
         p.dst_dtype = FUSP_E4M3;
         p.dst_slot_stride = int64_t(l.slot_stride);
         p.scale = nullptr;
         p.amax_bits = am[part];
         p.scale_bh_stride = l.fp8_block ? 1 : 0;
-        p.trailer = reinterpret_cast<float*>(b.send_in + l.blk * 4) + part * l.nsc_slot;
+        p.trailer = reinterpret_cast<float*>(b.send_in + l.off_tr) + part * l.nsc_slot;
         p.trailer_stride = int64_t(l.slot_stride / 4);
         ops[nops++] = p;
       }
@@ -405,61 +606,87 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
   log_a2a(c, l.ug, uint64_t(l.U - 1) * l.slot_bytes);
-  // unpack: source j contributed our heads over its sequence shard (protocols.cpp:163-179)
-  UnpackDesc u{};
-  u.b = l.B;
-  u.hp = l.hp;
-  u.sl = l.SL;
-  u.d = l.D;
-  u.u = l.U;
-  u.src = b.recv_in;
-  u.src_dtype = l.qk_dt;
-  u.src_slot_stride = se2;
-  u.dst = b.Qr_w;
-  u.dst_dtype = l.qk_dt;
-  // every operand of the attention leaves the receive slots in one unpack launch
-  UnpackDesc uops[5];
-  int nu = 0;
-  uops[nu++] = u;
-  if (!l.fp8) {
-    u.src = b.recv_in + l.blk * 2;
-    u.dst = b.Kr_w;
-    uops[nu++] = u;
-    u.src = b.recv_in + l.blk * 4;
-    u.src_dtype = FUSP_F16;
-    u.dst = b.Vr_w;
-    u.dst_dtype = FUSP_F16;
-    uops[nu++] = u;
-    FUSP_CHECK(launch_unpack_multi(uops, nu, s));
-  } else {
-    const float* scales = reinterpret_cast<const float*>(b.recv_in + l.blk * 4);
-    for (int part = 0; part < 2; ++part) {
-      u.src = b.recv_in + l.blk * 2 + part * l.blk;
-      u.src_dtype = FUSP_E4M3;
-      u.src_slot_stride = int64_t(l.slot_stride);
-      u.scales = scales + part * l.nsc_slot;
-      u.scale_stride = int64_t(l.slot_stride / 4);
-      u.scale_bh_stride = l.fp8_block ? 1 : 0;
-      u.dst = part == 0 ? b.Kr_w : b.Vr_w;
-      u.dst_dtype = part == 0 ? l.qk_dt : FUSP_F16;
-      uops[nu++] = u;
-      u.dst = part == 0 ? static_cast<void*>(b.Kc) : static_cast<void*>(b.Vc);
-      u.dst_dtype = FUSP_E4M3;
-      uops[nu++] = u;
+  // unpack + stage: source j contributed our heads over its sequence shard
+  // (protocols.cpp:163-179); every operand leaves the receive slots in one launch
+  StageOp ops[3];
+  if (l.reshard_q != nullptr) {
+    // detail::ulysses_input_reshard: the resharded Q, K, V themselves (FP8 K / V dequantized
+    // exactly, decode(code) * scale in f32 as fp8.cpp:125-130), in the caller's dtype
+    const float* scales = reinterpret_cast<const float*>(b.recv_in + l.off_tr);
+    void* dst[3] = {l.reshard_q, l.reshard_k, l.reshard_v};
+    for (int p = 0; p < 3; ++p) {
+      StageOp o{};
+      const bool codes = l.fp8 && p > 0;
+      o.src = b.recv_in + (p == 0 ? 0 : p == 1 ? l.off_k : l.off_v);
+      o.sdt = codes ? FUSP_E4M3 : l.in_dt;
+      o.src_slot_stride = codes ? int64_t(l.slot_stride) : sew;
+      if (codes) {
+        o.scales = scales + (p - 1) * l.nsc_slot;
+        o.scale_stride = int64_t(l.slot_stride / 4);
+        o.scale_bh_stride = l.fp8_block ? 1 : 0;
+      }
+      o.dst = dst[p];
+      o.ddt = l.reshard_dt;
+      ops[p] = o;
     }
-    FUSP_CHECK(launch_unpack_multi(uops, nu, s));
-    b.Ks = scales;
-    b.Vs = scales + l.nsc_slot;
-    b.s_stride = int64_t(l.slot_stride / 4);
-    b.bh_stride = l.fp8_block ? 1 : 0;
-    b.seg_rows = l.SL;
+    return launch_stage(ops, 3, hr, l.SL, l.D, l.U, s);
   }
+  StageOp oq{};
+  oq.src = b.recv_in;
+  oq.sdt = l.in_dt;
+  oq.src_slot_stride = sew;
+  oq.dst = b.Qr_w;
+  oq.ddt = l.qk_dt;
+  if (l.in_dt != l.qk_dt) {
+    oq.exps = b.exps;
+    oq.words = b.stage_w[0];
+    b.q_exp = b.exps;
+  }
+  ops[0] = oq;
+  if (!l.fp8) {
+    for (int p = 0; p < 2; ++p) {
+      StageOp o{};
+      o.src = b.recv_in + (p == 0 ? l.off_k : l.off_v);
+      o.sdt = l.in_dt;
+      o.src_slot_stride = sew;
+      o.dst = p == 0 ? b.Kr_w : b.Vr_w;
+      o.ddt = p == 0 ? l.qk_dt : FUSP_F16;
+      if (o.ddt != l.in_dt) {  // range-guarded, and the wire-dtype copy the ring forwards
+        o.exps = b.exps + (1 + p) * hr;
+        o.words = b.stage_w[1 + p];
+        o.raw = l.R > 1 ? const_cast<void*>(p == 0 ? b.Kw : b.Vw) : nullptr;
+        (p == 0 ? b.k_exp : b.v_exp) = o.exps;
+      }
+      ops[1 + p] = o;
+    }
+    return launch_stage(ops, 3, hr, l.SL, l.D, l.U, s);
+  }
+  const float* scales = reinterpret_cast<const float*>(b.recv_in + l.off_tr);
+  for (int p = 0; p < 2; ++p) {
+    StageOp o = guarded_op(b.recv_in + (p == 0 ? l.off_k : l.off_v), FUSP_E4M3,
+                           p == 0 ? b.Kr_w : b.Vr_w, b.exps + (1 + p) * hr, b.stage_w[1 + p]);
+    o.src_slot_stride = int64_t(l.slot_stride);
+    o.scales = scales + p * l.nsc_slot;
+    o.scale_stride = int64_t(l.slot_stride / 4);
+    o.scale_bh_stride = l.fp8_block ? 1 : 0;
+    o.raw = p == 0 ? static_cast<void*>(b.Kc) : static_cast<void*>(b.Vc);  // exact codes
+    ops[1 + p] = o;
+  }
+  b.k_exp = b.exps + hr;
+  b.v_exp = b.exps + 2 * hr;
+  FUSP_CHECK(launch_stage(ops, 3, hr, l.SL, l.D, l.U, s));
+  b.Ks = scales;
+  b.Vs = scales + l.nsc_slot;
+  b.s_stride = int64_t(l.slot_stride / 4);
+  b.bh_stride = l.fp8_block ? 1 : 0;
+  b.seg_rows = l.SL;
   return FUSP_OK;
 }
 
 // ---------------------------------------------------------------- attention step
-fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* V, bool first,
-                   bool last, void* out, float* lse_out, cudaStream_t s, int reserve_sms = 0) {
+fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* V, const int* k_exp,
+                   const int* v_exp, bool first, bool last, void* out, float* lse_out,
+                   cudaStream_t s, int reserve_sms = 0) {
   AttnLaunch a{};
   if (reserve_sms > 0) a.max_ctas = sm_count() - reserve_sms;
   a.split_ws = b.attn_ws;
@@ -470,6 +697,9 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
   a.q = b.Qr;
   a.k = K;
   a.v = V;
+  a.q_exp = b.q_exp;
+  a.k_exp = k_exp;
+  a.v_exp = v_exp;
   a.q_hs = a.k_hs = a.v_hs = int64_t(l.span) * l.D;
   a.heads = l.heads_r;
   a.sq = l.span;
@@ -492,6 +722,11 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
     }
     a.lse = lse_out;
     a.lse_hs = l.span;
+    if (!direct_out && lse_out != nullptr) {  // LSE into its own all-to-all slots [U][B][hp][SL]
+      a.lse = b.lse_send;
+      a.lse_hs = l.SL;
+      a.lse_cs = l.blk / l.D;
+    }
   } else {
     a.out = b.acc_o;
     a.out_dtype = FUSP_F32;
@@ -513,15 +748,16 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
 fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, const void* v_src,
                  void* out, float* lse_out, cudaStream_t s) {
   const int R = l.R;
+  const int hr = l.heads_r;
   const bool timing = !c->capturing && R <= fusp_ctx_s::kMaxSteps;
   c->timed_steps = timing ? R : 0;
-  const size_t C2 = size_t(l.C) * 2;
-  // wire part per K and per V: codes + f32 scale(s) (the reference's 4-byte scale + codes)
-  const size_t part_bytes = l.fp8 ? size_t(l.C) + 4 * size_t(l.nsc_chunk) : C2;
+  // wire part per K and per V: codes + f32 scale(s) (the reference's 4-byte scale + codes), or
+  // the chunk in the caller's dtype
+  const size_t part_bytes = l.fp8 ? size_t(l.C) + 4 * size_t(l.nsc_chunk) : size_t(l.C) * l.w_in;
   const int64_t block = l.fp8_block ? int64_t(l.span) * l.D : l.C;  // quantization block
   if (R == 1) {
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
-    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, true, out, lse_out, s));
+    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, b.k_exp, b.v_exp, true, true, out, lse_out, s));
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
     return FUSP_OK;
   }
@@ -554,6 +790,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     }
     return launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, st);
   };
+  // Transfer hop `hop` into buffer hop % 2, then stage the received chunk for the tensor cores
+  // on the same stream (under the previous step's compute when pipelined).
   auto exchange = [&](int hop, cudaStream_t st) -> fusp_status {
     const int into = hop % 2, from = (hop - 1) % 2;
     const void* snd[2];
@@ -562,8 +800,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
       snd[0] = b.sw[0];
       snd[1] = b.sw[1];
     } else if (hop == 1) {
-      snd[0] = b.Kr;
-      snd[1] = b.Vr;
+      snd[0] = b.Kw;
+      snd[1] = b.Vw;
     } else {
       snd[0] = b.rb[from][0];
       snd[1] = b.rb[from][1];
@@ -574,41 +812,43 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     c->send_bytes += 2 * part_bytes;
     log_send(c, l.rg, hop, part_bytes);  // K (protocols.cpp:253)
     log_send(c, l.rg, hop, part_bytes);  // V (protocols.cpp:254)
-    return FUSP_OK;
-  };
-  auto operands = [&](int hop, cudaStream_t st, const void** K, const void** V) -> fusp_status {
-    const int buf = hop % 2;
-    if (!l.fp8) {
-      *K = b.rb[buf][0];
-      *V = b.rb[buf][1];
-      return FUSP_OK;
+    StageOp ops[2];
+    int n = 0;
+    for (int p = 0; p < 2; ++p) {
+      void* dst = p == 0 ? b.Kd[into] : b.Vd[into];
+      if (dst == nullptr) continue;  // the chunk is already the MMA operand
+      StageOp o = guarded_op(b.rb[into][p], l.fp8 ? FUSP_E4M3 : l.in_dt, dst,
+                             b.exps + (3 + 2 * into + p) * hr, b.ring_w[into][p]);
+      if (l.fp8) {
+        o.scales = reinterpret_cast<const float*>(b.rb[into][p] + l.C);
+        o.scale_bh_stride = l.fp8_block ? 1 : 0;
+      }
+      ops[n++] = o;
     }
-    const char* wk = b.rb[buf][0];
-    const char* wv = b.rb[buf][1];
-    FUSP_CHECK(launch_dequantize_blocks(reinterpret_cast<const uint8_t*>(wk),
-                                        reinterpret_cast<const float*>(wk + l.C), block, l.C,
-                                        b.Kd, l.qk_dt, st));
-    FUSP_CHECK(launch_dequantize_blocks(reinterpret_cast<const uint8_t*>(wv),
-                                        reinterpret_cast<const float*>(wv + l.C), block, l.C,
-                                        b.Vd, FUSP_F16, st));
-    *K = b.Kd;
-    *V = b.Vd;
-    return FUSP_OK;
+    return launch_stage(ops, n, hr, l.span, l.D, 1, st);
+  };
+  auto operands = [&](int hop, const void** K, const void** V, const int** ke, const int** ve) {
+    const int buf = hop % 2;
+    *K = b.Kd[buf] ? b.Kd[buf] : b.rb[buf][0];
+    *V = b.Vd[buf] ? b.Vd[buf] : b.rb[buf][1];
+    *ke = b.Kd[buf] ? b.exps + (3 + 2 * buf) * hr : nullptr;
+    *ve = b.Vd[buf] ? b.exps + (4 + 2 * buf) * hr : nullptr;
   };
 
   if (!l.pipelined) {
     // ring_attention_serial (protocols.cpp:237-268): compute, then send/recv/compute per round.
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
-    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s));
+    FUSP_CHECK(attend(l, b, b.Kr, b.Vr, b.k_exp, b.v_exp, true, false, out, lse_out, s));
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
     for (int i = 1; i < R; ++i) {
       if (timing) FUSP_CUDA(cudaEventRecord(c->tm0[i], s));
       FUSP_CHECK(exchange(i, s));
       if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[i], s));
       const void *K, *V;
+      const int *ke, *ve;
+      operands(i, &K, &V, &ke, &ve);
       if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[i], s));
-      FUSP_CHECK(operands(i, s, &K, &V));
-      FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s));
+      FUSP_CHECK(attend(l, b, K, V, ke, ve, false, i == R - 1, out, lse_out, s));
       if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[i], s));
     }
     return FUSP_OK;
@@ -625,13 +865,13 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
   // compute steps that run beside a transfer leave its SMs free (NCCL kernels need them)
   const int reserve = c->comm->sms_in_flight();
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
-  FUSP_CHECK(attend(l, b, b.Kr, b.Vr, true, false, out, lse_out, s, reserve));
+  FUSP_CHECK(attend(l, b, b.Kr, b.Vr, b.k_exp, b.v_exp, true, false, out, lse_out, s, reserve));
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
   FUSP_CUDA(cudaEventRecord(c->ev_attn[0], s));
   for (int i = 1; i < R; ++i) {
     FUSP_CUDA(cudaStreamWaitEvent(s, c->ev_recv[i % 2], 0));
     if (i < R - 1) {
-      // buffer (i+1)%2 was last read by compute step i-1
+      // buffer (i+1)%2 (and its staged operands) was last read by compute step i-1
       FUSP_CUDA(cudaStreamWaitEvent(m, c->ev_attn[(i - 1) % 2], 0));
       if (timing) FUSP_CUDA(cudaEventRecord(c->tm0[i + 1], m));
       FUSP_CHECK(exchange(i + 1, m));
@@ -639,9 +879,10 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
       FUSP_CUDA(cudaEventRecord(c->ev_recv[(i + 1) % 2], m));
     }
     const void *K, *V;
+    const int *ke, *ve;
+    operands(i, &K, &V, &ke, &ve);
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[i], s));
-    FUSP_CHECK(operands(i, s, &K, &V));
-    FUSP_CHECK(attend(l, b, K, V, false, i == R - 1, out, lse_out, s, i < R - 1 ? reserve : 0));
+    FUSP_CHECK(attend(l, b, K, V, ke, ve, false, i == R - 1, out, lse_out, s, i < R - 1 ? reserve : 0));
     if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[i], s));
     FUSP_CUDA(cudaEventRecord(c->ev_attn[i % 2], s));
   }
@@ -651,22 +892,58 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
 }
 
 // ---------------------------------------------------------------- Ulysses output reshard
-fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, cudaStream_t s) {
-  if (l.mode == Mode::kRing || l.U == 1) return FUSP_OK;  // epilogue wrote `out` directly
+fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, float* lse_out,
+                        cudaStream_t s) {
+  if (!l.wire()) return FUSP_OK;  // epilogue wrote `out` (and `lse`) directly
   const size_t slot = size_t(l.blk) * l.wout;
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
   c->a2a_bytes += uint64_t(l.U - 1) * slot;
   log_a2a(c, l.ug, uint64_t(l.U - 1) * slot);
   if (l.B > 1)  // concat_heads (protocols.cpp:196-202)
     FUSP_CHECK(launch_unpack_heads(b.recv_out, l.blk, out, l.out_dt, l.B, l.hp, l.SL, l.D, l.U, s));
+  if (lse_out != nullptr) {
+    // The reference's usp_attention drops the LSE (protocols.cpp:339); fastusp returns it on
+    // request: the rows' LSE ride a second, small all-to-all back to their sequence shards
+    // (B = 1: straight into the caller's [1][H][SL] buffer, heads t*hp.. from member t).
+    const size_t ls = size_t(l.blk / l.D) * 4;
+    float* dst = l.B == 1 ? lse_out : b.lse_recv;
+    FUSP_CHECK(c->comm->all_to_all(l.ug, b.lse_send, dst, ls, ls, s));
+    c->a2a_bytes += uint64_t(l.U - 1) * ls;
+    log_a2a(c, l.ug, uint64_t(l.U - 1) * ls);
+    if (l.B > 1) {  // slot t [B][hp][SL] -> lse[b][t*hp + hl][SL]
+      const size_t row = size_t(l.hp) * l.SL * 4;
+      for (int t = 0; t < l.U; ++t)
+        FUSP_CUDA(cudaMemcpy2DAsync(lse_out + size_t(t) * l.hp * l.SL, size_t(l.H) * l.SL * 4,
+                                    reinterpret_cast<const char*>(b.lse_recv) + t * ls, row, row,
+                                    l.B, cudaMemcpyDeviceToDevice, s));
+    }
+  }
   return FUSP_OK;
+}
+
+// detail::ulysses_output_reshard (protocols.cpp:182-203) on its own: o [B][hp][U*SL][D] ->
+// slot t = rows [t*SL, (t+1)*SL) (one stage launch, the inverse of the unpack mapping) ->
+// all_to_all -> concat_heads.
+fusp_status output_reshard(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* o, int dt,
+                           void* out, cudaStream_t s) {
+  StageOp op{};
+  op.src = o;
+  op.sdt = dt;
+  op.src_slot_stride = int64_t(l.SL) * l.D;
+  op.src_bh_stride = int64_t(l.span) * l.D;
+  op.dst = b.send_out;
+  op.ddt = dt;
+  op.dst_slot_stride = l.blk;
+  op.dst_bh_stride = int64_t(l.SL) * l.D;
+  FUSP_CHECK(launch_stage(&op, 1, l.heads_r, l.SL, l.D, l.U, s));
+  return ulysses_out(c, l, b, out, nullptr, s);
 }
 
 fusp_status check_inputs(fusp_ctx_s* c, Mode mode, const Layer& l, const void* q, const void* k,
                          const void* v, cudaStream_t s) {
   size_t need = 256;
   FUSP_CHECK(ensure_arena(c, need));
-  uint32_t* flag = static_cast<uint32_t*>(c->arena);
+  uint32_t* flag = static_cast<uint32_t*>(c->ws->arena);
   FUSP_CUDA(cudaMemsetAsync(flag, 0, 4, s));
   const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
   FUSP_CHECK(launch_finite(q, l.in_dt, n, flag, s));
@@ -674,21 +951,28 @@ fusp_status check_inputs(fusp_ctx_s* c, Mode mode, const Layer& l, const void* q
   FUSP_CHECK(launch_finite(v, l.in_dt, n, flag, s));
   uint32_t h = 0;
   FUSP_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s));
-  FUSP_CUDA(cudaStreamSynchronize(s));
+  FUSP_CHECK(c->comm->wait(s, sync_timeout_s(), "check_finite"));
   if (h)  // check_local_qkv (protocols.cpp:102-104)
     return set_error(FUSP_ERR_INVALID_ARGUMENT,
                      std::string(tag(mode)) + ": non-finite element in protocol input");
   return FUSP_OK;
 }
 
-fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
-  Layer& l = *L;
+fusp_status validate_prologue(const fusp_qk_prologue* p) {
   if (!p) return FUSP_OK;
   const bool rope = p->rope_cos != nullptr || p->rope_sin != nullptr;
   if (rope && (p->rope_cos == nullptr || p->rope_sin == nullptr))
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: rope_cos and rope_sin go together");
   if (!(p->eps >= 0.f))
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: eps must be >= 0");
+  return FUSP_OK;
+}
+
+fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
+  Layer& l = *L;
+  if (!p) return FUSP_OK;
+  FUSP_CHECK(validate_prologue(p));
+  const bool rope = p->rope_cos != nullptr;
   l.pos0 = p->rope_pos0 < 0 ? int64_t(c->rank) * l.SL : p->rope_pos0;
   if (rope && (p->rope_rows < l.pos0 + l.SL))
     return set_error(FUSP_ERR_SHAPE, "qk prologue: rope table has " + std::to_string(p->rope_rows) +
@@ -709,60 +993,89 @@ fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
 // Producer of the layer's Q, K, V, called with the layer's own operand buffers (slots).
 using Produce = std::function<fusp_status(const QkvDst&)>;
 
+// Variants of a layer call beyond the mesh protocols.
+struct LayerCall {
+  const Group* grp = nullptr;      // ulysses / ring over this ProcessGroup (null: mesh / world)
+  bool reshard_in = false;         // detail::ulysses_input_reshard only: Q, K, V -> rq, rk, rv
+  void *rq = nullptr, *rk = nullptr, *rv = nullptr;
+  int rdt = FUSP_F32;
+  const void* reshard_out = nullptr;  // detail::ulysses_output_reshard only: o -> out
+};
+
 fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void* k,
                       const void* v, int in_dt, fusp_shape4 ls, void* out, float* lse_out,
                       const fusp_comm_options* opts, cudaStream_t s, bool size_only = false,
-                      const fusp_qk_prologue* pro = nullptr, const Produce* produce = nullptr) {
+                      const fusp_qk_prologue* pro = nullptr, const Produce* produce = nullptr,
+                      const LayerCall* call = nullptr) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
   FUSP_CUDA(cudaSetDevice(c->device));
   fusp_comm_options o{};
   o.out_dtype = FUSP_F32;
   if (opts) o = *opts;
+  const LayerCall none{};
+  if (call == nullptr) call = &none;
   Layer l;
-  FUSP_CHECK(plan_layer(c, mode, r, ls, in_dt, o, &l));
+  FUSP_CHECK(plan_layer(c, mode, r, ls, in_dt, o, &l, call->grp));
+  if (call->reshard_in || call->reshard_out != nullptr) {
+    l.force_wire = true;
+    if (call->reshard_in) {
+      l.reshard_q = call->rq;
+      l.reshard_k = call->rk;
+      l.reshard_v = call->rv;
+      l.reshard_dt = call->rdt;
+    }
+  }
   FUSP_CHECK(plan_prologue(c, pro, &l));
   if (c->nccl && l.U > 1 && l.R > 1) FUSP_CHECK(c->nccl->ensure_mesh(l.R));
   if (o.check_finite && !size_only) FUSP_CHECK(check_inputs(c, mode, l, q, k, v, s));
+  if (produce != nullptr) {
+    if (l.fp8 || l.pro != nullptr || l.mode == Mode::kRing || o.check_finite ||
+        (l.in_dt != FUSP_BF16 && l.in_dt != FUSP_F16))
+      return set_error(FUSP_ERR_UNSUPPORTED, "operand producer: bf16/f16 wire, no prologue, no check");
+    l.prepacked = true;
+  }
   Carve cv;
+  CarveWords cw;
   Buffers b;
-  carve(l, cv, &b, q, k, v, out);
-  FUSP_CHECK(ensure_arena(c, cv.off + 256));
   const size_t cnt_words = attention_counter_words(l.heads_r, l.span);
-  if (c->attn_cnt.words < cnt_words && c->capturing)
-    return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
-  FUSP_CHECK(ensure_counters(c->attn_cnt, cnt_words));
+  cw.take(cnt_words);
+  carve(l, cv, cw, &b, q, k, v, out);
+  FUSP_CHECK(ensure_arena(c, cv.off + 256));
+  FUSP_CHECK(ensure_words(c, cw.off));
   if (size_only) return FUSP_OK;
-  cv = Carve{static_cast<char*>(c->arena), 0};
+  cv = Carve{static_cast<char*>(c->ws->arena), 0};
+  cw = CarveWords{c->ws->words.ptr, 0};
   b = Buffers{};
-  carve(l, cv, &b, q, k, v, out);
-  b.attn_cnt = c->attn_cnt.ptr;
-  b.attn_cnt_words = c->attn_cnt.words;
+  b.attn_cnt = cw.take(cnt_words);
+  b.attn_cnt_words = cnt_words;
+  carve(l, cv, cw, &b, q, k, v, out);
   if (l.pro_k_pre) {
     FUSP_CHECK(launch_norm_rope_pack(k, l.in_dt, b.Kpro, FUSP_F32, 0, l.B, l.H, l.SL, l.D, 1,
                                      pro->k_norm_weight, pro->eps, pro->rope_cos, pro->rope_sin,
                                      l.pos0, s));
     k = b.Kpro;
+    if (l.mode == Mode::kRing || l.U == 1) b.Ks_src = b.Kw = b.Kpro;
   }
   if (produce != nullptr) {
-    if (l.fp8 || l.pro != nullptr || l.mode == Mode::kRing || o.check_finite)
-      return set_error(FUSP_ERR_UNSUPPORTED, "operand producer: bf16/f16 wire, no prologue, no check");
     QkvDst d{};
-    if (l.U > 1) {  // straight into the Ulysses send slots: [Q blk][K blk][V f16 blk] per slot
-      d = QkvDst{b.send_in, b.send_in + l.blk * 2, b.send_in + l.blk * 4, l.qk_dt, FUSP_F16, l.U,
-                 int64_t(l.slot_stride) / 2};
-    } else {        // the attention operands themselves (V as the f16 the P.V MMA reads)
-      d = QkvDst{b.Qr_w ? b.Qr_w : const_cast<void*>(q), b.Kr_w ? b.Kr_w : const_cast<void*>(k),
-                 b.Vr_w ? b.Vr_w : const_cast<void*>(v), l.qk_dt, FUSP_F16, 1, 0};
+    if (l.U > 1) {  // straight into the Ulysses send slots: [Q blk][K blk][V blk] per slot
+      d = QkvDst{b.send_in, b.send_in + l.off_k, b.send_in + l.off_v, l.in_dt, l.in_dt, l.U,
+                 int64_t(l.slot_stride / l.w_in)};
+    } else {        // the staging sources (Q, K: the attention operands themselves)
+      d = QkvDst{const_cast<void*>(b.Qs), const_cast<void*>(b.Ks_src), const_cast<void*>(b.Vs_src),
+                 l.in_dt, l.in_dt, 1, 0};
     }
     FUSP_CHECK((*produce)(d));
-    l.prepacked = true;
   }
-  const bool uly1 =l.mode != Mode::kRing && l.U == 1;  // the reference still runs a 1-member
-  if (uly1) log_a2a(c, l.ug, 0);                         // all_to_all (fabric.cpp:199-226)
+  if (call->reshard_out != nullptr) return output_reshard(c, l, b, call->reshard_out, l.out_dt, out, s);
+  if (call->reshard_in) return ulysses_in(c, l, b, q, k, v, s);
+  // the reference still runs a 1-member all_to_all (fabric.cpp:199-226)
+  const bool uly1 = l.mode != Mode::kRing && !l.wire();
+  if (uly1) log_a2a(c, l.ug, 0);
   FUSP_CHECK(ulysses_in(c, l, b, q, k, v, s));
   FUSP_CHECK(ring(c, l, b, k, v, out, lse_out, s));
-  FUSP_CHECK(ulysses_out(c, l, b, out, s));
+  FUSP_CHECK(ulysses_out(c, l, b, out, lse_out, s));
   if (uly1) log_a2a(c, l.ug, 0);
   c->tl_steps = c->timed_steps;
   c->tl_pipelined = l.pipelined && l.R > 1;
@@ -863,14 +1176,17 @@ fusp_status fusp_ctx_create_nccl(const uint8_t uid[128], int world, int rank, in
 }
 
 fusp_status fusp_ctx_destroy(fusp_ctx c) {
+  clear_error();
   if (!c) return FUSP_OK;
+  if (c->live_graphs > 0)
+    return set_error(FUSP_ERR_UNSUPPORTED, "context has " + std::to_string(c->live_graphs) +
+                                               " live graph(s): destroy them first");
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   c->comm.reset();
-  if (c->arena) cudaFree(c->arena);
-  if (c->attn_cnt.ptr) cudaFree(c->attn_cnt.ptr);
+  c->own.release();
   if (c->block_ws) cudaFree(c->block_ws);
-  if (c->host_stage) cudaFreeHost(c->host_stage);
+  c->host.reset();
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_recv[0], c->ev_recv[1], c->ev_attn[0], c->ev_attn[1]})
     if (e) cudaEventDestroy(e);
@@ -879,6 +1195,14 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
       if (e) cudaEventDestroy(e);
   delete c;
   return FUSP_OK;
+}
+
+fusp_status fusp_ctx_synchronize(fusp_ctx c, fusp_stream_t stream, double timeout_s) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  return c->comm->wait(reinterpret_cast<cudaStream_t>(stream),
+                       timeout_s > 0 ? timeout_s : sync_timeout_s(), "synchronize");
 }
 
 int fusp_ctx_rank(fusp_ctx c) { return c ? c->rank : -1; }
@@ -1046,6 +1370,7 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "usp_block: x must be bf16 or f16");
   if (batch <= 0 || s_local <= 0 || channels <= 0 || heads <= 0)
     return set_error(FUSP_ERR_SHAPE, "usp_block: empty shape");
+  FUSP_CHECK(validate_prologue(prologue));  // the projection epilogue dereferences cos AND sin
   const int64_t pos0 = prologue && prologue->rope_pos0 >= 0 ? prologue->rope_pos0 : int64_t(c->rank) * s_local;
   if (prologue && prologue->rope_cos && prologue->rope_rows < pos0 + s_local)
     return set_error(FUSP_ERR_SHAPE, "qk prologue: rope table has " + std::to_string(prologue->rope_rows) +
@@ -1089,6 +1414,121 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
   return fusp_out_projection(attn, x_dtype, ls, w_out, n_out, y, y_dtype, stream);
 }
 
+fusp_status fusp_group_create(fusp_ctx c, const int* members, int n, fusp_group* out) {
+  clear_error();
+  if (!c || !out) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context or output");
+  *out = nullptr;
+  Group g;
+  if (n < 0) return set_error(FUSP_ERR_COMM, "empty process group");
+  for (int i = 0; i < n; ++i) g.members.push_back(members[i]);
+  // validate_group (fabric.cpp:316-324)
+  for (int i = 0; i < n; ++i) {
+    const int m = members[i];
+    if (m < 0 || m >= c->world)
+      return set_error(FUSP_ERR_COMM, "group member " + std::to_string(m) + " out of range [0," +
+                                          std::to_string(c->world) + ")");
+    for (int j = 0; j < i; ++j)
+      if (members[j] == m)
+        return set_error(FUSP_ERR_COMM, "duplicate member " + std::to_string(m) + " in group " + g.key());
+    if (m == c->rank) g.pos = i;
+  }
+  FUSP_CUDA(cudaSetDevice(c->device));
+  if (c->nccl) FUSP_CHECK(c->nccl->split_group(g));  // collective over the world
+  if (n == 0) return FUSP_OK;  // joined the split without a group
+  if (g.pos < 0)
+    return set_error(FUSP_ERR_COMM, "rank " + std::to_string(c->rank) + " not in group " + g.key());
+  auto* h = new fusp_group_s;
+  h->g = g;
+  h->ctx = c;
+  *out = h;
+  return FUSP_OK;
+}
+
+fusp_status fusp_group_destroy(fusp_group g) {
+  delete g;
+  return FUSP_OK;
+}
+
+int fusp_group_size(fusp_group g) { return g ? g->g.size() : 0; }
+int fusp_group_position(fusp_group g) { return g ? g->g.pos : -1; }
+
+static fusp_status group_of(fusp_ctx c, fusp_group g, const Group** out) {
+  *out = nullptr;
+  if (g == nullptr) return FUSP_OK;  // the world
+  if (g->ctx != c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "group belongs to another context");
+  *out = &g->g;
+  return FUSP_OK;
+}
+
+fusp_status fusp_usp_attention_lse(fusp_ctx c, int ring_dim, const void* q, const void* k,
+                                   const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                   float* lse, const fusp_comm_options* opts, fusp_stream_t stream) {
+  return run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, lse, opts,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+fusp_status fusp_ulysses_attention_group(fusp_ctx c, fusp_group group, const void* q, const void* k,
+                                         const void* v, fusp_dtype in_dtype, fusp_shape4 ls,
+                                         void* out, float* lse, const fusp_comm_options* opts,
+                                         fusp_stream_t stream) {
+  clear_error();
+  LayerCall call;
+  FUSP_CHECK(group_of(c, group, &call.grp));
+  return run_layer(c, Mode::kUlysses, 1, q, k, v, in_dtype, ls, out, lse, opts,
+                   reinterpret_cast<cudaStream_t>(stream), false, nullptr, nullptr, &call);
+}
+
+fusp_status fusp_ring_attention_group(fusp_ctx c, fusp_group group, const void* q, const void* k,
+                                      const void* v, fusp_dtype in_dtype, fusp_shape4 ls, void* out,
+                                      float* lse, const fusp_comm_options* opts,
+                                      fusp_stream_t stream) {
+  clear_error();
+  LayerCall call;
+  FUSP_CHECK(group_of(c, group, &call.grp));
+  return run_layer(c, Mode::kRing, c ? c->world : 1, q, k, v, in_dtype, ls, out, lse, opts,
+                   reinterpret_cast<cudaStream_t>(stream), false, nullptr, nullptr, &call);
+}
+
+fusp_status fusp_ulysses_input_reshard(fusp_ctx c, fusp_group group, const void* q, const void* k,
+                                       const void* v, fusp_dtype in_dtype, fusp_shape4 ls,
+                                       void* q_out, void* k_out, void* v_out, fusp_dtype out_dtype,
+                                       const fusp_comm_options* opts, fusp_stream_t stream) {
+  clear_error();
+  if (out_dtype != FUSP_F32 && out_dtype != FUSP_BF16 && out_dtype != FUSP_F16)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "reshard: out_dtype must be f32, bf16 or f16");
+  LayerCall call;
+  FUSP_CHECK(group_of(c, group, &call.grp));
+  call.reshard_in = true;
+  call.rq = q_out;
+  call.rk = k_out;
+  call.rv = v_out;
+  call.rdt = out_dtype;
+  fusp_comm_options o{};
+  o.out_dtype = FUSP_F32;
+  if (opts) o = *opts;
+  o.pipelined_ring = 0;
+  return run_layer(c, Mode::kUlysses, 1, q, k, v, in_dtype, ls, nullptr, nullptr, &o,
+                   reinterpret_cast<cudaStream_t>(stream), false, nullptr, nullptr, &call);
+}
+
+fusp_status fusp_ulysses_output_reshard(fusp_ctx c, fusp_group group, const void* o, fusp_dtype dtype,
+                                        fusp_shape4 o_shape, void* out, fusp_stream_t stream) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  LayerCall call;
+  FUSP_CHECK(group_of(c, group, &call.grp));
+  const int u = call.grp ? call.grp->size() : c->world;
+  if (o_shape.s % u != 0)  // protocols.cpp:185-188
+    return set_error(FUSP_ERR_SHAPE, "ulysses: gathered sequence length S=" + std::to_string(o_shape.s) +
+                                         " not divisible by ulysses dimension U=" + std::to_string(u));
+  call.reshard_out = o;
+  fusp_comm_options opt{};
+  opt.out_dtype = dtype;
+  const fusp_shape4 ls{o_shape.b, o_shape.h * u, o_shape.s / u, o_shape.d};
+  return run_layer(c, Mode::kUlysses, 1, nullptr, nullptr, nullptr, dtype, ls, out, nullptr, &opt,
+                   reinterpret_cast<cudaStream_t>(stream), false, nullptr, nullptr, &call);
+}
+
 fusp_status fusp_ulysses_attention(fusp_ctx c, const void* q, const void* k, const void* v,
                                    fusp_dtype in_dtype, fusp_shape4 ls, void* out,
                                    const fusp_comm_options* opts, fusp_stream_t stream) {
@@ -1130,7 +1570,10 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
     return n > 0 ? n : 4;
   }();
   int hc = static_cast<int>(ls.h);
-  for (int cand = U; cand <= ls.h; cand += U)
+  // per-tensor FP8 quantizes over ALL local heads (fp8.cpp:107-123): one chunk keeps the
+  // reference's single scale; per-block scales are per head, so chunking is exact there
+  const bool whole = o.fp8_kv && !o.fp8_block;
+  for (int cand = U; cand <= ls.h && !whole; cand += U)
     if (ls.h % cand == 0 && ls.h / cand <= max_chunks) { hc = cand; break; }
   const int nch = static_cast<int>(ls.h / hc);
   const size_t esz_in = dtype_size(in_dtype), esz_out = dtype_size(out_dt);
@@ -1138,27 +1581,19 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   const size_t chunk_in = size_t(ls.b) * hc * head_elems * esz_in;
   const size_t chunk_out = size_t(ls.b) * hc * head_elems * esz_out;
   // device staging (its own allocation: the arena belongs to the layer), two slots
-  struct Stage {
-    void* d = nullptr;
-    size_t bytes = 0;
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t in_ready[2], computed[2], out_done[2];
-    uint32_t* flag = nullptr;
-    int device = -1;
-  };
-  static thread_local Stage st;
-  if (st.device != c->device) {
-    st = Stage{};
-    FUSP_CUDA(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
-    FUSP_CUDA(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
+  if (!c->host) {
+    auto h = std::make_unique<HostStage>();
+    FUSP_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    FUSP_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
-      FUSP_CUDA(cudaEventCreateWithFlags(&st.in_ready[i], cudaEventDisableTiming));
-      FUSP_CUDA(cudaEventCreateWithFlags(&st.computed[i], cudaEventDisableTiming));
-      FUSP_CUDA(cudaEventCreateWithFlags(&st.out_done[i], cudaEventDisableTiming));
+      FUSP_CUDA(cudaEventCreateWithFlags(&h->in_ready[i], cudaEventDisableTiming));
+      FUSP_CUDA(cudaEventCreateWithFlags(&h->computed[i], cudaEventDisableTiming));
+      FUSP_CUDA(cudaEventCreateWithFlags(&h->out_done[i], cudaEventDisableTiming));
     }
-    FUSP_CUDA(cudaMalloc(&st.flag, 256));
-    st.device = c->device;
+    FUSP_CUDA(cudaMalloc(&h->flag, 256));
+    c->host = std::move(h);
   }
+  HostStage& st = *c->host;
   const size_t slot = 3 * align_up(chunk_in, 256) + align_up(chunk_out, 256);
   if (st.bytes < 2 * slot) {
     if (st.d) FUSP_CUDA(cudaFree(st.d));
@@ -1219,7 +1654,7 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   if (nch >= 2) FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[(nch - 2) % 2], 0));
   uint32_t bad = 0;
   if (check) FUSP_CUDA(cudaMemcpyAsync(&bad, st.flag, 4, cudaMemcpyDeviceToHost, s));
-  FUSP_CUDA(cudaStreamSynchronize(s));
+  FUSP_CHECK(c->comm->wait(s, sync_timeout_s(), "usp_attention_host"));
   if (bad)  // check_local_qkv (protocols.cpp:102-104); the output is unspecified
     return set_error(FUSP_ERR_INVALID_ARGUMENT, "usp: non-finite element in protocol input");
   return FUSP_OK;
@@ -1239,11 +1674,20 @@ fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, cons
     return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
   FUSP_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // size the workspace before capture (no allocation inside the graph)
-  FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts, s, true));
-  FUSP_CUDA(cudaStreamSynchronize(s));
+  // the graph gets its own workspace, sized before capture (no allocation inside the graph):
+  // later eager calls on the context may regrow the context's without touching it
   auto* g = new fusp_graph_s;
   g->device = c->device;
+  g->ctx = c;
+  c->ws = &g->ws;
+  fusp_status st0 = run_layer(c, Mode::kUsp, ring_dim, q, k, v, in_dtype, ls, out, nullptr, opts, s, true);
+  if (st0 == FUSP_OK && cudaStreamSynchronize(s) != cudaSuccess) st0 = set_cuda_error(cudaGetLastError(), "cudaStreamSynchronize");
+  if (st0 != FUSP_OK) {
+    c->ws = &c->own;
+    g->ws.release();
+    delete g;
+    return st0;
+  }
   c->capturing = true;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   fusp_status st = e == cudaSuccess ? FUSP_OK : set_cuda_error(e, "cudaStreamBeginCapture");
@@ -1257,6 +1701,7 @@ fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, cons
   cudaGraph_t graph_raw = nullptr;
   e = cudaStreamEndCapture(s, &graph_raw);
   c->capturing = false;
+  c->ws = &c->own;
   if (st == FUSP_OK && e != cudaSuccess) st = set_cuda_error(e, "cudaStreamEndCapture");
   if (st == FUSP_OK) {
     g->graph = graph_raw;
@@ -1268,9 +1713,11 @@ fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, cons
   if (st != FUSP_OK) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);
+    g->ws.release();
     delete g;
     return st;
   }
+  c->live_graphs++;
   *graph = g;
   return FUSP_OK;
 }
@@ -1284,8 +1731,11 @@ fusp_status fusp_graph_launch(fusp_graph g, fusp_stream_t stream) {
 
 fusp_status fusp_graph_destroy(fusp_graph g) {
   if (!g) return FUSP_OK;
+  cudaSetDevice(g->device);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->graph) cudaGraphDestroy(g->graph);
+  g->ws.release();  // cudaFree waits for a replay still in flight
+  if (g->ctx) g->ctx->live_graphs--;
   delete g;
   return FUSP_OK;
 }

@@ -39,6 +39,39 @@ static void report(const char* name, double bytes, const std::function<void()>& 
 
 int main() {
   CK(cudaMalloc(&flushbuf, 256u << 20));
+  {  // operand staging at FLUX U = 1: V [24][4608][128] bf16 -> f16 (the layer's only mover)
+    const int heads = 24, rows = 4608;
+    const int64_t n = int64_t(heads) * rows * 128;
+    void *x, *y, *x32;
+    int* exps;
+    uint32_t* words;
+    CK(cudaMalloc(&x, n * 2)); CK(cudaMalloc(&y, n * 2)); CK(cudaMalloc(&x32, n * 4));
+    CK(cudaMalloc(&exps, 4096)); CK(cudaMalloc(&words, 4096)); CK(cudaMemset(words, 0, 4096));
+    {  // in-range data (the common path): bf16 / f32 1.0
+      std::vector<uint16_t> hb(n, 0x3f80);
+      std::vector<uint32_t> hf(n, 0x3f800000u);
+      CK(cudaMemcpy(x, hb.data(), n * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(x32, hf.data(), n * 4, cudaMemcpyHostToDevice));
+    }
+    StageOp g{};
+    g.src = x; g.sdt = FUSP_BF16; g.dst = y; g.ddt = FUSP_F16; g.exps = exps; g.words = words;
+    StageOp u = g;
+    u.exps = nullptr; u.words = nullptr;
+    StageOp g32 = g;
+    g32.src = x32; g32.sdt = FUSP_F32;
+    report("flux_u1 stage V bf16->f16 range-guarded (stage + decide)", n * 4.0,
+           [&] { launch_stage(&g, 1, heads, rows, 128, 1, 0); });
+    report("flux_u1 stage V bf16->f16 unguarded (stage only)", n * 4.0,
+           [&] { launch_stage(&u, 1, heads, rows, 128, 1, 0); });
+    report("flux_u1 bf16_to_f16_kernel (round-1 converter, no guard)", n * 4.0,
+           [&] { launch_convert(x, FUSP_BF16, y, FUSP_F16, n, 0); });
+    report("flux_u1 stage Q f32->f16 range-guarded", n * 6.0,
+           [&] { launch_stage(&g32, 1, heads, rows, 128, 1, 0); });
+    CK(cudaMemset(x, 0x3c, n * 2));  // |x| = 0.0115 < 2^-6: every head takes the rewrite
+    report("flux_u1 stage V bf16->f16 range-guarded, RARE path (all 24 heads rewritten)", n * 4.0,
+           [&] { launch_stage(&g, 1, heads, rows, 128, 1, 0); });
+    for (void* p : std::vector<void*>{x, y, x32, exps, words}) cudaFree(p);
+  }
   struct Cfg { const char* name; int h, sl, u; };
   const Cfg cfgs[] = {{"flux_u2", 24, 2304, 2}, {"flux_u8", 24, 576, 8}};
   for (const Cfg& c : cfgs) {
