@@ -163,6 +163,15 @@ fusp_status fusp_ctx_traffic_json(fusp_ctx ctx, char* buf, size_t cap, size_t* l
 /* Timeline::to_json (fabric.cpp:115-125) of the last layer call, protocol event order, plus
  * "t_ms": device time of the event from the first one (CUDA events on both streams). */
 fusp_status fusp_ctx_timeline_json(fusp_ctx ctx, char* buf, size_t cap, size_t* len);
+/* Debug (no reference counterpart): enable != 0 keeps a device copy of every payload this
+ * rank puts on the wire in later eager calls -- kind 0: the Ulysses-in send slots (all U
+ * slots, slot stride apart), kind 1 / 2: the ring K / V part of hop `round` -- so tests can
+ * compare FP8 codes and scale trailers byte for byte with the reference quantizer.  Enabling
+ * (or disabling) drops the records. */
+fusp_status fusp_ctx_debug_wire(fusp_ctx ctx, int enable);
+int fusp_ctx_debug_wire_count(fusp_ctx ctx);
+fusp_status fusp_ctx_debug_wire_get(fusp_ctx ctx, int index, int* kind, int* round, void* host,
+                                    size_t cap, size_t* bytes);
 /* Per-step device timings of the last ring call (ms): compute[i], comm[i] for i < R. */
 fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms, float* comm_ms,
                                   int* steps);

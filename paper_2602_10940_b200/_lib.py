@@ -139,6 +139,9 @@ _SIGS = {
                                                _P, ctypes.POINTER(CommOptions), _P]),
     "fusp_usp_attention_lse": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                               _P, _P, ctypes.POINTER(CommOptions), _P]),
+    "fusp_ctx_debug_wire": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fusp_ctx_debug_wire_count": (ctypes.c_int, [_P]),
+    "fusp_ctx_debug_wire_get": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_size_t, _P]),
     "fusp_ctx_synchronize": (ctypes.c_int, [_P, _P, ctypes.c_double]),
     "fusp_group_create": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
     "fusp_group_destroy": (ctypes.c_int, [_P]),

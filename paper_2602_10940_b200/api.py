@@ -407,6 +407,24 @@ class WorkerContext:
         """Timeline::to_json of the last layer call, with device timestamps t_ms."""
         return self._json(lib().fusp_ctx_timeline_json)
 
+    def debug_wire(self, enable: bool = True):
+        """fusp_ctx_debug_wire: record every payload this rank puts on the wire (eager calls)."""
+        check(lib().fusp_ctx_debug_wire(self.handle, int(enable)))
+
+    def wire_records(self):
+        """[(kind, round, bytes as np.uint8)]: kind 0 Ulysses-in send slots, 1/2 ring K/V part."""
+        import numpy as np
+        out = []
+        for i in range(lib().fusp_ctx_debug_wire_count(self.handle)):
+            kind, rnd, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+            check(lib().fusp_ctx_debug_wire_get(self.handle, i, ctypes.byref(kind), ctypes.byref(rnd),
+                                                None, 0, ctypes.byref(n)))
+            buf = np.empty(n.value, np.uint8)
+            check(lib().fusp_ctx_debug_wire_get(self.handle, i, None, None,
+                                                buf.ctypes.data_as(ctypes.c_void_p), n.value, None))
+            out.append((kind.value, rnd.value, buf))
+        return out
+
     def synchronize(self, stream=None, timeout_s: float = 0.0):
         """fusp_ctx_synchronize: bounded host wait; a stalled / failed peer raises
         DeadlockError (the NCCL communicators are aborted) instead of hanging."""

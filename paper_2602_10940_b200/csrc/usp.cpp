@@ -84,6 +84,18 @@ struct fusp_ctx_s {
   void* block_ws = nullptr;  // Q, K, V and attention output of fusp_usp_block
   size_t block_ws_bytes = 0;
   std::unique_ptr<HostStage> host;  // fusp_usp_attention_host's staging (created on first use)
+  // fusp_ctx_debug_wire: device copies of every payload this rank put on the wire (eager calls)
+  struct WireRec {
+    int kind, round;  // 0 Ulysses-in send slots, 1 / 2 ring K / V part (round = hop)
+    void* dev;
+    size_t bytes;
+  };
+  bool debug_wire = false;
+  std::vector<WireRec> wire;
+  void clear_wire() {
+    for (auto& r : wire) cudaFree(r.dev);
+    wire.clear();
+  }
   uint64_t a2a_bytes = 0, send_bytes = 0;
   // TrafficLog mirror (fabric.hpp:32-60): one entry per sender-side op, self traffic excluded
   struct Traffic {
@@ -146,6 +158,17 @@ void log_a2a(fusp_ctx_s* c, const Group& g, uint64_t bytes) {
   const int round = c->a2a_seq[key]++;
   c->traffic.push_back({"all_to_all", key, round, c->rank, bytes, uint64_t(g.size() - 1)});
 }
+// Debug capture of a wire payload (fusp_ctx_debug_wire): a device copy, stream-ordered.
+fusp_status record_wire(fusp_ctx_s* c, int kind, int round, const void* p, size_t bytes,
+                        cudaStream_t s) {
+  if (!c->debug_wire || c->capturing) return FUSP_OK;
+  void* d = nullptr;
+  FUSP_CUDA(cudaMalloc(&d, bytes ? bytes : 1));
+  FUSP_CUDA(cudaMemcpyAsync(d, p, bytes, cudaMemcpyDeviceToDevice, s));
+  c->wire.push_back({kind, round, d, bytes});
+  return FUSP_OK;
+}
+
 void log_send(fusp_ctx_s* c, const Group& g, int round, uint64_t bytes) {
   const int next = g.members[(g.pos + 1) % g.size()];
   c->traffic.push_back(
@@ -603,6 +626,7 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       FUSP_CHECK(launch_pack_multi(ops, nops, s));
     }
   }
+  FUSP_CHECK(record_wire(c, 0, 0, b.send_in, l.slot_stride * l.U, s));
   FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
   log_a2a(c, l.ug, uint64_t(l.U - 1) * l.slot_bytes);
@@ -808,6 +832,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     }
     void* rcv[2] = {b.rb[into][0], b.rb[into][1]};
     const size_t bytes[2] = {part_bytes, part_bytes};
+    FUSP_CHECK(record_wire(c, 1, hop, snd[0], part_bytes, st));
+    FUSP_CHECK(record_wire(c, 2, hop, snd[1], part_bytes, st));
     FUSP_CHECK(c->comm->ring_exchange(l.rg, snd, rcv, bytes, 2, st));
     c->send_bytes += 2 * part_bytes;
     log_send(c, l.rg, hop, part_bytes);  // K (protocols.cpp:253)
@@ -1185,6 +1211,7 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
   cudaDeviceSynchronize();
   c->comm.reset();
   c->own.release();
+  c->clear_wire();
   if (c->block_ws) cudaFree(c->block_ws);
   c->host.reset();
   if (c->side) cudaStreamDestroy(c->side);
@@ -1203,6 +1230,34 @@ fusp_status fusp_ctx_synchronize(fusp_ctx c, fusp_stream_t stream, double timeou
   FUSP_CUDA(cudaSetDevice(c->device));
   return c->comm->wait(reinterpret_cast<cudaStream_t>(stream),
                        timeout_s > 0 ? timeout_s : sync_timeout_s(), "synchronize");
+}
+
+fusp_status fusp_ctx_debug_wire(fusp_ctx c, int enable) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  FUSP_CUDA(cudaDeviceSynchronize());
+  c->clear_wire();
+  c->debug_wire = enable != 0;
+  return FUSP_OK;
+}
+
+int fusp_ctx_debug_wire_count(fusp_ctx c) { return c ? static_cast<int>(c->wire.size()) : 0; }
+
+fusp_status fusp_ctx_debug_wire_get(fusp_ctx c, int index, int* kind, int* round, void* host,
+                                    size_t cap, size_t* bytes) {
+  clear_error();
+  if (!c || index < 0 || index >= static_cast<int>(c->wire.size()))
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "debug wire: no record " + std::to_string(index));
+  const auto& r = c->wire[size_t(index)];
+  if (kind) *kind = r.kind;
+  if (round) *round = r.round;
+  if (bytes) *bytes = r.bytes;
+  if (host != nullptr) {
+    FUSP_CUDA(cudaSetDevice(c->device));
+    FUSP_CUDA(cudaMemcpy(host, r.dev, cap < r.bytes ? cap : r.bytes, cudaMemcpyDeviceToHost));
+  }
+  return FUSP_OK;
 }
 
 int fusp_ctx_rank(fusp_ctx c) { return c ? c->rank : -1; }
