@@ -13,6 +13,11 @@ from dataclasses import asdict, dataclass, field
 from typing import Dict, List, Optional
 
 
+# per-rank attention launches of the BASELINE meshes, measured on one B200 (f16 output)
+ATTN_MEASURED = {"24x4608": 1308.6, "12x4608": 1226.2, "6x4608": 949.8, "3x4608": 690.9,
+                 "12x4224": 1052.4, "6x3584": 794.4, "24x7168": 1207.7}
+
+
 @dataclass
 class HardwareProfile:
     """SPEC.md:373-376.  Defaults: one B200 on an NVSwitch node."""
@@ -21,13 +26,40 @@ class HardwareProfile:
     launch_overhead: float = 4e-6       # s per kernel launch, eager
     graph_residual: float = 0.05        # fraction of launch cost left under graph replay
     element_width: int = 2              # bytes per Q/K/V element on the wire (bf16/f16)
-    peak_tflops: float = 1651.9         # measured dense bf16 (MEASURED_PEAKS.json)
-    attn_efficiency: float = 0.73       # measured attention-kernel fraction of peak (FLUX)
+    peak_tflops: float = 1618.9         # measured dense bf16 burst (MEASURED_PEAKS.json)
+    attn_efficiency: float = 0.81       # fallback: attention-kernel fraction of peak at FLUX U=1
+    # Measured attention-kernel throughput (TFLOP/s) per per-rank launch shape "heads x span"
+    # (tools/ab_attn.py, profiles/r02_ab_attn.jsonl); attention_seconds interpolates it over
+    # log(FLOP per launch) -- small per-rank launches run well below the U=1 efficiency.
+    attn_tflops_measured: Dict[str, float] = field(default_factory=lambda: dict(ATTN_MEASURED))
 
     def __post_init__(self):
         for k, v in asdict(self).items():
+            if isinstance(v, dict):
+                continue
             if v <= 0:
                 raise ValueError(f"HardwareProfile.{k} must be positive")
+
+    def attn_tflops(self, flop: float) -> float:
+        """Attention throughput at a launch of `flop` FLOP: piecewise-linear in log(FLOP)
+        through the measured shapes (D = 128), clamped at the ends; the fallback efficiency
+        when no measurements are loaded."""
+        pts = []
+        for key, tf in self.attn_tflops_measured.items():
+            h, s = (int(x) for x in key.split("x"))
+            pts.append((math.log(4.0 * h * s * s * 128), tf))
+        if not pts:
+            return self.peak_tflops * self.attn_efficiency
+        pts.sort()
+        x = math.log(max(flop, 1.0))
+        if x <= pts[0][0]:
+            return pts[0][1]
+        if x >= pts[-1][0]:
+            return pts[-1][1]
+        for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+            if x0 <= x <= x1:
+                return y0 + (y1 - y0) * (x - x0) / (x1 - x0) if x1 > x0 else max(y0, y1)
+        return pts[-1][1]
 
 
 @dataclass
@@ -100,7 +132,7 @@ def pipeline_timeline(compute: float, comm: float, r: int) -> Dict[str, float]:
 
 def attention_seconds(hw: HardwareProfile, b: int, heads: int, s_q: int, s_kv: int, d: int) -> float:
     flop = 4.0 * b * heads * s_q * s_kv * d
-    return flop / (hw.peak_tflops * 1e12 * hw.attn_efficiency)
+    return flop / (hw.attn_tflops(flop) * 1e12)
 
 
 def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipelined: bool = True,

@@ -418,8 +418,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           for (int t = 0; t < 2; ++t) {
+            // every s_read phase is consumed (also a segment's last step, where nothing is
+            // issued early): arrive/wait stay paired, as compute-sanitizer synccheck requires
+            mbar_wait(&sm.s_read[t], it & 1);
             if (nxt) {
-              mbar_wait(&sm.s_read[t], it & 1);
               tc_fence_after();
               issue_qk_half(t, sn, 1);
             }
