@@ -928,8 +928,20 @@ Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
   const double fill = static_cast<double>(pl.sc.n_qb) / (static_cast<double>(waves) * sms);
   bool split = have_ws && pl.sc.n_kv >= 2 && fill < 0.96 && pl.sc.total > 0;
   if (g_sched_mode == 1) split = false;
-  if (g_sched_mode == 2) split = have_ws && pl.sc.n_kv >= 2 && pl.sc.total > 0;
+  if (g_sched_mode >= 2) split = have_ws && pl.sc.n_kv >= 2 && pl.sc.total > 0;
   pl.sc.split = split ? 1 : 0;
+  // aligned split: every q-block cut into nseg equal KV segments, one per CTA (grid =
+  // n_qb * nseg <= SMs): one partial merge per extra segment instead of stream-K's
+  // arbitrary cuts (2-3 partial slots per q-block at FLUX U=8)
+  const int nseg = pl.sc.n_qb > 0 ? sms / pl.sc.n_qb : 0;
+  if (split && g_sched_mode == 3 && nseg >= 2 && pl.sc.n_kv >= 2 * nseg) {
+    pl.grid = pl.sc.n_qb * nseg;
+    for (int c = 0; c <= pl.grid; ++c) {
+      const int qb = c / nseg, k = c % nseg;
+      pl.sc.begin[c] = qb * pl.sc.n_kv + (k * pl.sc.n_kv) / nseg;
+    }
+    return pl;
+  }
   if (split) {
     // at least 2 KV tiles per CTA so each segment amortises its Q load and epilogue
     const int g = pl.sc.total / 2;

@@ -246,6 +246,9 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
                                       uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s);
 fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
                                      int64_t n, void* y, int ydt, cudaStream_t s);
+// Ring forward of an E4M3 chunk that quantize produced as a whole: scales[i] <- RN(RN(448 s) /
+// 448) in place for `parts` trailers of n scales (the codes are unchanged; see usp.cpp ring()).
+fusp_status launch_fp8_forward_scales(float* const* scales, int parts, int n, cudaStream_t s);
 fusp_status launch_scatter_slot_scales(const float* scales, float* base, int64_t slot_stride_f,
                                        int b, int h, int u, int per_block, cudaStream_t s);
 fusp_status launch_finite(const void* x, int dt, int64_t n, uint32_t* flag, cudaStream_t s);

@@ -1469,3 +1469,27 @@ fusp_status launch_finite(const void* x, int dt, int64_t n, uint32_t* flag, cuda
 }
 
 }  // namespace fusp
+
+namespace fusp {
+namespace {
+// quantize(dequantize(chunk)) of a chunk quantize produced as a whole: amax = decode(0x7E) * s
+// (the block's largest code is +-448 by construction; an all-zero block has s = 1 and gives
+// the same), scale' = amax / 448 (fp8.cpp:119), IEEE roundings as the reference.
+__global__ void fp8_forward_scales_kernel(float* a, float* b, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float* p = blockIdx.x == 0 ? a : b;
+    const float amax = __fmul_rn(448.0f, p[i]);
+    p[i] = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  }
+}
+}  // namespace
+
+fusp_status launch_fp8_forward_scales(float* const* scales, int parts, int n, cudaStream_t s) {
+  if (n <= 0 || parts <= 0) return FUSP_OK;
+  if (parts > 2) return set_error(FUSP_ERR_INVALID_ARGUMENT, "fp8 forward scales: at most 2 parts");
+  fp8_forward_scales_kernel<<<parts, 256, 0, s>>>(scales[0], parts > 1 ? scales[1] : scales[0], n);
+  FUSP_LAUNCHED("fp8_forward_scales_kernel");
+  return FUSP_OK;
+}
+
+}  // namespace fusp

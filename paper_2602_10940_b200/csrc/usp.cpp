@@ -820,9 +820,24 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     const int into = hop % 2, from = (hop - 1) % 2;
     const void* snd[2];
     if (l.fp8) {
-      FUSP_CHECK(quantize_hop(hop, from, st));
-      snd[0] = b.sw[0];
-      snd[1] = b.sw[1];
+      if (hop == 1) {
+        FUSP_CHECK(quantize_hop(hop, from, st));
+        snd[0] = b.sw[0];
+        snd[1] = b.sw[1];
+      } else {
+        // Forwarding a chunk that quantize produced as a whole (one scale per quantization
+        // block): quantize(dequantize(chunk)) (protocols.cpp:309-310) keeps every code -- the
+        // block's max |value| is decode(0x7E) * s = RN(448 s), and RN(RN(d s) / s') = d (1 +
+        // O(2^-23)) rounds back to d for every E4M3 value d -- and only the scale becomes
+        // RN(RN(448 s) / 448).  So the received buffer is forwarded in place with its trailer
+        // updated (after its own staging read the old scale): no pass over the codes.
+        // tests/test_gpu_wire.py pins the forwarded bytes to the reference quantizer.
+        float* tr[2] = {reinterpret_cast<float*>(b.rb[from][0] + l.C),
+                        reinterpret_cast<float*>(b.rb[from][1] + l.C)};
+        FUSP_CHECK(launch_fp8_forward_scales(tr, 2, l.nsc_chunk, st));
+        snd[0] = b.rb[from][0];
+        snd[1] = b.rb[from][1];
+      }
     } else if (hop == 1) {
       snd[0] = b.Kw;
       snd[1] = b.Vw;

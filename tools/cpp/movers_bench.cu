@@ -117,8 +117,11 @@ int main() {
     uint8_t *ck2, *cv2;
     CK(cudaMalloc(&ck2, n)); CK(cudaMalloc(&cv2, n));
     uint8_t* cds2[2] = {ck2, cv2};
-    snprintf(nm, sizeof nm, "%s fp8 ring hop re-quantize K,V from e4m3", c.name);
+    snprintf(nm, sizeof nm, "%s fp8 ring hop re-quantize K,V from e4m3 (hop 1: multi-scale chunk)", c.name);
     report(nm, 2.0 * n * (1 + 1 + 1), [&] { launch_quantize_fp8_multi(esrc, 2, n, n, works, scs, cds2, nullptr, 0); });
+    float* trs[2] = {sc, sc + 64};
+    snprintf(nm, sizeof nm, "%s fp8 ring hop >= 2 forward (codes kept in place, scale trailer only)", c.name);
+    report(nm, 2.0 * n * (1 + 1 + 1), [&] { launch_fp8_forward_scales(trs, 2, 1, 0); });
     for (void* x : {q, k, v, slots, dq, dk, dv}) cudaFree(x);
     for (void* x : std::vector<void*>{ck, cv, sc, wk, ck2, cv2}) cudaFree(x);
   }
