@@ -14,8 +14,8 @@ from typing import Dict, List, Optional
 
 
 # per-rank attention launches of the BASELINE meshes, measured on one B200 (f16 output)
-ATTN_MEASURED = {"24x4608": 1308.6, "12x4608": 1226.2, "6x4608": 949.8, "3x4608": 690.9,
-                 "12x4224": 1052.4, "6x3584": 794.4, "24x7168": 1207.7}
+ATTN_MEASURED = {"24x4608": 1299.6, "12x4608": 1229.2, "6x4608": 1049.9, "3x4608": 803.5,
+                 "12x4224": 1161.2, "6x3584": 889.5, "24x7168": 1142.6}  # profiles/r02_vmesh.jsonl
 
 
 @dataclass
@@ -29,7 +29,7 @@ class HardwareProfile:
     peak_tflops: float = 1618.9         # measured dense bf16 burst (MEASURED_PEAKS.json)
     attn_efficiency: float = 0.81       # fallback: attention-kernel fraction of peak at FLUX U=1
     # Measured attention-kernel throughput (TFLOP/s) per per-rank launch shape "heads x span"
-    # (tools/ab_attn.py, profiles/r02_ab_attn.jsonl); attention_seconds interpolates it over
+    # (tools/virtual_mesh_bench.py, profiles/r02_vmesh.jsonl); attention_seconds interpolates it over
     # log(FLOP per launch) -- small per-rank launches run well below the U=1 efficiency.
     attn_tflops_measured: Dict[str, float] = field(default_factory=lambda: dict(ATTN_MEASURED))
 
