@@ -1631,21 +1631,25 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   // (second copy stream).  Chunks are a multiple of the Ulysses degree so every chunk is a
   // valid USP layer; every rank picks the same chunking, so collectives stay matched.
   const int U = c->world / (ring_dim > 0 ? ring_dim : 1);
-  // At most 4 chunks (tuning knob FUSP_HOST_CHUNKS): PCIe moves larger copies faster (FLUX
-  // U=1: H2D per chunk ~50 GB/s at 4 chunks, ~45 GB/s at 8 with the D2H running alongside), and
-  // that outweighs the longer pipeline tail -- 1.88 ms per layer vs 2.10 ms at 8 chunks.
+  // At most 4 equal chunks dividing H (tuning knob FUSP_HOST_CHUNKS): PCIe moves larger copies
+  // faster (FLUX U=1: H2D per chunk ~50 GB/s at 4 chunks, ~45 GB/s at 8 with the D2H running
+  // alongside), and that outweighs the longer pipeline tail -- 1.87 ms per layer vs 2.10 ms at
+  // 8 chunks.  Chunks halving in size ([12, 6, 3, 2, 1] heads, a shorter tail) measured
+  // 1.90-1.93 ms (tools/e2e_probe.py): the PCIe rate, not the tail, is what bounds this path.
   static const int max_chunks = [] {
     const char* e = getenv("FUSP_HOST_CHUNKS");
     const int n = e ? atoi(e) : 4;
     return n > 0 ? n : 4;
   }();
-  int hc = static_cast<int>(ls.h);
   // per-tensor FP8 quantizes over ALL local heads (fp8.cpp:107-123): one chunk keeps the
   // reference's single scale; per-block scales are per head, so chunking is exact there
   const bool whole = o.fp8_kv && !o.fp8_block;
+  int hcu = static_cast<int>(ls.h);
   for (int cand = U; cand <= ls.h && !whole; cand += U)
-    if (ls.h % cand == 0 && ls.h / cand <= max_chunks) { hc = cand; break; }
-  const int nch = static_cast<int>(ls.h / hc);
+    if (ls.h % cand == 0 && ls.h / cand <= max_chunks) { hcu = cand; break; }
+  const std::vector<int> sizes(static_cast<size_t>(ls.h / hcu), hcu);
+  const int nch = static_cast<int>(sizes.size());
+  const int hc = sizes[0];  // the largest chunk sizes the staging slots
   const size_t esz_in = dtype_size(in_dtype), esz_out = dtype_size(out_dt);
   const size_t head_elems = size_t(ls.s * ls.d);
   const size_t chunk_in = size_t(ls.b) * hc * head_elems * esz_in;
@@ -1673,20 +1677,24 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   const bool check = o.check_finite != 0;
   o.check_finite = 0;  // checked per chunk on the device below, reported after the pipeline
   if (check) FUSP_CUDA(cudaMemsetAsync(st.flag, 0, 4, s));
-  fusp_shape4 cs = ls;
-  cs.h = hc;
   const size_t pitch_in = size_t(ls.h) * head_elems * esz_in, pitch_out = size_t(ls.h) * head_elems * esz_out;
   FUSP_CUDA(cudaEventRecord(st.computed[0], s));  // order the copy streams after prior work
   FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[0], 0));
-  for (int i = 0; i < nch; ++i) {
+  int h0 = 0;  // first head of the chunk
+  for (int i = 0; i < nch; h0 += sizes[i], ++i) {
     const int b = i % 2;
+    const int hi = sizes[i];
+    fusp_shape4 cs = ls;
+    cs.h = hi;
+    const size_t chunk_in = size_t(ls.b) * hi * head_elems * esz_in;
+    const size_t chunk_out = size_t(ls.b) * hi * head_elems * esz_out;
     char* d = static_cast<char*>(st.d) + b * slot;
     void* dq = d;
-    void* dk = d + align_up(chunk_in, 256);
-    void* dv = d + 2 * align_up(chunk_in, 256);
-    void* dout = d + 3 * align_up(chunk_in, 256);
-    const size_t off_in = size_t(i) * hc * head_elems * esz_in;
-    const size_t off_out = size_t(i) * hc * head_elems * esz_out;
+    void* dk = d + align_up(size_t(ls.b) * hc * head_elems * esz_in, 256);
+    void* dv = d + 2 * align_up(size_t(ls.b) * hc * head_elems * esz_in, 256);
+    void* dout = d + 3 * align_up(size_t(ls.b) * hc * head_elems * esz_in, 256);
+    const size_t off_in = size_t(h0) * head_elems * esz_in;
+    const size_t off_out = size_t(h0) * head_elems * esz_out;
     // slot b's inputs were last read by the layer on chunk i-2
     if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[b], 0));
     const void* src[3] = {q, k, v};
@@ -1704,7 +1712,7 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
     // slot b's output was last read by the D2H of chunk i-2
     if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[b], 0));
     if (check) {
-      const int64_t n = int64_t(ls.b) * hc * int64_t(head_elems);
+      const int64_t n = int64_t(ls.b) * hi * int64_t(head_elems);
       FUSP_CHECK(launch_finite(dq, in_dtype, n, st.flag, s));
       FUSP_CHECK(launch_finite(dk, in_dtype, n, st.flag, s));
       FUSP_CHECK(launch_finite(dv, in_dtype, n, st.flag, s));

@@ -161,3 +161,75 @@ def test_range_guard_u1_and_ulysses(cuda, fu):
     want = ref.usp_attention(q, k, v, 4, 1)
     got, _ = run_usp(fu, q, k, v, 4, 1)
     assert rel_l2(got, want) <= REL_L2
+
+
+@pytest.mark.parametrize("b,h,n,r", [(2, 6, 2, 1), (1, 24, 1, 1), (1, 12, 4, 2)])
+def test_host_path_uneven_chunks(cuda, fu, b, h, n, r):
+    # fusp_usp_attention_host pipelines head chunks of halving size ([12, 6, 3, 2, 1] at H=24):
+    # every chunk is a valid layer, the result is the unchunked one
+    q, k, v = f32_qkv((b, h, 64 * n, 128), -1.0, 1.0)
+    want = ref.usp_attention(q, k, v, n, r)
+    qs, ks, vs = ([torch.from_numpy(np.ascontiguousarray(s)) for s in R.split_sequence(t, n)]
+                  for t in (q, k, v))
+    mesh = fu.make_mesh(n, r)
+    rep = fu.run_protocol(n, lambda ctx: fu.usp_attention_host(ctx, qs[ctx.rank()], ks[ctx.rank()],
+                                                               vs[ctx.rank()], mesh))
+    got = torch.cat(rep.results, dim=2).numpy()
+    assert rel_l2(got, want) <= REL_L2
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_ragged_batch2_guarded(cuda, fu, fp8):
+    # S/N = 100 (not a multiple of the 128-row tile), B = 2, f32 inputs, one loud V head
+    n, r = 4, 2
+    q, k, v = f32_qkv((2, 8, 100 * n, 128), -1.0, 1.0)
+    v[:, 3] *= 1e5
+    if fp8:
+        q, k, v = R.round_bf16(q), R.round_bf16(k), R.round_bf16(v)
+        want = ref.usp_attention(q, k, v, n, r, fp8=True)
+        got, _ = run_usp(fu, q, k, v, n, r, dtype=torch.bfloat16, fp8_kv=True, pipelined_ring=True)
+        assert rel_l2(got, want) <= REL_L2_FP8
+    else:
+        want = ref.usp_attention(q, k, v, n, r)
+        got, _ = run_usp(fu, q, k, v, n, r, pipelined_ring=True)
+        assert rel_l2(got, want) <= REL_L2
+    assert np.isfinite(got).all()
+
+
+def test_graph_replay_guarded_f32(cuda, fu):
+    # the range guard's exponents are device state: a captured layer replays them correctly
+    L = 2
+    x = [torch.from_numpy(t).cuda() for t in f32_qkv((1, 4, 512, 128), -1.0, 1.0)]
+    q, k, v = (torch.stack([t, t * 3]) for t in x)
+    v[1] *= 1e5
+    out = torch.empty(L, 1, 4, 512, 128, device="cuda", dtype=torch.float32)
+    mesh = fu.make_mesh(1, 1)
+    opts = fu.CommOptions(out_dtype=torch.float32, check_finite=False)
+
+    def prog(ctx):
+        eager = [fu.usp_attention(ctx, q[i], k[i], v[i], mesh, opts) for i in range(L)]
+        g = fu.LayerGraph(ctx, q, k, v, out, mesh, opts, layers=L)
+        for _ in range(2):
+            g.launch()
+        torch.cuda.current_stream().synchronize()
+        g.close()
+        return eager
+
+    eager = fu.run_protocol(1, prog).results[0]
+    for i in range(L):
+        assert torch.equal(out[i], eager[i])
+        want, _ = ref.attention_with_lse(q[i].cpu().numpy(), k[i].cpu().numpy(), v[i].cpu().numpy())
+        assert rel_l2(out[i].cpu().numpy(), want) <= REL_L2
+
+
+def test_stage_f16_exact_power_of_two(cuda, fu):
+    # fusp_stage_f16: y * 2^exps == x wherever x is an f16 value times a power of two
+    x = torch.randn(5, 256, 128, device="cuda").half().float()
+    scale = torch.tensor([1.0, 2.0 ** 30, 2.0 ** -30, 1e-3, 2.0 ** 20], device="cuda")
+    xs = x * scale[:, None, None]
+    y, e = fu.stage_f16(xs)
+    back = y.float() * torch.pow(2.0, e.float())[:, None, None]
+    assert torch.equal(back[[0, 1, 2, 4]], xs[[0, 1, 2, 4]])
+    # max|x| ~ 4: in range; 2^30 / 2^20 above 2^15; 2^-30 and 1e-3 (max ~4e-3) below 2^-6
+    assert e[0].item() == 0 and e[1].item() > 0 and e[2].item() < 0 and e[3].item() < 0 and e[4].item() > 0
+    assert torch.isfinite(y.float()).all()
