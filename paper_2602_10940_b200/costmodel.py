@@ -14,8 +14,8 @@ from typing import Dict, List, Optional
 
 
 # per-rank attention launches of the BASELINE meshes, measured on one B200 (f16 output)
-ATTN_MEASURED = {"24x4608": 1299.6, "12x4608": 1229.2, "6x4608": 1049.9, "3x4608": 803.5,
-                 "12x4224": 1161.2, "6x3584": 889.5, "24x7168": 1142.6}  # profiles/r02_vmesh.jsonl
+ATTN_MEASURED = {"24x4608": 1299.6, "12x4608": 1229.2, "6x4608": 1049.9, "3x4608": 877.4,
+                 "12x4224": 1161.2, "6x3584": 889.5, "24x7168": 1142.6}  # profiles/r02_vmesh.jsonl, 3x4608: attn_kv2_kernel (r02_ab_kv2.jsonl)
 
 
 @dataclass

@@ -884,6 +884,439 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- KV-split variant for few q-blocks ----------------------------------------------------
+// When a rank's launch has fewer 128-row Q tiles than SMs (FLUX U=8: 3 heads x 36 = 108 tiles
+// on 148 SMs) the stream-K schedule above cuts 256-row q-blocks over ~2.7 CTAs and pays the
+// partial-slot publish and finisher merge.  Here a work item is ONE 128-row Q tile, whole,
+// and the CTA's two softmax warpgroups split its KV range instead of taking two Q tiles:
+// chain t processes KV tiles j0 + t, j0 + t + 2, ... with its own S_t / O_t in TMEM, so the
+// two chains still ping-pong on the tensor core.  At the tile's end the chains merge inside
+// the CTA: (m, l) through shared memory, O through TMEM (warp w of either warpgroup reads the
+// same 32 lanes), each warpgroup finishing half of the columns.  No workspace, no tickets.
+// SMEM: Q 32 KB + K 4 x 32 KB (each chain keeps its next K tile in flight) + V 2 x 32 KB.
+#ifndef FUSP_KV2_KSTAGES
+#define FUSP_KV2_KSTAGES 4
+#endif
+#ifndef FUSP_KV2_VSTAGES
+#define FUSP_KV2_VSTAGES 2
+#endif
+constexpr int kKv2KStages = FUSP_KV2_KSTAGES;
+constexpr int kKv2VStages = FUSP_KV2_VSTAGES;
+struct __align__(1024) SmemKv2 {
+  uint8_t q[kTileBytes];
+  uint8_t k[kKv2KStages][kTileBytes];
+  uint8_t v[kKv2VStages][kTileBytes];
+  uint64_t q_full, q_empty;
+  uint64_t k_full[kKv2KStages], k_empty[kKv2KStages];
+  uint64_t v_full[kKv2VStages], v_empty[kKv2VStages];
+  uint64_t s_full[2], p_full[2], o_done[2];
+  uint64_t s_read[2], p_half[2];
+  uint32_t tmem_base;
+};
+
+// Named barrier over the 8 softmax warps (ids 1, 2 are the per-warpgroup ones).
+__device__ __forceinline__ void softmax_bar() {
+  __syncwarp();
+  asm volatile("bar.sync 3, 256;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_kv2_kernel(const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemKv2& sm = *reinterpret_cast<SmemKv2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~uintptr_t(1023));
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const Sched& sc = p.sc;  // whole Q tiles: qb = tile index, sc.split == 0
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 2);  // both warpgroups release the Q tile
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], kBM);
+      mbar_init(&sm.s_read[t], kBM);
+      mbar_init(&sm.p_half[t], kBM);
+      mbar_init(&sm.o_done[t], 1);
+    }
+    for (int s = 0; s < kKv2KStages; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kKv2VStages; ++s) {
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  if (tmem != 0u) __trap();
+  if (warp < 4) {
+    reg_dealloc<FUSP_PRODUCER_REGS>();
+    if (warp == 0) {
+      // ---------------- TMA producer: the Q tile, then the K tiles in KV order ----------------
+      if (lane == 0) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        SegIter si(sc);
+        Seg g;
+        uint32_t kt = 0, ns = 0;
+        while (si.next(sc, g)) {
+          const int head = g.qb / sc.qb_per_head;
+          const int row0 = (g.qb - head * sc.qb_per_head) * kBM;
+          mbar_wait(&sm.q_empty, (ns & 1) ^ 1);
+          mbar_expect_tx(&sm.q_full, kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            tma_load_3d(sm.q + h * kHalfBytes, &tm_q, &sm.q_full, h * 64, row0, head);
+          for (int j = g.j0; j < g.j1; ++j, ++kt) {
+            const int st = kt % kKv2KStages;
+            mbar_wait(&sm.k_empty[st], ((kt / kKv2KStages) & 1) ^ 1);
+            mbar_expect_tx(&sm.k_full[st], kTileBytes);
+            for (int h = 0; h < 2; ++h)
+              tma_load_3d(sm.k[st] + h * kHalfBytes, &tm_k, &sm.k_full[st], h * 64, j * kBN, head);
+          }
+          ++ns;
+        }
+      }
+    } else if (warp == 2) {
+      // ---------------- TMA producer: V tiles in KV order ----------------
+      if (lane == 0) {
+        prefetch_tmap(&tm_v);
+        SegIter si(sc);
+        Seg g;
+        uint32_t kt = 0;
+        while (si.next(sc, g)) {
+          const int head = g.qb / sc.qb_per_head;
+          for (int j = g.j0; j < g.j1; ++j, ++kt) {
+            const int st = kt % kKv2VStages;
+            mbar_wait(&sm.v_empty[st], ((kt / kKv2VStages) & 1) ^ 1);
+            mbar_expect_tx(&sm.v_full[st], kTileBytes);
+            for (int h = 0; h < 2; ++h)
+              tma_load_3d(sm.v[st] + h * kHalfBytes, &tm_v, &sm.v_full[st], h * 64, j * kBN, head);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------- tcgen05.mma issuer: two KV chains on one Q tile ----------------
+      const uint32_t idesc_qk = p.idesc_qk;
+      constexpr uint32_t idesc_pv = idesc_f16(0, 0, 0, 1, kBM, kD);
+      const uint32_t idesc_qk_h = (idesc_qk & ~(0x3Fu << 17)) | ((64u >> 3) << 17);
+      const uint64_t qdesc = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
+      auto issue_qk = [&](int t, int sk) {
+        const uint64_t kdesc = umma_desc_sw128(smem_u32(sm.k[sk]), 16, 1024);
+        if (elect_one()) {
+#pragma unroll kMmaUnroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t off16 = ((k >> 2) * kHalfBytes + (k & 3) * 32) / 16;
+            mma_ss(kTmemS + t * 128, qdesc + off16, kdesc + off16, idesc_qk, k > 0 ? 1u : 0u);
+          }
+        }
+        __syncwarp();
+      };
+      auto issue_qk_half = [&](int t, int sk, int half) {
+        const uint64_t kdesc = umma_desc_sw128(smem_u32(sm.k[sk]) + half * 64 * 128, 16, 1024);
+        if (elect_one()) {
+#pragma unroll kMmaUnroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t off16 = ((k >> 2) * kHalfBytes + (k & 3) * 32) / 16;
+            mma_ss(kTmemS + t * 128 + half * 64, qdesc + off16, kdesc + off16, idesc_qk_h, k > 0 ? 1u : 0u);
+          }
+        }
+        __syncwarp();
+      };
+      auto issue_pv_half = [&](int t, int st, int half, bool first) {
+        const uint64_t vdesc = umma_desc_sw128(smem_u32(sm.v[st]), kHalfBytes, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = half * 4; k < half * 4 + 4; ++k)
+            mma_ts(kTmemO + t * 128, kTmemS + t * 128 + k * 8, vdesc + uint64_t(k * 16 * 128 / 16),
+                   idesc_pv, (!first || k > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) mma_commit(bar);
+        __syncwarp();
+      };
+      SegIter si(sc);
+      Seg g;
+      uint32_t kt0 = 0, ns = 0, cnt[2] = {0, 0};
+      while (si.next(sc, g)) {
+        const int nt = g.j1 - g.j0;
+        const int nc[2] = {(nt + 1) / 2, nt / 2};
+        mbar_wait(&sm.q_full, ns & 1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {  // each chain's first S
+          if (nc[t] == 0) continue;
+          const uint32_t kt = kt0 + t;
+          mbar_wait(&sm.k_full[kt % kKv2KStages], (kt / kKv2KStages) & 1);
+          tc_fence_after();
+          issue_qk(t, kt % kKv2KStages);
+          commit(&sm.s_full[t]);
+        }
+        for (int s = 0; s < nc[0]; ++s) {
+          for (int t = 0; t < 2; ++t) {
+            if (s >= nc[t]) continue;
+            const uint32_t kt = kt0 + 2 * s + t, ktn = kt + 2;
+            const bool nxt = s + 1 < nc[t];
+            const int sk = kt % kKv2KStages, sn = ktn % kKv2KStages, sv = kt % kKv2VStages;
+            const uint32_t c = cnt[t]++;
+            if (nxt) {
+              mbar_wait(&sm.k_full[sn], (ktn / kKv2KStages) & 1);
+              tc_fence_after();
+            }
+            mbar_wait(&sm.s_read[t], c & 1);  // every phase consumed (synccheck)
+            if (nxt) {
+              tc_fence_after();
+              issue_qk_half(t, sn, 1);
+            }
+            mbar_wait(&sm.p_half[t], c & 1);
+            mbar_wait(&sm.v_full[sv], (kt / kKv2VStages) & 1);
+            tc_fence_after();
+            issue_pv_half(t, sv, 0, s == 0);
+            mbar_wait(&sm.p_full[t], c & 1);
+            tc_fence_after();
+            issue_pv_half(t, sv, 1, false);
+            if (nxt) {
+              issue_qk_half(t, sn, 0);
+              commit(&sm.s_full[t]);
+            } else {
+              commit(&sm.o_done[t]);
+            }
+            commit(&sm.k_empty[sk]);  // S(kt) completed before this point
+            commit(&sm.v_empty[sv]);
+          }
+        }
+        kt0 += nt;
+        ++ns;
+      }
+    }
+  } else {
+    reg_alloc<FUSP_SOFTMAX_REGS>();
+    // ---------------- softmax warpgroups: chain t of the Q tile ----------------
+    const int t = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    const int r_in_tile = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t t_s = kTmemS + lane_off + t * 128;
+    const uint32_t t_o0 = kTmemO + lane_off;  // chain 0's O (chain 1's at +128)
+    SegIter si(sc);
+    Seg g;
+    uint32_t c = 0, nd[2] = {0, 0};
+    while (si.next(sc, g)) {
+      const int head = g.qb / sc.qb_per_head;
+      const int e_qk = (p.q_exp != nullptr ? p.q_exp[head] : 0) + (p.k_exp != nullptr ? p.k_exp[head] : 0);
+      const float sl2 = p.scale_log2 * __int_as_float((127 + e_qk) << 23);
+      const float v_scale = p.v_exp != nullptr ? __int_as_float((127 + p.v_exp[head]) << 23) : 1.f;
+      const float2 sl2x2 = make_float2(sl2, sl2);
+      const int row = (g.qb - head * sc.qb_per_head) * kBM + r_in_tile;
+      const int nt = g.j1 - g.j0;
+      const int nc[2] = {(nt + 1) / 2, nt / 2};
+      float m_use = -INFINITY;
+      float l_sum = 0.f;
+      for (int i = 0; i < nc[t]; ++i, ++c) {
+        const int j = g.j0 + 2 * i + t;
+        mbar_wait(&sm.s_full[t], c & 1);
+        tc_fence_after();
+        uint32_t s[128];
+        tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+        tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&sm.s_read[t]);
+        const int valid = p.skv - j * kBN;
+        if (valid < kBN) {
+#pragma unroll
+          for (int cc = 0; cc < 128; ++cc)
+            if (cc >= valid) s[cc] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int cc = 0; cc < 128; cc += 8) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            mx4[q] = fmaxf(mx4[q], fmaxf(__uint_as_float(s[cc + q]), __uint_as_float(s[cc + 4 + q])));
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        float alpha = 1.f;
+        if (m_use == -INFINITY) {
+          m_use = mx;
+        } else if ((mx - m_use) * sl2 > kRescaleThreshold) {
+          alpha = ex2((m_use - mx) * sl2);
+          m_use = mx;
+        }
+        if (__any_sync(0xffffffffu, alpha != 1.f) && i > 0) {
+#pragma unroll 1
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(t_o0 + t * 128 + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+            tmem_st32(t_o0 + t * 128 + cc * 32, o);
+          }
+        }
+        const float neg_m = -m_use * sl2;
+        const float2 negm2 = make_float2(neg_m, neg_m);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int pi = 0; pi < 64; ++pi) {
+          const float2 x = ffma2(make_float2(__uint_as_float(s[2 * pi]), __uint_as_float(s[2 * pi + 1])),
+                                 sl2x2, negm2);
+          const float2 pp = (pi % kEmuEvery == kEmuEvery - 1) ? exp2_poly2(x)
+                                                             : make_float2(ex2(x.x), ex2(x.y));
+          acc[pi & 3] = fadd2(acc[pi & 3], pp);
+          s[pi] = pack_f16x2(pp.x, pp.y);
+          if (pi == 31) {
+            tmem_st32(t_s + 0, &s[0]);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.p_half[t]);
+          }
+        }
+        tmem_st32(t_s + 32, &s[32]);
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        const float2 a = fadd2(a01, a23);
+        l_sum = fmaf(l_sum, alpha, a.x + a.y);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
+      }
+      // ---------------- tile end: both chains' MMAs complete, then merge ----------------
+      for (int u = 0; u < 2; ++u) {
+        if (nc[u] == 0) continue;
+        mbar_wait(&sm.o_done[u], nd[u] & 1);
+        ++nd[u];
+      }
+      tc_fence_after();
+      // (m, l) exchange through the Q tile's shared memory: nothing reads Q any more (every
+      // MMA of the tile completed) and it is only reloaded after both warpgroups release it
+      float2* ml = reinterpret_cast<float2*>(sm.q);
+      ml[t * kBM + r_in_tile] = make_float2(m_use, l_sum);
+      softmax_bar();
+      const float2 o_ml = ml[(1 - t) * kBM + r_in_tile];
+      softmax_bar();
+      if (r_in_tile == 0) mbar_arrive(&sm.q_empty);
+      const float m0 = t == 0 ? m_use : o_ml.x, l0 = t == 0 ? l_sum : o_ml.y;
+      const float m1 = t == 0 ? o_ml.x : m_use, l1 = t == 0 ? o_ml.y : l_sum;
+      const bool has1 = nc[1] > 0;
+      const float m_fin = has1 ? fmaxf(m0, m1) : m0;
+      const float w0 = ex2((m0 - m_fin) * sl2);
+      const float w1 = has1 ? ex2((m1 - m_fin) * sl2) : 0.f;
+      const float l_fin = w0 * l0 + w1 * l1;
+      const bool in_range = row < p.sq;
+      const float lse_b = m_fin * (sl2 * 0.69314718055994530942f) + logf(l_fin);
+      const float inv_l = 1.f / l_fin;
+      float c_acc = 0.f, c_new = 1.f, lse_out = lse_b;
+      if (p.acc_o != nullptr && in_range) {
+        const float la = p.acc_lse[static_cast<int64_t>(head) * p.sq + row];
+        lse_out = merge_coeffs(la, lse_b, c_acc, c_new);
+      }
+      const float scale_new = c_new * inv_l * v_scale;
+      const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
+                            static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
+                            static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
+      const int e4 = lane & 3;
+      int64_t ob_g[4];
+      bool in_g[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ob_g[q] = __shfl_sync(0xffffffffu, obase, (lane & ~3) + q);
+        in_g[q] = row - e4 + q < p.sq;
+      }
+      const float* acc_h = p.acc_o != nullptr ? p.acc_o + static_cast<int64_t>(head) * p.sq * kD : nullptr;
+      // warpgroup t finishes columns [64 t, 64 t + 64): O = (w0 O0 + w1 O1) / l
+#pragma unroll 1
+      for (int cc = 2 * t; cc < 2 * t + 2; ++cc) {
+        uint32_t o[32];
+        float v[32];
+        tmem_ld32(t_o0 + cc * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = w0 * __uint_as_float(o[q]);
+        if (has1) {  // (warp-uniform: the tile's chain count)
+          tmem_ld32(t_o0 + 128 + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = fmaf(w1, __uint_as_float(o[q]), v[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] *= scale_new;
+        if (acc_h != nullptr) {
+          uint32_t av[32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+            if (in_g[q]) {
+              const float4* src =
+                  reinterpret_cast<const float4*>(acc_h + static_cast<int64_t>(row - e4 + q) * kD + cc * 32 + e4 * 8);
+              x0 = src[0];
+              x1 = src[1];
+            }
+            av[8 * q + 0] = __float_as_uint(x0.x); av[8 * q + 1] = __float_as_uint(x0.y);
+            av[8 * q + 2] = __float_as_uint(x0.z); av[8 * q + 3] = __float_as_uint(x0.w);
+            av[8 * q + 4] = __float_as_uint(x1.x); av[8 * q + 5] = __float_as_uint(x1.y);
+            av[8 * q + 6] = __float_as_uint(x1.z); av[8 * q + 7] = __float_as_uint(x1.w);
+          }
+          xpose4<8>(av, lane);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = fmaf(c_acc, __uint_as_float(av[q]), v[q]);
+        }
+        if (p.out_dtype != FUSP_F32) {
+          const bool f16 = p.out_dtype == FUSP_F16;
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            w[e] = f16 ? pack_f16x2(v[2 * e], v[2 * e + 1]) : pack_bf16x2(v[2 * e], v[2 * e + 1]);
+          xpose4<4>(w, lane);
+          uint16_t* o16p = static_cast<uint16_t*>(p.out);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (in_g[q])
+              *reinterpret_cast<uint4*>(o16p + ob_g[q] + cc * 32 + e4 * 8) =
+                  make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        } else {
+          uint32_t w[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) w[q] = __float_as_uint(v[q]);
+          xpose4<8>(w, lane);
+          float* o32p = static_cast<float*>(p.out);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (in_g[q]) {
+              uint4* dst = reinterpret_cast<uint4*>(o32p + ob_g[q] + cc * 32 + e4 * 8);
+              dst[0] = make_uint4(w[8 * q], w[8 * q + 1], w[8 * q + 2], w[8 * q + 3]);
+              dst[1] = make_uint4(w[8 * q + 4], w[8 * q + 5], w[8 * q + 6], w[8 * q + 7]);
+            }
+        }
+      }
+      if (t == 0 && in_range && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(head) * p.lse_hs + static_cast<int64_t>(row / p.out_chunk) * p.lse_cs +
+              row % p.out_chunk] = lse_out;
+      // both chains' O have been read before either chain's next-tile P.V can overwrite them
+      tc_fence_before();
+      softmax_bar();
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ---- host-side schedule ------------------------------------------------------------------
 int g_sched_mode = 0;  // 0 auto, 1 whole q-blocks, 2 stream-K split
 unsigned long long* g_trace = nullptr;  // debug event buffer (attention_trace), device memory
@@ -911,6 +1344,7 @@ namespace {
 struct Plan {
   Sched sc;
   int grid;
+  int kv2;  // 1: attn_kv2_kernel over whole 128-row Q tiles (chains split the KV range)
 };
 
 Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
@@ -930,6 +1364,25 @@ Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
   if (g_sched_mode == 1) split = false;
   if (g_sched_mode >= 2) split = have_ws && pl.sc.n_kv >= 2 && pl.sc.total > 0;
   pl.sc.split = split ? 1 : 0;
+  // KV-split CTAs (attn_kv2_kernel): whole 128-row Q tiles, one wave, no partial merges.
+  // Chosen (auto) where stream-K would otherwise cut 256-row q-blocks and the 128-row tiles
+  // fill most of one wave; mode 4 forces it.
+  {
+    const int tiles = heads * ((sq + kBM - 1) / kBM);
+    const bool fits = tiles <= sms && pl.sc.n_kv >= 4;
+    const bool auto_kv2 = split && g_sched_mode == 0 && fits && 10 * tiles >= 6 * sms;
+    if ((g_sched_mode == 4 && fits) || auto_kv2) {
+      Plan k{};
+      k.kv2 = 1;
+      k.sc.n_kv = pl.sc.n_kv;
+      k.sc.qb_per_head = (sq + kBM - 1) / kBM;
+      k.sc.n_qb = tiles;
+      k.sc.split = 0;
+      k.sc.total = tiles * pl.sc.n_kv;
+      k.grid = tiles;
+      return k;
+    }
+  }
   // aligned split: every q-block cut into nseg equal KV segments, one per CTA (grid =
   // n_qb * nseg <= SMs): one partial merge per extra segment instead of stream-K's
   // arbitrary cuts (2-3 partial slots per q-block at FLUX U=8)
@@ -1013,6 +1466,15 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   if (pl.sc.split) {
     p.counters = a.split_counters;
     p.slots = static_cast<float*>(a.split_ws);
+  }
+  if (pl.kv2) {
+    const int smem2 = static_cast<int>(sizeof(SmemKv2)) + 1024;
+    FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(attn_kv2_kernel), smem2, "attn_kv2_kernel"));
+    attn_kv2_kernel<<<pl.grid, kThreads, smem2, stream>>>(tq, tk, tv, p);
+    count_launch();
+    cudaError_t e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) return set_cuda_error(e2, "attn_kv2_kernel launch");
+    return FUSP_OK;
   }
   const int smem = static_cast<int>(sizeof(Smem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem, "attn_fwd_kernel"));

@@ -27,8 +27,8 @@ def load(spec):
                                                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
     if hasattr(L, "fusp_attention_schedule"):
         L.fusp_attention_schedule.argtypes = [ctypes.c_int, ctypes.c_int]
-        L.fusp_attention_schedule(int({"whole": 1, "split": 2, "aligned": 3}.get(mode, 0)), 0)
-    mode_id = int({"whole": 1, "split": 2, "aligned": 3}.get(mode, 0))
+        L.fusp_attention_schedule(int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4}.get(mode, 0)), 0)
+    mode_id = int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4}.get(mode, 0))
     sched = getattr(L, "fusp_attention_schedule", None)
 
     def fn(*a):  # the schedule knob is process-global per library: set it before every call
