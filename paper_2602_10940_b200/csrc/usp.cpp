@@ -53,16 +53,18 @@ struct HostStage {
   void* d = nullptr;
   size_t bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t h2d_x[2] = {nullptr, nullptr};  // extra H2D streams (FUSP_HOST_H2D_STREAMS)
   cudaEvent_t in_ready[2] = {nullptr, nullptr}, computed[2] = {nullptr, nullptr},
               out_done[2] = {nullptr, nullptr};
+  cudaEvent_t in_ready_x[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   uint32_t* flag = nullptr;
   ~HostStage() {
     if (d) cudaFree(d);
     if (flag) cudaFree(flag);
-    for (cudaStream_t x : {h2d, d2h})
+    for (cudaStream_t x : {h2d, d2h, h2d_x[0], h2d_x[1]})
       if (x) cudaStreamDestroy(x);
     for (int i = 0; i < 2; ++i)
-      for (cudaEvent_t e : {in_ready[i], computed[i], out_done[i]})
+      for (cudaEvent_t e : {in_ready[i], computed[i], out_done[i], in_ready_x[0][i], in_ready_x[1][i]})
         if (e) cudaEventDestroy(e);
   }
 };
@@ -1658,6 +1660,11 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   if (!c->host) {
     auto h = std::make_unique<HostStage>();
     FUSP_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    for (int x = 0; x < 2; ++x) {
+      FUSP_CUDA(cudaStreamCreateWithFlags(&h->h2d_x[x], cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i)
+        FUSP_CUDA(cudaEventCreateWithFlags(&h->in_ready_x[x][i], cudaEventDisableTiming));
+    }
     FUSP_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       FUSP_CUDA(cudaEventCreateWithFlags(&h->in_ready[i], cudaEventDisableTiming));
@@ -1680,6 +1687,14 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
   const size_t pitch_in = size_t(ls.h) * head_elems * esz_in, pitch_out = size_t(ls.h) * head_elems * esz_out;
   FUSP_CUDA(cudaEventRecord(st.computed[0], s));  // order the copy streams after prior work
   FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[0], 0));
+  // Q, K, V copies over 1-3 H2D streams (knob FUSP_HOST_H2D_STREAMS, default 1)
+  static const int n_h2d = [] {
+    const char* e = getenv("FUSP_HOST_H2D_STREAMS");
+    const int n = e ? atoi(e) : 1;
+    return n < 1 ? 1 : (n > 3 ? 3 : n);
+  }();
+  cudaStream_t h2ds[3] = {st.h2d, st.h2d_x[0], st.h2d_x[1]};
+  for (int x = 1; x < n_h2d; ++x) FUSP_CUDA(cudaStreamWaitEvent(h2ds[x], st.computed[0], 0));
   int h0 = 0;  // first head of the chunk
   for (int i = 0; i < nch; h0 += sizes[i], ++i) {
     const int b = i % 2;
@@ -1696,19 +1711,25 @@ fusp_status fusp_usp_attention_host(fusp_ctx c, int ring_dim, const void* q, con
     const size_t off_in = size_t(h0) * head_elems * esz_in;
     const size_t off_out = size_t(h0) * head_elems * esz_out;
     // slot b's inputs were last read by the layer on chunk i-2
-    if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(st.h2d, st.computed[b], 0));
+    if (i >= 2)
+      for (int x = 0; x < n_h2d; ++x) FUSP_CUDA(cudaStreamWaitEvent(h2ds[x], st.computed[b], 0));
     const void* src[3] = {q, k, v};
     void* dst[3] = {dq, dk, dv};
     for (int t = 0; t < 3; ++t) {
+      cudaStream_t hs = h2ds[t % n_h2d];
       if (ls.b == 1)
         FUSP_CUDA(cudaMemcpyAsync(dst[t], static_cast<const char*>(src[t]) + off_in, chunk_in,
-                                  cudaMemcpyHostToDevice, st.h2d));
+                                  cudaMemcpyHostToDevice, hs));
       else
         FUSP_CUDA(cudaMemcpy2DAsync(dst[t], chunk_in / ls.b, static_cast<const char*>(src[t]) + off_in,
-                                    pitch_in, chunk_in / ls.b, ls.b, cudaMemcpyHostToDevice, st.h2d));
+                                    pitch_in, chunk_in / ls.b, ls.b, cudaMemcpyHostToDevice, hs));
     }
     FUSP_CUDA(cudaEventRecord(st.in_ready[b], st.h2d));
     FUSP_CUDA(cudaStreamWaitEvent(s, st.in_ready[b], 0));
+    for (int x = 1; x < n_h2d; ++x) {
+      FUSP_CUDA(cudaEventRecord(st.in_ready_x[x - 1][b], h2ds[x]));
+      FUSP_CUDA(cudaStreamWaitEvent(s, st.in_ready_x[x - 1][b], 0));
+    }
     // slot b's output was last read by the D2H of chunk i-2
     if (i >= 2) FUSP_CUDA(cudaStreamWaitEvent(s, st.out_done[b], 0));
     if (check) {

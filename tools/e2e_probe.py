@@ -5,8 +5,8 @@ import os, statistics, subprocess, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 if len(sys.argv) == 1:
-    for n in (3, 4, 6, 8, 4, 6):
-        env = dict(os.environ, FUSP_HOST_CHUNKS=str(n))
+    for n, hs in ((4, 1), (4, 2), (4, 3), (3, 3), (6, 3), (8, 3), (4, 1), (4, 3)):
+        env = dict(os.environ, FUSP_HOST_CHUNKS=str(n), FUSP_HOST_H2D_STREAMS=str(hs))
         r = subprocess.run([sys.executable, __file__, "run"], env=env, capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-400:])
     sys.exit(0)
@@ -26,5 +26,5 @@ for _ in range(10):
     fu.usp_attention_host(ctx, q, k, v, mesh, opts, out=out)
     t.append((time.perf_counter() - t0) * 1e3)
 ms = statistics.median(t)
-print(f"chunks<={os.environ.get('FUSP_HOST_CHUNKS')}: {ms:.3f} ms  {4 * h * s * s * d / ms / 1e9:.1f} TFLOP/s "
+print(f"chunks<={os.environ.get('FUSP_HOST_CHUNKS')} h2d streams {os.environ.get('FUSP_HOST_H2D_STREAMS')}: {ms:.3f} ms  {4 * h * s * s * d / ms / 1e9:.1f} TFLOP/s "
       f"(h2d {3 * q.numel() * 2 / 1e6:.1f} MB, d2h {out.numel() * 2 / 1e6:.1f} MB)")
