@@ -104,7 +104,8 @@ fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, i
 /* attention_with_lse (tensor.cpp:193-202): q [B,H,Sq,D], k,v [B,H,Skv,D], all `in_dtype`
  * (F32/BF16/F16; computed as bf16 Q.K^T and f16 P.V with f32 accumulation).
  * out [B,H,Sq,D] in out_dtype; lse [B,H,Sq] f32 natural log (nullable). Skv = 0 gives
- * out = 0, lse = -inf (tensor.cpp:161-164).  D must be 128. */
+ * out = 0, lse = -inf (tensor.cpp:161-164).  D = 128 runs on the tcgen05 kernel; any other D
+ * that is a multiple of 8 (up to 256) on an f32 CUDA-core kernel (the protocols below too). */
 fusp_status fusp_attention_with_lse(const void* q, const void* k, const void* v,
                                     fusp_dtype in_dtype, fusp_shape4 q_shape, int64_t skv,
                                     void* out, fusp_dtype out_dtype, float* lse,

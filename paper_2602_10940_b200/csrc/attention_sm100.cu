@@ -900,6 +900,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef FUSP_KV2_VSTAGES
 #define FUSP_KV2_VSTAGES 2
 #endif
+#ifndef FUSP_KV2_EARLY_K
+#define FUSP_KV2_EARLY_K 1
+#endif
 constexpr int kKv2KStages = FUSP_KV2_KSTAGES;
 constexpr int kKv2VStages = FUSP_KV2_VSTAGES;
 struct __align__(1024) SmemKv2 {
@@ -1060,6 +1063,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           issue_qk(t, kt % kKv2KStages);
           commit(&sm.s_full[t]);
+#if FUSP_KV2_EARLY_K
+          commit(&sm.k_empty[kt % kKv2KStages]);  // K(kt) is free once S(kt) completed
+#endif
         }
         for (int s = 0; s < nc[0]; ++s) {
           for (int t = 0; t < 2; ++t) {
@@ -1087,10 +1093,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nxt) {
               issue_qk_half(t, sn, 0);
               commit(&sm.s_full[t]);
+#if FUSP_KV2_EARLY_K
+              // K(ktn) is released as soon as S(ktn) completes -- a chain step before its
+              // P.V -- so the producer refills the stage a step earlier (the next-next tile's
+              // S is needed right after the softmax loads this one: a short window)
+              commit(&sm.k_empty[sn]);
+#endif
             } else {
               commit(&sm.o_done[t]);
             }
+#if !FUSP_KV2_EARLY_K
             commit(&sm.k_empty[sk]);  // S(kt) completed before this point
+#endif
             commit(&sm.v_empty[sv]);
           }
         }
@@ -1411,8 +1425,7 @@ Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
 
 // Host launcher. q,k: bf16 [heads][sq|skv][128] (row stride 128); v: f16 [heads][skv][128].
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
-  if (a.d != kD) return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(a.d) +
-                                                      " unsupported by the sm_100a kernel (D=128)");
+  if (a.d != kD) return launch_attention_generic(a, stream);  // CUDA-core f32 path for other D
   if (a.sq <= 0 || a.heads <= 0) return FUSP_OK;
   if (a.skv <= 0) return set_error(FUSP_ERR_SHAPE, "attention kernel: empty KV (caller handles it)");
   CUtensorMap tq, tk, tv;

@@ -83,8 +83,13 @@ struct AttnLaunch {
   const int* q_exp = nullptr;  // per-head range-guard exponents (StageOp.exps) or null
   const int* k_exp = nullptr;
   const int* v_exp = nullptr;
+  // D != 128 (attention_generic.cu, CUDA cores in f32): operand dtypes F32 / F16 / BF16 each
+  int k_dtype = -1;            // -1: qk_dtype
+  int v_dtype = FUSP_F16;
 };
+// D = 128: the tcgen05 kernels; any other D (a multiple of 8 up to 256): launch_attention_generic.
 fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream);
+fusp_status launch_attention_generic(const AttnLaunch& a, cudaStream_t stream);
 // Workspace the persistent attention kernel needs for a (heads, sq, skv) problem (0 when the
 // q-blocks are scheduled whole).
 size_t attention_workspace_bytes(int heads, int sq, int skv);

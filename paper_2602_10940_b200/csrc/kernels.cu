@@ -794,10 +794,20 @@ __device__ __forceinline__ float stage_dispatch(const StageOp& o, const char* sr
                                                 char* raw, int slab_vecs, float sc) {
   const bool guard = o.exps != nullptr;
   if (o.dst == nullptr) return stage_main<SDT, -1, false, false>(src, raw, nullptr, slab_vecs, sc);
-  if (o.ddt == SDT && !guard) return stage_main<SDT, -1, false, false>(src, dst, nullptr, slab_vecs, sc);
+  if (o.ddt == SDT && !guard) {
+    if (raw != nullptr) return stage_main<SDT, -1, false, true>(src, dst, raw, slab_vecs, sc);
+    return stage_main<SDT, -1, false, false>(src, dst, nullptr, slab_vecs, sc);
+  }
   if (guard) {
     if (raw != nullptr) return stage_main<SDT, FUSP_F16, true, true>(src, dst, raw, slab_vecs, sc);
     return stage_main<SDT, FUSP_F16, true, false>(src, dst, nullptr, slab_vecs, sc);
+  }
+  if (raw != nullptr) {  // e.g. FP8 codes kept exact beside an f32 operand (other head dims)
+    switch (o.ddt) {
+      case FUSP_F16: return stage_main<SDT, FUSP_F16, false, true>(src, dst, raw, slab_vecs, sc);
+      case FUSP_BF16: return stage_main<SDT, FUSP_BF16, false, true>(src, dst, raw, slab_vecs, sc);
+      default: return stage_main<SDT, FUSP_F32, false, true>(src, dst, raw, slab_vecs, sc);
+    }
   }
   switch (o.ddt) {
     case FUSP_F16: return stage_main<SDT, FUSP_F16, false, false>(src, dst, nullptr, slab_vecs, sc);
@@ -874,6 +884,30 @@ __global__ void __launch_bounds__(256) stage_decide_kernel(const __grid_constant
       for (int k = 0; k < 8; ++k) x.f[k] *= f;
       store8(o.dst, o.ddt, dj + int64_t(v) * 8, x);
     }
+  }
+}
+
+// Element-wise staging (any alignment; no range guard): the stage_kernel mapping per element.
+__global__ void stage_scalar_kernel(const __grid_constant__ StageArgs a, int64_t total) {
+  const StageOp& o = a.op[blockIdx.y];
+  const int esz = o.sdt == FUSP_F32 ? 4 : (o.sdt == FUSP_E4M3 ? 1 : 2);
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t slab = e / a.slab_elems, i = e - slab * a.slab_elems;
+    const int j = static_cast<int>(slab / a.bhp), bh = static_cast<int>(slab - int64_t(j) * a.bhp);
+    const int64_t si = int64_t(j) * o.src_slot_stride + int64_t(bh) * o.src_bh_stride + i;
+    const int64_t di = int64_t(j) * o.dst_slot_stride + int64_t(bh) * o.dst_bh_stride + i;
+    if (o.raw != nullptr)
+      for (int b = 0; b < esz; ++b)
+        static_cast<uint8_t*>(o.raw)[di * esz + b] = static_cast<const uint8_t*>(o.src)[si * esz + b];
+    if (o.dst == nullptr) continue;
+    float x;
+    if (o.sdt == FUSP_E4M3)
+      x = __fmul_rn(dec_e4m3(static_cast<const uint8_t*>(o.src)[si]),
+                    o.scales[j * o.scale_stride + bh * o.scale_bh_stride]);
+    else
+      x = load_as_f32(o.src, o.sdt, si);
+    store_from_f32(o.dst, o.ddt, di, x);
   }
 }
 
@@ -1197,24 +1231,40 @@ fusp_status launch_stage(const StageOp* ops, int n, int bhp, int sl, int d, int 
   if (d % 8 != 0 || slabs > 65535 || slab_elems / 8 >= (int64_t(1) << 31))
     return set_error(FUSP_ERR_SHAPE, "stage: unsupported operand shape");
   StageArgs a{};
+  bool vec = true, guarded_any = false;
   for (int i = 0; i < n; ++i) {
     const StageOp& o = ops[i];
     const int64_t esz = int64_t(dtype_size(o.sdt));
-    const bool ok = aligned16(o.src) && (o.src_slot_stride * esz) % 16 == 0 &&
-                    (o.dst == nullptr || aligned16(o.dst)) && (o.raw == nullptr || aligned16(o.raw)) &&
-                    (o.sdt != FUSP_E4M3 || o.scales != nullptr) &&
+    const bool ok = (o.sdt != FUSP_E4M3 || o.scales != nullptr) &&
                     (o.exps == nullptr || (o.words != nullptr && o.dst != nullptr && o.ddt == FUSP_F16)) &&
                     (o.dst == nullptr || o.ddt != FUSP_E4M3);
-    if (!ok) return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: operand not 16-byte aligned or malformed");
+    if (!ok) return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: malformed operand");
     a.op[i] = o;
     StageOp& x = a.op[i];
     if (x.src_bh_stride == 0) x.src_bh_stride = slab_elems;
     if (x.dst_slot_stride == 0) x.dst_slot_stride = slab_elems;
     if (x.dst_bh_stride == 0) x.dst_bh_stride = int64_t(u) * slab_elems;
     const int64_t dsz = x.dst != nullptr ? int64_t(dtype_size(x.ddt)) : esz;
-    if ((x.src_bh_stride * esz) % 16 != 0 || (x.dst_slot_stride * dsz) % 16 != 0 ||
-        (x.dst_bh_stride * dsz) % 16 != 0)
-      return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: strides not 16-byte granular");
+    vec = vec && aligned16(o.src) && (o.dst == nullptr || aligned16(o.dst)) &&
+          (o.raw == nullptr || aligned16(o.raw)) && (x.src_slot_stride * esz) % 16 == 0 &&
+          (x.src_bh_stride * esz) % 16 == 0 && (x.dst_slot_stride * dsz) % 16 == 0 &&
+          (x.dst_bh_stride * dsz) % 16 == 0 &&
+          (x.raw == nullptr || ((x.dst_slot_stride * esz) % 16 == 0 && (x.dst_bh_stride * esz) % 16 == 0));
+    guarded_any = guarded_any || o.exps != nullptr;
+  }
+  if (!vec) {
+    // small head dims (attention_generic.cu) can leave slabs off 16-byte boundaries: an
+    // element-wise pass with the same mapping (never range-guarded: those operands are f32 or
+    // the caller's dtype)
+    if (guarded_any)
+      return set_error(FUSP_ERR_INVALID_ARGUMENT, "stage: range-guarded operand not 16-byte aligned");
+    a.bhp = bhp;
+    a.u = u;
+    a.slab_elems = slab_elems;
+    const int64_t total = slab_elems * slabs;
+    stage_scalar_kernel<<<dim3(static_cast<unsigned>(grid_for(total)), n), kBlock, 0, s>>>(a, total);
+    FUSP_LAUNCHED("stage_scalar_kernel");
+    return FUSP_OK;
   }
   a.bhp = bhp;
   a.u = u;

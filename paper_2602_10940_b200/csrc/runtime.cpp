@@ -339,9 +339,31 @@ fusp_status fusp_attention_with_lse_ex(const void* q, const void* k, const void*
     if (lse) FUSP_CHECK(launch_fill(lse, FUSP_F32, heads * qs.s, -INFINITY, s));
     return FUSP_OK;
   }
-  if (qs.d != 128)
-    return set_error(FUSP_ERR_SHAPE, "attention: head dim D=" + std::to_string(qs.d) +
-                                         " unsupported by the sm_100a kernel (D=128)");
+  if (qs.d != 128) {
+    // other head dims: CUDA cores in f32, reading the caller's operands as they are
+    AttnLaunch g{};
+    g.q = q;
+    g.k = k;
+    g.v = v;
+    g.qk_dtype = qk_dtype;
+    g.k_dtype = qk_dtype;
+    g.v_dtype = v_dtype;
+    g.q_hs = qs.s * qs.d;
+    g.k_hs = skv * qs.d;
+    g.v_hs = skv * qs.d;
+    g.heads = static_cast<int>(heads);
+    g.sq = static_cast<int>(qs.s);
+    g.skv = static_cast<int>(skv);
+    g.d = static_cast<int>(qs.d);
+    g.out = out;
+    g.out_dtype = out_dtype;
+    g.out_chunk = static_cast<int>(qs.s);
+    g.out_hs = qs.s * qs.d;
+    g.out_rs = qs.d;
+    g.lse = lse;
+    g.lse_hs = qs.s;
+    return launch_attention_generic(g, s);
+  }
   const int64_t nkv = heads * skv * qs.d;
   if (heads > 65535 / 1 || qs.s > (int64_t(1) << 30) || skv > (int64_t(1) << 30))
     return set_error(FUSP_ERR_SHAPE, "attention: shape too large " + shape_str(qs));

@@ -231,6 +231,11 @@ struct Layer {
   // significant bits instead of bf16's 8, and the FP8 path's decode(code)*scale values too.
   // Every staging into f16 from a wider-range source is range-guarded (fastusp_internal.h).
   int qk_dt;
+  // operand dtypes of K and V as the attention kernel reads them: qk_dt and f16 on the tcgen05
+  // path (D = 128); for other D (attention_generic.cu, f32 CUDA cores) the caller's dtype, or
+  // f32 for dequantized FP8 chunks -- and no range guard (nothing is staged into f16)
+  int k_op = FUSP_BF16, v_op = FUSP_F16;
+  bool generic = false;
   size_t w_in;  // bytes per element of the caller's dtype = of the wire (non-FP8 Q/K/V, FP8 Q)
   size_t wout;
   Group ug, rg;
@@ -333,9 +338,10 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
     return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": head count H=" +
                                          std::to_string(l.H) + " not divisible by ulysses dimension U=" +
                                          std::to_string(l.U));
-  if (l.D != 128)
+  if (l.D != 128 && (l.D % 8 != 0 || l.D > 256))
     return set_error(FUSP_ERR_SHAPE, std::string(tag(mode)) + ": head dim D=" + std::to_string(l.D) +
-                                         " unsupported by the sm_100a kernel (D=128)");
+                                         " unsupported (D = 128 on tcgen05; other D a multiple of 8 up to 256)");
+  l.generic = l.D != 128;
   l.hp = l.H / l.U;
   l.heads_r = l.B * l.hp;
   l.span = l.U * l.SL;
@@ -346,6 +352,12 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   l.in_dt = in_dt;
   l.k_dt = in_dt;
   l.qk_dt = (in_dt == FUSP_BF16 && !l.fp8) ? FUSP_BF16 : FUSP_F16;
+  l.k_op = l.qk_dt;
+  l.v_op = FUSP_F16;
+  if (l.generic) {
+    l.qk_dt = in_dt;
+    l.k_op = l.v_op = l.fp8 ? FUSP_F32 : in_dt;
+  }
   l.w_in = dtype_size(in_dt);
   l.out_dt = o.out_dtype;
   l.wout = dtype_size(o.out_dtype);
@@ -381,7 +393,9 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
 // attention can read them as they are).
 void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q, const void* k,
            const void* v, void* out) {
-  const size_t C2 = size_t(l.C) * 2;  // one 16-bit operand chunk
+  const size_t CQ = size_t(l.C) * dtype_size(l.qk_dt);  // operand chunks in their dtypes
+  const size_t CK = size_t(l.C) * dtype_size(l.k_op);
+  const size_t CV = size_t(l.C) * dtype_size(l.v_op);
   const size_t C4 = size_t(l.C) * 4;
   const bool uly = l.mode != Mode::kRing;
   const int hr = l.heads_r;
@@ -393,15 +407,15 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
   if (wire) {
     b->send_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
     b->recv_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
-    b->Qr = b->Qr_w = cv.take(C2);
-    b->Kr = b->Kr_w = cv.take(C2);
-    b->Vr = b->Vr_w = cv.take(C2);
+    b->Qr = b->Qr_w = cv.take(CQ);
+    b->Kr = b->Kr_w = cv.take(CK);
+    b->Vr = b->Vr_w = cv.take(CV);
     if (l.fp8) {
       b->Kc = static_cast<uint8_t*>(cv.take(l.C));
       b->Vc = static_cast<uint8_t*>(cv.take(l.C));
     } else if (l.R > 1) {  // the ring forwards the chunk in the wire dtype
-      b->Kw = l.in_dt == l.qk_dt ? b->Kr : cv.take(size_t(l.C) * l.w_in);
-      b->Vw = l.in_dt == FUSP_F16 ? b->Vr : cv.take(size_t(l.C) * l.w_in);
+      b->Kw = l.in_dt == l.k_op ? b->Kr : cv.take(size_t(l.C) * l.w_in);
+      b->Vw = l.in_dt == l.v_op ? b->Vr : cv.take(size_t(l.C) * l.w_in);
     }
   } else {
     // U == 1: no transfer; the operands are the caller's tensors when already in the MMA dtype.
@@ -410,7 +424,7 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
     // MMA dtype when that is the caller's dtype, else an f32 copy that is staged
     if (l.pro_q || l.prepacked) {
       if (l.in_dt == l.qk_dt) {
-        b->Qr = b->Qr_w = cv.take(C2);
+        b->Qr = b->Qr_w = cv.take(CQ);
         b->Qs = b->Qr;
         b->qs_dt = l.qk_dt;
       } else {
@@ -423,14 +437,14 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
     }
     if (b->Qr == nullptr) {
       if (b->qs_dt == l.qk_dt) b->Qr = b->Qs;
-      else b->Qr = b->Qr_w = cv.take(C2);
+      else b->Qr = b->Qr_w = cv.take(CQ);
     }
     // K source likewise (the FP8 path with a K prologue reads the f32 Kpro copy instead)
     if (l.pro_k || l.prepacked) {
-      if (l.in_dt == l.qk_dt) {
-        b->Kr = b->Kr_w = cv.take(C2);
+      if (l.in_dt == l.k_op) {
+        b->Kr = b->Kr_w = cv.take(CK);
         b->Ks_src = b->Kr;
-        b->ks_dt = l.qk_dt;
+        b->ks_dt = l.k_op;
       } else {
         b->Ks_src = b->Ktmp = cv.take(C4);
         b->ks_dt = FUSP_F32;
@@ -440,19 +454,19 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
       b->ks_dt = l.k_dt;
     }
     if (b->Kr == nullptr) {
-      if (b->ks_dt == l.qk_dt && !fq) b->Kr = b->Ks_src;
-      else b->Kr = b->Kr_w = cv.take(C2);
+      if (b->ks_dt == l.k_op && !fq) b->Kr = b->Ks_src;
+      else b->Kr = b->Kr_w = cv.take(CK);
     }
-    if (l.prepacked && l.in_dt != FUSP_F16) {
+    if (l.prepacked && l.in_dt != l.v_op) {
       b->Vs_src = b->Vtmp = cv.take(size_t(l.C) * l.w_in);
     } else if (l.prepacked) {
-      b->Vs_src = b->Vr = b->Vr_w = cv.take(C2);
+      b->Vs_src = b->Vr = b->Vr_w = cv.take(CV);
     } else {
       b->Vs_src = v;
     }
     if (b->Vr == nullptr) {
-      if (l.in_dt == FUSP_F16 && !fq) b->Vr = b->Vs_src;
-      else b->Vr = b->Vr_w = cv.take(C2);
+      if (l.in_dt == l.v_op && !fq) b->Vr = b->Vs_src;
+      else b->Vr = b->Vr_w = cv.take(CV);
     }
     b->Kw = b->Ks_src;
     b->Vw = b->Vs_src;
@@ -473,8 +487,8 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
     if (l.fp8)
       for (int p = 0; p < 2; ++p) b->sw[p] = static_cast<char*>(cv.take(part));
     for (int i = 0; i < 2; ++i) {
-      if (l.fp8 || l.in_dt != l.qk_dt) b->Kd[i] = cv.take(C2);
-      if (l.fp8 || l.in_dt != FUSP_F16) b->Vd[i] = cv.take(C2);
+      if (l.fp8 || l.in_dt != l.k_op) b->Kd[i] = cv.take(CK);
+      if (l.fp8 || l.in_dt != l.v_op) b->Vd[i] = cv.take(CV);
     }
     b->acc_o = static_cast<float*>(cv.take(C4));
     b->acc_lse = static_cast<float*>(cv.take(size_t(l.heads_r) * l.span * 4));
@@ -491,15 +505,18 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
   }
 }
 
-// A range-guarded f16 staging op (fastusp_internal.h).
-StageOp guarded_op(const void* src, int sdt, void* dst, int* exps, uint32_t* words) {
+// A staging op into the operand dtype `ddt`, range-guarded when that is f16 and the source has
+// a wider range (fastusp_internal.h).
+StageOp staged_op(const void* src, int sdt, void* dst, int ddt, int* exps, uint32_t* words) {
   StageOp o{};
   o.src = src;
   o.sdt = sdt;
   o.dst = dst;
-  o.ddt = FUSP_F16;
-  o.exps = exps;
-  o.words = words;
+  o.ddt = ddt;
+  if (ddt == FUSP_F16 && sdt != FUSP_F16) {
+    o.exps = exps;
+    o.words = words;
+  }
   return o;
 }
 
@@ -525,8 +542,8 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     StageOp ops[3];
     int n = 0;
     if (b.Qr_w != nullptr && b.Qr != b.Qs) {
-      ops[n++] = guarded_op(b.Qs, b.qs_dt, b.Qr_w, b.exps, b.stage_w[0]);
-      b.q_exp = b.exps;
+      ops[n++] = staged_op(b.Qs, b.qs_dt, b.Qr_w, l.qk_dt, b.exps, b.stage_w[0]);
+      b.q_exp = ops[n - 1].exps;
     }
     if (uly && l.fp8) {
       // quantize the whole local K and V (protocols.cpp:139-142; or per (b,h) slab), and the
@@ -539,14 +556,13 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       uint8_t* cds[2] = {b.Kc, b.Vc};
       FUSP_CHECK(launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, s));
       for (int p = 0; p < 2; ++p) {
-        StageOp o = guarded_op(cds[p], FUSP_E4M3, p == 0 ? b.Kr_w : b.Vr_w, b.exps + (1 + p) * hr,
-                               b.stage_w[1 + p]);
+        StageOp o = staged_op(cds[p], FUSP_E4M3, p == 0 ? b.Kr_w : b.Vr_w, p == 0 ? l.k_op : l.v_op,
+                              b.exps + (1 + p) * hr, b.stage_w[1 + p]);
         o.scales = scs[p];
         o.scale_bh_stride = l.fp8_block ? 1 : 0;
         ops[n++] = o;
+        (p == 0 ? b.k_exp : b.v_exp) = o.exps;
       }
-      b.k_exp = b.exps + hr;
-      b.v_exp = b.exps + 2 * hr;
       b.Ks = b.qscale;
       b.Vs = b.qscale + l.nsc_local;
       b.s_stride = 0;
@@ -554,12 +570,12 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       b.seg_rows = l.span;
     } else {
       if (b.Kr_w != nullptr && b.Kr != b.Ks_src) {
-        ops[n++] = guarded_op(b.Ks_src, b.ks_dt, b.Kr_w, b.exps + hr, b.stage_w[1]);
-        b.k_exp = b.exps + hr;
+        ops[n++] = staged_op(b.Ks_src, b.ks_dt, b.Kr_w, l.k_op, b.exps + hr, b.stage_w[1]);
+        b.k_exp = ops[n - 1].exps;
       }
       if (b.Vr_w != nullptr && b.Vr != b.Vs_src) {
-        ops[n++] = guarded_op(b.Vs_src, l.in_dt, b.Vr_w, b.exps + 2 * hr, b.stage_w[2]);
-        b.v_exp = b.exps + 2 * hr;
+        ops[n++] = staged_op(b.Vs_src, l.in_dt, b.Vr_w, l.v_op, b.exps + 2 * hr, b.stage_w[2]);
+        b.v_exp = ops[n - 1].exps;
       }
     }
     return launch_stage(ops, n, hr, l.span, l.D, 1, s);
@@ -657,29 +673,17 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     }
     return launch_stage(ops, 3, hr, l.SL, l.D, l.U, s);
   }
-  StageOp oq{};
-  oq.src = b.recv_in;
-  oq.sdt = l.in_dt;
+  StageOp oq = staged_op(b.recv_in, l.in_dt, b.Qr_w, l.qk_dt, b.exps, b.stage_w[0]);
   oq.src_slot_stride = sew;
-  oq.dst = b.Qr_w;
-  oq.ddt = l.qk_dt;
-  if (l.in_dt != l.qk_dt) {
-    oq.exps = b.exps;
-    oq.words = b.stage_w[0];
-    b.q_exp = b.exps;
-  }
+  b.q_exp = oq.exps;
   ops[0] = oq;
   if (!l.fp8) {
     for (int p = 0; p < 2; ++p) {
-      StageOp o{};
-      o.src = b.recv_in + (p == 0 ? l.off_k : l.off_v);
-      o.sdt = l.in_dt;
+      StageOp o = staged_op(b.recv_in + (p == 0 ? l.off_k : l.off_v), l.in_dt,
+                            p == 0 ? b.Kr_w : b.Vr_w, p == 0 ? l.k_op : l.v_op,
+                            b.exps + (1 + p) * hr, b.stage_w[1 + p]);
       o.src_slot_stride = sew;
-      o.dst = p == 0 ? b.Kr_w : b.Vr_w;
-      o.ddt = p == 0 ? l.qk_dt : FUSP_F16;
-      if (o.ddt != l.in_dt) {  // range-guarded, and the wire-dtype copy the ring forwards
-        o.exps = b.exps + (1 + p) * hr;
-        o.words = b.stage_w[1 + p];
+      if (o.ddt != l.in_dt) {  // staged (range-guarded into f16): the ring forwards the wire copy
         o.raw = l.R > 1 ? const_cast<void*>(p == 0 ? b.Kw : b.Vw) : nullptr;
         (p == 0 ? b.k_exp : b.v_exp) = o.exps;
       }
@@ -689,17 +693,17 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
   }
   const float* scales = reinterpret_cast<const float*>(b.recv_in + l.off_tr);
   for (int p = 0; p < 2; ++p) {
-    StageOp o = guarded_op(b.recv_in + (p == 0 ? l.off_k : l.off_v), FUSP_E4M3,
-                           p == 0 ? b.Kr_w : b.Vr_w, b.exps + (1 + p) * hr, b.stage_w[1 + p]);
+    StageOp o = staged_op(b.recv_in + (p == 0 ? l.off_k : l.off_v), FUSP_E4M3,
+                          p == 0 ? b.Kr_w : b.Vr_w, p == 0 ? l.k_op : l.v_op,
+                          b.exps + (1 + p) * hr, b.stage_w[1 + p]);
     o.src_slot_stride = int64_t(l.slot_stride);
     o.scales = scales + p * l.nsc_slot;
     o.scale_stride = int64_t(l.slot_stride / 4);
     o.scale_bh_stride = l.fp8_block ? 1 : 0;
     o.raw = p == 0 ? static_cast<void*>(b.Kc) : static_cast<void*>(b.Vc);  // exact codes
     ops[1 + p] = o;
+    (p == 0 ? b.k_exp : b.v_exp) = o.exps;
   }
-  b.k_exp = b.exps + hr;
-  b.v_exp = b.exps + 2 * hr;
   FUSP_CHECK(launch_stage(ops, 3, hr, l.SL, l.D, l.U, s));
   b.Ks = scales;
   b.Vs = scales + l.nsc_slot;
@@ -720,6 +724,8 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
   a.split_counters = b.attn_cnt;
   a.split_counter_words = b.attn_cnt_words;
   a.qk_dtype = l.qk_dt;
+  a.k_dtype = l.k_op;
+  a.v_dtype = l.v_op;
   a.q = b.Qr;
   a.k = K;
   a.v = V;
@@ -860,8 +866,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     for (int p = 0; p < 2; ++p) {
       void* dst = p == 0 ? b.Kd[into] : b.Vd[into];
       if (dst == nullptr) continue;  // the chunk is already the MMA operand
-      StageOp o = guarded_op(b.rb[into][p], l.fp8 ? FUSP_E4M3 : l.in_dt, dst,
-                             b.exps + (3 + 2 * into + p) * hr, b.ring_w[into][p]);
+      StageOp o = staged_op(b.rb[into][p], l.fp8 ? FUSP_E4M3 : l.in_dt, dst, p == 0 ? l.k_op : l.v_op,
+                            b.exps + (3 + 2 * into + p) * hr, b.ring_w[into][p]);
       if (l.fp8) {
         o.scales = reinterpret_cast<const float*>(b.rb[into][p] + l.C);
         o.scale_bh_stride = l.fp8_block ? 1 : 0;
@@ -874,8 +880,8 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     const int buf = hop % 2;
     *K = b.Kd[buf] ? b.Kd[buf] : b.rb[buf][0];
     *V = b.Vd[buf] ? b.Vd[buf] : b.rb[buf][1];
-    *ke = b.Kd[buf] ? b.exps + (3 + 2 * buf) * hr : nullptr;
-    *ve = b.Vd[buf] ? b.exps + (4 + 2 * buf) * hr : nullptr;
+    *ke = b.Kd[buf] && l.k_op == FUSP_F16 ? b.exps + (3 + 2 * buf) * hr : nullptr;  // guarded
+    *ve = b.Vd[buf] && l.v_op == FUSP_F16 ? b.exps + (4 + 2 * buf) * hr : nullptr;
   };
 
   if (!l.pipelined) {
@@ -1015,6 +1021,7 @@ fusp_status plan_prologue(fusp_ctx_s* c, const fusp_qk_prologue* p, Layer* L) {
   Layer& l = *L;
   if (!p) return FUSP_OK;
   FUSP_CHECK(validate_prologue(p));
+  if (l.D != 128) return set_error(FUSP_ERR_SHAPE, "qk prologue: head dim must be 128");
   const bool rope = p->rope_cos != nullptr;
   l.pos0 = p->rope_pos0 < 0 ? int64_t(c->rank) * l.SL : p->rope_pos0;
   if (rope && (p->rope_rows < l.pos0 + l.SL))
