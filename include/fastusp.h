@@ -61,7 +61,9 @@ const char* fusp_version(void);
 /* Number of fastusp CUDA kernels launched so far by this process (all devices). */
 uint64_t fusp_kernel_launch_count(void);
 /* Tuning knob (no reference counterpart): attention work schedule, 0 = auto, 1 = whole
- * 256-row q-blocks per CTA, 2 = stream-K split of (q-block x KV tile) units over the SMs;
+ * 256-row q-blocks per CTA, 2 = stream-K split of (q-block x KV tile) units over the SMs,
+ * 3 = aligned split (equal KV segments per q-block), 4 = KV-split CTAs (whole 128-row Q tiles,
+ * the two softmax warpgroups splitting the KV range; auto picks it for one-wave shapes);
  * max_ctas caps the persistent grid (0 = every SM; leave SMs free for concurrent NCCL). */
 fusp_status fusp_attention_schedule(int mode, int max_ctas);
 /* Debug timeline (no reference counterpart): enable != 0 records per-CTA globaltimer events
@@ -102,7 +104,8 @@ fusp_status fusp_dequantize_e4m3(const uint8_t* codes, const float* scale_dev, i
 
 /* ---- single-GPU attention numerics (tensor.hpp:91-98) ----------------------------------- */
 /* attention_with_lse (tensor.cpp:193-202): q [B,H,Sq,D], k,v [B,H,Skv,D], all `in_dtype`
- * (F32/BF16/F16; computed as bf16 Q.K^T and f16 P.V with f32 accumulation).
+ * (F32/BF16/F16; Q.K^T in bf16 for bf16 inputs, f16 otherwise, P.V in f16, f32 accumulation;
+ * every f16 staging range-guarded per head by an exact power of two).
  * out [B,H,Sq,D] in out_dtype; lse [B,H,Sq] f32 natural log (nullable). Skv = 0 gives
  * out = 0, lse = -inf (tensor.cpp:161-164).  D = 128 runs on the tcgen05 kernel; any other D
  * that is a multiple of 8 (up to 256) on an f32 CUDA-core kernel (the protocols below too). */
