@@ -63,7 +63,8 @@ uint64_t fusp_kernel_launch_count(void);
 /* Tuning knob (no reference counterpart): attention work schedule, 0 = auto, 1 = whole
  * 256-row q-blocks per CTA, 2 = stream-K split of (q-block x KV tile) units over the SMs,
  * 3 = aligned split (equal KV segments per q-block), 4 = KV-split CTAs (whole 128-row Q tiles,
- * the two softmax warpgroups splitting the KV range; auto picks it for one-wave shapes);
+ * the two softmax warpgroups splitting the KV range; auto picks it for one-wave shapes),
+ * 5 = KV-split CTAs with stream-K over the 128-row tiles (every SM busy);
  * max_ctas caps the persistent grid (0 = every SM; leave SMs free for concurrent NCCL). */
 fusp_status fusp_attention_schedule(int mode, int max_ctas);
 /* Debug timeline (no reference counterpart): enable != 0 records per-CTA globaltimer events

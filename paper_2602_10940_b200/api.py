@@ -199,7 +199,7 @@ def stage_f16(x: torch.Tensor):
     return y, exps
 
 
-_SCHEDULES = {"auto": 0, "whole": 1, "split": 2, "aligned": 3, "kv2": 4}
+_SCHEDULES = {"auto": 0, "whole": 1, "split": 2, "aligned": 3, "kv2": 4, "kv2split": 5}
 
 
 @contextlib.contextmanager

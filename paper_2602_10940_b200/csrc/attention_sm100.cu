@@ -165,6 +165,26 @@ __device__ __forceinline__ int sk_cta_of(const Sched& s, int u) {
   while (c + 1 < static_cast<int>(gridDim.x) && s.begin[c + 1] <= u) ++c;
   return c;
 }
+// ctaid / nctaid read through volatile asm: values derived from them at a tile's end are
+// not hoisted out of the KV loop (where they would hold registers across the softmax)
+__device__ __forceinline__ int cta_id_v() {
+  int v;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ int n_cta_v() {
+  int v;
+  asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ int sk_cta_of_v(const Sched& s, int u) {
+  const int g = n_cta_v();
+  int c = static_cast<int>(static_cast<float>(u) * g / static_cast<float>(s.total));
+  c = c < 0 ? 0 : (c >= g ? g - 1 : c);
+  while (c > 0 && s.begin[c] > u) --c;
+  while (c + 1 < g && s.begin[c + 1] <= u) ++c;
+  return c;
+}
 struct Seg {
   int qb, j0, j1;
 };
@@ -199,6 +219,14 @@ __device__ __forceinline__ float* seg_slot(const Params& p, int c, int qb, int t
   const int which = qb == first_qb ? 0 : 1;
   return p.slots + (static_cast<size_t>(c) * 2 + which) * (2 * kSlotTileFloats) +
          static_cast<size_t>(t) * kSlotTileFloats;
+}
+
+// Slot of segment k of a tile whose segments start at CTA c_first: segments k >= 1 are their
+// CTAs' first (slot 0); segment 0 is CTA c_first's first only when that CTA's range starts
+// inside the tile (which0 = 0), else its last (slot 1).
+__device__ __forceinline__ float* tile_slot(float* slots, int c_first, int which0, int k) {
+  const int which = k == 0 ? which0 : 0;
+  return slots + (static_cast<size_t>(c_first + k) * 2 + which) * (2 * kSlotTileFloats);
 }
 
 // The 128 threads of softmax warpgroup t.  bar.sync counts a diverged warp once per divergent
@@ -915,6 +943,7 @@ struct __align__(1024) SmemKv2 {
   uint64_t s_full[2], p_full[2], o_done[2];
   uint64_t s_read[2], p_half[2];
   uint32_t tmem_base;
+  uint32_t ticket;  // stream-K: the tile's arrival count seen by this CTA
 };
 
 // Named barrier over the 8 softmax warps (ids 1, 2 are the per-warpgroup ones).
@@ -923,6 +952,7 @@ __device__ __forceinline__ void softmax_bar() {
   asm volatile("bar.sync 3, 256;" ::: "memory");
 }
 
+template <bool kSplit>  // kSplit: stream-K segments over the tiles (sc.split == 1)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_kv2_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -932,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             ~uintptr_t(1023));
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const Sched& sc = p.sc;  // whole Q tiles: qb = tile index, sc.split == 0
+  const Sched& sc = p.sc;  // qb = 128-row tile index; stream-K unit ranges when kSplit
 
   if (warp == 0 && lane == 0) {
     mbar_init(&sm.q_full, 1);
@@ -961,6 +991,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   if (tmem != 0u) __trap();
+  if (threadIdx.x == 0) FUSP_TRACE(p, 0);
   if (warp < 4) {
     reg_dealloc<FUSP_PRODUCER_REGS>();
     if (warp == 0) {
@@ -1123,8 +1154,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t_o0 = kTmemO + lane_off;  // chain 0's O (chain 1's at +128)
     SegIter si(sc);
     Seg g;
-    uint32_t c = 0, nd[2] = {0, 0};
+    uint32_t c = 0, nd = 0;  // bit u: o_done[u] phase
+    int seg_no = 0;  // debug trace: per-segment events at slots 2 + 8 seg + e (8 segments)
+    const bool tr = threadIdx.x == 128;
     while (si.next(sc, g)) {
+      const int tslot = 2 + 8 * (seg_no < 8 ? seg_no : 7);
+      ++seg_no;
       const int head = g.qb / sc.qb_per_head;
       const int e_qk = (p.q_exp != nullptr ? p.q_exp[head] : 0) + (p.k_exp != nullptr ? p.k_exp[head] : 0);
       const float sl2 = p.scale_log2 * __int_as_float((127 + e_qk) << 23);
@@ -1139,6 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int j = g.j0 + 2 * i + t;
         mbar_wait(&sm.s_full[t], c & 1);
         tc_fence_after();
+        if (tr && i == 0) FUSP_TRACE(p, tslot + 0);
         uint32_t s[128];
         tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
@@ -1207,10 +1243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sm.p_full[t]);
       }
       // ---------------- tile end: both chains' MMAs complete, then merge ----------------
+      if (tr) FUSP_TRACE(p, tslot + 1);
       for (int u = 0; u < 2; ++u) {
         if (nc[u] == 0) continue;
-        mbar_wait(&sm.o_done[u], nd[u] & 1);
-        ++nd[u];
+        mbar_wait(&sm.o_done[u], (nd >> u) & 1);
+        nd ^= 1u << u;
       }
       tc_fence_after();
       // (m, l) exchange through the Q tile's shared memory: nothing reads Q any more (every
@@ -1221,13 +1258,150 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 o_ml = ml[(1 - t) * kBM + r_in_tile];
       softmax_bar();
       if (r_in_tile == 0) mbar_arrive(&sm.q_empty);
+      if (tr) FUSP_TRACE(p, tslot + 2);
       const float m0 = t == 0 ? m_use : o_ml.x, l0 = t == 0 ? l_sum : o_ml.y;
       const float m1 = t == 0 ? o_ml.x : m_use, l1 = t == 0 ? o_ml.y : l_sum;
       const bool has1 = nc[1] > 0;
-      const float m_fin = has1 ? fmaxf(m0, m1) : m0;
-      const float w0 = ex2((m0 - m_fin) * sl2);
-      const float w1 = has1 ? ex2((m1 - m_fin) * sl2) : 0.f;
-      const float l_fin = w0 * l0 + w1 * l1;
+      const float m_self = has1 ? fmaxf(m0, m1) : m0;
+      const float w0 = ex2((m0 - m_self) * sl2);
+      const float w1 = has1 ? ex2((m1 - m_self) * sl2) : 0.f;
+      const float l_self = w0 * l0 + w1 * l1;
+      // this CTA's part of the tile, columns [32 cc, 32 cc + 32): X = w0 O0 + w1 O1 (frame m_self)
+      auto self_chunk = [&](int cc, float (&v)[32], float a0, float a1, bool h1) {
+        uint32_t o[32];
+        tmem_ld32(t_o0 + cc * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = a0 * __uint_as_float(o[q]);
+        if (h1) {  // (warp-uniform: the tile's chain count)
+          tmem_ld32(t_o0 + 128 + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = fmaf(a1, __uint_as_float(o[q]), v[q]);
+        }
+      };
+      // Stream-K over whole tiles (sc.split): the tile's key range may be cut into segments
+      // owned by consecutive CTAs.  Same publish-then-count protocol as attn_fwd_kernel, one
+      // ticket per tile: every segment but the finisher stores X and (m_self, l_self) to its
+      // slot and counts; the segment that brings the count to nseg merges all of them in
+      // segment order (its own X from TMEM, bit-equal to what it would have stored), so the
+      // result does not depend on which CTA finishes.  The tile's first segment (processed last
+      // by its CTA) checks the count first and skips publishing when it is already the last.
+      int nseg = 1, kself = 0, c_first = 0, which0 = 0;
+      if (kSplit) {
+        const int u0 = g.qb * sc.n_kv;
+        c_first = sk_cta_of_v(sc, u0);
+        nseg = sk_cta_of_v(sc, u0 + sc.n_kv - 1) - c_first + 1;
+        kself = cta_id_v() - c_first;
+        which0 = sc.begin[c_first] >= u0 ? 0 : 1;
+      }
+      float m_fin = m_self, l_fin = l_self;
+      float e_w0 = w0, e_w1 = w1;  // epilogue weights of O0 / O1
+      bool e_has1 = has1;
+      if (nseg > 1) {
+        uint32_t* cnt = p.counters + static_cast<size_t>(g.qb) * 2;
+        bool last = false;
+        if (kself == 0) {
+          if (threadIdx.x == 128) sm.ticket = ld_acquire(cnt);
+          softmax_bar();
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket) + 1 == static_cast<uint32_t>(nseg);
+          softmax_bar();  // every thread read the ticket before it is rewritten
+        }
+        if (!last) {
+          float* slot = tile_slot(p.slots, c_first, which0, kself);
+#pragma unroll 1
+          for (int cc = 2 * t; cc < 2 * t + 2; ++cc) {
+            float v[32];
+            self_chunk(cc, v, w0, w1, has1);
+            float4* q4 = reinterpret_cast<float4*>(slot) + (cc * 8) * kBM + r_in_tile;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              __stcg(q4 + i * kBM, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+          }
+          if (t == 0) {
+            __stcg(slot + kD * kBM + r_in_tile, m_self);
+            __stcg(slot + kD * kBM + kBM + r_in_tile, l_self);
+          }
+          if (tr) FUSP_TRACE(p, tslot + 3);
+          softmax_bar();  // every slot store happens-before thread 128's release
+          if (threadIdx.x == 128) sm.ticket = atom_add_acq_rel(cnt, 1u);
+          softmax_bar();
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket) + 1 == static_cast<uint32_t>(nseg);
+          if (!last) {
+            if (tr) FUSP_TRACE(p, tslot + 6);
+            // both chains' O were read before the next tile's P.V overwrites them
+            tc_fence_before();
+            softmax_bar();
+            continue;
+          }
+        }
+        if (tr) FUSP_TRACE(p, tslot + 4);
+        if (threadIdx.x == 128) *cnt = 0u;  // every segment has counted: zero for the next launch
+        m_fin = -INFINITY;
+        for (int k = 0; k < nseg; ++k) {
+          const float mk = k == kself ? m_self : __ldcg(tile_slot(p.slots, c_first, which0, k) + kD * kBM + r_in_tile);
+          m_fin = fmaxf(m_fin, mk);
+        }
+        l_fin = 0.f;
+        for (int k = 0; k < nseg; ++k) {
+          const float* sl = tile_slot(p.slots, c_first, which0, k);
+          const float mk = k == kself ? m_self : __ldcg(sl + kD * kBM + r_in_tile);
+          const float lk = k == kself ? l_self : __ldcg(sl + kD * kBM + kBM + r_in_tile);
+          l_fin = fmaf(ex2((mk - m_fin) * sl2), lk, l_fin);
+        }
+        // merged O (frame m_fin) over this warpgroup's columns, back into O0's TMEM columns:
+        // the epilogue below then reads it with weights (1, -)
+#pragma unroll 1
+        for (int cc = 2 * t; cc < 2 * t + 2; ++cc) {
+          float v[32];
+#pragma unroll 1
+          for (int k = 0; k < nseg; ++k) {
+            const float* sl = tile_slot(p.slots, c_first, which0, k);
+            const float mk = k == kself ? m_self : __ldcg(sl + kD * kBM + r_in_tile);
+            const float wk = ex2((mk - m_fin) * sl2);
+            // 16 columns at a time (register pressure here spills the KV loop's state)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              float x[16];
+              if (k == kself) {  // X_self exactly as self_chunk computes (and publishes) it
+                uint32_t o[16];
+                tmem_ld16(t_o0 + cc * 32 + hh * 16, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 16; ++q) x[q] = w0 * __uint_as_float(o[q]);
+                if (has1) {
+                  tmem_ld16(t_o0 + 128 + cc * 32 + hh * 16, o);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) x[q] = fmaf(w1, __uint_as_float(o[q]), x[q]);
+                }
+              } else {
+                const float4* x4 = reinterpret_cast<const float4*>(sl) + (cc * 8 + hh * 4) * kBM + r_in_tile;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float4 y = __ldcg(x4 + i * kBM);
+                  x[4 * i] = y.x; x[4 * i + 1] = y.y; x[4 * i + 2] = y.z; x[4 * i + 3] = y.w;
+                }
+              }
+              if (k == 0) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[hh * 16 + q] = wk * x[q];
+              } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[hh * 16 + q] = fmaf(wk, x[q], v[hh * 16 + q]);
+              }
+            }
+          }
+          uint32_t vo[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) vo[q] = __float_as_uint(v[q]);
+          tmem_st32(t_o0 + cc * 32, vo);
+        }
+        tmem_wait_st();
+        e_w0 = 1.f;
+        e_has1 = false;
+        if (tr) FUSP_TRACE(p, tslot + 5);
+      }
       const bool in_range = row < p.sq;
       const float lse_b = m_fin * (sl2 * 0.69314718055994530942f) + logf(l_fin);
       const float inv_l = 1.f / l_fin;
@@ -1252,18 +1426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // warpgroup t finishes columns [64 t, 64 t + 64): O = (w0 O0 + w1 O1) / l
 #pragma unroll 1
       for (int cc = 2 * t; cc < 2 * t + 2; ++cc) {
-        uint32_t o[32];
         float v[32];
-        tmem_ld32(t_o0 + cc * 32, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = w0 * __uint_as_float(o[q]);
-        if (has1) {  // (warp-uniform: the tile's chain count)
-          tmem_ld32(t_o0 + 128 + cc * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = fmaf(w1, __uint_as_float(o[q]), v[q]);
-        }
+        self_chunk(cc, v, e_w0, e_w1, e_has1);
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] *= scale_new;
         if (acc_h != nullptr) {
@@ -1317,6 +1481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t == 0 && in_range && p.lse != nullptr)
         p.lse[static_cast<int64_t>(head) * p.lse_hs + static_cast<int64_t>(row / p.out_chunk) * p.lse_cs +
               row % p.out_chunk] = lse_out;
+      if (tr) FUSP_TRACE(p, tslot + 6);
       // both chains' O have been read before either chain's next-tile P.V can overwrite them
       tc_fence_before();
       softmax_bar();
@@ -1325,6 +1490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 128) FUSP_TRACE(p, 1);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -1383,6 +1549,23 @@ Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
   // fill most of one wave; mode 4 forces it.
   {
     const int tiles = heads * ((sq + kBM - 1) / kBM);
+    const int64_t units = static_cast<int64_t>(tiles) * pl.sc.n_kv;
+    // KV-split CTAs with stream-K over whole tiles: every SM busy, at least 4 KV tiles per
+    // CTA (two per chain); mode 5 forces it
+    if (g_sched_mode == 5 && have_ws && pl.sc.n_kv >= 2 && units < (int64_t(1) << 31)) {
+      Plan k{};
+      k.kv2 = 1;
+      k.sc.n_kv = pl.sc.n_kv;
+      k.sc.qb_per_head = (sq + kBM - 1) / kBM;
+      k.sc.n_qb = tiles;
+      k.sc.split = 1;
+      k.sc.total = static_cast<int>(units);
+      const int g = k.sc.total / 4;
+      k.grid = g < sms ? (g > 0 ? g : 1) : sms;
+      for (int c = 0; c <= k.grid; ++c)
+        k.sc.begin[c] = static_cast<int>(static_cast<int64_t>(c) * k.sc.total / k.grid);
+      return k;
+    }
     const bool fits = tiles <= sms && pl.sc.n_kv >= 4;
     const bool auto_kv2 = split && g_sched_mode == 0 && fits && 10 * tiles >= 6 * sms;
     if ((g_sched_mode == 4 && fits) || auto_kv2) {
@@ -1480,10 +1663,16 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
     p.counters = a.split_counters;
     p.slots = static_cast<float*>(a.split_ws);
   }
+  if (g_trace_on) {
+    if (g_trace == nullptr) FUSP_CUDA(cudaMalloc(&g_trace, sizeof(unsigned long long) * kMaxGrid * kTraceSlots));
+    FUSP_CUDA(cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * kMaxGrid * kTraceSlots, stream));
+    p.trace = g_trace;
+  }
   if (pl.kv2) {
     const int smem2 = static_cast<int>(sizeof(SmemKv2)) + 1024;
-    FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(attn_kv2_kernel), smem2, "attn_kv2_kernel"));
-    attn_kv2_kernel<<<pl.grid, kThreads, smem2, stream>>>(tq, tk, tv, p);
+    auto* kern = pl.sc.split ? attn_kv2_kernel<true> : attn_kv2_kernel<false>;
+    FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem2, "attn_kv2_kernel"));
+    kern<<<pl.grid, kThreads, smem2, stream>>>(tq, tk, tv, p);
     count_launch();
     cudaError_t e2 = cudaGetLastError();
     if (e2 != cudaSuccess) return set_cuda_error(e2, "attn_kv2_kernel launch");
@@ -1491,11 +1680,6 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   }
   const int smem = static_cast<int>(sizeof(Smem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel), smem, "attn_fwd_kernel"));
-  if (g_trace_on) {
-    if (g_trace == nullptr) FUSP_CUDA(cudaMalloc(&g_trace, sizeof(unsigned long long) * kMaxGrid * kTraceSlots));
-    FUSP_CUDA(cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * kMaxGrid * kTraceSlots, stream));
-    p.trace = g_trace;
-  }
   attn_fwd_kernel<<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
   count_launch();
   cudaError_t e = cudaGetLastError();

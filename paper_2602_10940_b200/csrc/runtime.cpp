@@ -201,8 +201,8 @@ fusp_status fusp_out_projection(const void* o, fusp_dtype o_dtype, fusp_shape4 o
 
 fusp_status fusp_attention_schedule(int mode, int max_ctas) {
   clear_error();
-  if (mode < 0 || mode > 4 || max_ctas < 0)
-    return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention schedule: mode in {0,1,2,3,4}, max_ctas >= 0");
+  if (mode < 0 || mode > 5 || max_ctas < 0)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention schedule: mode in {0,...,5}, max_ctas >= 0");
   set_attention_schedule(mode, max_ctas);
   return FUSP_OK;
 }

@@ -1,6 +1,6 @@
 """Interleaved A/B timing of attention-kernel variants in ONE process (each variant .so loaded
 with RTLD_LOCAL), so clock/thermal drift hits every variant alike.
-usage: python tools/ab_attn.py VAR[:mode] VAR[:mode] ...   (VAR 'main' = lib/libfastusp.so)"""
+usage: python tools/ab_attn.py VAR[:mode[:max_ctas]] ...   (VAR 'main' = lib/libfastusp.so)"""
 import ctypes, json, os, statistics, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import torch
@@ -18,7 +18,9 @@ class Shape4(ctypes.Structure):
 
 
 def load(spec):
-    name, _, mode = spec.partition(":")
+    name, _, rest = spec.partition(":")
+    mode, _, ctas = rest.partition(":")
+    ctas = int(ctas) if ctas else 0
     path = os.path.join(PKG, "lib" if name == "main" else f"variants/{name}", "libfastusp.so")
     L = ctypes.CDLL(path)
     f = L.fusp_attention_with_lse_ex
@@ -27,13 +29,13 @@ def load(spec):
                                                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
     if hasattr(L, "fusp_attention_schedule"):
         L.fusp_attention_schedule.argtypes = [ctypes.c_int, ctypes.c_int]
-        L.fusp_attention_schedule(int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4}.get(mode, 0)), 0)
-    mode_id = int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4}.get(mode, 0))
+        L.fusp_attention_schedule(int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4, "kv2split": 5}.get(mode, 0)), ctas)
+    mode_id = int({"whole": 1, "split": 2, "aligned": 3, "kv2": 4, "kv2split": 5}.get(mode, 0))
     sched = getattr(L, "fusp_attention_schedule", None)
 
     def fn(*a):  # the schedule knob is process-global per library: set it before every call
         if sched is not None:
-            sched(mode_id, 0)
+            sched(mode_id, ctas)
         return f(*a)
     return spec, fn
 

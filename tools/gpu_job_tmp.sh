@@ -1,3 +1,7 @@
-timeout 300 python tools/kv2_check.py > gpurun_out/kv2_check.jsonl 2>&1
-SHAPES=flux_u8 timeout 300 python tools/ab_attn.py main:split latek:kv2 main:kv2 k3v3e:kv2 latek:kv2 main:kv2 > gpurun_out/ab_kv2e.jsonl 2>&1
-grep kv2 gpurun_out/kv2_check.jsonl | cut -c1-150; cat gpurun_out/ab_kv2e.jsonl
+# scratch GPU job: kv2 stream-K trace
+mkdir -p gpurun_out
+bash tools/build_variants.sh trace:-DFUSP_TRACE_BUILD=1 > gpurun_out/tmp_build.log 2>&1
+for cfg in "kv2split 0" "kv2split 120" "kv2split 108" "kv2 0"; do
+  echo "== $cfg"; FUSP_VARIANT=trace timeout 120 python tools/attn_trace_kv2.py 3 4608 $cfg
+done > gpurun_out/tmp_trace.log 2>&1
+cat gpurun_out/tmp_trace.log

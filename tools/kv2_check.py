@@ -11,13 +11,13 @@ def rel(a, b):
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
-for heads, sq, skv in [(3, 512, 640), (2, 200, 300), (3, 4608, 4608), (1, 128, 128), (2, 384, 1000), (5, 256, 129)]:
+for heads, sq, skv in [(3, 512, 640), (2, 200, 300), (3, 4608, 4608), (1, 128, 128), (2, 384, 1000), (5, 256, 129), (6, 4608, 4608), (24, 4608, 4608), (3, 4224, 4224)]:
     g = torch.Generator().manual_seed(heads * 7 + sq)
     q = torch.empty(1, heads, sq, 128).uniform_(-1, 1, generator=g).bfloat16()
     k = torch.empty(1, heads, skv, 128).uniform_(-1, 1, generator=g).bfloat16()
     v = torch.empty(1, heads, skv, 128).uniform_(-1, 1, generator=g).bfloat16()
     acc = {}
-    for mode in ("auto", "kv2"):
+    for mode in ("auto", "kv2", "kv2split"):
         with fu.attention_schedule(mode):
             r = fu.attention_with_lse(q.cuda(), k.cuda(), v.cuda())
         torch.cuda.synchronize()

@@ -18,11 +18,11 @@ import paper_2602_10940_b200 as fu  # noqa: E402
 def attention():
     q = torch.randn(1, 3, 640, 128, device="cuda", dtype=torch.bfloat16)
     k, v = torch.randn_like(q), torch.randn_like(q).half()
-    for mode in ("whole", "split", "kv2"):
+    for mode in ("whole", "split", "kv2", "kv2split"):
         with fu.attention_schedule(mode):
             fu.attention_with_lse(q, k, v, out_dtype=torch.float16)
     torch.cuda.synchronize()
-    print("attention whole+split+kv2 ok", flush=True)
+    print("attention whole+split+kv2+kv2split ok", flush=True)
 
 
 def staging():
