@@ -8,7 +8,9 @@ A step is one USP attention layer (Ulysses all-to-all -> ring attention -> Ulyss
 all-to-all) over FLUX-shaped synthetic tensors, B=1 S=4608 H=24 D=128, bf16 in, f16 out,
 U=N R=1 by default (BASELINE configs[1]); total work is fixed as N grows (strong scaling).
 `value` = whole-job TFLOP/s = 4*B*H*S^2*D / (max over ranks of the device time per step).
-L2 (126 MB) is flushed between timed steps by a 256 MiB write outside the per-step events.
+L2 (126 MB) is flushed between timed steps outside the per-step events: a 256 MiB write, then a
+256 MiB read, so the step starts with none of its inputs in L2 and no dirty flush lines left to
+write back (a write-only flush leaves ~126 MB of dirty lines whose write-back the next step pays).
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref, the
 uspsim library compiled from the reference sources) on this host's cores instead.
@@ -285,6 +287,11 @@ def run_fastusp(args):
                           out_dtype=torch.float16, check_finite=False)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+    flush_rd = torch.ones(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+
+    def flush_l2(i):
+        flush.fill_(float(i))  # evicts everything (leaves dirty lines) ...
+        flush_rd.sum()         # ... whose write-back this read pays, outside the step events
 
     def barrier():
         if n > 1:
@@ -313,7 +320,7 @@ def run_fastusp(args):
         barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
-            flush.fill_(float(i))
+            flush_l2(i)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -339,7 +346,7 @@ def run_fastusp(args):
         # context's per-step CUDA events around each attention launch on the compute stream
         inl = []
         for i in range(args.steps):
-            flush.fill_(float(i))
+            flush_l2(i)
             fu.usp_attention(ctx, q, k, v, mesh, opts)
             stream.synchronize()
             comp, _ = ctx.ring_timings()
@@ -375,7 +382,7 @@ def run_fastusp(args):
                        "mesh": {"ulysses": n // r, "ring": r}, "parallelism": f"usp_u{n // r}_r{r}",
                        "fp8_kv": bool(args.fp8), "pipelined_ring": not args.serial,
                        "cuda_graph": bool(args.graph), "out_dtype": "f16",
-                       "l2": "flushed between steps (256 MiB write outside the step events)",
+                       "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)",
                        "flop_per_layer": flop},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,

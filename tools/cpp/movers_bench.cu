@@ -5,6 +5,7 @@
 //   make -C tools/cpp && tools/cpp/movers_bench
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <functional>
 #include "../../paper_2602_10940_b200/csrc/fastusp_internal.h"
@@ -19,18 +20,21 @@ static double peak = 6548.5;
 static void report(const char* name, double bytes, const std::function<void()>& f) {
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int i = 0; i < 3; ++i) f();
+  // MOVERS_ONCE=1: one warm-up and one timed call (for ncu: every kernel captured once)
+  static const bool once = getenv("MOVERS_ONCE") != nullptr;
+  for (int i = 0; i < (once ? 1 : 3); ++i) f();
   cudaDeviceSynchronize();
-  const int reps = 50;
+  const int reps = once ? 1 : 50;
   cudaEventRecord(a);
   for (int i = 0; i < reps; ++i) f();
   cudaEventRecord(b); cudaEventSynchronize(b);
   float hot; cudaEventElapsedTime(&hot, a, b); hot /= reps;
   float cold = 0;
-  for (int i = 0; i < 10; ++i) {
+  const int creps = once ? 1 : 10;
+  for (int i = 0; i < creps; ++i) {
     cudaMemsetAsync(flushbuf, i, 256u << 20);
     cudaEventRecord(a); f(); cudaEventRecord(b); cudaEventSynchronize(b);
-    float t; cudaEventElapsedTime(&t, a, b); cold += t / 10;
+    float t; cudaEventElapsedTime(&t, a, b); cold += t / creps;
   }
   printf("{\"kernel\": \"%s\", \"bytes\": %.0f, \"hot_us\": %.2f, \"hot_gbs\": %.0f, \"cold_us\": %.2f, \"cold_gbs\": %.0f, \"cold_frac_of_hbm\": %.3f}\n",
          name, bytes, hot * 1e3, bytes / (hot * 1e-3) / 1e9, cold * 1e3, bytes / (cold * 1e-3) / 1e9,
