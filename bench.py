@@ -255,6 +255,8 @@ def run_fastusp(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:  # bound every device-side wait of the peer self-check (read once by the lib)
+        os.environ.setdefault("FUSP_TIMEOUT_S", "30")
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE",
               file=sys.stderr)
@@ -286,6 +288,10 @@ def run_fastusp(args):
     opts = fu.CommOptions(fp8_kv=args.fp8, pipelined_ring=not args.serial,
                           out_dtype=torch.float16, check_finite=False)
     stream = torch.cuda.Stream(device=dev)
+    transport = "nccl" if n > 1 else "local (world 1)"
+    if n > 1 and args.peer != "off":
+        with torch.cuda.stream(stream):
+            transport = setup_peer(fu, ctx, dist, dev, q, k, v, mesh, opts, n, r, args)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
     flush_rd = torch.ones(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
 
@@ -382,6 +388,7 @@ def run_fastusp(args):
                        "mesh": {"ulysses": n // r, "ring": r}, "parallelism": f"usp_u{n // r}_r{r}",
                        "fp8_kv": bool(args.fp8), "pipelined_ring": not args.serial,
                        "cuda_graph": bool(args.graph), "out_dtype": "f16",
+                       "ulysses_transport": transport,
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)",
                        "flop_per_layer": flop},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -394,6 +401,49 @@ def run_fastusp(args):
     if n > 1:
         dist.destroy_process_group()
     return 0
+
+
+def setup_peer(fu, ctx, dist, dev, q, k, v, mesh, opts, n, r, args):
+    """Peer-memory Ulysses transport for N > 1 (fusp_ctx_peer_*): windows created locally,
+    handles all-gathered over torch.distributed, mapped (CUDA IPC); then a self-check layer
+    must match the NCCL layer bit for bit on every rank, else every rank falls back to NCCL.
+    Returns the transport description for the JSON line."""
+    import torch
+
+    def agree(ok: bool) -> bool:
+        t = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    ref = fu.usp_attention(ctx, q, k, v, mesh, opts).clone()
+    torch.cuda.current_stream().synchronize()
+    why = ""
+    try:
+        wb = fu.peer_window_bytes(n, r, tuple(q.shape), q.dtype, opts)
+        h = ctx.peer_window(wb)
+        ok = True
+    except Exception as e:  # noqa: BLE001 -- reported, NCCL stays the transport
+        ok, why = False, f"window: {e}"
+    if not agree(ok):
+        return f"nccl (peer windows unavailable{': ' + why if why else ''})"
+    handles = [None] * n
+    dist.all_gather_object(handles, h)
+    try:
+        ctx.peer_open(handles)
+        got = fu.usp_attention(ctx, q, k, v, mesh, opts).clone()
+        ctx.synchronize()
+        ok = torch.equal(got, ref) and ctx.peer_stats()[0] >= 1
+        if not ok:
+            why = "self-check mismatch"
+    except Exception as e:  # noqa: BLE001
+        ok, why = False, f"self-check: {e}"
+    if agree(ok):
+        return "peer-memory (pack / attention-epilogue stores into NVLink-mapped windows)"
+    try:
+        ctx.disable_peer_memory()
+    except Exception:  # noqa: BLE001
+        pass
+    return f"nccl (peer path rejected: {why or 'another rank failed'})"
 
 
 def graph_kernel_count(fu, ctx, q, k, v, mesh, opts):
@@ -527,6 +577,9 @@ def main():
     ap.add_argument("--ref-seq", type=int, default=1536,
                     help="tokens per head of the reference CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--peer", choices=["auto", "off"], default="auto",
+                    help="N > 1: Ulysses reshards through peer-memory windows (self-checked "
+                         "against NCCL, falls back to it) or NCCL only")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

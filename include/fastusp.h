@@ -181,6 +181,37 @@ fusp_status fusp_ctx_debug_wire_get(fusp_ctx ctx, int index, int* kind, int* rou
 fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms, float* comm_ms,
                                   int* steps);
 
+/* ---- peer-memory Ulysses transport (no reference counterpart: B200 / NVSwitch) ----------------
+ * The reference moves the Ulysses payloads through its fabric (all_to_all, fabric.cpp:199-226);
+ * with peer windows enabled, the two Ulysses reshards of usp_attention / ulysses_attention
+ * (protocols.cpp:125-203) are fused into the kernels around them: the pack kernel stores every
+ * member's slot straight into that member's window and the attention epilogue stores O (and the
+ * LSE) rows straight into their owner's window, over NVLink / NVSwitch, each followed by one tiny
+ * signal-and-wait kernel.  Results and TrafficLog bytes are identical to the comm path; the ring
+ * (R > 1) still uses the context's backend.  Windows serve one Ulysses group per context (the
+ * first layer's); other layers (other groups, the QK prologue / producer variants, D != 128,
+ * wire debugging, shapes larger than a window) fall back to the backend -- counted by
+ * fusp_ctx_peer_stats.  A peer-path layer at ring_dim 1 needs no host rendezvous, so it is
+ * graph-capturable on any context.
+ * fusp_ctx_peer_enable is collective over the world: every rank allocates `window_bytes` of
+ * device memory (fusp_peer_window_bytes sizes it for a layer), the 128-byte handles are
+ * all-gathered through the context's own backend and mapped (CUDA IPC between processes of one
+ * node; the pointer itself between threads of one process). */
+#define FUSP_PEER_HANDLE_BYTES 128
+fusp_status fusp_ctx_peer_enable(fusp_ctx ctx, size_t window_bytes);
+/* The same in two steps for callers with their own bootstrap: create this rank's window and
+ * its handle; then map the world's handles (world x FUSP_PEER_HANDLE_BYTES, rank order). */
+fusp_status fusp_ctx_peer_window(fusp_ctx ctx, size_t window_bytes, void* handle_out);
+fusp_status fusp_ctx_peer_open(fusp_ctx ctx, const void* handles);
+/* Window bytes one layer needs on every member (world ranks, mesh make_mesh(world, ring_dim)). */
+fusp_status fusp_peer_window_bytes(int world, int ring_dim, fusp_dtype in_dtype, fusp_shape4 local_shape,
+                                   const fusp_comm_options* opts, size_t* bytes);
+/* Drop the windows (waits for the context's device work): later layers use the backend again.
+ * Collective in effect: every rank of a group must agree on the transport of each layer. */
+fusp_status fusp_ctx_peer_disable(fusp_ctx ctx);
+/* Layers whose Ulysses reshards used the windows / fell back to the backend since enabling. */
+fusp_status fusp_ctx_peer_stats(fusp_ctx ctx, uint64_t* layers, uint64_t* fallbacks);
+
 /* ---- distributed protocols (protocols.hpp:47-71) ------------------------------------------ */
 /* usp_attention (protocols.cpp:321-340) on mesh make_mesh(world, ring_dim).
  * q,k,v: local shards [B,H,S/N,D] (in_dtype F32/BF16/F16); out: [B,H,S/N,D] in opts->out_dtype. */

@@ -13,6 +13,6 @@ from .api import (AttnResult, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGr
                   ring_attention_pipelined, ring_attention_serial, run_protocol, split_sequence,
                   ulysses_attention, usp_attention, usp_attention_host, out_projection,
                   usp_attention_proj, usp_block, usp_attention_with_lse, Resharded, detail, stage_f16, kFp8Max, kFp8MaxCode,
-                  kFp8NanCode)
+                  kFp8NanCode, peer_window_bytes)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -158,6 +158,13 @@ _SIGS = {
     "fusp_graph_capture_usp": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                               _P, ctypes.POINTER(CommOptions), ctypes.c_int, _I64,
                                               _I64, _P, _P]),
+    "fusp_ctx_peer_enable": (ctypes.c_int, [_P, ctypes.c_size_t]),
+    "fusp_ctx_peer_window": (ctypes.c_int, [_P, ctypes.c_size_t, _P]),
+    "fusp_ctx_peer_open": (ctypes.c_int, [_P, _P]),
+    "fusp_peer_window_bytes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, Shape4,
+                                              ctypes.POINTER(CommOptions), _P]),
+    "fusp_ctx_peer_stats": (ctypes.c_int, [_P, _P, _P]),
+    "fusp_ctx_peer_disable": (ctypes.c_int, [_P]),
     "fusp_graph_launch": (ctypes.c_int, [_P, _P]),
     "fusp_graph_destroy": (ctypes.c_int, [_P]),
 }

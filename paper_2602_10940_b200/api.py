@@ -425,6 +425,34 @@ class WorkerContext:
             out.append((kind.value, rnd.value, buf))
         return out
 
+    def enable_peer_memory(self, window_bytes: int):
+        """fusp_ctx_peer_enable (collective over the world): the Ulysses reshards of later
+        layers are fused into the pack kernel and the attention epilogue, which store straight
+        into the members' windows (NVLink / NVSwitch peer memory); see fastusp.h."""
+        check(lib().fusp_ctx_peer_enable(self.handle, int(window_bytes)))
+
+    def peer_window(self, window_bytes: int) -> bytes:
+        """Two-step form (own bootstrap): create this rank's window, return its handle."""
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib().fusp_ctx_peer_window(self.handle, int(window_bytes), buf))
+        return bytes(buf)
+
+    def peer_open(self, handles) -> None:
+        """Map the world's window handles (rank order) created by peer_window."""
+        blob = b"".join(handles)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(lib().fusp_ctx_peer_open(self.handle, buf))
+
+    def disable_peer_memory(self) -> None:
+        """fusp_ctx_peer_disable: back to the backend transport (every rank of a group)."""
+        check(lib().fusp_ctx_peer_disable(self.handle))
+
+    def peer_stats(self):
+        """(layers on the peer path, layers that fell back to the backend) since enabling."""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().fusp_ctx_peer_stats(self.handle, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def synchronize(self, stream=None, timeout_s: float = 0.0):
         """fusp_ctx_synchronize: bounded host wait; a stalled / failed peer raises
         DeadlockError (the NCCL communicators are aborted) instead of hanging."""
@@ -444,6 +472,17 @@ class WorkerContext:
                 lib().fusp_group_destroy(h)
             lib().fusp_ctx_destroy(self.handle)
             self.handle = None
+
+
+def peer_window_bytes(world: int, ring_dim: int, local_shape, dtype=torch.bfloat16,
+                      opts: Optional["CommOptions"] = None) -> int:
+    """fusp_peer_window_bytes: window bytes a USP layer of this local shape [B,H,S/N,D] needs
+    on every member."""
+    o = opts or CommOptions()
+    n = ctypes.c_size_t()
+    check(lib().fusp_peer_window_bytes(world, ring_dim, _DT[dtype], Shape4(*local_shape),
+                                       ctypes.byref(o._c()), ctypes.byref(n)))
+    return n.value
 
 
 @dataclass

@@ -23,6 +23,7 @@ class HardwareProfile:
     """SPEC.md:373-376.  Defaults: one B200 on an NVSwitch node."""
     link_bandwidth: float = 770e9       # B/s per direction per GPU (measured peer copy)
     link_latency: float = 6e-6          # s per NCCL group call (launch + handshake)
+    peer_signal: float = 2e-6           # s per peer-window signal-and-wait kernel (fused path)
     launch_overhead: float = 4e-6       # s per kernel launch, eager
     graph_residual: float = 0.05        # fraction of launch cost left under graph replay
     element_width: int = 2              # bytes per Q/K/V element on the wire (bf16/f16)
@@ -135,17 +136,40 @@ def attention_seconds(hw: HardwareProfile, b: int, heads: int, s_q: int, s_kv: i
     return flop / (hw.attn_tflops(flop) * 1e12)
 
 
+def attention_waves(hw: HardwareProfile, b: int, heads: int, s_q: int, sms: int = 148) -> float:
+    """Waves of output tiles the per-rank attention launch stores: 256-row q-blocks on the
+    persistent kernel, whole 128-row tiles on the KV-split kernel when they fit one wave."""
+    tiles128 = b * heads * -(-s_q // 128)
+    if tiles128 <= sms:
+        return 1.0
+    return b * heads * -(-s_q // 256) / sms
+
+
 def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipelined: bool = True,
-                 compiled: bool = True, fp8: bool = False) -> LatencyBreakdown:
+                 compiled: bool = True, fp8: bool = False, peer: bool = False,
+                 out_width: Optional[int] = None) -> LatencyBreakdown:
     """SPEC.md:407-414 per denoising step: attention compute split over the mesh, Ulysses
-    all-to-alls exposed, ring transfers through pipeline_timeline, launch term."""
+    all-to-alls exposed, ring transfers through pipeline_timeline, launch term.
+
+    peer=True models the peer-memory transport (csrc/peer.cu): the input reshard is the pack
+    kernel's own stores into the members' windows (its bytes at link bandwidth plus one
+    signal kernel, no NCCL group call), and the output reshard is the attention epilogue's
+    stores -- overlapped with the compute of later tiles except for the last wave's."""
     if n % r or w.H % (n // r) or w.S % n:
         raise ValueError(f"infeasible mesh N={n} R={r} for H={w.H}, S={w.S}")
     u = n // r
     hp, span = w.H // u, w.S // r
     step_compute = attention_seconds(hw, w.B, hp, span, span, w.D)  # one ring step per rank
-    a2a = comm_volume_ulysses(w, u, hw.element_width, fp8, n=n) / hw.link_bandwidth
-    a2a += (2 * hw.link_latency) if u > 1 else 0.0
+    ow = hw.element_width if out_width is None else out_width
+    if peer and u > 1:
+        total = comm_volume_ulysses(w, u, hw.element_width, fp8, out_width=ow, n=n)
+        out_b = (u - 1) * w.B * hp * (w.S // n) * w.D * ow
+        waves = attention_waves(hw, w.B, hp, span)
+        a2a = (total - out_b) / hw.link_bandwidth + hw.peer_signal
+        a2a += out_b / hw.link_bandwidth / max(waves, 1.0) + hw.peer_signal
+    else:
+        a2a = comm_volume_ulysses(w, u, hw.element_width, fp8, out_width=ow, n=n) / hw.link_bandwidth
+        a2a += (2 * hw.link_latency) if u > 1 else 0.0
     per_round_comm = (comm_volume_ring(w, r, u, hw.element_width, fp8) / max(r - 1, 1)
                       / hw.link_bandwidth + hw.link_latency) if r > 1 else 0.0
     tl = pipeline_timeline(step_compute, per_round_comm, r)

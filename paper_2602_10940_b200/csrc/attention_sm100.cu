@@ -122,6 +122,11 @@ struct Params {
   float* lse;        // [heads][lse_hs] natural-log LSE or null
   int64_t lse_hs;
   int64_t lse_cs;    // floats between output chunks (the output all-to-all slots), like out_cs
+  // Peer-memory output reshard (usp.cpp, PeerWindow): chunk t of the rows is stored straight
+  // into Ulysses member t's window over NVLink; its element offset relative to `out` / `lse`
+  // (one unified address space) replaces t * out_cs / t * lse_cs.  0 chunks: the strided form.
+  int peer_chunks;
+  int64_t out_coff[kMaxPeerChunks], lse_coff[kMaxPeerChunks];
   const float* acc_o;    // fp32 [heads][sq][D] running accumulator or null
   const float* acc_lse;  // [heads][sq]
   const int* q_exp;      // per-head f16 range-guard exponents of the operands (null = 0)
@@ -132,6 +137,12 @@ struct Params {
   float* slots;          // split: [gridDim.x][2 (first/last segment)][2 tiles][kSlotTileFloats]
   unsigned long long* trace;  // optional per-CTA globaltimer events (attention_trace), or null
 };
+__device__ __forceinline__ int64_t out_chunk_off(const Params& p, int t) {
+  return p.peer_chunks ? p.out_coff[t] : static_cast<int64_t>(t) * p.out_cs;
+}
+__device__ __forceinline__ int64_t lse_chunk_off(const Params& p, int t) {
+  return p.peer_chunks ? p.lse_coff[t] : static_cast<int64_t>(t) * p.lse_cs;
+}
 // per CTA (SM cycles): start, end, [4 segments][2 tiles][8 events], 70: end (warp 4); then
 // [2 tiles][64 KV steps of the first segment][S ready, P published]
 constexpr int kTraceSlots = 72 + 2 * 64 * 2;
@@ -820,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float scale_new = c_new * inv_l * v_scale;
       const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
-                            static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
+                            out_chunk_off(p, row / p.out_chunk) +
                             static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
       // O leaves (and the ring accumulator comes in) through accesses where the 4 lanes of a
       // group cover one row's contiguous 32-column chunk: row addresses of the group's 4 rows
@@ -892,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (FUSP_TRACE_EPI && tr) FUSP_TRACE(p, tslot + 4);
       if (in_range && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(head) * p.lse_hs + static_cast<int64_t>(row / p.out_chunk) * p.lse_cs +
+        p.lse[static_cast<int64_t>(head) * p.lse_hs + lse_chunk_off(p, row / p.out_chunk) +
               row % p.out_chunk] = lse_out;
       if (tr) FUSP_TRACE(p, tslot + 7);
       tc_fence_before();
@@ -902,6 +913,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // bar.sync counts a diverged warp once per divergent arrival: reconverge first, or the
   // producer warps (lane 0 vs 1..31) would release the barrier before the softmax warps finish.
   __syncwarp();
+  // peer-memory output: every store this thread made to another GPU's window is visible
+  // system-wide before the exchange kernel that follows signals it
+  if (p.peer_chunks) __threadfence_system();
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) FUSP_TRACE(p, 1);
@@ -1412,7 +1426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float scale_new = c_new * inv_l * v_scale;
       const int64_t obase = static_cast<int64_t>(head) * p.out_hs +
-                            static_cast<int64_t>(row / p.out_chunk) * p.out_cs +
+                            out_chunk_off(p, row / p.out_chunk) +
                             static_cast<int64_t>(row % p.out_chunk) * p.out_rs;
       const int e4 = lane & 3;
       int64_t ob_g[4];
@@ -1479,7 +1493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (t == 0 && in_range && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(head) * p.lse_hs + static_cast<int64_t>(row / p.out_chunk) * p.lse_cs +
+        p.lse[static_cast<int64_t>(head) * p.lse_hs + lse_chunk_off(p, row / p.out_chunk) +
               row % p.out_chunk] = lse_out;
       if (tr) FUSP_TRACE(p, tslot + 6);
       // both chains' O have been read before either chain's next-tile P.V can overwrite them
@@ -1488,6 +1502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncwarp();
+  if (p.peer_chunks) __threadfence_system();  // as attn_fwd_kernel
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 128) FUSP_TRACE(p, 1);
@@ -1634,6 +1649,22 @@ fusp_status launch_attention(const AttnLaunch& a, cudaStream_t stream) {
   p.lse = a.lse;
   p.lse_hs = a.lse_hs;
   p.lse_cs = a.lse_cs;
+  if (a.peer_chunks > 0) {
+    if (a.peer_chunks > kMaxPeerChunks || (p.sq + p.out_chunk - 1) / p.out_chunk > a.peer_chunks)
+      return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention: peer chunk table too small");
+    p.peer_chunks = a.peer_chunks;
+    const int64_t esz = a.out_dtype == FUSP_F32 ? 4 : 2;
+    for (int t = 0; t < a.peer_chunks; ++t) {
+      const int64_t d = reinterpret_cast<const char*>(a.out_peer[t]) - static_cast<const char*>(a.out);
+      if (d % esz != 0) return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention: misaligned peer chunk");
+      p.out_coff[t] = d / esz;
+      if (a.lse != nullptr) {
+        const int64_t dl = reinterpret_cast<const char*>(a.lse_peer[t]) - reinterpret_cast<const char*>(a.lse);
+        if (dl % 4 != 0) return set_error(FUSP_ERR_INVALID_ARGUMENT, "attention: misaligned peer LSE chunk");
+        p.lse_coff[t] = dl / 4;
+      }
+    }
+  }
   p.acc_o = a.acc_o;
   p.acc_lse = a.acc_lse;
   p.q_exp = a.q_exp;
@@ -1701,19 +1732,18 @@ size_t attention_counter_words(int heads, int sq) {
   return static_cast<size_t>(heads) * ((sq + kQB - 1) / kQB) * 4;
 }
 
-fusp_status ensure_counters(CounterBuf& b, size_t words) {
+fusp_status ensure_counters(CounterBuf& b, size_t words, cudaStream_t s) {
   int dev = 0;
   FUSP_CUDA(cudaGetDevice(&dev));
   if (b.ptr != nullptr && b.words >= words && b.device == dev) return FUSP_OK;
   if (b.ptr != nullptr) {
-    FUSP_CUDA(cudaDeviceSynchronize());
-    FUSP_CUDA(cudaFree(b.ptr));
+    FUSP_CUDA(cudaFreeAsync(b.ptr, s));
     b.ptr = nullptr;
     b.words = 0;
   }
   const size_t n = words < 4096 ? 4096 : words;
-  FUSP_CUDA(cudaMalloc(&b.ptr, n * 4));
-  FUSP_CUDA(cudaMemset(b.ptr, 0, n * 4));
+  FUSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.ptr), n * 4, s));
+  FUSP_CUDA(cudaMemsetAsync(b.ptr, 0, n * 4, s));
   b.words = n;
   b.device = dev;
   return FUSP_OK;

@@ -2,6 +2,7 @@
 #include "comm.h"
 
 #include <algorithm>
+#include <cstring>
 #include <chrono>
 #include <sstream>
 #include <thread>
@@ -101,6 +102,34 @@ fusp_status LocalComm::exchange(const Group& g, const char* op, std::vector<cons
   // Peers finished reading my buffers at their done events: later writes wait for them.
   for (int j = 0; j < n; ++j)
     if (j != g.pos) FUSP_CUDA(cudaStreamWaitEvent(s, posts[j].done, 0));
+  return FUSP_OK;
+}
+
+fusp_status LocalComm::allgather_host(const void* mine, size_t bytes, void* all) {
+  const int n = fabric_->world;
+  std::unique_lock<std::mutex> lk(fabric_->mu);
+  const std::string key = "allgather_host";
+  auto& seqv = fabric_->seq[key];
+  if (seqv.empty()) seqv.assign(static_cast<size_t>(n), 0);
+  const uint64_t seq = seqv[rank_]++;
+  auto& slot = fabric_->slots[{key, seq}];
+  if (slot.posts.empty()) slot.posts.resize(static_cast<size_t>(n));
+  slot.posts[rank_].sends = {mine};
+  slot.arrived++;
+  fabric_->cv.notify_all();
+  const auto deadline = std::chrono::steady_clock::now() +
+                        std::chrono::milliseconds(static_cast<int64_t>(fabric_->timeout_s * 1000));
+  if (!fabric_->cv.wait_until(lk, deadline, [&] { return slot.arrived == n; }))
+    return set_error(FUSP_ERR_DEADLOCK, "deadlock: rank " + std::to_string(rank_) +
+                                            " stalled in allgather (" + std::to_string(slot.arrived) +
+                                            "/" + std::to_string(n) + " arrived)");
+  for (int j = 0; j < n; ++j)  // host memory of the posting threads, still alive: they wait below
+    std::memcpy(static_cast<char*>(all) + size_t(j) * bytes, slot.posts[j].sends[0], bytes);
+  slot.done_arrived++;
+  fabric_->cv.notify_all();
+  if (!fabric_->cv.wait_until(lk, deadline, [&] { return slot.done_arrived == n; }))
+    return set_error(FUSP_ERR_DEADLOCK, "deadlock: rank " + std::to_string(rank_) + " stalled in allgather");
+  if (++slot.left == n) fabric_->slots.erase({key, seq});
   return FUSP_OK;
 }
 
@@ -259,6 +288,44 @@ fusp_status NcclComm::all_to_all(const Group& g, const void* send, void* recv, s
   }
   FUSP_NCCL(ncclGroupEnd());
   return check_async("all_to_all", g);
+}
+
+// Grouped point-to-point to and from every rank (what ncclAllGather does; send/recv keeps the
+// set of NCCL calls fastusp makes small).  Setup only: synchronous.
+fusp_status NcclComm::allgather_host(const void* mine, size_t bytes, void* all) {
+  if (aborted_) return set_error(FUSP_ERR_COMM, "NCCL communicators were aborted after a failure");
+  // Stream-ordered buffer and copies: no device-wide wait (ranks sharing a GPU may already have
+  // peer-exchange kernels spinning on it for work this rank enqueues next).
+  char* dev = nullptr;
+  cudaStream_t s = nullptr;
+  FUSP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  FUSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dev), bytes * size_t(nranks_), s));
+  fusp_status st = FUSP_OK;
+  auto run = [&]() -> fusp_status {
+    FUSP_CUDA(cudaMemcpyAsync(dev + size_t(rank_) * bytes, mine, bytes, cudaMemcpyHostToDevice, s));
+    if (nranks_ > 1) {
+      FUSP_NCCL(ncclGroupStart());
+      for (int j = 0; j < nranks_; ++j) {
+        if (j == rank_) continue;
+        FUSP_NCCL(ncclSend(dev + size_t(rank_) * bytes, bytes, ncclUint8, j, world_, s));
+        FUSP_NCCL(ncclRecv(dev + size_t(j) * bytes, bytes, ncclUint8, j, world_, s));
+      }
+      FUSP_NCCL(ncclGroupEnd());
+      Group w;
+      for (int j = 0; j < nranks_; ++j) w.members.push_back(j);
+      w.pos = rank_;
+      FUSP_CHECK(check_async("allgather", w));
+      FUSP_CHECK(wait(s, 120.0, "allgather"));
+    }
+    FUSP_CUDA(cudaMemcpyAsync(all, dev, bytes * size_t(nranks_), cudaMemcpyDeviceToHost, s));
+    FUSP_CUDA(cudaStreamSynchronize(s));
+    return FUSP_OK;
+  };
+  st = run();
+  cudaFreeAsync(dev, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return st;
 }
 
 fusp_status NcclComm::ring_exchange(const Group& g, const void* const* send, void* const* recv,

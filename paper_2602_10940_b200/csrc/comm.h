@@ -51,6 +51,9 @@ class Comm {
   virtual fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                                     const size_t* bytes, int nparts, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;
+  // Host all-gather of `bytes` per rank over the whole world (blocking; setup only): rank r's
+  // `mine` lands at all + r * bytes on every rank.
+  virtual fusp_status allgather_host(const void* mine, size_t bytes, void* all) = 0;
   // Host wait until `s` drained, bounded by timeout_s: a stalled or failed peer becomes
   // FUSP_ERR_DEADLOCK (the reference's DeadlockError, fabric.hpp:112-116) instead of a hang.
   virtual fusp_status wait(cudaStream_t s, double timeout_s, const char* what);
@@ -91,6 +94,7 @@ class LocalComm : public Comm {
   fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                             const size_t* bytes, int nparts, cudaStream_t s) override;
   bool capturable() const override { return fabric_->world == 1; }
+  fusp_status allgather_host(const void* mine, size_t bytes, void* all) override;
 
  private:
   // Generic pull-based exchange: for every peer j in `srcs`, copy the chunk at
@@ -119,6 +123,7 @@ class NcclComm : public Comm {
   fusp_status ring_exchange(const Group& g, const void* const* send, void* const* recv,
                             const size_t* bytes, int nparts, cudaStream_t s) override;
   bool capturable() const override { return true; }
+  fusp_status allgather_host(const void* mine, size_t bytes, void* all) override;
   // FUSP_NCCL_SMS overrides; 8 covers the p2p channels NCCL uses for one send/recv pair.
   int sms_in_flight() const override {
     static const int n = [] {
@@ -150,5 +155,42 @@ class NcclComm : public Comm {
 };
 
 fusp_status nccl_error(ncclResult_t r, const std::string& where);
+
+// ---- peer-memory windows (peer.cu) --------------------------------------------------------
+// One device window per rank, mapped by every rank of the world (one node): a 4 KB control
+// block of uint32 words -- [0][src] input-reshard signals, [1][src] output-reshard signals,
+// [2][src] / [3][src] completed waits per source, [4][0] timeout flag; src = world rank -- and
+// the data region the Ulysses receive slots live in.
+constexpr int kPeerMaxWorld = 64;
+constexpr size_t kPeerCtlBytes = 4096;
+constexpr uint64_t kPeerMagic = 0x46555350504545ull;  // "FUSPPEE"
+struct PeerHandle {  // FUSP_PEER_HANDLE_BYTES on the wire
+  uint64_t magic;
+  int32_t pid, device;
+  uint64_t ptr, bytes;
+  cudaIpcMemHandle_t ipc;
+  uint8_t pad[128 - 32 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(PeerHandle) == 128, "peer handle is 128 bytes");
+struct PeerWindow {
+  int device = -1, rank = 0, world = 0;
+  char* base = nullptr;       // my window: control block + data
+  size_t data_bytes = 0;
+  std::vector<char*> peer;    // world rank -> that rank's window in my address space
+  std::vector<bool> opened;   // mapped with cudaIpcOpenMemHandle (closed on destruction)
+  std::vector<uint64_t> bytes_of;  // data bytes of every rank's window
+  std::string group;          // the one Ulysses group the peer path serves (usp.cpp)
+  ~PeerWindow();
+  char* data(int r) const { return peer[r] + kPeerCtlBytes; }
+  uint32_t* ctl(int r) const { return reinterpret_cast<uint32_t*>(peer[r]); }
+};
+fusp_status peer_window_create(PeerWindow* w, int rank, int world, int device, size_t data_bytes,
+                               PeerHandle* mine);
+fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all);
+// kind 0: input reshard, 1: output reshard.  Signals every other member of g, then waits
+// until each has signalled me once more than before (timeout -> the flag peer_window_check reads).
+fusp_status launch_peer_exchange(const PeerWindow& w, int kind, const Group& g, double timeout_s,
+                                 cudaStream_t s);
+fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_t s);
 
 }  // namespace fusp

@@ -59,6 +59,7 @@ fusp_status launch_qkv_proj(const void* x, int x_dtype, int b, int s, int c, con
                             cudaStream_t stream);
 
 // ---- attention kernel -----------------------------------------------------------------
+constexpr int kMaxPeerChunks = 16;  // Ulysses members a kernel stores into directly (NVLink domain)
 struct AttnLaunch {
   const void* q;  // bf16|f16 [heads][sq][128], head stride q_hs elements
   const void* k;  // bf16|f16 [heads][skv][128]
@@ -73,6 +74,12 @@ struct AttnLaunch {
   float* lse;
   int64_t lse_hs;
   int64_t lse_cs = 0;  // floats between output chunks (LSE riding the output all-to-all)
+  // Peer-memory output reshard: chunk t (rows [t*out_chunk, ...)) is written at out_peer[t]
+  // (+ head * out_hs + row % out_chunk * out_rs) -- Ulysses member t's window, mapped here --
+  // instead of out + t * out_cs; LSE likewise at lse_peer[t].  0: the strided form.
+  int peer_chunks = 0;
+  void* out_peer[kMaxPeerChunks] = {};
+  float* lse_peer[kMaxPeerChunks] = {};
   const float* acc_o;    // merge into (acc_o, acc_lse) when non-null
   const float* acc_lse;
   void* split_ws;        // stream-K partial slots (attention_workspace_bytes)
@@ -106,7 +113,11 @@ struct CounterBuf {
   size_t words = 0;
   int device = -1;
 };
-fusp_status ensure_counters(CounterBuf& b, size_t words);
+// Growth is stream-ordered on `s` (cudaFreeAsync / cudaMallocAsync / cudaMemsetAsync): never a
+// device-wide wait -- with peer windows, ranks sharing a GPU have exchange kernels spinning on
+// it for work another rank's thread has not enqueued yet.  The caller guarantees the old buffer's
+// users are ordered before `s`.
+fusp_status ensure_counters(CounterBuf& b, size_t words, cudaStream_t s = nullptr);
 
 // ---- elementwise / data-movement kernels (kernels.cu) -----------------------------------
 fusp_status launch_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,
@@ -142,7 +153,12 @@ struct PackDesc {
 };
 fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
 // Up to 6 packs / unpacks with one launch (same B, H, SL, D, U; else one launch each).
-fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s);
+// pdl: launched as a programmatic dependent of the previous kernel (the FP8 amax pass): only
+// the E4M3 operands wait for it (griddepcontrol.wait), plain copies run alongside.
+// peer_slot_boff (peer-memory Ulysses): slot t is peer_slot_boff[t] bytes from slot 0 (member
+// t's window) instead of t * dst_slot_stride; every CTA fences system-wide before it exits.
+fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s, bool pdl = false,
+                              const int64_t* peer_slot_boff = nullptr);
 // Fused QK RMSNorm (w != null) + interleaved RoPE (cosv != null, rows pos0 + s) + pack into
 // slot t = h / (H/u) at t * slot_stride elements (u = 1: plain [B][H][SL][D] output).
 // One operand of a batched prologue pack (w / cos / sin null = that step skipped).
@@ -241,11 +257,18 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
                                uint32_t* work, uint32_t* nonfinite, cudaStream_t s);
 fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_elems,
                                    const float* scales, uint8_t* codes, cudaStream_t s);
-// amax + scales + codes in one call; `work` holds >= nblocks words.
+// amax + scales + codes in one call; `work` holds >= nblocks + 1 ZERO words (left zero).
 fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elems, uint32_t* work,
                                 float* scales, uint8_t* codes, uint32_t* nonfinite,
                                 cudaStream_t s);
-// K and V (parts = 2) quantized with one amax launch and one quantize launch.
+// Pass 1 of the quantizer for 1-2 sources (K, V) in one launch: per-block amax into the ZERO
+// words work[p][0..nblocks) (work[0][nblocks] is the launch's ticket, so work[1] starts past
+// it); the last CTA writes scales[p][blk] = amax / 448 (1 if 0) and zeroes the words again.
+fusp_status launch_amax_scales(const Fp8Src* src, int parts, int64_t block_elems, int nblocks,
+                               uint32_t* const* work, float* const* scales, uint32_t* nonfinite,
+                               cudaStream_t s);
+// K and V (parts = 2) quantized with one amax launch (scales finalized in it) and one quantize
+// launch (its programmatic dependent).  `work` as for launch_amax_scales.
 fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
                                       uint32_t* const* work, float* const* scales,
                                       uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s);

@@ -16,6 +16,23 @@ namespace {
 
 constexpr int kBlock = 256;
 
+// Programmatic dependent launch (PDL): the kernel may become resident while the previous
+// kernel on `s` drains; it must execute griddepcontrol.wait before touching that kernel's output.
+template <typename Args>
+cudaError_t launch_pdl(void (*kernel)(Args), dim3 grid, cudaStream_t s, const Args& args,
+                       int block = 256) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args);
+}
+
 inline int grid_for(int64_t work_items, int per_sm = 8) {  // grid-stride kernels
   int64_t g = (work_items + kBlock - 1) / kBlock;
   if (g > int64_t(sm_count()) * per_sm) g = int64_t(sm_count()) * per_sm;
@@ -553,6 +570,10 @@ struct PackArgs {
   PackOp op[kMaxMoveOps];
   int h, hp, slab_vecs;  // slab_vecs = SL*D/8
   int64_t slab_elems;
+  // Peer-memory Ulysses pack (peer = 1): slot t lives in member t's window, slot_boff[t] bytes
+  // from slot 0 (ops' dst / trailer address slot 0); replaces t * slot_stride / trailer_stride.
+  int peer;
+  int64_t slot_boff[kMaxPeerChunks];
 };
 // Ulysses pack (protocols.cpp:143-153): slab (b, h) -> slot h / hp, position (b, h % hp).
 __global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ PackArgs a) {
@@ -561,20 +582,26 @@ __global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ 
   const int hh = slab % a.h, bb = slab / a.h;
   const int t = hh / a.hp, hl = hh - t * a.hp;
   const int64_t s0 = int64_t(slab) * a.slab_elems;
-  const int64_t d0 = int64_t(t) * o.slot_stride + (int64_t(bb) * a.hp + hl) * a.slab_elems;
+  const int64_t desz = o.ddt == FUSP_E4M3 ? 1 : (o.ddt == FUSP_F32 ? 4 : 2);
+  const int64_t d0 = (a.peer ? a.slot_boff[t] / desz : int64_t(t) * o.slot_stride) +
+                     (int64_t(bb) * a.hp + hl) * a.slab_elems;
   float qs = 1.f;
   if (o.ddt == FUSP_E4M3) {
+    // (programmatic dependent of the amax pass: its scales are complete after the wait; a
+    // no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (o.amax != nullptr) {  // finalize fused in: scale = amax / 448, 1 for an all-zero block
       const float am = __uint_as_float(o.amax[slab * o.scale_bh_stride]);
       qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;
     } else {
-      qs = o.scale[slab * o.scale_bh_stride];
+      qs = __ldcg(&o.scale[slab * o.scale_bh_stride]);
     }
     // slot trailer (QuantizedTensor::slice_heads keeps the tensor-wide scale, fp8.cpp:100-105;
     // per block: the scales of this slot's slabs in [b][hl] order)
     if (o.trailer != nullptr && blockIdx.x == 0 && threadIdx.x == 0 &&
         (o.scale_bh_stride != 0 || (bb == 0 && hl == 0)))
-      o.trailer[t * o.trailer_stride + (o.scale_bh_stride != 0 ? bb * a.hp + hl : 0)] = qs;
+      o.trailer[(a.peer ? a.slot_boff[t] / 4 : t * o.trailer_stride) +
+                (o.scale_bh_stride != 0 ? bb * a.hp + hl : 0)] = qs;
   }
   const int stride = gridDim.x * blockDim.x;
   const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -590,6 +617,7 @@ __global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ 
       for (int e = 0; e < 4; ++e)
         if (v + e * stride < a.slab_vecs) dst[v + e * stride] = x[e];
     }
+    if (a.peer) __threadfence_system();  // remote stores visible before the exchange signal
     return;
   }
   for (int v = v0; v < a.slab_vecs; v += 4 * stride) {
@@ -607,6 +635,7 @@ __global__ void __launch_bounds__(256) pack_slab_kernel(const __grid_constant__ 
         store8(o.dst, o.ddt, d0 + i, x[e]);
     }
   }
+  if (a.peer) __threadfence_system();
 }
 
 struct UnpackOp {
@@ -841,10 +870,17 @@ __global__ void __launch_bounds__(256, FUSP_STAGE_MINB) stage_kernel(const __gri
     default: m = stage_dispatch<FUSP_E4M3>(o, src, dst, raw, a.slab_vecs, sc); break;
   }
   if (!guard) return;
-  // per-warp max -> one relaxed atomic per warp; no CTA barrier, no fence: the per-head
-  // decision runs in stage_decide_kernel, ordered after this kernel by the stream
+  // CTA max -> one relaxed atomic per CTA (per-warp atomics on the head's word serialised at
+  // L2: ~4600 warps on 6 words at FLUX U=8); no fence: the per-head decision runs in
+  // stage_decide_kernel, ordered after this kernel by the stream
   for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(&o.words[bh], __float_as_uint(m));
+  __shared__ float wm[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kBlock / 32; ++w) m = fmaxf(m, wm[w]);
+    if (m > 0.f) atomicMax(&o.words[bh], __float_as_uint(m));
+  }
 }
 
 // Per (head, guarded op), kFixParts CTAs: each derives e from the head's max|x| word; part 0
@@ -941,11 +977,18 @@ __device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, int64_t i) {
 // Pass 1 per block, 8 elements per step; grid.y = block, grid.z = tensor (K, V).
 struct AmaxArgs {
   Fp8Src src[2];
-  uint32_t* amax[2];
+  uint32_t* amax[2];  // zero on entry when `ticket` is set (the finalize leaves them zero)
   int64_t block_vecs;
   uint32_t* nonfinite;
+  // Finalize in the last CTA (ticket != null): scales[p][blk] = amax / 448 (1 if 0), then the
+  // amax words and the ticket are reset to zero for the next launch -- no memset before, no
+  // separate finalize kernel after (threadFenceReduction pattern).
+  float* scales[2];
+  uint32_t* ticket;
+  int nblocks, parts;
 };
 __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ AmaxArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the quantize / pack pass gets scheduled
   const Fp8Src& s = a.src[blockIdx.z];
   const int64_t base = int64_t(blockIdx.y) * a.block_vecs;
   float m = 0.f, nf = 0.f;
@@ -994,24 +1037,49 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
     atomicMax(&a.amax[blockIdx.z][blockIdx.y], __float_as_uint(bm));
     if (bb && a.nonfinite) atomicOr(a.nonfinite, 1u);
   }
+  if (a.ticket == nullptr) return;
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();  // our amax contribution before our ticket
+    last = atomicAdd(a.ticket, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < a.parts * a.nblocks; i += blockDim.x) {
+    const int p = i / a.nblocks, blk = i - p * a.nblocks;
+    const float am = __uint_as_float(__ldcg(&a.amax[p][blk]));
+    a.scales[p][blk] = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;  // fp8.cpp:119
+    a.amax[p][blk] = 0u;
+  }
+  if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
 // Pass 2: scale = amax/448 (1 if 0) per block, written by the block's first vector;
 // codes = encode(x / scale), IEEE division (fp8.cpp:119-121).
 struct QuantArgs {
   Fp8Src src[2];
-  const uint32_t* amax[2];
+  const uint32_t* amax[2];   // scale = amax / 448 (1 if 0), written to scales[] ...
+  const float* qscale[2];    // ... or, when set, the scale the amax pass finalized
   float* scales[2];
   uint8_t* codes[2];
   int64_t block_vecs;
 };
-// grid.y = block, grid.z = part: the block's scale is computed once per CTA.
+// grid.y = block, grid.z = part: the block's scale is computed once per CTA.  Launched as a
+// programmatic dependent of amax_vec_kernel: resident as the amax grid drains, waits for its
+// completion (griddepcontrol.wait; a no-op for an ordinary launch) before reading the scale.
 __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant__ QuantArgs a) {
   const int z = blockIdx.z, blk = blockIdx.y;
-  const float am = __uint_as_float(a.amax[z][blk]);
-  const float qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  float qs;
+  if (a.qscale[z] != nullptr) {
+    qs = __ldcg(&a.qscale[z][blk]);
+  } else {
+    const float am = __uint_as_float(a.amax[z][blk]);
+    qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.scales[z]) a.scales[z][blk] = qs;
+  }
   const float inv = __frcp_rn(qs);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && a.scales[z]) a.scales[z][blk] = qs;
   const int64_t base = int64_t(blk) * a.block_vecs;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const Fp8Src& s = a.src[z];
@@ -1155,7 +1223,8 @@ int slab_grid_x(int64_t slab_vecs, int64_t slabs) {
 }
 }  // namespace
 
-fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s) {
+fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s, bool pdl,
+                              const int64_t* peer_slot_boff) {
   if (n <= 0) return FUSP_OK;
   const PackDesc& p0 = ps[0];
   const int64_t slab_elems = int64_t(p0.sl) * p0.d;
@@ -1170,11 +1239,21 @@ fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s) {
            p.src_dtype != FUSP_E4M3;
   }
   if (!fast) {
+    if (peer_slot_boff != nullptr)
+      return set_error(FUSP_ERR_UNSUPPORTED, "peer pack: shape not 16-byte granular");
     for (int i = 0; i < n; ++i) FUSP_CHECK(launch_pack_generic(ps[i], s));
     return FUSP_OK;
   }
   if (slabs == 0 || slab_elems == 0) return FUSP_OK;
   PackArgs a{};
+  if (peer_slot_boff != nullptr) {
+    if (p0.u > kMaxPeerChunks) return set_error(FUSP_ERR_UNSUPPORTED, "peer pack: too many members");
+    a.peer = 1;
+    for (int t = 0; t < p0.u; ++t) {
+      a.slot_boff[t] = peer_slot_boff[t];
+      if (peer_slot_boff[t] % 16 != 0) return set_error(FUSP_ERR_INVALID_ARGUMENT, "peer pack: misaligned slot");
+    }
+  }
   for (int i = 0; i < n; ++i) {
     a.op[i] = PackOp{ps[i].src, ps[i].dst, ps[i].scale, ps[i].amax_bits, ps[i].trailer,
                      ps[i].trailer_stride, ps[i].scale_bh_stride, ps[i].dst_slot_stride,
@@ -1184,8 +1263,9 @@ fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s) {
   a.hp = p0.h / p0.u;
   a.slab_vecs = static_cast<int>(slab_elems / 8);
   a.slab_elems = slab_elems;
-  pack_slab_kernel<<<dim3(slab_grid_x(a.slab_vecs, slabs * n), static_cast<unsigned>(slabs), n),
-                     kBlock, 0, s>>>(a);
+  const dim3 grid(slab_grid_x(a.slab_vecs, slabs * n), static_cast<unsigned>(slabs), n);
+  if (pdl) FUSP_CUDA(launch_pdl(pack_slab_kernel, grid, s, a));
+  else pack_slab_kernel<<<grid, kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("pack_slab_kernel");
   return FUSP_OK;
 }
@@ -1406,6 +1486,16 @@ fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_e
 }
 
 namespace {
+// CTAs along a block for the FP8 passes: every thread takes >= 8 vectors (two rounds of 4 in
+// flight), at most 4 CTAs per SM over all blocks and parts -- few CTAs, so the per-CTA atomics
+// on the block's amax word and the finalize ticket (one address each) stay off the critical
+// path (ncu: 1184 CTAs x 2 same-address atomics cost ~3 us at FLUX U=8).
+int fp8_grid_x(int64_t block_vecs, int blocks_total) {
+  int64_t gx = (block_vecs + kBlock * 8 - 1) / (kBlock * 8);
+  const int64_t cap = (int64_t(sm_count()) * 4 + blocks_total - 1) / blocks_total;
+  if (gx > cap) gx = cap;
+  return gx < 1 ? 1 : static_cast<int>(gx);
+}
 bool fp8_vec_ok(const Fp8Src& src, int64_t n, int64_t block_elems, const void* codes) {
   return n % 8 == 0 && block_elems % 8 == 0 && src.d % 8 == 0 && aligned16(src.x) &&
          aligned16(codes);
@@ -1455,27 +1545,43 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
     return FUSP_OK;
   }
   if (n <= 0) return FUSP_OK;
-  for (int p = 0; p < parts; ++p) FUSP_CUDA(cudaMemsetAsync(work[p], 0, sizeof(uint32_t) * nblocks, s));
+  for (int p = 0; p < parts; ++p)
+    if (scales[p] == nullptr) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: no scale output");
   if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
-  AmaxArgs a{};
+  // pass 1 finalizes the scales in its last CTA and leaves `work` zero again; pass 2 is its
+  // programmatic dependent (launch latency hidden under pass 1, second read of x from L2)
+  const int gx = fp8_grid_x(block_elems / 8, nblocks * parts);
+  FUSP_CHECK(launch_amax_scales(src, parts, block_elems, nblocks, work, scales, nonfinite, s));
   QuantArgs q{};
   for (int p = 0; p < parts; ++p) {
-    a.src[p] = q.src[p] = src[p];
-    a.amax[p] = work[p];
-    q.amax[p] = work[p];
-    q.scales[p] = scales[p];
+    q.src[p] = src[p];
+    q.qscale[p] = scales[p];
     q.codes[p] = codes[p];
+  }
+  q.block_vecs = block_elems / 8;
+  FUSP_CUDA(launch_pdl(quantize_vec_kernel, dim3(gx, nblocks, parts), s, q));
+  FUSP_LAUNCHED("quantize_vec_kernel");
+  return FUSP_OK;
+}
+
+fusp_status launch_amax_scales(const Fp8Src* src, int parts, int64_t block_elems, int nblocks,
+                               uint32_t* const* work, float* const* scales, uint32_t* nonfinite,
+                               cudaStream_t s) {
+  if (parts < 1 || parts > 2 || nblocks <= 0 || nblocks > 65535 || block_elems % 8 != 0)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "amax: unsupported block layout");
+  AmaxArgs a{};
+  for (int p = 0; p < parts; ++p) {
+    a.src[p] = src[p];
+    a.amax[p] = work[p];
+    a.scales[p] = scales[p];
   }
   a.block_vecs = block_elems / 8;
   a.nonfinite = nonfinite;
-  int gx = grid_for(a.block_vecs, 8);
-  const int cap = (sm_count() * 8 + nblocks * parts - 1) / (nblocks * parts);
-  if (gx > cap) gx = cap < 1 ? 1 : cap;
-  amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
+  a.ticket = work[0] + nblocks;
+  a.nblocks = nblocks;
+  a.parts = parts;
+  amax_vec_kernel<<<dim3(fp8_grid_x(a.block_vecs, nblocks * parts), nblocks, parts), kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("amax_vec_kernel");
-  q.block_vecs = block_elems / 8;
-  quantize_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(q);
-  FUSP_LAUNCHED("quantize_vec_kernel");
   return FUSP_OK;
 }
 
@@ -1487,6 +1593,7 @@ fusp_status launch_quantize_fp8(const Fp8Src& src, int64_t n, int64_t block_elem
     return launch_quantize_fp8_multi(&src, 1, n, block_elems, &work, &scales, &codes, nonfinite, s);
   FUSP_CHECK(launch_amax_blocks(src, block_elems, nblocks, work, nonfinite, s));
   FUSP_CUDA(cudaMemcpyAsync(scales, work, sizeof(float) * nblocks, cudaMemcpyDeviceToDevice, s));
+  FUSP_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t) * nblocks, s));  // zero again (contract)
   return launch_quantize_blocks(src, n, block_elems, scales, codes, s);
 }
 

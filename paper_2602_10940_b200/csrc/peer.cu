@@ -1,0 +1,175 @@
+// Peer-memory Ulysses transport: every rank exposes one device window to the other ranks of its
+// node (CUDA IPC across processes, the raw pointer between threads of one process), and the
+// Ulysses all-to-alls become stores of the PRODUCING kernels straight into the members' windows
+// over NVLink / NVSwitch:
+//   * input reshard (protocols.cpp:125-180): the pack kernel writes slot t -- heads
+//     [t*hp, (t+1)*hp) of Q, K, V (FP8 codes + scale trailers included) -- into member t's
+//     receive region at my position;
+//   * output reshard (protocols.cpp:182-203): the attention epilogue stores O (and the LSE)
+//     rows [t*SL, (t+1)*SL) straight into member t's output region, tile by tile, so the
+//     transfer overlaps the math and no output all-to-all is left.
+// Each reshard then needs one tiny exchange kernel: it signals every member (a system-scope
+// release add on the member's word for my world rank) and spins until every member has
+// signalled me as often as I have waited for it (per-source counters in my own window, so the
+// protocol is graph-replay safe: all state is on the device).
+//
+// Why single-buffered regions are safe: member A writes B's input region for layer i+1 only
+// after A's output exchange of layer i observed B's signal, which B sends after its layer-i
+// staging read that region; A writes B's output region for layer i+1 only after A's input
+// exchange of layer i+1 observed B's signal, which B sends after copying out layer i.  This
+// holds when every peer-path layer of a rank uses the same Ulysses group (usp.cpp enforces it).
+#include "comm.h"
+
+#include <unistd.h>
+
+#include <cstring>
+
+namespace fusp {
+namespace {
+
+struct ExchArgs {
+  uint32_t* remote[kMaxPeerChunks];  // member t's word for me (null for myself)
+  int src[kMaxPeerChunks];           // world rank of member t
+  uint32_t* sig;                     // my words, indexed by source world rank
+  uint32_t* expect;                  // my per-source counters of completed waits
+  uint32_t* err;                     // timeout flag (read by PeerWindow::check)
+  unsigned long long timeout_ns;
+  int n, self;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One warp: lane t < n handles member t.
+__global__ void peer_exchange_kernel(const __grid_constant__ ExchArgs a) {
+  const int t = threadIdx.x;
+  const bool peer = t < a.n && t != a.self;
+  if (peer) {
+    // everything this stream wrote before (the producing kernel fenced its remote stores
+    // system-wide before exiting) happens-before the member's acquire of this add
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.remote[t]) : "memory");
+  }
+  if (peer) {
+    const int src = a.src[t];
+    const uint32_t target = a.expect[src] + 1u;
+    const unsigned long long t0 = globaltimer();
+    while (static_cast<int32_t>(ld_acquire_sys(&a.sig[src]) - target) < 0) {
+      __nanosleep(100);
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicOr(a.err, 1u);
+        break;
+      }
+    }
+    a.expect[src] = target;
+  }
+}
+
+}  // namespace
+
+PeerWindow::~PeerWindow() {
+  if (device >= 0) cudaSetDevice(device);
+  for (size_t r = 0; r < peer.size(); ++r)
+    if (opened.size() > r && opened[r]) cudaIpcCloseMemHandle(peer[r]);
+  if (base) cudaFree(base);
+}
+
+fusp_status peer_window_create(PeerWindow* w, int rank, int world, int device, size_t data_bytes,
+                               PeerHandle* mine) {
+  if (world > kPeerMaxWorld)
+    return set_error(FUSP_ERR_UNSUPPORTED, "peer window: world above " + std::to_string(kPeerMaxWorld));
+  FUSP_CUDA(cudaSetDevice(device));
+  w->device = device;
+  w->rank = rank;
+  w->world = world;
+  w->data_bytes = (data_bytes + 255) / 256 * 256;
+  FUSP_CUDA(cudaMalloc(&w->base, kPeerCtlBytes + w->data_bytes));
+  FUSP_CUDA(cudaMemset(w->base, 0, kPeerCtlBytes));
+  std::memset(mine, 0, sizeof(*mine));
+  mine->magic = kPeerMagic;
+  mine->pid = static_cast<int32_t>(getpid());
+  mine->device = device;
+  mine->ptr = reinterpret_cast<uint64_t>(w->base);
+  mine->bytes = w->data_bytes;
+  FUSP_CUDA(cudaIpcGetMemHandle(&mine->ipc, w->base));
+  return FUSP_OK;
+}
+
+fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all) {
+  FUSP_CUDA(cudaSetDevice(w->device));
+  w->peer.assign(static_cast<size_t>(w->world), nullptr);
+  w->opened.assign(static_cast<size_t>(w->world), false);
+  w->bytes_of.assign(static_cast<size_t>(w->world), 0);
+  const int32_t pid = static_cast<int32_t>(getpid());
+  for (int r = 0; r < w->world; ++r) {
+    const PeerHandle& h = all[r];
+    if (h.magic != kPeerMagic)
+      return set_error(FUSP_ERR_COMM, "peer window: bad handle from rank " + std::to_string(r));
+    w->bytes_of[r] = h.bytes;
+    if (r == w->rank) {
+      w->peer[r] = w->base;
+      continue;
+    }
+    if (h.pid == pid) {  // ranks that are threads of this process: the pointer itself
+      w->peer[r] = reinterpret_cast<char*>(h.ptr);
+      if (h.device != w->device) {
+        int can = 0;
+        FUSP_CUDA(cudaDeviceCanAccessPeer(&can, w->device, h.device));
+        if (!can)
+          return set_error(FUSP_ERR_COMM, "peer window: device " + std::to_string(w->device) +
+                                              " cannot access device " + std::to_string(h.device));
+        cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return set_cuda_error(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+    } else {
+      void* p = nullptr;
+      FUSP_CUDA(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+      w->peer[r] = static_cast<char*>(p);
+      w->opened[r] = true;
+    }
+  }
+  return FUSP_OK;
+}
+
+fusp_status launch_peer_exchange(const PeerWindow& w, int kind, const Group& g, double timeout_s,
+                                 cudaStream_t s) {
+  if (g.size() > kMaxPeerChunks) return set_error(FUSP_ERR_UNSUPPORTED, "peer exchange: group too large");
+  ExchArgs a{};
+  a.n = g.size();
+  a.self = g.pos;
+  for (int t = 0; t < a.n; ++t) {
+    const int m = g.members[t];
+    a.src[t] = m;
+    a.remote[t] = t == g.pos ? nullptr : w.ctl(m) + kind * kPeerMaxWorld + w.rank;
+  }
+  a.sig = w.ctl(w.rank) + kind * kPeerMaxWorld;
+  a.expect = w.ctl(w.rank) + (2 + kind) * kPeerMaxWorld;
+  a.err = w.ctl(w.rank) + 4 * kPeerMaxWorld;
+  a.timeout_ns = static_cast<unsigned long long>((timeout_s > 0 ? timeout_s : 120.0) * 1e9);
+  peer_exchange_kernel<<<1, 32, 0, s>>>(a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "peer_exchange_kernel");
+  return FUSP_OK;
+}
+
+fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_t s) {
+  uint32_t err = 0;  // (stream-ordered: a legacy-stream copy could wait on other ranks' spins)
+  FUSP_CUDA(cudaMemcpyAsync(&err, w.ctl(w.rank) + 4 * kPeerMaxWorld, 4, cudaMemcpyDeviceToHost, s));
+  FUSP_CUDA(cudaStreamSynchronize(s));
+  if (err)
+    return set_error(FUSP_ERR_DEADLOCK, std::string("deadlock: rank ") + std::to_string(w.rank) +
+                                            " stalled in " + what + " (peer-memory exchange timed out)");
+  return FUSP_OK;
+}
+
+}  // namespace fusp

@@ -111,6 +111,7 @@ struct StreamWs {
   void* ptr = nullptr;
   size_t bytes = 0;
   CounterBuf cnt;  // zero-initialised words (stream-K tickets, staging amax / tickets)
+  CounterBuf qw;   // zero-initialised words of the FP8 amax pass (left zero by each launch)
 };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, std::unique_ptr<StreamWs>> g_ws;
@@ -133,13 +134,12 @@ fusp_status ws_scratch(StreamWs* w, cudaStream_t s, size_t bytes, void** out) {
     if (cs != cudaStreamCaptureStatusNone)
       return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
     if (w->ptr) {
-      FUSP_CUDA(cudaStreamSynchronize(s));  // the old buffer's last users ran on `s`
-      FUSP_CUDA(cudaFree(w->ptr));
+      FUSP_CUDA(cudaFreeAsync(w->ptr, s));  // the old buffer's last users ran on `s`
       w->ptr = nullptr;
       w->bytes = 0;
     }
     const size_t n = bytes < (size_t(1) << 20) ? (size_t(1) << 20) : bytes;
-    FUSP_CUDA(cudaMalloc(&w->ptr, n));
+    FUSP_CUDA(cudaMallocAsync(&w->ptr, n, s));
     w->bytes = n;
   }
   *out = w->ptr;
@@ -152,10 +152,21 @@ fusp_status ws_words(StreamWs* w, cudaStream_t s, size_t words, uint32_t** out) 
     FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
     if (cs != cudaStreamCaptureStatusNone)
       return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
-    if (w->cnt.ptr) FUSP_CUDA(cudaStreamSynchronize(s));
   }
-  FUSP_CHECK(ensure_counters(w->cnt, words));
+  FUSP_CHECK(ensure_counters(w->cnt, words, s));  // stream-ordered: the old words' users ran on s
   *out = w->cnt.ptr;
+  return FUSP_OK;
+}
+
+fusp_status ws_qwords(StreamWs* w, cudaStream_t s, size_t words, uint32_t** out) {
+  if (w->qw.words < words || w->qw.ptr == nullptr) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
+  }
+  FUSP_CHECK(ensure_counters(w->qw, words, s));
+  *out = w->qw.ptr;
   return FUSP_OK;
 }
 
@@ -277,10 +288,10 @@ fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n
   StreamWs* w = nullptr;
   FUSP_CHECK(stream_ws(s, &w));
   std::lock_guard<std::mutex> lk(w->mu);
-  void* ws = nullptr;
-  FUSP_CHECK(ws_scratch(w, s, static_cast<size_t>(nblocks) * 4 + 256, &ws));
+  uint32_t* work = nullptr;
+  FUSP_CHECK(ws_qwords(w, s, static_cast<size_t>(nblocks) + 1, &work));
   const Fp8Src src{x, dtype, nullptr, 0, 0, 1, 1, 1};
-  return launch_quantize_fp8(src, n, block, static_cast<uint32_t*>(ws), scales_dev, codes, nullptr, s);
+  return launch_quantize_fp8(src, n, block, work, scales_dev, codes, nullptr, s);
 }
 
 fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_dev, int64_t n,
@@ -295,12 +306,11 @@ fusp_status fusp_requantize_e4m3(const uint8_t* codes, const float* seg_scales_d
   StreamWs* w = nullptr;
   FUSP_CHECK(stream_ws(s, &w));
   std::lock_guard<std::mutex> lk(w->mu);
-  void* ws = nullptr;
-  FUSP_CHECK(ws_scratch(w, s, 256, &ws));
+  uint32_t* work = nullptr;
+  FUSP_CHECK(ws_qwords(w, s, 2, &work));
   // the ring-hop source: rows of 8 codes, one bh, a scale per `seg / 8` rows
   const Fp8Src src{codes, FUSP_E4M3, seg_scales_dev, 1, 0, 8, static_cast<int>(n / 8),
                    static_cast<int>(seg / 8)};
-  uint32_t* work = static_cast<uint32_t*>(ws);
   return launch_quantize_fp8_multi(&src, 1, n, n, &work, &scale_dev, &codes_out, nullptr, s);
 }
 

@@ -73,6 +73,13 @@ struct fusp_ctx_s {
   int rank = 0, world = 1, device = 0;
   std::unique_ptr<Comm> comm;
   NcclComm* nccl = nullptr;
+  // peer-memory Ulysses transport (fusp_ctx_peer_enable): null = the comm backend moves bytes
+  std::unique_ptr<PeerWindow> peer;
+  bool peer_open = false;
+  cudaStream_t last_stream = nullptr;  // stream of the previous layer call (workspace users)
+  bool last_stream_valid = false;
+  uint64_t peer_layers = 0;     // layers whose Ulysses reshards went through the windows
+  uint64_t peer_fallbacks = 0;  // layers that could not (see peer_eligible) and used `comm`
   cudaStream_t side = nullptr;  // ring communication stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_attn[2] = {nullptr, nullptr};
@@ -189,25 +196,39 @@ struct Carve {
   }
 };
 
-fusp_status ensure_arena(fusp_ctx_s* c, size_t bytes) {
+// Workspace growth is stream-ordered on the layer's stream `s` and never waits on the whole
+// device: with peer windows, ranks sharing one GPU (tests) have exchange kernels spinning on it
+// for work that another rank's thread has not enqueued yet, and a cudaDeviceSynchronize /
+// cudaFree here would wait for them forever.  The old buffers' last users ran on the stream of
+// the previous call (host-synchronized here when it differs) or on the side stream, which every
+// layer joins back into its stream before returning.
+fusp_status quiesce_previous(fusp_ctx_s* c, cudaStream_t s) {
+  if (c->last_stream != s && c->last_stream_valid) FUSP_CUDA(cudaStreamSynchronize(c->last_stream));
+  return FUSP_OK;
+}
+
+fusp_status ensure_arena(fusp_ctx_s* c, size_t bytes, cudaStream_t s) {
   Workspace& w = *c->ws;
   if (w.bytes >= bytes) return FUSP_OK;
   if (c->capturing)
     return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
-  FUSP_CUDA(cudaDeviceSynchronize());
-  if (w.arena) FUSP_CUDA(cudaFree(w.arena));
+  if (w.arena) {
+    FUSP_CHECK(quiesce_previous(c, s));
+    FUSP_CUDA(cudaFreeAsync(w.arena, s));
+  }
   w.arena = nullptr;
   w.bytes = 0;
-  FUSP_CUDA(cudaMalloc(&w.arena, bytes));
+  FUSP_CUDA(cudaMallocAsync(&w.arena, bytes, s));
   w.bytes = bytes;
   return FUSP_OK;
 }
 
-fusp_status ensure_words(fusp_ctx_s* c, size_t words) {
+fusp_status ensure_words(fusp_ctx_s* c, size_t words, cudaStream_t s) {
   if (c->ws->words.ptr != nullptr && c->ws->words.words >= words) return FUSP_OK;
   if (c->capturing)
     return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
-  return ensure_counters(c->ws->words, words);
+  if (c->ws->words.ptr != nullptr) FUSP_CHECK(quiesce_previous(c, s));
+  return ensure_counters(c->ws->words, words, s);
 }
 
 // Bump allocator over the zero-initialised words.
@@ -264,6 +285,12 @@ struct Layer {
   void *reshard_q = nullptr, *reshard_k = nullptr, *reshard_v = nullptr;
   int reshard_dt = FUSP_F32;
   bool wire() const { return mode != Mode::kRing && (U > 1 || force_wire); }
+  // Peer-memory Ulysses (PeerWindow, peer.cu): the pack writes the members' receive regions and
+  // the attention epilogue their output regions directly; offsets inside every window's data
+  bool peer = false;
+  char* pw[kMaxPeerChunks] = {};  // data region of member t's window (group order)
+  size_t pw_out = 0, pw_lse = 0;  // output / LSE regions (the receive slots start at 0)
+  size_t pw_need = 0;             // data bytes the layer needs in every member's window
 };
 
 struct Buffers {
@@ -288,7 +315,8 @@ struct Buffers {
   int64_t bh_stride = 0;    // floats between the scales of consecutive (b,h) slabs
   int seg_rows = 0;
   float* qscale = nullptr;  // K scales then V scales of a locally quantized chunk
-  uint32_t* amax = nullptr; // scratch: per-block amax / scale words
+  uint32_t* amax = nullptr;   // zero words: per-block amax of the FP8 passes (+ tickets)
+  float* pscale = nullptr;    // FP8 Ulysses pack: K scales then V scales (amax pass output)
   // ring
   char* rb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buf][K|V] wire parts
   char* sw[2] = {nullptr, nullptr};                           // fp8 send wire parts
@@ -389,6 +417,32 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
   return FUSP_OK;
 }
 
+// Whether this layer's Ulysses reshards go through the peer windows (the fused pack / epilogue
+// stores) or through c->comm.  The windows serve ONE Ulysses group per context (the hazard
+// argument in peer.cu needs every peer-path exchange of a rank to involve the same members):
+// the first eligible layer's group.  Not on the peer path: the QK prologue / producer variants
+// (their pack kernels write local slots), other head dims, wire debugging, layers larger than
+// any member's window.
+bool plan_peer(fusp_ctx_s* c, Layer& l) {
+  l.peer = false;
+  if (!c->peer || !c->peer_open || !l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks || l.generic ||
+      l.pro != nullptr || l.prepacked || c->debug_wire)
+    return false;
+  const std::string key = l.ug.key();
+  if (!c->peer->group.empty() && c->peer->group != key) return false;
+  if (l.slot_stride % 16 != 0 || (size_t(l.blk) * l.wout) % 16 != 0) return false;
+  const size_t in = l.slot_stride * l.U;
+  l.pw_out = align_up(in, 256);
+  l.pw_lse = l.pw_out + align_up(size_t(l.blk) * l.wout * l.U, 256);
+  l.pw_need = l.pw_lse + align_up(size_t(l.blk / l.D) * 4 * l.U, 256);
+  for (int t = 0; t < l.U; ++t)
+    if (c->peer->bytes_of[size_t(l.ug.members[t])] < l.pw_need) return false;
+  for (int t = 0; t < l.U; ++t) l.pw[t] = c->peer->data(l.ug.members[t]);
+  c->peer->group = key;
+  l.peer = true;
+  return true;
+}
+
 // Assign workspace for a layer. `q`, `k`, `v` are the caller's tensors (zero-copy when the
 // attention can read them as they are).
 void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q, const void* k,
@@ -405,8 +459,12 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
   for (int i = 0; i < 2; ++i)
     for (int p = 0; p < 2; ++p) b->ring_w[i][p] = cw.take(stage_words(hr));
   if (wire) {
-    b->send_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
-    b->recv_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
+    if (l.peer) {  // receive slots in my window; the pack writes the members' windows
+      b->recv_in = l.pw[l.ug.pos];
+    } else {
+      b->send_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
+      b->recv_in = static_cast<char*>(cv.take(l.slot_stride * l.U));
+    }
     b->Qr = b->Qr_w = cv.take(CQ);
     b->Kr = b->Kr_w = cv.take(CK);
     b->Vr = b->Vr_w = cv.take(CV);
@@ -478,7 +536,10 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
   if (l.pro_k_pre) b->Kpro = static_cast<float*>(cv.take(C4));
   const int nsc = l.nsc_local > l.nsc_chunk ? l.nsc_local : l.nsc_chunk;
   b->qscale = static_cast<float*>(cv.take(sizeof(float) * 2 * nsc));
-  b->amax = static_cast<uint32_t*>(cv.take(sizeof(uint32_t) * 4 * (nsc + 1)));
+  // amax words of the FP8 passes: zero-initialised, and the amax pass's last CTA leaves them
+  // zero (launch_amax_scales), so no memset precedes a quantization
+  b->amax = cw.take(4 * (size_t(nsc) + 1));
+  b->pscale = static_cast<float*>(cv.take(sizeof(float) * 2 * (size_t(nsc) + 1)));
   if (l.R > 1) {
     const size_t part = l.fp8 ? align_up(size_t(l.C) + 4 * size_t(l.nsc_chunk), 256)
                               : size_t(l.C) * l.w_in;
@@ -495,7 +556,10 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
   }
   b->attn_ws_bytes = attention_workspace_bytes(l.heads_r, l.span, l.span);
   if (b->attn_ws_bytes) b->attn_ws = cv.take(b->attn_ws_bytes);
-  if (wire) {
+  if (wire && l.peer) {  // the epilogue stores into the members' windows; mine receives
+    b->recv_out = l.pw[l.ug.pos] + l.pw_out;
+    b->lse_recv = reinterpret_cast<float*>(l.pw[l.ug.pos] + l.pw_lse);
+  } else if (wire) {
     b->send_out = static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
     b->recv_out = l.B == 1 ? static_cast<char*>(out)
                            : static_cast<char*>(cv.take(size_t(l.blk) * l.wout * l.U));
@@ -581,6 +645,15 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     return launch_stage(ops, n, hr, l.span, l.D, 1, s);
   }
   const int64_t sew = int64_t(l.slot_stride / l.w_in);  // slot stride in wire elements
+  // Peer-memory pack: slot t is my slot in member t's receive region (its window), so the pack
+  // kernel's stores ARE the all-to-all; slot 0's address plus per-slot byte offsets
+  char* sbase = b.send_in;
+  int64_t boff[kMaxPeerChunks] = {};
+  if (l.peer) {
+    sbase = l.pw[0] + size_t(l.ug.pos) * l.slot_stride;
+    for (int t = 0; t < l.U; ++t) boff[t] = l.pw[t] - l.pw[0];
+  }
+  const int64_t* pboff = l.peer ? boff : nullptr;
   if (!l.prepacked) {
     // pack: destination slot t <- heads [t*hp, (t+1)*hp) (protocols.cpp:143-153); Q, K, V
     // keep the caller's dtype on the wire (the receiver stages them for the tensor cores)
@@ -592,7 +665,7 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     p.u = l.U;
     p.src = q;
     p.src_dtype = l.in_dt;
-    p.dst = b.send_in;
+    p.dst = sbase;
     p.dst_dtype = l.in_dt;
     p.dst_slot_stride = sew;
     PackDesc ops[3];
@@ -610,12 +683,12 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     } else if (!l.fp8) {
       ops[nops++] = p;
       p.src = k;
-      p.dst = b.send_in + l.off_k;
+      p.dst = sbase + l.off_k;
       ops[nops++] = p;
       p.src = v;
-      p.dst = b.send_in + l.off_v;
+      p.dst = sbase + l.off_v;
       ops[nops++] = p;
-      FUSP_CHECK(launch_pack_multi(ops, nops, s));
+      FUSP_CHECK(launch_pack_multi(ops, nops, s, false, pboff));
     } else {
       if (l.pro_q) FUSP_CHECK(prologue(true, q, b.send_in, l.in_dt, sew, l.U));
       else ops[nops++] = p;
@@ -626,26 +699,34 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       const int64_t block = l.fp8_block ? int64_t(l.SL) * l.D : n;
       const Fp8Src srcs[2] = {Fp8Src{k, l.k_dt, nullptr, 0, 0, l.D, l.SL, l.SL},
                               Fp8Src{v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL}};
-      uint32_t* am[2] = {b.amax, b.amax + l.nsc_local};
-      FUSP_CHECK(launch_amax_multi(srcs, 2, block, l.nsc_local, am, s));
+      uint32_t* am[2] = {b.amax, b.amax + l.nsc_local + 1};
+      float* sc[2] = {b.pscale, b.pscale + l.nsc_local};
+      FUSP_CHECK(launch_amax_scales(srcs, 2, block, l.nsc_local, am, sc, nullptr, s));
       for (int part = 0; part < 2; ++part) {
         p.src = srcs[part].x;
         p.src_dtype = srcs[part].dt;
-        p.dst = b.send_in + (part == 0 ? l.off_k : l.off_v);
+        p.dst = sbase + (part == 0 ? l.off_k : l.off_v);
         p.dst_dtype = FUSP_E4M3;
         p.dst_slot_stride = int64_t(l.slot_stride);
-        p.scale = nullptr;
-        p.amax_bits = am[part];
+        p.scale = sc[part];
+        p.amax_bits = nullptr;
         p.scale_bh_stride = l.fp8_block ? 1 : 0;
-        p.trailer = reinterpret_cast<float*>(b.send_in + l.off_tr) + part * l.nsc_slot;
+        p.trailer = reinterpret_cast<float*>(sbase + l.off_tr) + part * l.nsc_slot;
         p.trailer_stride = int64_t(l.slot_stride / 4);
         ops[nops++] = p;
       }
-      FUSP_CHECK(launch_pack_multi(ops, nops, s));
+      // programmatic dependent of the amax pass: the Q copy overlaps it, the E4M3 operands
+      // wait for its scales
+      FUSP_CHECK(launch_pack_multi(ops, nops, s, /*pdl=*/true, pboff));
     }
   }
-  FUSP_CHECK(record_wire(c, 0, 0, b.send_in, l.slot_stride * l.U, s));
-  FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
+  if (l.peer) {
+    // the members' pack kernels wrote my receive slots: signal mine, wait for theirs
+    FUSP_CHECK(launch_peer_exchange(*c->peer, 0, l.ug, sync_timeout_s(), s));
+  } else {
+    FUSP_CHECK(record_wire(c, 0, 0, b.send_in, l.slot_stride * l.U, s));
+    FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_in, b.recv_in, l.slot_stride, l.slot_bytes, s));
+  }
   c->a2a_bytes += uint64_t(l.U - 1) * l.slot_bytes;
   log_a2a(c, l.ug, uint64_t(l.U - 1) * l.slot_bytes);
   // unpack + stage: source j contributed our heads over its sequence shard
@@ -758,6 +839,18 @@ fusp_status attend(const Layer& l, const Buffers& b, const void* K, const void* 
       a.lse = b.lse_send;
       a.lse_hs = l.SL;
       a.lse_cs = l.blk / l.D;
+    }
+    if (!direct_out && l.peer) {
+      // the output reshard fused into the epilogue: rows [t*SL, (t+1)*SL) go straight to my
+      // slot of member t's output region over NVLink (protocols.cpp:182-203)
+      a.peer_chunks = l.U;
+      const size_t os = size_t(l.blk) * l.wout, ls = size_t(l.blk / l.D) * 4;
+      for (int t = 0; t < l.U; ++t) {
+        a.out_peer[t] = l.pw[t] + l.pw_out + size_t(l.ug.pos) * os;
+        a.lse_peer[t] = reinterpret_cast<float*>(l.pw[t] + l.pw_lse + size_t(l.ug.pos) * ls);
+      }
+      a.out = a.out_peer[0];
+      if (lse_out != nullptr) a.lse = a.lse_peer[0];
     }
   } else {
     a.out = b.acc_o;
@@ -945,7 +1038,14 @@ fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, fl
                         cudaStream_t s) {
   if (!l.wire()) return FUSP_OK;  // epilogue wrote `out` (and `lse`) directly
   const size_t slot = size_t(l.blk) * l.wout;
-  FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
+  if (l.peer) {
+    // the members' epilogues wrote my output region: signal mine, wait for theirs, then the
+    // region is the concatenation over heads (B = 1: exactly `out`)
+    FUSP_CHECK(launch_peer_exchange(*c->peer, 1, l.ug, sync_timeout_s(), s));
+    if (l.B == 1) FUSP_CUDA(cudaMemcpyAsync(out, b.recv_out, slot * l.U, cudaMemcpyDeviceToDevice, s));
+  } else {
+    FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
+  }
   c->a2a_bytes += uint64_t(l.U - 1) * slot;
   log_a2a(c, l.ug, uint64_t(l.U - 1) * slot);
   if (l.B > 1)  // concat_heads (protocols.cpp:196-202)
@@ -956,7 +1056,11 @@ fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, fl
     // (B = 1: straight into the caller's [1][H][SL] buffer, heads t*hp.. from member t).
     const size_t ls = size_t(l.blk / l.D) * 4;
     float* dst = l.B == 1 ? lse_out : b.lse_recv;
-    FUSP_CHECK(c->comm->all_to_all(l.ug, b.lse_send, dst, ls, ls, s));
+    if (l.peer) {  // already in my window with O (same exchange)
+      if (l.B == 1) FUSP_CUDA(cudaMemcpyAsync(lse_out, b.lse_recv, ls * l.U, cudaMemcpyDeviceToDevice, s));
+    } else {
+      FUSP_CHECK(c->comm->all_to_all(l.ug, b.lse_send, dst, ls, ls, s));
+    }
     c->a2a_bytes += uint64_t(l.U - 1) * ls;
     log_a2a(c, l.ug, uint64_t(l.U - 1) * ls);
     if (l.B > 1) {  // slot t [B][hp][SL] -> lse[b][t*hp + hl][SL]
@@ -991,7 +1095,7 @@ fusp_status output_reshard(fusp_ctx_s* c, const Layer& l, Buffers& b, const void
 fusp_status check_inputs(fusp_ctx_s* c, Mode mode, const Layer& l, const void* q, const void* k,
                          const void* v, cudaStream_t s) {
   size_t need = 256;
-  FUSP_CHECK(ensure_arena(c, need));
+  FUSP_CHECK(ensure_arena(c, need, s));
   uint32_t* flag = static_cast<uint32_t*>(c->ws->arena);
   FUSP_CUDA(cudaMemsetAsync(flag, 0, 4, s));
   const int64_t n = int64_t(l.B) * l.H * l.SL * l.D;
@@ -1085,14 +1189,26 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
       return set_error(FUSP_ERR_UNSUPPORTED, "operand producer: bf16/f16 wire, no prologue, no check");
     l.prepacked = true;
   }
+  if (c->peer && l.wire()) {
+    if (plan_peer(c, l)) {
+      if (!size_only) c->peer_layers++;
+    } else if (!size_only) {
+      c->peer_fallbacks++;
+    }
+  }
+  if (c->capturing && !c->comm->capturable() && ((l.wire() && !l.peer) || l.R > 1))
+    return set_error(FUSP_ERR_UNSUPPORTED,
+                     "graph capture: this layer needs the in-process fabric's host rendezvous");
   Carve cv;
   CarveWords cw;
   Buffers b;
   const size_t cnt_words = attention_counter_words(l.heads_r, l.span);
   cw.take(cnt_words);
   carve(l, cv, cw, &b, q, k, v, out);
-  FUSP_CHECK(ensure_arena(c, cv.off + 256));
-  FUSP_CHECK(ensure_words(c, cw.off));
+  FUSP_CHECK(ensure_arena(c, cv.off + 256, s));
+  FUSP_CHECK(ensure_words(c, cw.off, s));
+  c->last_stream = s;
+  c->last_stream_valid = true;
   if (size_only) return FUSP_OK;
   cv = Carve{static_cast<char*>(c->ws->arena), 0};
   cw = CarveWords{c->ws->words.ptr, 0};
@@ -1233,6 +1349,7 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
                                                " live graph(s): destroy them first");
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  c->peer.reset();
   c->comm.reset();
   c->own.release();
   c->clear_wire();
@@ -1248,12 +1365,97 @@ fusp_status fusp_ctx_destroy(fusp_ctx c) {
   return FUSP_OK;
 }
 
+fusp_status fusp_ctx_peer_window(fusp_ctx c, size_t window_bytes, void* handle_out) {
+  clear_error();
+  if (!c || !handle_out) return set_error(FUSP_ERR_INVALID_ARGUMENT, "peer window: null argument");
+  if (c->live_graphs > 0)
+    return set_error(FUSP_ERR_UNSUPPORTED, "peer window: the context has live graphs");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  FUSP_CUDA(cudaDeviceSynchronize());
+  auto w = std::make_unique<PeerWindow>();
+  PeerHandle h{};
+  FUSP_CHECK(peer_window_create(w.get(), c->rank, c->world, c->device, window_bytes, &h));
+  std::memcpy(handle_out, &h, sizeof(h));
+  c->peer = std::move(w);
+  c->peer_layers = c->peer_fallbacks = 0;
+  c->peer_open = false;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_peer_open(fusp_ctx c, const void* handles) {
+  clear_error();
+  if (!c || !c->peer || !handles)
+    return set_error(FUSP_ERR_INVALID_ARGUMENT, "peer open: create the window first");
+  fusp_status st = peer_window_open(c->peer.get(), static_cast<const PeerHandle*>(handles));
+  if (st != FUSP_OK) {
+    c->peer.reset();
+    return st;
+  }
+  c->peer_open = true;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_peer_enable(fusp_ctx c, size_t window_bytes) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  PeerHandle mine{};
+  FUSP_CHECK(fusp_ctx_peer_window(c, window_bytes, &mine));
+  std::vector<PeerHandle> all(static_cast<size_t>(c->world));
+  fusp_status st = c->comm->allgather_host(&mine, sizeof(mine), all.data());
+  if (st != FUSP_OK) {
+    c->peer.reset();
+    return st;
+  }
+  return fusp_ctx_peer_open(c, all.data());
+}
+
+fusp_status fusp_peer_window_bytes(int world, int ring_dim, fusp_dtype in_dtype, fusp_shape4 ls,
+                                   const fusp_comm_options* opts, size_t* bytes) {
+  clear_error();
+  if (!bytes || world < 1) return set_error(FUSP_ERR_INVALID_ARGUMENT, "peer window bytes: bad argument");
+  fusp_ctx_s tmp;
+  tmp.world = world;
+  tmp.rank = 0;
+  fusp_comm_options o{};
+  o.out_dtype = FUSP_F32;
+  if (opts) o = *opts;
+  Layer l;
+  FUSP_CHECK(plan_layer(&tmp, Mode::kUsp, ring_dim, ls, in_dtype, o, &l));
+  const size_t in = l.slot_stride * l.U;
+  *bytes = align_up(in, 256) + align_up(size_t(l.blk) * l.wout * l.U, 256) +
+           align_up(size_t(l.blk / l.D) * 4 * l.U, 256);
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_peer_disable(fusp_ctx c) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  if (c->live_graphs > 0)
+    return set_error(FUSP_ERR_UNSUPPORTED, "peer disable: the context has live graphs");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  if (c->last_stream_valid) FUSP_CUDA(cudaStreamSynchronize(c->last_stream));
+  FUSP_CUDA(cudaStreamSynchronize(c->side));
+  c->peer.reset();
+  c->peer_open = false;
+  return FUSP_OK;
+}
+
+fusp_status fusp_ctx_peer_stats(fusp_ctx c, uint64_t* layers, uint64_t* fallbacks) {
+  clear_error();
+  if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
+  if (layers) *layers = c->peer_layers;
+  if (fallbacks) *fallbacks = c->peer_fallbacks;
+  return FUSP_OK;
+}
+
 fusp_status fusp_ctx_synchronize(fusp_ctx c, fusp_stream_t stream, double timeout_s) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
   FUSP_CUDA(cudaSetDevice(c->device));
-  return c->comm->wait(reinterpret_cast<cudaStream_t>(stream),
-                       timeout_s > 0 ? timeout_s : sync_timeout_s(), "synchronize");
+  FUSP_CHECK(c->comm->wait(reinterpret_cast<cudaStream_t>(stream),
+                           timeout_s > 0 ? timeout_s : sync_timeout_s(), "synchronize"));
+  if (c->peer) FUSP_CHECK(peer_window_check(*c->peer, "synchronize", reinterpret_cast<cudaStream_t>(stream)));
+  return FUSP_OK;
 }
 
 fusp_status fusp_ctx_debug_wire(fusp_ctx c, int enable) {
@@ -1458,11 +1660,14 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
   const size_t one = align_up(size_t(batch) * heads * s_local * 128 * 2, 256);
   if (c->block_ws_bytes < 4 * one) {
     if (c->capturing) return set_error(FUSP_ERR_UNSUPPORTED, "workspace growth during graph capture");
-    FUSP_CUDA(cudaDeviceSynchronize());
-    if (c->block_ws) FUSP_CUDA(cudaFree(c->block_ws));
+    // stream-ordered like the layer workspace (no device-wide wait: see ensure_arena)
+    if (c->block_ws) {
+      FUSP_CHECK(quiesce_previous(c, st));
+      FUSP_CUDA(cudaFreeAsync(c->block_ws, st));
+    }
     c->block_ws = nullptr;
     c->block_ws_bytes = 0;
-    FUSP_CUDA(cudaMalloc(&c->block_ws, 4 * one));
+    FUSP_CUDA(cudaMallocAsync(&c->block_ws, 4 * one, st));
     c->block_ws_bytes = 4 * one;
   }
   char* ws = static_cast<char*>(c->block_ws);
@@ -1773,9 +1978,10 @@ fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, cons
                                    fusp_graph* graph) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
-  if (!c->comm->capturable())
+  if (!c->comm->capturable() && !(c->peer && ring_dim == 1))
     return set_error(FUSP_ERR_UNSUPPORTED,
-                     "graph capture needs an NCCL context (or a world-1 local context)");
+                     "graph capture needs an NCCL context, a world-1 local context, or peer "
+                     "windows with ring_dim 1");
   if (opts && opts->check_finite)
     return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
   FUSP_CUDA(cudaSetDevice(c->device));

@@ -161,6 +161,38 @@ def dead_peer():
     emit(check="dead_peer_deadlock_error", ok=bool(ok), result=repr(r0), error=repr(err))
 
 
+def peer_cases():
+    # peer-memory windows set up through NcclComm (handles all-gathered by grouped
+    # ncclSend/ncclRecv): the Ulysses reshards bypass NCCL, the ring (R > 1) still uses it
+    h = 8
+    for n, r, fp8 in [(2, 1, False), (4, 1, True), (4, 2, False)]:
+        s = 128 * n
+        q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(161 + n, 162 + r, 163))
+        qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+        mesh = fu.make_mesh(n, r)
+        opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False)
+        wb = fu.peer_window_bytes(n, r, (1, h, s // n, 128), torch.bfloat16, opts)
+
+        def prog(ctx):
+            ctx.enable_peer_memory(wb)
+            outs = [fu.usp_attention(ctx, qs[ctx.rank()], ks[ctx.rank()], vs[ctx.rank()], mesh, opts).clone()
+                    for _ in range(3)]
+            ctx.synchronize()
+            return outs, ctx.traffic(), ctx.peer_stats()
+
+        res, err = nccl_world(n, prog)
+        if any(e is not None for e in err):
+            emit(check=f"peer_n{n}_r{r}", ok=False, error=repr([e for e in err if e][0]))
+            continue
+        loc = fu.run_protocol(n, lambda ctx: (fu.usp_attention(
+            ctx, qs[ctx.rank()], ks[ctx.rank()], vs[ctx.rank()], mesh, opts), ctx.traffic()))
+        same = all(torch.equal(o, b[0]) for a, b in zip(res, loc.results) for o in a[0])
+        traffic_ok = all(a[1][0] == 3 * b[1][0] and a[1][1] == 3 * b[1][1] for a, b in zip(res, loc.results))
+        stats = [list(x[2]) for x in res]
+        emit(check=f"peer_n{n}_r{r}_fp8{int(fp8)}", ok=bool(same and traffic_ok and all(st == [3, 0] for st in stats)),
+             bit_identical_to_local=same, traffic_ok=traffic_ok, stats=stats)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("all", "usp"):
@@ -169,3 +201,5 @@ if __name__ == "__main__":
         subgroups()
     if which in ("all", "dead"):
         dead_peer()
+    if which in ("all", "peer"):
+        peer_cases()

@@ -109,6 +109,29 @@ def test_quantize_blocks_equal_reference_per_slice(cuda, fu, dtype):
     assert np.array_equal(back, R.fake_quant(t, per_block=True))
 
 
+def test_quantize_words_reset_between_calls(cuda, fu):
+    # the amax pass finalizes the scales in its last CTA and leaves its zero words zero: a large
+    # amax followed by a small one (and block counts that change) must each be bit-exact, and
+    # so must the ring-hop requantize of the multi-scale codes just produced
+    for i, (lo, hi, block) in enumerate([(-300, 300, 64 * 128), (-0.01, 0.01, 64 * 128),
+                                         (-5, 5, 4 * 64 * 128), (-1e-3, 1e-3, 2 * 64 * 128)]):
+        t = R.round_bf16(R.rng_tensor(500 + i, (1, 4, 64, 128), lo, hi))
+        nb = t.size // block
+        flat = t.reshape(nb, block)
+        for _ in range(2):
+            codes, scales = fu.quantize_blocks(T(t, torch.bfloat16), block)
+            codes, scales = codes.cpu().numpy().reshape(nb, block), scales.cpu().numpy()
+            for j in range(nb):
+                c, sc = R.quantize(flat[j:j + 1])
+                assert np.array_equal(codes[j], c.reshape(-1)) and scales[j] == sc
+        deq = np.concatenate([R.dequantize(codes[j], scales[j]) for j in range(nb)])
+        wc, ws = R.quantize(deq)
+        for _ in range(2):
+            q2 = fu.requantize(T(codes.reshape(-1), torch.uint8), T(scales[:nb]), block)
+            assert np.array_equal(q2.codes.cpu().numpy().reshape(-1), wc.reshape(-1))
+            assert q2.scale == ws
+
+
 def test_quantize_rejects_non_finite_like_reference(cuda, fu):
     t = torch.zeros(1, 1, 2, 8, device="cuda")
     t[0, 0, 1, 3] = float("inf")

@@ -50,3 +50,8 @@ def test_nccl_backend_subgroups(cuda, fu):
 def test_nccl_dead_peer_raises_deadlock(cuda, fu):
     lines, p = run("dead")
     assert all(x["ok"] for x in lines), (lines, p.stderr[-2000:])
+
+
+def test_nccl_backend_peer_windows(cuda, fu):
+    lines, p = run("peer")
+    assert len(lines) == 3 and all(x["ok"] for x in lines), (lines, p.stderr[-2000:])

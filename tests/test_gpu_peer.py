@@ -1,0 +1,226 @@
+"""GPU: the peer-memory Ulysses transport (fusp_ctx_peer_enable, csrc/peer.cu).
+
+With peer windows the two Ulysses reshards of a USP layer (protocols.cpp:125-203) are fused into
+the kernels around them: the pack kernel stores every member's slot straight into that member's
+window, the attention epilogue stores O / LSE rows straight into their owner's window, and one
+signal-and-wait kernel per reshard replaces the all-to-all.  Ranks are threads on cuda:0 here (a
+window of another rank is then plain device memory: the same kernels and the same protocol as
+over NVLink).  The transport must not change a single bit: outputs, LSE and TrafficLog bytes are
+compared with the same layer over the in-process fabric, and with the reference's output."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import restate as R
+from oracle.make_golden import qkv
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def shards(x, n, dtype=torch.bfloat16):
+    return [torch.from_numpy(np.ascontiguousarray(s)).cuda().to(dtype) for s in R.split_sequence(x, n)]
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def window(fu, n, r, sl, h=8, opts=None):
+    return fu.peer_window_bytes(n, r, (1, h, sl, 128), torch.bfloat16, opts)
+
+
+def layer(fu, qs, ks, vs, mesh, opts, peer_bytes=0, lse=False):
+    """One USP layer per rank; per rank (output or (out, lse), traffic, peer stats)."""
+    def prog(ctx):
+        if peer_bytes:
+            ctx.enable_peer_memory(peer_bytes)
+        q, k, v = qs[ctx.rank()], ks[ctx.rank()], vs[ctx.rank()]
+        if lse:
+            a = fu.usp_attention_with_lse(ctx, q, k, v, mesh, opts)
+            out = (a.out.clone(), a.lse.clone())
+        else:
+            out = fu.usp_attention(ctx, q, k, v, mesh, opts).clone()
+        ctx.synchronize()
+        return [out], ctx.traffic(), ctx.peer_stats() if peer_bytes else None
+    return fu.run_protocol(len(qs), prog)
+
+
+@pytest.mark.parametrize("n,r,fp8,block", [(2, 1, False, 0), (4, 1, False, 0), (8, 1, False, 0),
+                                           (4, 2, False, 0), (8, 2, False, 0), (4, 1, True, 0),
+                                           (8, 1, True, 1), (8, 4, True, 0)])
+def test_peer_usp_bit_identical_to_fabric(cuda, fu, n, r, fp8, block):
+    h, s = 8, 128 * n
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(200 + n, 201 + r, 202 + int(fp8)))
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(fp8_kv=fp8, fp8_block=block, pipelined_ring=True, check_finite=False,
+                          out_dtype=torch.float32)
+    ref = layer(fu, qs, ks, vs, mesh, opts)
+    got = layer(fu, qs, ks, vs, mesh, opts, peer_bytes=window(fu, n, r, s // n, h, opts))
+    for a, b in zip(got.results, ref.results):
+        assert torch.equal(a[0][0], b[0][0])
+        assert a[1] == b[1]                   # TrafficLog bytes: the transport is invisible
+        assert a[2] == (1, 0) if n // r > 1 else True  # the layer took the peer path
+    out = torch.cat([x[0][0] for x in got.results], dim=2).cpu().numpy()
+    want = R.usp_attention(q, k, v, n, r, fp8=True, per_block=bool(block)) if fp8 \
+        else R.attention_with_lse(q, k, v)[0]
+    assert rel_l2(out, want) <= (2e-3 if fp8 else 1e-3)
+
+
+def test_peer_lse_and_output_dtypes(cuda, fu):
+    n, h, s = 4, 8, 512
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(211, 212, 213))
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    mesh = fu.make_mesh(n, 1)
+    for odt in (torch.float16, torch.bfloat16, torch.float32):
+        opts = fu.CommOptions(check_finite=False, out_dtype=odt)
+        ref = layer(fu, qs, ks, vs, mesh, opts, lse=True)
+        got = layer(fu, qs, ks, vs, mesh, opts, peer_bytes=window(fu, n, 1, s // n, h, opts), lse=True)
+        for a, b in zip(got.results, ref.results):
+            assert torch.equal(a[0][0][0], b[0][0][0]) and torch.equal(a[0][0][1], b[0][0][1])
+
+
+def test_peer_batch2(cuda, fu):
+    # B > 1: the output region is [member][B][hp][SL][D] and is concatenated over heads
+    n, h, s = 4, 8, 256
+    q, k, v = qkv((2, h, s, 128), (2, h, s, 128), seeds=(221, 222, 223))
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float32)
+    wb = fu.peer_window_bytes(n, 1, (2, h, s // n, 128), torch.bfloat16, opts)
+    ref = layer(fu, qs, ks, vs, mesh, opts, lse=True)
+    got = layer(fu, qs, ks, vs, mesh, opts, peer_bytes=wb, lse=True)
+    for a, b in zip(got.results, ref.results):
+        assert torch.equal(a[0][0][0], b[0][0][0]) and torch.equal(a[0][0][1], b[0][0][1])
+        assert a[2] == (1, 0)
+
+
+def test_peer_back_to_back_layers_no_buffer_race(cuda, fu):
+    # single-buffered windows: consecutive layers reuse every member's regions; a rank that
+    # runs ahead must never overwrite data a slower member has not consumed (peer.cu header).
+    # 12 layers with different inputs per layer, 8 ranks racing on one GPU.
+    n, h, s = 8, 8, 1024
+    probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(300 + i, 400 + i, 500 + i)) for i in range(3)]
+    per = [[shards(t, n) for t in p] for p in probs]
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float16)
+    wb = window(fu, n, 1, s // n, h, opts)
+
+    def prog(peer):
+        def body(ctx):
+            if peer:
+                ctx.enable_peer_memory(wb)
+            outs = []
+            for i in range(12):
+                q, k, v = (t[ctx.rank()] for t in per[i % 3])
+                outs.append(fu.usp_attention(ctx, q, k, v, mesh, opts).clone())
+            ctx.synchronize()
+            return outs, ctx.peer_stats() if peer else None
+        return fu.run_protocol(n, body)
+
+    ref, got = prog(False), prog(True)
+    for a, b in zip(got.results, ref.results):
+        assert a[1] == (12, 0)
+        for x, y in zip(a[0], b[0]):
+            assert torch.equal(x, y)
+
+
+def test_peer_other_group_falls_back(cuda, fu):
+    # the windows serve the first group they were used with; a layer over another group goes
+    # through the fabric (counted), still correct
+    n, h, s = 4, 4, 256
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(231, 232, 233))
+    full = shards(q, n), shards(k, n), shards(v, n)
+    halves = [shards(t, 2) for t in (q, k, v)]
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(check_finite=False)
+    wb = window(fu, n, 1, s // n, h, opts)
+
+    def prog(ctx):
+        ctx.enable_peer_memory(wb)
+        a = fu.usp_attention(ctx, *(t[ctx.rank()] for t in full), mesh, opts)
+        g = [0, 1] if ctx.rank() < 2 else [2, 3]
+        ctx.create_group(g)
+        b = fu.ulysses_attention(ctx, *(t[g.index(ctx.rank())] for t in halves), group=fu.ProcessGroup(g))
+        ctx.synchronize()
+        return a, b, ctx.peer_stats()
+
+    rep = fu.run_protocol(n, prog)
+    want = R.attention_with_lse(q, k, v)[0]
+    got = torch.cat([x[0].float() for x in rep.results], dim=2).cpu().numpy()
+    assert rel_l2(got, want) <= 1e-3
+    for m in (0, 2):
+        sub = torch.cat([rep.results[m][1].float(), rep.results[m + 1][1].float()], dim=2).cpu().numpy()
+        assert rel_l2(sub, want) <= 1e-3
+    assert all(x[2] == (1, 1) for x in rep.results)
+
+
+def test_peer_graph_capture_multi_rank(cuda, fu):
+    # a peer-path layer at ring_dim 1 needs no host rendezvous: capturable on in-process
+    # ranks (the fabric path is not); 3 replays with new inputs each match eager
+    n, h, s = 4, 8, 512
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float16)
+    wb = window(fu, n, 1, s // n, h, opts)
+    probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(240 + i, 250 + i, 260 + i)) for i in range(3)]
+    per = [[shards(t, n) for t in p] for p in probs]
+
+    def prog(ctx):
+        ctx.enable_peer_memory(wb)
+        r = ctx.rank()
+        q, k, v = (per[0][t][r].clone() for t in range(3))
+        out = torch.empty_like(q, dtype=torch.float16)
+        g = fu.LayerGraph(ctx, q[None], k[None], v[None], out[None], mesh, opts, 1)
+        res = []
+        for i in range(3):
+            for dst, t in zip((q, k, v), range(3)):
+                dst.copy_(per[i][t][r])
+            g.launch()
+            res.append(out.clone())
+            eager = fu.usp_attention(ctx, per[i][0][r], per[i][1][r], per[i][2][r], mesh, opts)
+            res.append(eager.clone())
+        ctx.synchronize()
+        g.close()
+        return res
+
+    rep = fu.run_protocol(n, prog)
+    for r in rep.results:
+        for i in range(3):
+            assert torch.equal(r[2 * i], r[2 * i + 1])
+
+
+def test_peer_stalled_member_raises_deadlock(cuda, fu):
+    # a member that never joins: the exchange kernel's bounded spin sets the timeout flag and
+    # fusp_ctx_synchronize raises DeadlockError instead of hanging (FUSP_TIMEOUT_S=3)
+    code = r"""
+import threading, torch, paper_2602_10940_b200 as fu
+q = torch.randn(1, 4, 128, 128, device="cuda", dtype=torch.bfloat16)
+mesh = fu.make_mesh(2, 1)
+opts = fu.CommOptions(check_finite=False)
+wb = fu.peer_window_bytes(2, 1, (1, 4, 128, 128))
+done = threading.Event()
+def prog(ctx):
+    ctx.enable_peer_memory(wb)
+    if ctx.rank() == 1:  # joins the setup, never the layer; keeps its window alive meanwhile
+        done.wait(120)
+        return "absent"
+    try:
+        fu.usp_attention(ctx, q, q, q, mesh, opts)
+        ctx.synchronize()
+    except fu.DeadlockError as e:
+        return "DeadlockError: " + str(e)
+    finally:
+        done.set()
+    return "no error"
+print(fu.run_protocol(2, prog).results[0])
+"""
+    env = dict(os.environ, FUSP_TIMEOUT_S="3", PYTHONPATH=os.path.dirname(HERE))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+    assert "DeadlockError: deadlock: rank 0" in p.stdout, p.stdout + p.stderr[-2000:]

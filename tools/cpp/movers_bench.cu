@@ -107,7 +107,7 @@ int main() {
     report(nm, 3.0 * n * 4, [&] { launch_unpack_multi(u, 3, 0); });
     // FP8: K and V amax + quantize (per-tensor block), codes into a buffer
     uint8_t *ck, *cv; float* sc; uint32_t* wk;
-    CK(cudaMalloc(&ck, n)); CK(cudaMalloc(&cv, n)); CK(cudaMalloc(&sc, 4096)); CK(cudaMalloc(&wk, 4096));
+    CK(cudaMalloc(&ck, n)); CK(cudaMalloc(&cv, n)); CK(cudaMalloc(&sc, 4096)); CK(cudaMalloc(&wk, 4096)); CK(cudaMemset(wk, 0, 4096));  // zero words (the amax pass leaves them zero)
     Fp8Src src[2] = {Fp8Src{k, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}, Fp8Src{v, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}};
     uint32_t* works[2] = {wk, wk + 64};
     float* scs[2] = {sc, sc + 64};

@@ -134,6 +134,51 @@ def hbm(path, dest, peak_gbs=None):
     print(dest)
 
 
+def movers(rep, dest, peak_gbs=None):
+    """One row per launch of a --set full capture: duration, DRAM bytes, achieved GB/s, issue
+    activity and the top warp-stall reasons (smsp__average_warps_issue_stalled_*)."""
+    if peak_gbs is None:
+        try:
+            peak_gbs = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+        except (OSError, ValueError, KeyError):
+            peak_gbs = 7700.0
+    rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
+             "msecond": 1e3}
+
+    def val(vals, key):
+        if key not in hdr:
+            return 0.0
+        i = hdr.index(key)
+        try:
+            return float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+        except ValueError:
+            return 0.0
+    stall = [k for k in hdr if k.startswith("smsp__average_warps_issue_stalled_")
+             and k.endswith("_per_issue_active.ratio") and "not_issued" not in k]
+    lines = [f"# ncu --set full, one row per launch: `{rep}`", "",
+             f"DRAM GB/s = (dram__bytes_read + dram__bytes_write) / gpu__time_duration; peak {peak_gbs} "
+             "GB/s (MEASURED_PEAKS.json). Cold caches (ncu --cache-control all), serialised.", "",
+             "| # | kernel | grid | us | DRAM MB | GB/s | of peak | issue active % | top stalls (warps per issue) |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    for n, vals in enumerate(rows[2:]):
+        name = re.sub(r"\(.*", "", vals[hdr.index("Kernel Name")]).replace("fusp::<unnamed>::", "")[:40]
+        us = val(vals, "gpu__time_duration.sum")
+        mb = (val(vals, "dram__bytes_read.sum") + val(vals, "dram__bytes_write.sum")) / 1e6
+        gbs = mb * 1e6 / (us * 1e3) if us else 0.0
+        issue = val(vals, "sm__inst_issued.avg.pct_of_peak_sustained_active")
+        st = sorted(((val(vals, k), k) for k in stall), reverse=True)[:3]
+        sts = ", ".join(f"{k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]} {v:.1f}"
+                        for v, k in st if v > 0)
+        grid = vals[hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else ""
+        lines.append(f"| {n} | `{name}` | {grid} | {us:.2f} | {mb:.2f} | {gbs:.0f} | "
+                     f"{gbs / peak_gbs * 100:.0f}% | {issue:.1f} | {sts} |")
+    with open(dest, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print(dest)
+
+
 if __name__ == "__main__":
     mode, src, dst = sys.argv[1:4]
-    {"full": full, "launches": launches, "hbm": hbm}[mode](src, dst)
+    {"full": full, "launches": launches, "hbm": hbm, "movers": movers}[mode](src, dst)
