@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <vector>
+
 #include "fastusp_internal.h"
 
 namespace fusp {
@@ -181,6 +183,11 @@ fusp_status launch_attention_generic(const AttnLaunch& a, cudaStream_t stream) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "attn_generic_kernel launch");
   return FUSP_OK;
+}
+
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_attention_generic(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(attn_generic_kernel));
 }
 
 }  // namespace fusp

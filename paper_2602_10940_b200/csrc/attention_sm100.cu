@@ -1767,4 +1767,11 @@ void set_attention_schedule(int mode, int max_ctas) {
   g_max_ctas = max_ctas;
 }
 
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_attention(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(attn_fwd_kernel));
+  v.push_back(reinterpret_cast<const void*>(attn_kv2_kernel<false>));
+  v.push_back(reinterpret_cast<const void*>(attn_kv2_kernel<true>));
+}
+
 }  // namespace fusp

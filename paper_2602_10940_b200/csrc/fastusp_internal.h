@@ -30,6 +30,8 @@ void count_launch(int n = 1);
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) attribute: set it
 // once per (kernel, device), thread-safely, before the first launch on that device.
 fusp_status ensure_smem_attr(const void* kernel, int bytes, const char* name);
+// Load every kernel of the library on the current device now (lazy module loading; runtime.cpp).
+fusp_status preload_kernels();
 
 // ---- TMA descriptors ------------------------------------------------------------------
 // 3-D map over [heads][rows][128] 16-bit elements with a head stride of `head_stride`
@@ -49,6 +51,9 @@ struct QkvDst {  // where the QKV projection writes: plain [B][H][S][128] (u = 1
   int qk_dtype, v_dtype;
   int u;
   int64_t slot_stride;  // elements between slots
+  // Peer-memory Ulysses (csrc/peer.cu): slot t lives in member t's window, slot_boff[t] bytes
+  // from slot 0 (q / k / v address slot 0); null = t * slot_stride in one buffer
+  const int64_t* slot_boff = nullptr;
 };
 fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, const void* w, int heads,
                                const QkvDst& dst, const float* wq, const float* wk, float eps,

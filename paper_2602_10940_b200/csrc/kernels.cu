@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <vector>
+
 #include "fastusp_internal.h"
 
 namespace fusp {
@@ -947,25 +949,49 @@ __global__ void stage_scalar_kernel(const __grid_constant__ StageArgs a, int64_t
   }
 }
 
+// Unsigned division by a run-time constant as a multiply-high and a shift (x < 2^31):
+// l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1, x / d = (umulhi(x, m) + x) >> l.  The
+// E4M3 sources look up a per-segment scale for every 8 codes; three hardware-less 32-bit
+// divisions per vector made those passes instruction-bound (ncu: issue-active 50 %).
+struct FDiv {
+  uint32_t d, m;
+  int l;
+};
+inline FDiv make_fdiv(uint32_t d) {
+  int l = 0;
+  while ((uint64_t(1) << l) < d) ++l;
+  return FDiv{d, static_cast<uint32_t>(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1), l};
+}
+__device__ __forceinline__ uint32_t fdiv(const FDiv& f, uint32_t x) {
+  return (__umulhi(x, f.m) + x) >> f.l;
+}
+struct Fp8Div {  // i / d, row / span, r / seg_rows of an Fp8Src
+  FDiv d, span, seg;
+};
+inline Fp8Div make_fp8div(const Fp8Src& s) {
+  return Fp8Div{make_fdiv(uint32_t(s.d)), make_fdiv(uint32_t(s.span)), make_fdiv(uint32_t(s.seg_rows))};
+}
+// Scale of the segment holding element i of an E4M3 source.
+__device__ __forceinline__ float e4m3_scale(const Fp8Src& s, const Fp8Div& dv, int64_t i) {
+  const uint32_t row = fdiv(dv.d, static_cast<uint32_t>(i));
+  const uint32_t bh = fdiv(dv.span, row);
+  const uint32_t r = row - bh * static_cast<uint32_t>(s.span);
+  return s.scales[int64_t(fdiv(dv.seg, r)) * s.seg_stride + int64_t(bh) * s.bh_stride];
+}
+
 // Source value of 8 consecutive elements (one row segment) for the FP8 passes.
-__device__ __forceinline__ Vec8 src_vec8(const Fp8Src& s, int64_t i) {  // i < 2^31 (launcher)
+__device__ __forceinline__ Vec8 src_vec8(const Fp8Src& s, const Fp8Div& dv, int64_t i) {  // i < 2^31
   if (s.dt != FUSP_E4M3) return load8(s.x, s.dt, i);
-  const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
-  const uint32_t bh = row / static_cast<uint32_t>(s.span);
-  const int r = static_cast<int>(row - bh * s.span);
-  const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
-  return decode8(__ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i)), sc);
+  return decode8(__ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i)),
+                 e4m3_scale(s, dv, i));
 }
 
 // |value| maximum of 8 codes of an E4M3 source in one step: decode(c) * scale is monotone in
 // the code magnitude (sign-magnitude encoding, RN multiply), so the maximum is the decoded
 // largest magnitude -- a byte-SIMD max and one decode instead of eight.  A NaN code (0x7F)
 // is the largest magnitude and decodes to NaN, which the caller flags as non-finite.
-__device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, int64_t i) {
-  const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
-  const uint32_t bh = row / static_cast<uint32_t>(s.span);
-  const int r = static_cast<int>(row - bh * s.span);
-  const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
+__device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, const Fp8Div& dv, int64_t i) {
+  const float sc = e4m3_scale(s, dv, i);
   const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i));
   uint32_t m = __vmaxu4(w.x & 0x7F7F7F7Fu, w.y & 0x7F7F7F7Fu);
   m = max(max(m & 0xFFu, (m >> 8) & 0xFFu), max((m >> 16) & 0xFFu, m >> 24));
@@ -977,6 +1003,7 @@ __device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, int64_t i) {
 // Pass 1 per block, 8 elements per step; grid.y = block, grid.z = tensor (K, V).
 struct AmaxArgs {
   Fp8Src src[2];
+  Fp8Div div[2];
   uint32_t* amax[2];  // zero on entry when `ticket` is set (the finalize leaves them zero)
   int64_t block_vecs;
   uint32_t* nonfinite;
@@ -996,7 +1023,7 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if (s.dt == FUSP_E4M3) {
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
-      const float x = e4m3_vec_absmax(s, (base + v) * 8);
+      const float x = e4m3_vec_absmax(s, a.div[blockIdx.z], (base + v) * 8);
       nf = fmaf(x, 0.f, nf);
       m = fmaxf(m, x);
     }
@@ -1005,7 +1032,7 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
     Vec8 x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (v + u * stride < a.block_vecs) x[u] = src_vec8(s, (base + v + u * stride) * 8);
+      if (v + u * stride < a.block_vecs) x[u] = src_vec8(s, a.div[blockIdx.z], (base + v + u * stride) * 8);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (v + u * stride >= a.block_vecs) break;
@@ -1059,6 +1086,7 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
 // codes = encode(x / scale), IEEE division (fp8.cpp:119-121).
 struct QuantArgs {
   Fp8Src src[2];
+  Fp8Div div[2];
   const uint32_t* amax[2];   // scale = amax / 448 (1 if 0), written to scales[] ...
   const float* qscale[2];    // ... or, when set, the scale the amax pass finalized
   float* scales[2];
@@ -1091,10 +1119,7 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
     // first hop every segment of a chunk shares the chunk's scale, so later hops are copies.
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
       const int64_t i = (base + v) * 8;
-      const uint32_t row = static_cast<uint32_t>(i) / static_cast<uint32_t>(s.d);
-      const uint32_t bh = row / static_cast<uint32_t>(s.span);
-      const int r = static_cast<int>(row - bh * s.span);
-      const float sc = s.scales[(r / s.seg_rows) * s.seg_stride + bh * s.bh_stride];
+      const float sc = e4m3_scale(s, a.div[z], i);
       const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.x) + i));
       *reinterpret_cast<uint2*>(a.codes[z] + i) = sc == qs ? w : encode8_finite(decode8(w, sc), qs, inv);
     }
@@ -1104,7 +1129,7 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
     Vec8 x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (v + u * stride < a.block_vecs) x[u] = src_vec8(a.src[z], (base + v + u * stride) * 8);
+      if (v + u * stride < a.block_vecs) x[u] = src_vec8(a.src[z], a.div[z], (base + v + u * stride) * 8);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (v + u * stride < a.block_vecs)
@@ -1114,12 +1139,12 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
 
 __global__ void __launch_bounds__(256) dequantize_vec_kernel(const uint8_t* __restrict__ c,
                                                              const float* __restrict__ scales,
-                                                             int64_t block_vecs, int64_t n_vecs,
+                                                             FDiv block_vecs, int64_t n_vecs,
                                                              void* __restrict__ y, int ydt) {
   for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n_vecs;
        v += int64_t(gridDim.x) * blockDim.x)
     store8(y, ydt, v * 8, decode8(__ldg(reinterpret_cast<const uint2*>(c + v * 8)),
-                                  scales[static_cast<uint32_t>(v) / static_cast<uint32_t>(block_vecs)]));
+                                  scales[fdiv(block_vecs, static_cast<uint32_t>(v))]));
 }
 
 }  // namespace
@@ -1453,6 +1478,7 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
       block_elems * nblocks < (int64_t(1) << 31)) {
     AmaxArgs a{};
     a.src[0] = src;
+    a.div[0] = make_fp8div(src);
     a.amax[0] = amax;
     a.block_vecs = block_elems / 8;
     a.nonfinite = nonfinite;
@@ -1522,6 +1548,7 @@ fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems,
   AmaxArgs a{};
   for (int p = 0; p < parts; ++p) {
     a.src[p] = src[p];
+    a.div[p] = make_fp8div(src[p]);
     a.amax[p] = amax[p];
   }
   a.block_vecs = block_elems / 8;
@@ -1555,6 +1582,7 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
   QuantArgs q{};
   for (int p = 0; p < parts; ++p) {
     q.src[p] = src[p];
+    q.div[p] = make_fp8div(src[p]);
     q.qscale[p] = scales[p];
     q.codes[p] = codes[p];
   }
@@ -1572,6 +1600,7 @@ fusp_status launch_amax_scales(const Fp8Src* src, int parts, int64_t block_elems
   AmaxArgs a{};
   for (int p = 0; p < parts; ++p) {
     a.src[p] = src[p];
+    a.div[p] = make_fp8div(src[p]);
     a.amax[p] = work[p];
     a.scales[p] = scales[p];
   }
@@ -1602,7 +1631,8 @@ fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int6
   if (n <= 0) return FUSP_OK;
   if (n % 8 == 0 && block_elems % 8 == 0 && aligned16(c) && aligned16(y) && ydt != FUSP_E4M3 &&
       n < (int64_t(1) << 31)) {
-    dequantize_vec_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(c, scales, block_elems / 8, n / 8, y, ydt);
+    dequantize_vec_kernel<<<grid_for(n / 8), kBlock, 0, s>>>(c, scales, make_fdiv(uint32_t(block_elems / 8)),
+                                                              n / 8, y, ydt);
     FUSP_LAUNCHED("dequantize_vec_kernel");
     return FUSP_OK;
   }
@@ -1647,6 +1677,37 @@ fusp_status launch_fp8_forward_scales(float* const* scales, int parts, int n, cu
   fp8_forward_scales_kernel<<<parts, 256, 0, s>>>(scales[0], parts > 1 ? scales[1] : scales[0], n);
   FUSP_LAUNCHED("fp8_forward_scales_kernel");
   return FUSP_OK;
+}
+
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_kernels(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(convert_kernel));
+  v.push_back(reinterpret_cast<const void*>(bf16_to_f16_kernel));
+  v.push_back(reinterpret_cast<const void*>(encode_kernel));
+  v.push_back(reinterpret_cast<const void*>(decode_kernel));
+  v.push_back(reinterpret_cast<const void*>(amax_kernel));
+  v.push_back(reinterpret_cast<const void*>(quantize_kernel));
+  v.push_back(reinterpret_cast<const void*>(dequantize_kernel));
+  v.push_back(reinterpret_cast<const void*>(merge_kernel));
+  v.push_back(reinterpret_cast<const void*>(fill_kernel));
+  v.push_back(reinterpret_cast<const void*>(pack_kernel));
+  v.push_back(reinterpret_cast<const void*>(unpack_kernel));
+  v.push_back(reinterpret_cast<const void*>(unpack_heads_kernel));
+  v.push_back(reinterpret_cast<const void*>(amax_blocks_kernel));
+  v.push_back(reinterpret_cast<const void*>(finalize_scales_kernel));
+  v.push_back(reinterpret_cast<const void*>(quantize_blocks_kernel));
+  v.push_back(reinterpret_cast<const void*>(dequantize_blocks_kernel));
+  v.push_back(reinterpret_cast<const void*>(scatter_slot_scales_kernel));
+  v.push_back(reinterpret_cast<const void*>(finite_kernel));
+  v.push_back(reinterpret_cast<const void*>(pack_slab_kernel));
+  v.push_back(reinterpret_cast<const void*>(unpack_slab_kernel));
+  v.push_back(reinterpret_cast<const void*>(stage_kernel));
+  v.push_back(reinterpret_cast<const void*>(stage_decide_kernel));
+  v.push_back(reinterpret_cast<const void*>(stage_scalar_kernel));
+  v.push_back(reinterpret_cast<const void*>(amax_vec_kernel));
+  v.push_back(reinterpret_cast<const void*>(quantize_vec_kernel));
+  v.push_back(reinterpret_cast<const void*>(dequantize_vec_kernel));
+  v.push_back(reinterpret_cast<const void*>(fp8_forward_scales_kernel));
 }
 
 }  // namespace fusp

@@ -22,7 +22,10 @@
 
 #include <unistd.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace fusp {
 namespace {
@@ -92,7 +95,11 @@ fusp_status peer_window_create(PeerWindow* w, int rank, int world, int device, s
   w->world = world;
   w->data_bytes = (data_bytes + 255) / 256 * 256;
   FUSP_CUDA(cudaMalloc(&w->base, kPeerCtlBytes + w->data_bytes));
+  // The zeroed control words must be in memory before the handle leaves this rank: a member's
+  // first signal (from its own non-blocking stream, unordered with this memset's stream) could
+  // otherwise land before the memset and be wiped -- a lost signal, i.e. a deadlock.
   FUSP_CUDA(cudaMemset(w->base, 0, kPeerCtlBytes));
+  FUSP_CUDA(cudaDeviceSynchronize());
   std::memset(mine, 0, sizeof(*mine));
   mine->magic = kPeerMagic;
   mine->pid = static_cast<int32_t>(getpid());
@@ -166,10 +173,25 @@ fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_
   uint32_t err = 0;  // (stream-ordered: a legacy-stream copy could wait on other ranks' spins)
   FUSP_CUDA(cudaMemcpyAsync(&err, w.ctl(w.rank) + 4 * kPeerMaxWorld, 4, cudaMemcpyDeviceToHost, s));
   FUSP_CUDA(cudaStreamSynchronize(s));
+  if (err && getenv("FUSP_PEER_DEBUG") != nullptr) {  // post-mortem: who signalled whom
+    std::vector<uint32_t> ctl(5 * kPeerMaxWorld);
+    cudaMemcpy(ctl.data(), w.ctl(w.rank), ctl.size() * 4, cudaMemcpyDeviceToHost);
+    for (int kind = 0; kind < 2; ++kind) {
+      fprintf(stderr, "[peer] rank %d kind %d sig/expect:", w.rank, kind);
+      for (int r = 0; r < w.world; ++r)
+        fprintf(stderr, " %u/%u", ctl[kind * kPeerMaxWorld + r], ctl[(2 + kind) * kPeerMaxWorld + r]);
+      fprintf(stderr, "\n");
+    }
+  }
   if (err)
     return set_error(FUSP_ERR_DEADLOCK, std::string("deadlock: rank ") + std::to_string(w.rank) +
                                             " stalled in " + what + " (peer-memory exchange timed out)");
   return FUSP_OK;
+}
+
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_peer(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(peer_exchange_kernel));
 }
 
 }  // namespace fusp

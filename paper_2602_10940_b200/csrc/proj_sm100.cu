@@ -19,6 +19,8 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <vector>
+
 #include "fastusp_internal.h"
 #include "sm100_ptx.cuh"
 
@@ -63,6 +65,8 @@ struct ProjParams {
   int part_dt[3];       // Q, K, V output dtypes (bf16 / f16)
   int u;                // Ulysses slots: head h -> slot h / (heads / u), position h % (heads / u)
   int64_t slot_stride;  // elements between slots (u = 1: unused)
+  int peer;             // slot t at slot_eoff[t] elements from slot 0 (members' peer windows)
+  int64_t slot_eoff[kMaxPeerChunks];
   const float* norm_w[2];
   float eps;
   const float* cosv;
@@ -214,7 +218,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           const int64_t pos = p.pos0 + s;
           const int hp = p.heads / p.u, slot = head / hp, hl = head - slot * hp;
-          uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) + slot * p.slot_stride +
+          uint16_t* dst = static_cast<uint16_t*>(p.qkv[part]) +
+                          (p.peer ? p.slot_eoff[slot] : slot * p.slot_stride) +
                           ((static_cast<int64_t>(bb) * hp + hl) * p.s + s) * 128;
           const bool o_f16 = p.part_dt[part] == FUSP_F16;
           const int e4 = lane & 3;  // stores: the 4 lanes of a group write one row's 64-byte chunk
@@ -306,6 +311,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       tc_fence_before();
       mbar_arrive(&sm.acc_empty[ab]);
     }
+    // peer-memory slots: this thread's stores into other GPUs' windows are visible system-wide
+    // before the stream's exchange kernel signals the members
+    if constexpr (kQkv)
+      if (p.peer) __threadfence_system();
   }
   __syncwarp();
   tc_fence_before();
@@ -443,6 +452,15 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   p.part_dt[2] = dst.v_dtype;
   p.u = dst.u;
   p.slot_stride = dst.slot_stride;
+  if (dst.slot_boff != nullptr) {
+    if (dst.u > kMaxPeerChunks) return set_error(FUSP_ERR_UNSUPPORTED, "qkv projection: too many peer slots");
+    p.peer = 1;
+    for (int t = 0; t < dst.u; ++t) {
+      if (dst.slot_boff[t] % 16 != 0)
+        return set_error(FUSP_ERR_INVALID_ARGUMENT, "qkv projection: misaligned peer slot");
+      p.slot_eoff[t] = dst.slot_boff[t] / 2;
+    }
+  }
   p.norm_w[0] = wq;
   p.norm_w[1] = wk;
   p.eps = eps;
@@ -473,6 +491,14 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "qkv_proj kernel launch");
   return FUSP_OK;
+}
+
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_proj(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(out_proj_kernel<128, false>));
+  v.push_back(reinterpret_cast<const void*>(out_proj_kernel<128, true>));
+  v.push_back(reinterpret_cast<const void*>(out_proj_kernel<256, false>));
+  v.push_back(reinterpret_cast<const void*>(out_proj_kernel<256, true>));
 }
 
 }  // namespace fusp

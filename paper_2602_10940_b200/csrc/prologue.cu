@@ -13,6 +13,8 @@
 
 #include <cstdint>
 
+#include <vector>
+
 #include "fastusp_internal.h"
 
 namespace fusp {
@@ -143,6 +145,11 @@ fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
                                   int64_t pos0, cudaStream_t s) {
   const ProPack op{src, dst, w, cosv, sinv, sdt, ddt};
   return launch_norm_rope_pack_multi(&op, 1, slot_stride, b, h, sl, d, u, eps, pos0, s);
+}
+
+// Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
+void append_kernels_prologue(std::vector<const void*>& v) {
+  v.push_back(reinterpret_cast<const void*>(norm_rope_pack_kernel));
 }
 
 }  // namespace fusp

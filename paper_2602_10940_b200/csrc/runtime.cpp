@@ -50,6 +50,42 @@ fusp_status ensure_smem_attr(const void* kernel, int bytes, const char* name) {
   return FUSP_OK;
 }
 
+// With lazy module loading (CUDA_MODULE_LOADING=LAZY, the default since CUDA 12.2) the first
+// launch of a kernel loads it, and loading may synchronize the whole context.  A rank whose
+// peer-exchange kernel spins for another rank's signal (peer.cu) would then block every rank
+// sharing the context that launches a kernel for the first time -- a deadlock when that
+// launch is on the path to the awaited signal (ranks as threads of one process, or the
+// side stream of one rank).  So every kernel of the library is loaded up front, before the
+// first spinning kernel can exist (fusp_ctx_peer_window), once per device.
+void append_kernels_kernels(std::vector<const void*>& v);
+void append_kernels_attention(std::vector<const void*>& v);
+void append_kernels_attention_generic(std::vector<const void*>& v);
+void append_kernels_prologue(std::vector<const void*>& v);
+void append_kernels_proj(std::vector<const void*>& v);
+void append_kernels_peer(std::vector<const void*>& v);
+
+fusp_status preload_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return FUSP_OK;
+  std::vector<const void*> ks;
+  append_kernels_kernels(ks);
+  append_kernels_attention(ks);
+  append_kernels_attention_generic(ks);
+  append_kernels_prologue(ks);
+  append_kernels_proj(ks);
+  append_kernels_peer(ks);
+  for (const void* k : ks) {
+    cudaFuncAttributes a{};
+    FUSP_CUDA(cudaFuncGetAttributes(&a, k));
+  }
+  done.insert(dev);
+  return FUSP_OK;
+}
+
 // ---- TMA ------------------------------------------------------------------------------
 namespace {
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,

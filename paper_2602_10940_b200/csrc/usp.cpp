@@ -279,6 +279,9 @@ struct Layer {
   // Q, K, V were written into the layer's own buffers by a producer (fusp_usp_block's QKV
   // projection): the Ulysses pack (U > 1) or the operand conversion (U = 1) is skipped
   bool prepacked = false;
+  // consumer reads the output where it landed: with peer windows and B = 1 the output region
+  // of my window IS the output (concatenation over heads), so *out_view = it and no copy runs
+  const void** out_view = nullptr;
   // detail::ulysses_input_reshard (fusp_ulysses_input_reshard): the wire path runs even for a
   // one-member group and the unpack writes the caller's buffers in `reshard_dt`, unstaged
   bool force_wire = false;
@@ -420,13 +423,14 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
 // Whether this layer's Ulysses reshards go through the peer windows (the fused pack / epilogue
 // stores) or through c->comm.  The windows serve ONE Ulysses group per context (the hazard
 // argument in peer.cu needs every peer-path exchange of a rank to involve the same members):
-// the first eligible layer's group.  Not on the peer path: the QK prologue / producer variants
-// (their pack kernels write local slots), other head dims, wire debugging, layers larger than
-// any member's window.
+// the first eligible layer's group.  A producer (fusp_usp_block's QKV projection) stores into
+// the members' windows itself: GEMM epilogue and all-to-all in one kernel.  Not on the peer
+// path: the QK prologue variants (their pack kernels write local slots), other head dims, wire
+// debugging, layers larger than any member's window.
 bool plan_peer(fusp_ctx_s* c, Layer& l) {
   l.peer = false;
   if (!c->peer || !c->peer_open || !l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks || l.generic ||
-      l.pro != nullptr || l.prepacked || c->debug_wire)
+      l.pro != nullptr || c->debug_wire)
     return false;
   const std::string key = l.ug.key();
   if (!c->peer->group.empty() && c->peer->group != key) return false;
@@ -1042,7 +1046,8 @@ fusp_status ulysses_out(fusp_ctx_s* c, const Layer& l, Buffers& b, void* out, fl
     // the members' epilogues wrote my output region: signal mine, wait for theirs, then the
     // region is the concatenation over heads (B = 1: exactly `out`)
     FUSP_CHECK(launch_peer_exchange(*c->peer, 1, l.ug, sync_timeout_s(), s));
-    if (l.B == 1) FUSP_CUDA(cudaMemcpyAsync(out, b.recv_out, slot * l.U, cudaMemcpyDeviceToDevice, s));
+    if (l.B == 1 && l.out_view != nullptr && lse_out == nullptr) *l.out_view = b.recv_out;
+    else if (l.B == 1) FUSP_CUDA(cudaMemcpyAsync(out, b.recv_out, slot * l.U, cudaMemcpyDeviceToDevice, s));
   } else {
     FUSP_CHECK(c->comm->all_to_all(l.ug, b.send_out, b.recv_out, slot, slot, s));
   }
@@ -1154,6 +1159,7 @@ struct LayerCall {
   void *rq = nullptr, *rk = nullptr, *rv = nullptr;
   int rdt = FUSP_F32;
   const void* reshard_out = nullptr;  // detail::ulysses_output_reshard only: o -> out
+  const void** out_view = nullptr;    // see Layer::out_view (fusp_usp_block's out projection)
 };
 
 fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void* k,
@@ -1171,6 +1177,7 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   if (call == nullptr) call = &none;
   Layer l;
   FUSP_CHECK(plan_layer(c, mode, r, ls, in_dt, o, &l, call->grp));
+  l.out_view = call->out_view;
   if (call->reshard_in || call->reshard_out != nullptr) {
     l.force_wire = true;
     if (call->reshard_in) {
@@ -1225,7 +1232,13 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
   }
   if (produce != nullptr) {
     QkvDst d{};
-    if (l.U > 1) {  // straight into the Ulysses send slots: [Q blk][K blk][V blk] per slot
+    int64_t boff[kMaxPeerChunks] = {};
+    if (l.U > 1 && l.peer) {  // straight into my slot of every member's receive region
+      char* sbase = l.pw[0] + size_t(l.ug.pos) * l.slot_stride;
+      for (int t = 0; t < l.U; ++t) boff[t] = l.pw[t] - l.pw[0];
+      d = QkvDst{sbase, sbase + l.off_k, sbase + l.off_v, l.in_dt, l.in_dt, l.U,
+                 int64_t(l.slot_stride / l.w_in), boff};
+    } else if (l.U > 1) {  // straight into the Ulysses send slots: [Q blk][K blk][V blk] per slot
       d = QkvDst{b.send_in, b.send_in + l.off_k, b.send_in + l.off_v, l.in_dt, l.in_dt, l.U,
                  int64_t(l.slot_stride / l.w_in)};
     } else {        // the staging sources (Q, K: the attention operands themselves)
@@ -1374,6 +1387,8 @@ fusp_status fusp_ctx_peer_window(fusp_ctx c, size_t window_bytes, void* handle_o
   FUSP_CUDA(cudaDeviceSynchronize());
   auto w = std::make_unique<PeerWindow>();
   PeerHandle h{};
+  FUSP_CUDA(cudaSetDevice(c->device));
+  FUSP_CHECK(preload_kernels());  // no lazy module load may wait behind a spinning exchange
   FUSP_CHECK(peer_window_create(w.get(), c->rank, c->world, c->device, window_bytes, &h));
   std::memcpy(handle_out, &h, sizeof(h));
   c->peer = std::move(w);
@@ -1672,6 +1687,7 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
   }
   char* ws = static_cast<char*>(c->block_ws);
   void *q = ws, *k = ws + one, *v = ws + 2 * one, *attn = ws + 3 * one;
+  const void* attn_at = attn;
   fusp_comm_options o{};
   if (opts) o = *opts;
   o.out_dtype = x_dtype;  // the layer's output in the projection's input dtype
@@ -1688,14 +1704,20 @@ fusp_status fusp_usp_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x
     // the projection writes Q, K, V straight into the layer's Ulysses send slots (U = 1: the
     // attention operands, V already f16), so neither the pack nor the V conversion runs
     const Produce produce = qkv;
+    // with peer windows the QKV projection's epilogue stores into the members' windows (GEMM +
+    // input all-to-all in one kernel) and the out projection reads O where the members'
+    // attention epilogues put it (the window is not rewritten before this rank's next input
+    // exchange, which follows the out projection on this stream -- peer.cu)
+    LayerCall call;
+    call.out_view = &attn_at;
     FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st, false,
-                         nullptr, &produce));
+                         nullptr, &produce, &call));
   } else {
     FUSP_CHECK(qkv(QkvDst{q, k, v, x_dtype, x_dtype, 1, 0}));
     FUSP_CHECK(run_layer(c, Mode::kUsp, ring_dim, q, k, v, x_dtype, ls, attn, nullptr, &o, st));
   }
   // consumer: output projection
-  return fusp_out_projection(attn, x_dtype, ls, w_out, n_out, y, y_dtype, stream);
+  return fusp_out_projection(attn_at, x_dtype, ls, w_out, n_out, y, y_dtype, stream);
 }
 
 fusp_status fusp_group_create(fusp_ctx c, const int* members, int n, fusp_group* out) {

@@ -224,3 +224,41 @@ print(fu.run_protocol(2, prog).results[0])
     env = dict(os.environ, FUSP_TIMEOUT_S="3", PYTHONPATH=os.path.dirname(HERE))
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
     assert "DeadlockError: deadlock: rank 0" in p.stdout, p.stdout + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,r", [(2, 1), (4, 1), (8, 1), (4, 2), (8, 2)])
+def test_peer_block_producer_and_consumer(cuda, fu, n, r):
+    # fusp_usp_block on the peer path: the QKV projection's epilogue stores Q, K, V into the
+    # members' windows (GEMM and input all-to-all in one kernel) and the output projection
+    # reads O where the members' attention epilogues stored it (no copy-out).  Three blocks
+    # back to back with different inputs (single-buffered windows reused); bit-identical to
+    # the same blocks over the in-process fabric.
+    heads, s, c, nout = 8, 256 * n, 256, 256
+    rs = np.random.RandomState(70 + n + r)
+    xs_all = [R.round_bf16(rs.uniform(-1, 1, (1, s, c)).astype(np.float32)) for _ in range(3)]
+    wqkv = R.round_bf16((rs.uniform(-1, 1, (c, 3 * heads * 128)) / np.sqrt(c)).astype(np.float32))
+    wout = R.round_bf16((rs.uniform(-1, 1, (heads * 128, nout)) / np.sqrt(heads * 128)).astype(np.float32))
+    xs = [[torch.from_numpy(np.ascontiguousarray(t)).cuda().bfloat16() for t in np.split(x, n, axis=1)]
+          for x in xs_all]
+    wq_d, wo_d = torch.from_numpy(wqkv).cuda().bfloat16(), torch.from_numpy(wout).cuda().bfloat16()
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(check_finite=False)
+    wb = fu.peer_window_bytes(n, r, (1, heads, s // n, 128), torch.bfloat16,
+                              fu.CommOptions(check_finite=False, out_dtype=torch.bfloat16))
+
+    def prog(peer):
+        def body(ctx):
+            if peer:
+                ctx.enable_peer_memory(wb)
+            ys = [fu.usp_block(ctx, xs[i][ctx.rank()], wq_d, heads, wo_d, mesh, opts=opts,
+                               out_dtype=torch.float32).clone() for i in range(3)]
+            ctx.synchronize()
+            return ys, ctx.traffic(), ctx.peer_stats() if peer else None
+        return fu.run_protocol(n, body)
+
+    ref, got = prog(False), prog(True)
+    for a, b in zip(got.results, ref.results):
+        assert a[2] == (3, 0)       # every block's reshards took the peer path
+        assert a[1] == b[1]         # same TrafficLog bytes
+        for x, y in zip(a[0], b[0]):
+            assert torch.equal(x, y)
