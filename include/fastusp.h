@@ -189,10 +189,17 @@ fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms
  * LSE) rows straight into their owner's window, over NVLink / NVSwitch, each followed by one tiny
  * signal-and-wait kernel.  Results and TrafficLog bytes are identical to the comm path; the ring
  * (R > 1) still uses the context's backend.  Windows serve one Ulysses group per context (the
- * first layer's); other layers (other groups, the QK prologue / producer variants, D != 128,
- * wire debugging, shapes larger than a window) fall back to the backend -- counted by
- * fusp_ctx_peer_stats.  A peer-path layer at ring_dim 1 needs no host rendezvous, so it is
- * graph-capturable on any context.
+ * first layer's); other layers (other groups, the QK prologue variants, D != 128, wire
+ * debugging, shapes larger than a window) fall back to the backend -- counted by
+ * fusp_ctx_peer_stats.  fusp_usp_block's QKV projection is the producer on this path: its
+ * epilogue stores Q, K, V into the members' windows (GEMM and input all-to-all in one kernel),
+ * and its output projection reads O where the members' epilogues stored it.  A peer-path layer
+ * at ring_dim 1 needs no host rendezvous, so it is graph-capturable on any context.
+ * Every kernel of the library is loaded when the window is created (lazy module loading could
+ * otherwise synchronise the context behind a spinning exchange).  Ranks that are threads of one
+ * process sharing one device need a hardware queue per stream: CUDA_DEVICE_MAX_CONNECTIONS >=
+ * 2 x those ranks, set before CUDA initialises; fusp_ctx_peer_open refuses (FUSP_ERR_UNSUPPORTED)
+ * otherwise, since streams sharing a queue would wait behind another rank's spin.
  * fusp_ctx_peer_enable is collective over the world: every rank allocates `window_bytes` of
  * device memory (fusp_peer_window_bytes sizes it for a layer), the 128-byte handles are
  * all-gathered through the context's own backend and mapped (CUDA IPC between processes of one

@@ -17,6 +17,10 @@ namespace fusp {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef FUSP_FP8_UNROLL
+#define FUSP_FP8_UNROLL 8
+#endif
+constexpr int kFp8Unroll = FUSP_FP8_UNROLL;  // raw vectors in flight per thread (FP8 passes)
 
 // Programmatic dependent launch (PDL): the kernel may become resident while the previous
 // kernel on `s` drains; it must execute griddepcontrol.wait before touching that kernel's output.
@@ -454,6 +458,76 @@ __global__ void finite_kernel(const void* __restrict__ x, int dt, int64_t n, uin
 struct Vec8 {
   float f[8];
 };
+// Raw 8-element vector (16 B for 16-bit types, 32 B for f32) and its f32 values: the FP8 passes
+// issue every load of a thread's stride before converting any (bytes in flight per SM).
+struct Raw8 {  // 8 source elements as loaded: f32 = a,b; 16-bit = a; e4m3 = a.x, a.y
+  uint4 a, b;
+};
+__device__ __forceinline__ Raw8 load_raw8(const void* base, int sdt, int64_t i) {
+  Raw8 r;
+  if (sdt == FUSP_F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const float*>(base) + i);
+    r.a = __ldg(p);
+    r.b = __ldg(p + 1);
+  } else if (sdt == FUSP_E4M3) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(base) + i));
+    r.a = make_uint4(w.x, w.y, 0u, 0u);
+  } else {
+    r.a = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + i));
+  }
+  return r;
+}
+__device__ __forceinline__ Vec8 cvt8(const Raw8& r, int dt) {
+  Vec8 v;
+  const uint32_t w[8] = {r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, r.b.y, r.b.z, r.b.w};
+  if (dt == FUSP_F32) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v.f[e] = __uint_as_float(w[e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = dt == FUSP_F16 ? __half22float2(*reinterpret_cast<const __half2*>(&w[e]))
+                                      : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      v.f[2 * e] = x.x;
+      v.f[2 * e + 1] = x.y;
+    }
+  }
+  return v;
+}
+// |x| maximum of a raw vector on the bit patterns: sign-magnitude floats order like their
+// magnitude bits, so the maximum is an integer SIMD max (no conversions).  `mag` accumulates
+// magnitude bits (two 16-bit lanes, or one 32-bit value for f32); a vector holding a NaN
+// (magnitude bits above the infinity pattern) is left to the float path (fmaxf ignores NaN,
+// as the amax always did) and `inf_or_nan` is raised for it and for infinities.
+__device__ __forceinline__ bool absmax_raw8(const Raw8& r, int dt, uint32_t& mag, bool& inf_or_nan) {
+  if (dt == FUSP_F32) {
+    const uint32_t w[8] = {r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, r.b.y, r.b.z, r.b.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m = max(m, w[e] & 0x7FFFFFFFu);
+    if (m >= 0x7F800000u) {
+      inf_or_nan = true;
+      if (m > 0x7F800000u) return false;  // a NaN: float path
+    }
+    mag = max(mag, m);
+    return true;
+  }
+  const uint32_t inf2 = dt == FUSP_F16 ? 0x7C007C00u : 0x7F807F80u;
+  const uint32_t m = __vmaxu2(__vmaxu2(r.a.x & 0x7FFF7FFFu, r.a.y & 0x7FFF7FFFu),
+                              __vmaxu2(r.a.z & 0x7FFF7FFFu, r.a.w & 0x7FFF7FFFu));
+  if (__vcmpgeu2(m, inf2) != 0u) {
+    inf_or_nan = true;
+    if (__vcmpgtu2(m, inf2) != 0u) return false;
+  }
+  mag = __vmaxu2(mag, m);
+  return true;
+}
+__device__ __forceinline__ float mag_to_f32(uint32_t mag, int dt) {
+  if (dt == FUSP_F32) return __uint_as_float(mag);
+  const uint32_t h = max(mag & 0xFFFFu, mag >> 16);
+  return dt == FUSP_F16 ? __half2float(__ushort_as_half(static_cast<unsigned short>(h)))
+                        : __uint_as_float(h << 16);
+}
 __device__ __forceinline__ Vec8 load8(const void* base, int dt, int64_t i) {
   Vec8 v;
   if (dt == FUSP_F32) {
@@ -711,23 +785,6 @@ __global__ void __launch_bounds__(256) unpack_slab_kernel(const __grid_constant_
 }
 
 // ---- operand staging with the f16 range guard (fastusp_internal.h, StageOp) ---------------
-struct Raw8 {  // 8 source elements as loaded: f32 = a,b; 16-bit = a; e4m3 = a.x, a.y
-  uint4 a, b;
-};
-__device__ __forceinline__ Raw8 load_raw8(const void* base, int sdt, int64_t i) {
-  Raw8 r;
-  if (sdt == FUSP_F32) {
-    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const float*>(base) + i);
-    r.a = __ldg(p);
-    r.b = __ldg(p + 1);
-  } else if (sdt == FUSP_E4M3) {
-    const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(base) + i));
-    r.a = make_uint4(w.x, w.y, 0u, 0u);
-  } else {
-    r.a = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + i));
-  }
-  return r;
-}
 __device__ __forceinline__ void store_raw8(void* base, int sdt, int64_t i, const Raw8& r) {
   if (sdt == FUSP_F32) {
     uint4* p = reinterpret_cast<uint4*>(static_cast<float*>(base) + i);
@@ -1000,6 +1057,46 @@ __device__ __forceinline__ float e4m3_vec_absmax(const Fp8Src& s, const Fp8Div& 
   return f[0];
 }
 
+// Wide (f32 / f16 / bf16) sources of the FP8 passes, specialised per dtype: every load of a
+// thread's share (128 B: 8 vectors of 16-bit values, 4 of f32) is issued before any is used.
+template <int DT>
+__device__ __forceinline__ void amax_wide(const void* x, int64_t base, int64_t v0, int64_t stride,
+                                          int64_t nv, float& m, bool& bad) {
+  constexpr int U = DT == FUSP_F32 ? kFp8Unroll / 2 : kFp8Unroll;
+  uint32_t mag = 0;
+  for (int64_t v = v0; v < nv; v += U * stride) {
+    Raw8 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v + u * stride < nv) r[u] = load_raw8(x, DT, (base + v + u * stride) * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (v + u * stride >= nv) break;
+      if (!absmax_raw8(r[u], DT, mag, bad)) {
+        const Vec8 f = cvt8(r[u], DT);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f.f[e]));
+      }
+    }
+  }
+  m = fmaxf(m, mag_to_f32(mag, DT));
+}
+template <int DT>
+__device__ __forceinline__ void quant_wide(const void* x, uint8_t* codes, int64_t base, int64_t v0,
+                                           int64_t stride, int64_t nv, float qs, float inv) {
+  constexpr int U = DT == FUSP_F32 ? kFp8Unroll / 2 : kFp8Unroll;
+  for (int64_t v = v0; v < nv; v += U * stride) {
+    Raw8 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v + u * stride < nv) r[u] = load_raw8(x, DT, (base + v + u * stride) * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v + u * stride < nv)
+        *reinterpret_cast<uint2*>(codes + (base + v + u * stride) * 8) = encode8_finite(cvt8(r[u], DT), qs, inv);
+  }
+}
+
 // Pass 1 per block, 8 elements per step; grid.y = block, grid.z = tensor (K, V).
 struct AmaxArgs {
   Fp8Src src[2];
@@ -1027,23 +1124,14 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
       nf = fmaf(x, 0.f, nf);
       m = fmaxf(m, x);
     }
-  } else
-  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
-    Vec8 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (v + u * stride < a.block_vecs) x[u] = src_vec8(s, a.div[blockIdx.z], (base + v + u * stride) * 8);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (v + u * stride >= a.block_vecs) break;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        nf = fmaf(x[u].f[e], 0.f, nf);  // stays 0 unless some element is inf / NaN
-        m = fmaxf(m, fabsf(x[u].f[e]));
-      }
-    }
+  } else {
+    // 128 B of raw vectors in flight per thread; max |x| on the bit patterns
+    const int64_t v0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (s.dt == FUSP_F32) amax_wide<FUSP_F32>(s.x, base, v0, stride, a.block_vecs, m, bad);
+    else if (s.dt == FUSP_F16) amax_wide<FUSP_F16>(s.x, base, v0, stride, a.block_vecs, m, bad);
+    else amax_wide<FUSP_BF16>(s.x, base, v0, stride, a.block_vecs, m, bad);
   }
-  bad = nf != 0.f;
+  bad = bad || nf != 0.f;
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   bad = __any_sync(0xffffffffu, bad);
   __shared__ float wm[kBlock / 32];
@@ -1125,16 +1213,10 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
     }
     return;
   }
-  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += 4 * stride) {
-    Vec8 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (v + u * stride < a.block_vecs) x[u] = src_vec8(a.src[z], a.div[z], (base + v + u * stride) * 8);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (v + u * stride < a.block_vecs)
-        *reinterpret_cast<uint2*>(a.codes[z] + (base + v + u * stride) * 8) = encode8_finite(x[u], qs, inv);
-  }
+  const int64_t v0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (s.dt == FUSP_F32) quant_wide<FUSP_F32>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
+  else if (s.dt == FUSP_F16) quant_wide<FUSP_F16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
+  else quant_wide<FUSP_BF16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
 }
 
 __global__ void __launch_bounds__(256) dequantize_vec_kernel(const uint8_t* __restrict__ c,
@@ -1517,8 +1599,9 @@ namespace {
 // on the block's amax word and the finalize ticket (one address each) stay off the critical
 // path (ncu: 1184 CTAs x 2 same-address atomics cost ~3 us at FLUX U=8).
 int fp8_grid_x(int64_t block_vecs, int blocks_total) {
-  int64_t gx = (block_vecs + kBlock * 8 - 1) / (kBlock * 8);
-  const int64_t cap = (int64_t(sm_count()) * 4 + blocks_total - 1) / blocks_total;
+  // one pass of kFp8Unroll vectors per thread when the grid allows, up to 8 CTAs per SM
+  int64_t gx = (block_vecs + kBlock * kFp8Unroll - 1) / (kBlock * kFp8Unroll);
+  const int64_t cap = (int64_t(sm_count()) * 8 + blocks_total - 1) / blocks_total;
   if (gx > cap) gx = cap;
   return gx < 1 ? 1 : static_cast<int>(gx);
 }

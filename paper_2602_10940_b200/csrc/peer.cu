@@ -116,6 +116,23 @@ fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all) {
   w->opened.assign(static_cast<size_t>(w->world), false);
   w->bytes_of.assign(static_cast<size_t>(w->world), 0);
   const int32_t pid = static_cast<int32_t>(getpid());
+  // Ranks of this process sharing my device (threads as ranks): every one of them enqueues on
+  // its own stream and side stream, and a spinning exchange kernel blocks whatever the
+  // hardware queues behind it.  CUDA maps streams onto CUDA_DEVICE_MAX_CONNECTIONS hardware
+  // queues (default 8); two ranks' streams in one queue make a rank's progress wait behind
+  // another rank's spin on it -- a deadlock.  Refuse rather than hang.
+  int sharing = 0;
+  for (int r = 0; r < w->world; ++r) sharing += all[r].pid == pid && all[r].device == w->device;
+  if (sharing > 1) {
+    const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int conns = e != nullptr ? atoi(e) : 8;
+    if (conns < 2 * sharing)
+      return set_error(FUSP_ERR_UNSUPPORTED,
+                       "peer window: " + std::to_string(sharing) + " ranks of this process share device " +
+                           std::to_string(w->device) + "; their spinning exchange kernels need a hardware "
+                           "queue per stream: set CUDA_DEVICE_MAX_CONNECTIONS >= " +
+                           std::to_string(2 * sharing) + " (at most 32) before CUDA initialises");
+  }
   for (int r = 0; r < w->world; ++r) {
     const PeerHandle& h = all[r];
     if (h.magic != kPeerMagic)

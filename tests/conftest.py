@@ -4,6 +4,13 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# The GPU tests run up to 8 ranks as threads on ONE device, each with its own stream and side
+# stream.  With CUDA's default 8 hardware work queues, streams share queues, and work queued
+# behind another rank's spinning peer-exchange kernel cannot start (a false dependency that
+# deadlocks the exchange: fastusp.h, peer-memory transport).  One queue per stream; must be set
+# before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

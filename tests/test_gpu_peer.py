@@ -262,3 +262,28 @@ def test_peer_block_producer_and_consumer(cuda, fu, n, r):
         assert a[1] == b[1]         # same TrafficLog bytes
         for x, y in zip(a[0], b[0]):
             assert torch.equal(x, y)
+
+
+def test_peer_refuses_shared_hardware_queues(cuda, fu):
+    # ranks as threads on one device with too few hardware queues for their streams would wait
+    # behind each other's spinning exchange kernels: enabling the windows fails loudly instead
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd())
+import torch
+import paper_2602_10940_b200 as fu
+def prog(ctx):
+    try:
+        ctx.enable_peer_memory(1 << 20)
+    except fu.FuspError as e:
+        return str(e)
+    return "enabled"
+rep = fu.run_protocol(4, prog)
+print("RESULTS", rep.results)
+'''
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="4")
+    p = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(HERE), env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = [x for x in p.stdout.splitlines() if x.startswith("RESULTS")][0]
+    assert line.count("CUDA_DEVICE_MAX_CONNECTIONS >= 8") == 4, line

@@ -17,7 +17,17 @@ using namespace fusp;
 static void* flushbuf = nullptr;
 static double peak = 6548.5;
 
-static void report(const char* name, double bytes, const std::function<void()>& f) {
+static void* cpa = nullptr;
+static void* cpb = nullptr;
+static void report(const char* name, double bytes, const std::function<void()>& f, bool with_copy = true);
+// The same algorithmic bytes moved by a device-to-device cudaMemcpy (bytes / 2 read + written):
+// the practical ceiling for a kernel of that size, launch and DRAM ramp included.
+static void copy_ref(double bytes) {
+  const size_t half = static_cast<size_t>(bytes / 2) / 256 * 256;
+  report("  (same bytes as cudaMemcpy D2D)", 2.0 * half,
+         [&] { cudaMemcpyAsync(cpb, cpa, half, cudaMemcpyDeviceToDevice); }, false);
+}
+static void report(const char* name, double bytes, const std::function<void()>& f, bool with_copy) {
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   // MOVERS_ONCE=1: one warm-up and one timed call (for ncu: every kernel captured once)
@@ -39,10 +49,13 @@ static void report(const char* name, double bytes, const std::function<void()>& 
   printf("{\"kernel\": \"%s\", \"bytes\": %.0f, \"hot_us\": %.2f, \"hot_gbs\": %.0f, \"cold_us\": %.2f, \"cold_gbs\": %.0f, \"cold_frac_of_hbm\": %.3f}\n",
          name, bytes, hot * 1e3, bytes / (hot * 1e-3) / 1e9, cold * 1e3, bytes / (cold * 1e-3) / 1e9,
          bytes / (cold * 1e-3) / 1e9 / peak);
+  if (with_copy && getenv("MOVERS_ONCE") == nullptr) copy_ref(bytes);
 }
 
 int main() {
   CK(cudaMalloc(&flushbuf, 256u << 20));
+  CK(cudaMalloc(&cpa, 128u << 20));
+  CK(cudaMalloc(&cpb, 128u << 20));
   {  // operand staging at FLUX U = 1: V [24][4608][128] bf16 -> f16 (the layer's only mover)
     const int heads = 24, rows = 4608;
     const int64_t n = int64_t(heads) * rows * 128;
@@ -112,8 +125,8 @@ int main() {
     uint32_t* works[2] = {wk, wk + 64};
     float* scs[2] = {sc, sc + 64};
     uint8_t* cds[2] = {ck, cv};
-    snprintf(nm, sizeof nm, "%s fp8 amax+quantize K,V (2 passes)", c.name);
-    report(nm, 2.0 * n * (2 + 2 + 1), [&] { launch_quantize_fp8_multi(src, 2, n, n, works, scs, cds, nullptr, 0); });
+    snprintf(nm, sizeof nm, "%s fp8 amax+quantize K,V (2 passes; bytes: 2 read + 1 written per element)", c.name);
+    report(nm, 2.0 * n * (2 + 1), [&] { launch_quantize_fp8_multi(src, 2, n, n, works, scs, cds, nullptr, 0); });
     snprintf(nm, sizeof nm, "%s fp8 dequantize K -> bf16", c.name);
     report(nm, double(n) * (1 + 2), [&] { launch_dequantize_blocks(ck, sc, n, n, dk, FUSP_BF16, 0); });
     // ring hop: re-quantize an E4M3 chunk (per-segment scales) -- the FP8 ring forward
@@ -121,8 +134,8 @@ int main() {
     uint8_t *ck2, *cv2;
     CK(cudaMalloc(&ck2, n)); CK(cudaMalloc(&cv2, n));
     uint8_t* cds2[2] = {ck2, cv2};
-    snprintf(nm, sizeof nm, "%s fp8 ring hop re-quantize K,V from e4m3 (hop 1: multi-scale chunk)", c.name);
-    report(nm, 2.0 * n * (1 + 1 + 1), [&] { launch_quantize_fp8_multi(esrc, 2, n, n, works, scs, cds2, nullptr, 0); });
+    snprintf(nm, sizeof nm, "%s fp8 ring hop re-quantize K,V from e4m3 (hop 1: multi-scale chunk; bytes: 1 read + 1 written)", c.name);
+    report(nm, 2.0 * n * (1 + 1), [&] { launch_quantize_fp8_multi(esrc, 2, n, n, works, scs, cds2, nullptr, 0); });
     float* trs[2] = {sc, sc + 64};
     snprintf(nm, sizeof nm, "%s fp8 ring hop >= 2 forward (codes kept in place, scale trailer only)", c.name);
     report(nm, 2.0 * n * (1 + 1 + 1), [&] { launch_fp8_forward_scales(trs, 2, 1, 0); });

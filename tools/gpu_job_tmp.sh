@@ -1,8 +1,6 @@
 mkdir -p gpurun_out
-export FUSP_PEER_DEBUG=1
-for i in 1 2; do
-FUSP_TIMEOUT_S=20 timeout 900 python -m pytest tests/test_gpu_peer.py tests/test_gpu_nccl_shim.py -q -p no:cacheprovider > gpurun_out/peer_tests_$i.log 2>&1; echo "peer rc=$?" >> gpurun_out/peer_tests_$i.log
-tail -4 gpurun_out/peer_tests_$i.log; grep "\[peer\]" gpurun_out/peer_tests_$i.log | head -5
-done
-timeout 900 python -m pytest tests/test_gpu_wire.py tests/test_gpu_kernels.py tests/test_gpu_configs.py -q -p no:cacheprovider > gpurun_out/fp8_tests.log 2>&1; echo "rc=$?" >> gpurun_out/fp8_tests.log; tail -4 gpurun_out/fp8_tests.log
-timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; cut -c1-200 gpurun_out/movers.jsonl
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpuinfo.txt 2>&1
+FUSP_TIMEOUT_S=60 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+tail -6 gpurun_out/gpu_tests.log
+timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; cut -c1-230 gpurun_out/movers.jsonl
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; cut -c1-600 gpurun_out/bench.json
