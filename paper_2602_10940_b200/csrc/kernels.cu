@@ -21,6 +21,7 @@ constexpr int kBlock = 256;
 #define FUSP_FP8_UNROLL 8
 #endif
 constexpr int kFp8Unroll = FUSP_FP8_UNROLL;  // raw vectors in flight per thread (FP8 passes)
+constexpr int kE4Unroll = 4;  // 16-code loads in flight per thread (E4M3 sources)
 
 // Programmatic dependent launch (PDL): the kernel may become resident while the previous
 // kernel on `s` drains; it must execute griddepcontrol.wait before touching that kernel's output.
@@ -582,10 +583,13 @@ __device__ __forceinline__ uint32_t enc_pair(float a, float b) {  // (a -> low b
 // RN(x/qs) sits near an E4M3 rounding boundary -- the midpoint pattern 0x80000 in the low 20
 // mantissa bits (normal range), or anywhere in the E4M3 subnormal range (|q| < 2^-6).  Those
 // rare values take the exact division.  Above 448 everything saturates to 448 either way.
+// The IEEE division, out of line: taken for |q| < 2^-6 (E4M3 subnormals) and near rounding
+// boundaries only, and the unrolled FP8 loops would otherwise inline it at every element.
+__device__ __noinline__ float qdiv_slow(float x, float qs) { return __fdiv_rn(x, qs); }
 __device__ __forceinline__ float qdiv(float x, float qs, float inv) {
   const float q = x * inv;
   const uint32_t b = __float_as_uint(q) & 0x7fffffffu;
-  if (b < 0x3c800000u || ((b & 0xFFFFFu) - 0x7FFF8u) < 16u) return __fdiv_rn(x, qs);
+  if (b < 0x3c800000u || ((b & 0xFFFFFu) - 0x7FFF8u) < 16u) return qdiv_slow(x, qs);
   return q;
 }
 __device__ __forceinline__ uint2 encode8(const Vec8& v, float qs) {  // IEEE x / scale, RNE sat
@@ -1111,14 +1115,43 @@ struct AmaxArgs {
   uint32_t* ticket;
   int nblocks, parts;
 };
-__global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ AmaxArgs a) {
+// SDT: the sources' dtype when every part shares it (the common case: each instance then
+// holds only its own path's registers -- 4 resident CTAs per SM, one wave), -1 = per part.
+template <int SDT>
+__global__ void __launch_bounds__(256, 4) amax_vec_kernel(const __grid_constant__ AmaxArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");  // the quantize / pack pass gets scheduled
   const Fp8Src& s = a.src[blockIdx.z];
+  const int sdt = SDT >= 0 ? SDT : s.dt;
   const int64_t base = int64_t(blockIdx.y) * a.block_vecs;
   float m = 0.f, nf = 0.f;
   bool bad = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  if (s.dt == FUSP_E4M3) {
+  if (sdt == FUSP_E4M3 && s.d % 16 == 0 && a.block_vecs % 2 == 0) {
+    // 16 codes (one row piece, one scale) per load, kFp8Unroll loads in flight per thread
+    const int64_t nv = a.block_vecs / 2, e0 = base * 8;
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += kE4Unroll * stride) {
+      uint4 w[kE4Unroll];
+      float sc[kE4Unroll];
+#pragma unroll
+      for (int u = 0; u < kE4Unroll; ++u)
+        if (v + u * stride < nv) {
+          const int64_t i = e0 + (v + u * stride) * 16;
+          w[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(s.x) + i));
+          sc[u] = e4m3_scale(s, a.div[blockIdx.z], i);
+        }
+#pragma unroll
+      for (int u = 0; u < kE4Unroll; ++u) {
+        if (v + u * stride >= nv) break;
+        uint32_t mm = __vmaxu4(__vmaxu4(w[u].x & 0x7F7F7F7Fu, w[u].y & 0x7F7F7F7Fu),
+                               __vmaxu4(w[u].z & 0x7F7F7F7Fu, w[u].w & 0x7F7F7F7Fu));
+        mm = max(max(mm & 0xFFu, (mm >> 8) & 0xFFu), max((mm >> 16) & 0xFFu, mm >> 24));
+        float f[4];
+        dec4(mm, sc[u], f);
+        nf = fmaf(f[0], 0.f, nf);
+        m = fmaxf(m, f[0]);
+      }
+    }
+  } else if (sdt == FUSP_E4M3) {
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
       const float x = e4m3_vec_absmax(s, a.div[blockIdx.z], (base + v) * 8);
       nf = fmaf(x, 0.f, nf);
@@ -1127,8 +1160,8 @@ __global__ void __launch_bounds__(256) amax_vec_kernel(const __grid_constant__ A
   } else {
     // 128 B of raw vectors in flight per thread; max |x| on the bit patterns
     const int64_t v0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (s.dt == FUSP_F32) amax_wide<FUSP_F32>(s.x, base, v0, stride, a.block_vecs, m, bad);
-    else if (s.dt == FUSP_F16) amax_wide<FUSP_F16>(s.x, base, v0, stride, a.block_vecs, m, bad);
+    if (sdt == FUSP_F32) amax_wide<FUSP_F32>(s.x, base, v0, stride, a.block_vecs, m, bad);
+    else if (sdt == FUSP_F16) amax_wide<FUSP_F16>(s.x, base, v0, stride, a.block_vecs, m, bad);
     else amax_wide<FUSP_BF16>(s.x, base, v0, stride, a.block_vecs, m, bad);
   }
   bad = bad || nf != 0.f;
@@ -1184,7 +1217,8 @@ struct QuantArgs {
 // grid.y = block, grid.z = part: the block's scale is computed once per CTA.  Launched as a
 // programmatic dependent of amax_vec_kernel: resident as the amax grid drains, waits for its
 // completion (griddepcontrol.wait; a no-op for an ordinary launch) before reading the scale.
-__global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant__ QuantArgs a) {
+template <int SDT>  // as amax_vec_kernel
+__global__ void __launch_bounds__(256, 4) quantize_vec_kernel(const __grid_constant__ QuantArgs a) {
   const int z = blockIdx.z, blk = blockIdx.y;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   float qs;
@@ -1199,12 +1233,39 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
   const int64_t base = int64_t(blk) * a.block_vecs;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const Fp8Src& s = a.src[z];
-  if (s.dt == FUSP_E4M3) {
+  const int sdt = SDT >= 0 ? SDT : s.dt;
+  if (sdt == FUSP_E4M3) {
     // Ring hop (protocols.cpp:113-115): codes = encode(RN(decode(c) * s_src) / s_new).  When
     // s_new == s_src the result is c itself: RN(RN(d * s) / s) = d (1 + e), |e| <= 2^-23, and
     // every E4M3 neighbour of d is >= 2^-4 away relatively (2^-9 absolutely near 0; 448 is
     // the saturation value), so the nearest code is d's own -- the vector is copied.  After the
     // first hop every segment of a chunk shares the chunk's scale, so later hops are copies.
+    if (s.d % 16 == 0 && a.block_vecs % 2 == 0) {  // 16 codes per load, loads in flight
+      const int64_t nv = a.block_vecs / 2, e0 = base * 8;
+      for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += kE4Unroll * stride) {
+        uint4 w[kE4Unroll];
+        float sc[kE4Unroll];
+#pragma unroll
+        for (int u = 0; u < kE4Unroll; ++u)
+          if (v + u * stride < nv) {
+            const int64_t i = e0 + (v + u * stride) * 16;
+            w[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(s.x) + i));
+            sc[u] = e4m3_scale(s, a.div[z], i);
+          }
+#pragma unroll
+        for (int u = 0; u < kE4Unroll; ++u)
+          if (v + u * stride < nv) {
+            uint4 o = w[u];
+            if (sc[u] != qs) {
+              const uint2 lo = encode8_finite(decode8(make_uint2(w[u].x, w[u].y), sc[u]), qs, inv);
+              const uint2 hi = encode8_finite(decode8(make_uint2(w[u].z, w[u].w), sc[u]), qs, inv);
+              o = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            }
+            *reinterpret_cast<uint4*>(a.codes[z] + e0 + (v + u * stride) * 16) = o;
+          }
+      }
+      return;
+    }
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < a.block_vecs; v += stride) {
       const int64_t i = (base + v) * 8;
       const float sc = e4m3_scale(s, a.div[z], i);
@@ -1214,8 +1275,8 @@ __global__ void __launch_bounds__(256) quantize_vec_kernel(const __grid_constant
     return;
   }
   const int64_t v0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (s.dt == FUSP_F32) quant_wide<FUSP_F32>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
-  else if (s.dt == FUSP_F16) quant_wide<FUSP_F16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
+  if (sdt == FUSP_F32) quant_wide<FUSP_F32>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
+  else if (sdt == FUSP_F16) quant_wide<FUSP_F16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
   else quant_wide<FUSP_BF16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
 }
 
@@ -1551,6 +1612,51 @@ fusp_status launch_amax_blocks_raw(const Fp8Src& src, int64_t block_elems, int n
   return FUSP_OK;
 }
 
+namespace {
+// CTAs along a block for the FP8 passes: every thread takes >= 8 vectors (two rounds of 4 in
+// flight), at most 4 CTAs per SM over all blocks and parts -- few CTAs, so the per-CTA atomics
+// on the block's amax word and the finalize ticket (one address each) stay off the critical
+// path (ncu: 1184 CTAs x 2 same-address atomics cost ~3 us at FLUX U=8).
+int fp8_grid_x(int64_t block_vecs, int blocks_total) {
+  // one pass of kFp8Unroll vectors per thread when the grid allows, at most one resident
+  // wave (the kernels' 4 CTAs per SM)
+  int64_t gx = (block_vecs + kBlock * kFp8Unroll - 1) / (kBlock * kFp8Unroll);
+  const int64_t cap = (int64_t(sm_count()) * 4 + blocks_total - 1) / blocks_total;
+  if (gx > cap) gx = cap;
+  return gx < 1 ? 1 : static_cast<int>(gx);
+}
+// The FP8 pass instance for the sources' common dtype (-1: mixed, resolved per part).
+int fp8_common_dt(const Fp8Src* src, int parts) {
+  for (int p = 1; p < parts; ++p)
+    if (src[p].dt != src[0].dt) return -1;
+  return src[0].dt;
+}
+using AmaxKern = void (*)(AmaxArgs);
+using QuantKern = void (*)(QuantArgs);
+AmaxKern amax_kernel_for(int dt) {
+  switch (dt) {
+    case FUSP_BF16: return amax_vec_kernel<FUSP_BF16>;
+    case FUSP_F16: return amax_vec_kernel<FUSP_F16>;
+    case FUSP_F32: return amax_vec_kernel<FUSP_F32>;
+    case FUSP_E4M3: return amax_vec_kernel<FUSP_E4M3>;
+    default: return amax_vec_kernel<-1>;
+  }
+}
+QuantKern quantize_kernel_for(int dt) {
+  switch (dt) {
+    case FUSP_BF16: return quantize_vec_kernel<FUSP_BF16>;
+    case FUSP_F16: return quantize_vec_kernel<FUSP_F16>;
+    case FUSP_F32: return quantize_vec_kernel<FUSP_F32>;
+    case FUSP_E4M3: return quantize_vec_kernel<FUSP_E4M3>;
+    default: return quantize_vec_kernel<-1>;
+  }
+}
+bool fp8_vec_ok(const Fp8Src& src, int64_t n, int64_t block_elems, const void* codes) {
+  return n % 8 == 0 && block_elems % 8 == 0 && src.d % 8 == 0 && aligned16(src.x) &&
+         aligned16(codes);
+}
+}  // namespace
+
 fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nblocks,
                                uint32_t* amax, uint32_t* nonfinite, cudaStream_t s) {
   FUSP_CUDA(cudaMemsetAsync(amax, 0, sizeof(uint32_t) * nblocks, s));
@@ -1564,10 +1670,8 @@ fusp_status launch_amax_blocks(const Fp8Src& src, int64_t block_elems, int nbloc
     a.amax[0] = amax;
     a.block_vecs = block_elems / 8;
     a.nonfinite = nonfinite;
-    int gx = grid_for(a.block_vecs, 8);
-    const int cap = (sm_count() * 8 + nblocks - 1) / nblocks;
-    if (gx > cap) gx = cap < 1 ? 1 : cap;
-    amax_vec_kernel<<<dim3(gx, nblocks, 1), kBlock, 0, s>>>(a);
+    const int gx = fp8_grid_x(a.block_vecs, nblocks);
+    amax_kernel_for(src.dt)<<<dim3(gx, nblocks, 1), kBlock, 0, s>>>(a);
     FUSP_LAUNCHED("amax_vec_kernel");
     finalize_scales_kernel<<<(nblocks + kBlock - 1) / kBlock, kBlock, 0, s>>>(
         amax, nblocks, reinterpret_cast<float*>(amax));
@@ -1593,23 +1697,6 @@ fusp_status launch_quantize_blocks(const Fp8Src& src, int64_t n, int64_t block_e
   return FUSP_OK;
 }
 
-namespace {
-// CTAs along a block for the FP8 passes: every thread takes >= 8 vectors (two rounds of 4 in
-// flight), at most 4 CTAs per SM over all blocks and parts -- few CTAs, so the per-CTA atomics
-// on the block's amax word and the finalize ticket (one address each) stay off the critical
-// path (ncu: 1184 CTAs x 2 same-address atomics cost ~3 us at FLUX U=8).
-int fp8_grid_x(int64_t block_vecs, int blocks_total) {
-  // one pass of kFp8Unroll vectors per thread when the grid allows, up to 8 CTAs per SM
-  int64_t gx = (block_vecs + kBlock * kFp8Unroll - 1) / (kBlock * kFp8Unroll);
-  const int64_t cap = (int64_t(sm_count()) * 8 + blocks_total - 1) / blocks_total;
-  if (gx > cap) gx = cap;
-  return gx < 1 ? 1 : static_cast<int>(gx);
-}
-bool fp8_vec_ok(const Fp8Src& src, int64_t n, int64_t block_elems, const void* codes) {
-  return n % 8 == 0 && block_elems % 8 == 0 && src.d % 8 == 0 && aligned16(src.x) &&
-         aligned16(codes);
-}
-}  // namespace
 
 fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems, int nblocks,
                               uint32_t* const* amax, cudaStream_t s) {
@@ -1635,10 +1722,8 @@ fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems,
     a.amax[p] = amax[p];
   }
   a.block_vecs = block_elems / 8;
-  int gx = grid_for(a.block_vecs, 8);
-  const int cap = (sm_count() * 8 + nblocks * parts - 1) / (nblocks * parts);
-  if (gx > cap) gx = cap < 1 ? 1 : cap;
-  amax_vec_kernel<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
+  const int gx = fp8_grid_x(a.block_vecs, nblocks * parts);
+  amax_kernel_for(fp8_common_dt(src, parts))<<<dim3(gx, nblocks, parts), kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("amax_vec_kernel");
   return FUSP_OK;
 }
@@ -1670,7 +1755,7 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
     q.codes[p] = codes[p];
   }
   q.block_vecs = block_elems / 8;
-  FUSP_CUDA(launch_pdl(quantize_vec_kernel, dim3(gx, nblocks, parts), s, q));
+  FUSP_CUDA(launch_pdl(quantize_kernel_for(fp8_common_dt(src, parts)), dim3(gx, nblocks, parts), s, q));
   FUSP_LAUNCHED("quantize_vec_kernel");
   return FUSP_OK;
 }
@@ -1692,7 +1777,8 @@ fusp_status launch_amax_scales(const Fp8Src* src, int parts, int64_t block_elems
   a.ticket = work[0] + nblocks;
   a.nblocks = nblocks;
   a.parts = parts;
-  amax_vec_kernel<<<dim3(fp8_grid_x(a.block_vecs, nblocks * parts), nblocks, parts), kBlock, 0, s>>>(a);
+  amax_kernel_for(fp8_common_dt(src, parts))<<<dim3(fp8_grid_x(a.block_vecs, nblocks * parts), nblocks, parts),
+                                              kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("amax_vec_kernel");
   return FUSP_OK;
 }
@@ -1787,8 +1873,14 @@ void append_kernels_kernels(std::vector<const void*>& v) {
   v.push_back(reinterpret_cast<const void*>(stage_kernel));
   v.push_back(reinterpret_cast<const void*>(stage_decide_kernel));
   v.push_back(reinterpret_cast<const void*>(stage_scalar_kernel));
-  v.push_back(reinterpret_cast<const void*>(amax_vec_kernel));
-  v.push_back(reinterpret_cast<const void*>(quantize_vec_kernel));
+  for (const void* k : {reinterpret_cast<const void*>(amax_vec_kernel<-1>), reinterpret_cast<const void*>(amax_vec_kernel<FUSP_BF16>),
+                        reinterpret_cast<const void*>(amax_vec_kernel<FUSP_F16>), reinterpret_cast<const void*>(amax_vec_kernel<FUSP_F32>),
+                        reinterpret_cast<const void*>(amax_vec_kernel<FUSP_E4M3>)})
+    v.push_back(k);
+  for (const void* k : {reinterpret_cast<const void*>(quantize_vec_kernel<-1>), reinterpret_cast<const void*>(quantize_vec_kernel<FUSP_BF16>),
+                        reinterpret_cast<const void*>(quantize_vec_kernel<FUSP_F16>), reinterpret_cast<const void*>(quantize_vec_kernel<FUSP_F32>),
+                        reinterpret_cast<const void*>(quantize_vec_kernel<FUSP_E4M3>)})
+    v.push_back(k);
   v.push_back(reinterpret_cast<const void*>(dequantize_vec_kernel));
   v.push_back(reinterpret_cast<const void*>(fp8_forward_scales_kernel));
 }

@@ -1,5 +1,6 @@
 // QKV projection (with / without the QK prologue epilogue) and output projection timings at
-// the FLUX shape, CUDA events over back-to-back launches.
+// the FLUX shape and its per-rank token counts at N = 2, 4, 8 (S / N rows: the block's GEMMs at
+// U = N), CUDA events over back-to-back launches.
 #include <cuda_runtime.h>
 #include <cstdio>
 #include "../../paper_2602_10940_b200/csrc/fastusp_internal.h"
@@ -15,7 +16,7 @@ __global__ void fill_bf16(uint16_t* p, size_t n, float a, uint32_t seed) {
   }
 }
 int main() {
-  const int s = 4608, c = 3072, h = 24, n = 3 * h * 128;
+  const int s = 4608, c = 3072, h = 24, n = 3 * h * 128;  // allocation at the full sequence
   void *x, *w, *q, *k, *v, *wo, *y;
   float *wq, *cs;
   cudaMalloc(&x, size_t(s) * c * 2); cudaMalloc(&w, size_t(c) * n * 2);
@@ -33,12 +34,14 @@ int main() {
     for (int i = 0; i < 20; ++i) f();
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); ms /= 20;
-    printf("{\"kernel\": \"%s\", \"us\": %.1f, \"tflops\": %.1f}\n", name, ms * 1e3, flop / (ms * 1e-3) / 1e12);
+    printf("{\"kernel\": \"%s\", \"tokens\": %d, \"us\": %.1f, \"tflops\": %.1f}\n", name, s, ms * 1e3, flop / (ms * 1e-3) / 1e12);
   };
+  for (const int s : {4608, 2304, 1152, 576}) {
   const double fq = 2.0 * s * c * n, fo = 2.0 * s * h * 128 * c;
   run("qkv projection, plain epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, nullptr, nullptr, 0.f, nullptr, nullptr, 0, 0); });
   run("qkv projection + RMSNorm + RoPE epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, wq, wq, 1e-6f, cs, cs, 0, 0); });
   run("output projection", fo, [&] { launch_out_proj(q, FUSP_BF16, 1, h, s, wo, c, y, FUSP_BF16, 0); });
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;

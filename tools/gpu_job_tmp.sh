@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpuinfo.txt 2>&1
-FUSP_TIMEOUT_S=60 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
-tail -6 gpurun_out/gpu_tests.log
-timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; cut -c1-230 gpurun_out/movers.jsonl
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; cut -c1-600 gpurun_out/bench.json
+timeout 300 tools/cpp/proj_bench > gpurun_out/proj.jsonl 2>&1; cat gpurun_out/proj.jsonl
+TAG=movers_r2c bash tools/gpu_job_movers_ncu.sh > /dev/null 2>&1
+head -80 gpurun_out/movers_r2c_ncu.md | cut -c1-250
+cat gpurun_out/movers_r2c_layer_u8.md gpurun_out/movers_r2c_layer_u2r4.md | cut -c1-200
