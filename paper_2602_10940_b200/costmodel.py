@@ -18,6 +18,12 @@ ATTN_MEASURED = {"24x4608": 1299.6, "12x4608": 1229.2, "6x4608": 1049.9, "3x4608
                  "12x4224": 1161.2, "6x3584": 889.5, "24x7168": 1142.6}  # profiles/r02_vmesh.jsonl, 3x4608: attn_kv2_kernel (r02_ab_kv2.jsonl)
 
 
+# tcgen05 projection GEMMs of the FLUX block (C = 3072, H = 24) at per-rank token counts S/N,
+# measured on one B200 (tools/cpp/proj_bench, profiles/r02_proj_tokens.jsonl):
+# tokens -> (QKV projection incl. the QK RMSNorm + RoPE epilogue us, output projection us)
+PROJ_MEASURED_US = {4608: (178.2, 51.4), 2304: (97.4, 35.0), 1152: (70.8, 20.6), 576: (37.0, 14.5)}
+
+
 @dataclass
 class HardwareProfile:
     """SPEC.md:373-376.  Defaults: one B200 on an NVSwitch node."""
@@ -184,6 +190,44 @@ def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipeli
     return LatencyBreakdown(per_layer.compute * L + w.other_compute_per_step,
                             per_layer.exposed_comm * L, per_layer.hidden_comm * L,
                             per_layer.launch * L)
+
+
+def block_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, peer: bool = True,
+                  movers_us: Optional[float] = None) -> Dict[str, float]:
+    """The whole FLUX joint-attention block per rank at U = N, R = 1 (fusp_usp_block): QKV
+    projection -> USP layer -> output projection, from the measured per-rank GEMM times
+    (PROJ_MEASURED_US; the block's C and H are the table's) and step_latency's layer.
+
+    peer=True models the fused producer (csrc/peer.cu + proj_sm100.cu): the QKV projection's
+    epilogue stores Q, K, V into the members' windows as its tiles complete, so the input
+    all-to-all costs only what the link cannot move while the GEMM runs (plus one signal
+    kernel); the output all-to-all is the attention epilogue's stores (step_latency peer);
+    the output projection reads O in place.  movers_us: the operand staging of V and its
+    range decision at N = 1 (8.2 us, profiles/r02_launches.md), the unpack-stage of the
+    received Q, K, V slots and its decision at N > 1 (~6 us, profiles/r02_movers.jsonl)."""
+    if movers_us is None:
+        movers_us = 8.2 if n == 1 else 6.0
+    if w.S // n not in PROJ_MEASURED_US:
+        raise ValueError(f"no projection measurement at {w.S // n} tokens")
+    qkv_us, out_us = PROJ_MEASURED_US[w.S // n]
+    u = n
+    hp = w.H // u
+    attn = attention_seconds(hw, w.B, hp, w.S, w.S, w.D)
+    if u == 1:
+        comm = 0.0
+    else:
+        blk = w.B * hp * (w.S // n) * w.D
+        in_bytes = (u - 1) * 3 * blk * hw.element_width
+        out_bytes = (u - 1) * blk * hw.element_width
+        waves = attention_waves(hw, w.B, hp, w.S)
+        if peer:
+            comm = max(0.0, in_bytes / hw.link_bandwidth - qkv_us * 1e-6) + hw.peer_signal
+            comm += out_bytes / hw.link_bandwidth / max(waves, 1.0) + hw.peer_signal
+        else:
+            comm = (in_bytes + out_bytes) / hw.link_bandwidth + 2 * hw.link_latency
+    total = qkv_us * 1e-6 + attn + movers_us * 1e-6 + comm + out_us * 1e-6
+    return {"n": n, "qkv_proj_us": qkv_us, "attention_us": attn * 1e6, "movers_us": movers_us,
+            "exposed_comm_us": comm * 1e6, "out_proj_us": out_us, "total_us": total * 1e6}
 
 
 def speedup_report(base: LatencyBreakdown, opt: LatencyBreakdown) -> Dict[str, float]:

@@ -78,3 +78,18 @@ def test_cli_cost_csv_and_exit_codes():
                         "--max-ring", "1", "--dims", "1x3x64x128"], capture_output=True, text=True,
                        timeout=120)
     assert p.returncode == 2 and "invalid configuration" in p.stderr
+
+
+def test_block_latency_peer_hides_input_alltoall():
+    hw, w = cm.HardwareProfile(), cm.WorkloadProfile()
+    one = cm.block_latency(hw, w, 1)
+    assert one["exposed_comm_us"] == 0.0
+    for n in (2, 4, 8):
+        fused, nccl = cm.block_latency(hw, w, n, peer=True), cm.block_latency(hw, w, n, peer=False)
+        # the QKV projection's epilogue carries the input all-to-all: what is left exposed is
+        # the signal kernels and the last attention wave's output stores
+        assert fused["exposed_comm_us"] < nccl["exposed_comm_us"]
+        assert fused["total_us"] < one["total_us"]
+        parts = fused["qkv_proj_us"] + fused["attention_us"] + fused["movers_us"] + \
+            fused["exposed_comm_us"] + fused["out_proj_us"]
+        assert abs(parts - fused["total_us"]) < 1e-6

@@ -28,15 +28,17 @@ int main() {
   fill_bf16<<<1184, 256>>>(static_cast<uint16_t*>(wo), size_t(h) * 128 * c, 0.02f, 3);
   fill_bf16<<<1184, 256>>>(static_cast<uint16_t*>(q), size_t(s) * h * 128, 1.f, 4); cudaMemset(wq, 0, 128 * 4); cudaMemset(cs, 0, size_t(s) * 64 * 4);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  int cur = s;  // the token count being timed (printed)
   auto run = [&](const char* name, double flop, auto f) {
     for (int i = 0; i < 3; ++i) f();
     cudaEventRecord(a);
     for (int i = 0; i < 20; ++i) f();
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); ms /= 20;
-    printf("{\"kernel\": \"%s\", \"tokens\": %d, \"us\": %.1f, \"tflops\": %.1f}\n", name, s, ms * 1e3, flop / (ms * 1e-3) / 1e12);
+    printf("{\"kernel\": \"%s\", \"tokens\": %d, \"us\": %.1f, \"tflops\": %.1f}\n", name, cur, ms * 1e3, flop / (ms * 1e-3) / 1e12);
   };
   for (const int s : {4608, 2304, 1152, 576}) {
+  cur = s;
   const double fq = 2.0 * s * c * n, fo = 2.0 * s * h * 128 * c;
   run("qkv projection, plain epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, nullptr, nullptr, 0.f, nullptr, nullptr, 0, 0); });
   run("qkv projection + RMSNorm + RoPE epilogue", fq, [&] { launch_qkv_proj(x, FUSP_BF16, 1, s, c, w, h, q, k, v, FUSP_BF16, wq, wq, 1e-6f, cs, cs, 0, 0); });
