@@ -1280,6 +1280,153 @@ __global__ void __launch_bounds__(256, 4) quantize_vec_kernel(const __grid_const
   else quant_wide<FUSP_BF16>(s.x, a.codes[z], base, v0, stride, a.block_vecs, qs, inv);
 }
 
+// ---- one-launch per-tensor quantize for tensors that fit in the grid's registers ----------
+// quantize (fp8.cpp:107-123) needs the whole tensor's amax before its first code, so it is two
+// dependent passes -- two launches whose fixed costs dominate at the small per-rank sizes of
+// U = 8 (FLUX: 3.5 MB per tensor; a memcpy of the same bytes reaches 0.1-0.2 of HBM).  Here
+// one cooperative launch (every CTA co-resident) keeps each thread's share in registers
+// (up to kFusedHold 16-byte pieces), reduces the amax, crosses a grid barrier, and encodes
+// from the registers: one read of the source, one write of the codes, one launch.
+// The barrier word (zero on entry, zero again on exit) packs arrivals in its low 16 bits and
+// departures in its high 16 bits; the last CTA to depart also zeroes the amax words.
+constexpr int kFusedHold = 6;
+struct FusedQArgs {
+  Fp8Src src[2];
+  Fp8Div div[2];
+  uint32_t* amax[2];      // one word per part (per-tensor), zero on entry and on exit
+  float* scales[2];
+  uint8_t* codes[2];
+  int64_t units[2];       // 16-byte source pieces per part
+  int cta0[3];            // CTAs [cta0[p], cta0[p+1]) serve part p
+  uint32_t* barrier;      // zero on entry and on exit
+  uint32_t* nonfinite;    // optional
+  int parts;
+};
+template <int SDT>
+__global__ void __launch_bounds__(256, 4) quantize_fused_kernel(const __grid_constant__ FusedQArgs a) {
+  const int p = blockIdx.x >= static_cast<unsigned>(a.cta0[1]) ? 1 : 0;
+  const Fp8Src& s = a.src[p];
+  const int64_t per = int64_t(a.cta0[p + 1] - a.cta0[p]) * blockDim.x;
+  const int64_t t0 = int64_t(blockIdx.x - a.cta0[p]) * blockDim.x + threadIdx.x;
+  constexpr int kElems = SDT == FUSP_E4M3 ? 16 : SDT == FUSP_F32 ? 4 : 8;  // per 16-byte piece
+  uint4 w[kFusedHold];
+  float sc[kFusedHold];
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k) {
+    const int64_t u = t0 + k * per;
+    if (u < a.units[p]) {
+      w[k] = __ldg(reinterpret_cast<const uint4*>(s.x) + u);
+      if (SDT == FUSP_E4M3) sc[k] = e4m3_scale(s, a.div[p], u * 16);
+    }
+  }
+  float m = 0.f;
+  bool bad = false;
+  uint32_t mag = 0;
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k) {
+    if (t0 + k * per >= a.units[p]) break;
+    if (SDT == FUSP_E4M3) {
+      uint32_t mm = __vmaxu4(__vmaxu4(w[k].x & 0x7F7F7F7Fu, w[k].y & 0x7F7F7F7Fu),
+                             __vmaxu4(w[k].z & 0x7F7F7F7Fu, w[k].w & 0x7F7F7F7Fu));
+      mm = max(max(mm & 0xFFu, (mm >> 8) & 0xFFu), max((mm >> 16) & 0xFFu, mm >> 24));
+      float f[4];
+      dec4(mm, sc[k], f);
+      bad = bad || !(fabsf(f[0]) <= 3.402823466e38f);  // a NaN code (0x7F) decodes to NaN
+      if (f[0] == f[0]) m = fmaxf(m, f[0]);
+    } else {
+      Raw8 r;
+      r.a = w[k];
+      r.b = make_uint4(0, 0, 0, 0);
+      if (SDT == FUSP_F32) {  // 4 floats per piece: reuse the 8-lane helper on a padded vector
+        uint32_t mm = max(max(w[k].x & 0x7FFFFFFFu, w[k].y & 0x7FFFFFFFu),
+                          max(w[k].z & 0x7FFFFFFFu, w[k].w & 0x7FFFFFFFu));
+        if (mm >= 0x7F800000u) {
+          bad = true;
+          const float f[4] = {__uint_as_float(w[k].x), __uint_as_float(w[k].y), __uint_as_float(w[k].z),
+                              __uint_as_float(w[k].w)};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) m = fmaxf(m, fabsf(f[e]));
+        } else {
+          mag = max(mag, mm);
+        }
+      } else if (!absmax_raw8(r, SDT, mag, bad)) {
+        const Vec8 f = cvt8(r, SDT);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f.f[e]));
+      }
+    }
+  }
+  if (SDT != FUSP_E4M3) m = fmaxf(m, mag_to_f32(mag, SDT));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ float wm[kBlock / 32];
+  __shared__ int wb[kBlock / 32];
+  __shared__ float qs_sh;
+  if ((threadIdx.x & 31) == 0) {
+    wm[threadIdx.x >> 5] = m;
+    wb[threadIdx.x >> 5] = bad;
+  }
+  __syncthreads();
+  const unsigned G = gridDim.x;
+  if (threadIdx.x == 0) {
+    float bm = 0.f;
+    int bb = 0;
+    for (int i = 0; i < kBlock / 32; ++i) {
+      bm = fmaxf(bm, wm[i]);
+      bb |= wb[i];
+    }
+    if (!(bm >= 0.f)) bm = 0.f;
+    atomicMax(a.amax[p], __float_as_uint(bm));
+    if (bb && a.nonfinite) atomicOr(a.nonfinite, 1u);
+    // grid barrier: every CTA's amax contribution before anyone reads the amax
+    __threadfence();
+    atomicAdd(a.barrier, 1u);
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.barrier) : "memory");
+      if ((v & 0xFFFFu) == G) break;
+      __nanosleep(32);
+    } while (true);
+    const float am = __uint_as_float(__ldcg(a.amax[p]));
+    const float qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;  // fp8.cpp:119
+    qs_sh = qs;
+    if (blockIdx.x == static_cast<unsigned>(a.cta0[p])) *a.scales[p] = qs;
+  }
+  __syncthreads();
+  const float qs = qs_sh, inv = __frcp_rn(qs);
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k) {
+    const int64_t u = t0 + k * per;
+    if (u >= a.units[p]) break;
+    if (SDT == FUSP_E4M3) {
+      uint4 o = w[k];
+      if (sc[k] != qs) {  // same scale: the codes themselves (see quantize_vec_kernel)
+        const uint2 lo = encode8_finite(decode8(make_uint2(w[k].x, w[k].y), sc[k]), qs, inv);
+        const uint2 hi = encode8_finite(decode8(make_uint2(w[k].z, w[k].w), sc[k]), qs, inv);
+        o = make_uint4(lo.x, lo.y, hi.x, hi.y);
+      }
+      reinterpret_cast<uint4*>(a.codes[p])[u] = o;
+    } else if (SDT == FUSP_F32) {
+      const float f0 = qdiv(__uint_as_float(w[k].x), qs, inv), f1 = qdiv(__uint_as_float(w[k].y), qs, inv);
+      const float f2 = qdiv(__uint_as_float(w[k].z), qs, inv), f3 = qdiv(__uint_as_float(w[k].w), qs, inv);
+      reinterpret_cast<uint32_t*>(a.codes[p])[u] = enc_pair_finite(f0, f1) | (enc_pair_finite(f2, f3) << 16);
+    } else {
+      Raw8 r;
+      r.a = w[k];
+      r.b = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint2*>(a.codes[p])[u] = encode8_finite(cvt8(r, SDT), qs, inv);
+    }
+  }
+  if (threadIdx.x == 0) {  // depart; the last CTA out leaves the words zero for the next launch
+    const uint32_t old = atomicAdd(a.barrier, 0x10000u);
+    if ((old >> 16) == G - 1) {
+      for (int q = 0; q < a.parts; ++q) *a.amax[q] = 0u;
+      __threadfence();
+      *a.barrier = 0u;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) dequantize_vec_kernel(const uint8_t* __restrict__ c,
                                                              const float* __restrict__ scales,
                                                              FDiv block_vecs, int64_t n_vecs,
@@ -1728,6 +1875,62 @@ fusp_status launch_amax_multi(const Fp8Src* src, int parts, int64_t block_elems,
   return FUSP_OK;
 }
 
+namespace {
+// quantize_fused_kernel when the tensors fit the grid's registers (per-tensor scale, one common
+// source dtype, 16-byte pieces, not under graph capture); *done = false otherwise.
+fusp_status try_quantize_fused(const Fp8Src* src, int parts, int64_t n, uint32_t* const* work,
+                               float* const* scales, uint8_t* const* codes, uint32_t* nonfinite,
+                               cudaStream_t s, bool* done) {
+  *done = false;
+  static const bool off = getenv("FUSP_FP8_FUSED") != nullptr && atoi(getenv("FUSP_FP8_FUSED")) == 0;
+  const int dt = fp8_common_dt(src, parts);
+  if (off || dt < 0 || n <= 0) return FUSP_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return FUSP_OK;
+  const int64_t w = static_cast<int64_t>(dtype_size(dt));
+  FusedQArgs a{};
+  a.parts = parts;
+  a.cta0[0] = 0;
+  for (int p = 0; p < parts; ++p) {
+    if ((n * w) % 16 != 0 || !aligned16(src[p].x) || !aligned16(codes[p]) || scales[p] == nullptr) return FUSP_OK;
+    if (dt == FUSP_E4M3 && src[p].d % 16 != 0) return FUSP_OK;
+    a.src[p] = src[p];
+    a.div[p] = make_fp8div(src[p]);
+    a.amax[p] = work[p];
+    a.scales[p] = scales[p];
+    a.codes[p] = codes[p];
+    a.units[p] = n * w / 16;
+    a.cta0[p + 1] = a.cta0[p] + static_cast<int>((a.units[p] + int64_t(kBlock) * kFusedHold - 1) /
+                                                  (int64_t(kBlock) * kFusedHold));
+  }
+  if (parts == 1) a.cta0[2] = a.cta0[1];
+  a.barrier = work[0] + 1;  // the 2-pass finalize ticket word (zero on entry and exit)
+  a.nonfinite = nonfinite;
+  void (*k)(FusedQArgs) = dt == FUSP_BF16 ? quantize_fused_kernel<FUSP_BF16>
+                        : dt == FUSP_F16 ? quantize_fused_kernel<FUSP_F16>
+                        : dt == FUSP_F32 ? quantize_fused_kernel<FUSP_F32>
+                                         : quantize_fused_kernel<FUSP_E4M3>;
+  static int per_sm[4] = {-1, -1, -1, -1};
+  if (per_sm[dt] < 0) FUSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dt], k, kBlock, 0));
+  const int grid = a.cta0[parts];
+  if (grid > per_sm[dt] * sm_count() || grid >= 0xFFFF) return FUSP_OK;  // not co-resident
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA resident before any runs: the barrier
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FUSP_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  FUSP_LAUNCHED("quantize_fused_kernel");
+  *done = true;
+  return FUSP_OK;
+}
+}  // namespace
+
 fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
                                       uint32_t* const* work, float* const* scales,
                                       uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s) {
@@ -1743,6 +1946,11 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
   for (int p = 0; p < parts; ++p)
     if (scales[p] == nullptr) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: no scale output");
   if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
+  if (nblocks == 1) {  // per tensor and small enough: one launch (quantize_fused_kernel)
+    bool done = false;
+    FUSP_CHECK(try_quantize_fused(src, parts, n, work, scales, codes, nonfinite, s, &done));
+    if (done) return FUSP_OK;
+  }
   // pass 1 finalizes the scales in its last CTA and leaves `work` zero again; pass 2 is its
   // programmatic dependent (launch latency hidden under pass 1, second read of x from L2)
   const int gx = fp8_grid_x(block_elems / 8, nblocks * parts);
@@ -1883,6 +2091,9 @@ void append_kernels_kernels(std::vector<const void*>& v) {
     v.push_back(k);
   v.push_back(reinterpret_cast<const void*>(dequantize_vec_kernel));
   v.push_back(reinterpret_cast<const void*>(fp8_forward_scales_kernel));
+  for (const void* k : {reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_BF16>), reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_F16>),
+                        reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_F32>), reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_E4M3>)})
+    v.push_back(k);
 }
 
 }  // namespace fusp

@@ -276,6 +276,24 @@ fusp_status fusp_quantize_e4m3(const void* x, fusp_dtype dtype, int64_t n, uint8
   FUSP_CHECK(ws_scratch(w, s, 256, &ws));
   uint32_t* amax = static_cast<uint32_t*>(ws);
   uint32_t* bad = amax + 1;
+  if (n > 0 && n % 8 == 0 && n / 8 < (int64_t(1) << 31) &&
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) % 16 == 0) {
+    // the vectorised per-tensor passes (one cooperative launch when the tensor fits the
+    // grid's registers); the non-finite flag comes out of the same amax reduction
+    uint32_t* work = nullptr;
+    FUSP_CHECK(ws_qwords(w, s, 2, &work));
+    const int rows = static_cast<int>(n / 8);
+    const Fp8Src src{x, dtype, nullptr, 0, 0, 8, rows, rows};
+    FUSP_CHECK(launch_quantize_fp8_multi(&src, 1, n, n, &work, &scale_dev, &codes, bad, s));
+    if (check_finite) {
+      uint32_t flag = 0;
+      FUSP_CUDA(cudaMemcpyAsync(&flag, bad, 4, cudaMemcpyDeviceToHost, s));
+      FUSP_CUDA(cudaStreamSynchronize(s));
+      if (!flag) return FUSP_OK;
+    } else {
+      return FUSP_OK;
+    }
+  }
   FUSP_CHECK(launch_amax(x, dtype, n, amax, bad, s));
   if (check_finite) {
     uint32_t flag = 0;
@@ -326,7 +344,10 @@ fusp_status fusp_quantize_e4m3_blocks(const void* x, fusp_dtype dtype, int64_t n
   std::lock_guard<std::mutex> lk(w->mu);
   uint32_t* work = nullptr;
   FUSP_CHECK(ws_qwords(w, s, static_cast<size_t>(nblocks) + 1, &work));
-  const Fp8Src src{x, dtype, nullptr, 0, 0, 1, 1, 1};
+  // rows of 8 elements when they tile the blocks (the vectorised passes), else scalar
+  const bool v8 = n % 8 == 0 && block % 8 == 0 && n / 8 < (int64_t(1) << 31);
+  const int rows = v8 ? static_cast<int>(n / 8) : 1;
+  const Fp8Src src{x, dtype, nullptr, 0, 0, v8 ? 8 : 1, rows, rows};
   return launch_quantize_fp8(src, n, block, work, scales_dev, codes, nullptr, s);
 }
 

@@ -332,3 +332,31 @@ def test_requantize_ring_hop_bit_exact(cuda, fu, seg_scales):
     q2 = fu.requantize(q.codes, q.scale_dev, q.codes.numel())
     want2, ws2 = R.quantize(R.dequantize(got, np.float32(q.scale)))
     assert q2.scale == ws2 and np.array_equal(q2.codes.cpu().numpy(), want2)
+
+
+@pytest.mark.parametrize("shape", [(1, 3, 576, 128), (1, 24, 576, 128), (1, 24, 2304, 128),
+                                   (1, 24, 6912, 128)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_quantize_one_launch_and_two_pass_bit_exact(cuda, fu, shape, dtype):
+    # per-tensor quantize: tensors that fit the grid's registers take the one-launch
+    # cooperative kernel (quantize_fused_kernel), larger ones the two dependent passes; both
+    # bit-exact vs the reference quantizer (fp8.cpp:107-123), twice in a row (the barrier and
+    # amax words must be left zero)
+    rng = np.random.default_rng(sum(shape))
+    x = rng.uniform(-2.5, 2.5, size=shape).astype(np.float32)
+    x.ravel()[::97] *= np.float32(1e-5)          # the E4M3 subnormal range (exact division)
+    xt = T(x, dtype)
+    want, ws = R.quantize(xt.float().cpu().numpy())
+    for _ in range(2):
+        n0 = fu.kernel_launch_count()
+        q = fu.quantize(xt, check_finite=False)
+        launches = fu.kernel_launch_count() - n0
+        assert q.scale == ws
+        got = q.codes.cpu().numpy().reshape(-1)
+        bad = np.flatnonzero(got != want.reshape(-1))
+        assert bad.size == 0, (bad[:5], got[bad[:5]], want.reshape(-1)[bad[:5]])
+    nbytes = x.size * (2 if dtype == torch.bfloat16 else 4)
+    if nbytes <= 4 << 20:       # well inside one resident wave's registers: one launch
+        assert launches == 1, launches
+    elif nbytes >= 30 << 20:    # beyond them: the two dependent passes
+        assert launches == 2, launches

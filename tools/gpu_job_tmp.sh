@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 300 tools/cpp/proj_bench > gpurun_out/proj.jsonl 2>&1; cat gpurun_out/proj.jsonl
-TAG=movers_r2c bash tools/gpu_job_movers_ncu.sh > /dev/null 2>&1
-head -80 gpurun_out/movers_r2c_ncu.md | cut -c1-250
-cat gpurun_out/movers_r2c_layer_u8.md gpurun_out/movers_r2c_layer_u2r4.md | cut -c1-200
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_wire.py tests/test_gpu_configs.py tests/test_gpu_protocols.py tests/test_gpu_numerics.py -q -p no:cacheprovider -x > gpurun_out/fp8_tests.log 2>&1; echo "rc=$?" >> gpurun_out/fp8_tests.log; tail -15 gpurun_out/fp8_tests.log
+timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; grep -A1 "fp8" gpurun_out/movers.jsonl | cut -c1-200
