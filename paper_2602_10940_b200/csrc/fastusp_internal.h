@@ -273,10 +273,15 @@ fusp_status launch_amax_scales(const Fp8Src* src, int parts, int64_t block_elems
                                uint32_t* const* work, float* const* scales, uint32_t* nonfinite,
                                cudaStream_t s);
 // K and V (parts = 2) quantized with one amax launch (scales finalized in it) and one quantize
-// launch (its programmatic dependent).  `work` as for launch_amax_scales.
+// launch (its programmatic dependent).  `work` as for launch_amax_scales.  one_launch: per-tensor
+// scales on tensors that fit one resident wave's registers run as ONE cooperative launch
+// (quantize_fused_kernel) -- which needs the whole GPU free to start, so callers running
+// beside another kernel (the pipelined ring's side stream, beside the attention) pass false
+// and keep the two passes, which fill whatever SMs the compute leaves free.
 fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
                                       uint32_t* const* work, float* const* scales,
-                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s);
+                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s,
+                                      bool one_launch = true);
 fusp_status launch_dequantize_blocks(const uint8_t* c, const float* scales, int64_t block_elems,
                                      int64_t n, void* y, int ydt, cudaStream_t s);
 // Ring forward of an E4M3 chunk that quantize produced as a whole: scales[i] <- RN(RN(448 s) /

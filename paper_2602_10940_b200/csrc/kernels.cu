@@ -1933,7 +1933,8 @@ fusp_status try_quantize_fused(const Fp8Src* src, int parts, int64_t n, uint32_t
 
 fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, int64_t block_elems,
                                       uint32_t* const* work, float* const* scales,
-                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s) {
+                                      uint8_t* const* codes, uint32_t* nonfinite, cudaStream_t s,
+                                      bool one_launch) {
   const int nblocks = static_cast<int>((n + block_elems - 1) / block_elems);
   bool fast = parts >= 1 && parts <= 2 && nblocks <= 65535 && n < (int64_t(1) << 31);
   for (int p = 0; p < parts && fast; ++p) fast = fp8_vec_ok(src[p], n, block_elems, codes[p]);
@@ -1946,7 +1947,7 @@ fusp_status launch_quantize_fp8_multi(const Fp8Src* src, int parts, int64_t n, i
   for (int p = 0; p < parts; ++p)
     if (scales[p] == nullptr) return set_error(FUSP_ERR_INVALID_ARGUMENT, "quantize: no scale output");
   if (nonfinite) FUSP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), s));
-  if (nblocks == 1) {  // per tensor and small enough: one launch (quantize_fused_kernel)
+  if (nblocks == 1 && one_launch) {  // per tensor and small enough: one launch (quantize_fused_kernel)
     bool done = false;
     FUSP_CHECK(try_quantize_fused(src, parts, n, work, scales, codes, nonfinite, s, &done));
     if (done) return FUSP_OK;

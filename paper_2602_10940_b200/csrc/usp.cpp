@@ -917,7 +917,9 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
       scs[p] = scales;
       cds[p] = codes;
     }
-    return launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, st);
+    // beside the attention (pipelined: the side stream) the two-pass form, which runs on the
+    // SMs the compute leaves free; the one-launch form needs the whole GPU to start
+    return launch_quantize_fp8_multi(srcs, 2, l.C, block, works, scs, cds, nullptr, st, st == s);
   };
   // Transfer hop `hop` into buffer hop % 2, then stage the received chunk for the tensor cores
   // on the same stream (under the previous step's compute when pipelined).
