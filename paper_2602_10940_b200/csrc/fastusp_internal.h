@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/fastusp.h"
@@ -30,6 +31,11 @@ void count_launch(int n = 1);
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) attribute: set it
 // once per (kernel, device), thread-safely, before the first launch on that device.
 fusp_status ensure_smem_attr(const void* kernel, int bytes, const char* name);
+// The projection GEMMs' stream-K workspace of stream `s` (>= `words` zeroed counters, >= `bytes`
+// of partial slots), held while `launch` enqueues its kernel; launch(nullptr, nullptr) when it
+// cannot grow (graph capture): the caller then runs without the split.
+fusp_status with_proj_workspace(cudaStream_t s, size_t words, size_t bytes,
+                                const std::function<fusp_status(uint32_t*, float*)>& launch);
 // Load every kernel of the library on the current device now (lazy module loading; runtime.cpp).
 fusp_status preload_kernels();
 

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 
@@ -1911,10 +1912,18 @@ fusp_status try_quantize_fused(const Fp8Src* src, int parts, int64_t n, uint32_t
                         : dt == FUSP_F16 ? quantize_fused_kernel<FUSP_F16>
                         : dt == FUSP_F32 ? quantize_fused_kernel<FUSP_F32>
                                          : quantize_fused_kernel<FUSP_E4M3>;
-  static int per_sm[4] = {-1, -1, -1, -1};
-  if (per_sm[dt] < 0) FUSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dt], k, kBlock, 0));
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  int occ = 0;  // resident CTAs per SM (per device and instance; racing threads agree)
+  static std::atomic<int> per_sm[16][4];
+  if (dev < 16 && per_sm[dev][dt].load() > 0) {
+    occ = per_sm[dev][dt].load();
+  } else {
+    FUSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBlock, 0));
+    if (dev < 16) per_sm[dev][dt].store(occ);
+  }
   const int grid = a.cta0[parts];
-  if (grid > per_sm[dt] * sm_count() || grid >= 0xFFFF) return FUSP_OK;  // not co-resident
+  if (grid > occ * sm_count() || grid >= 0xFFFF) return FUSP_OK;  // not co-resident
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);

@@ -44,6 +44,7 @@ struct __align__(1024) ProjSmem {
   uint64_t full[kPStages], empty[kPStages];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
+  uint32_t ticket;  // stream-K: the tile's arrival count seen by this CTA
 };
 
 struct ProjParams {
@@ -67,6 +68,16 @@ struct ProjParams {
   int64_t slot_stride;  // elements between slots (u = 1: unused)
   int peer;             // slot t at slot_eoff[t] elements from slot 0 (members' peer windows)
   int64_t slot_eoff[kMaxPeerChunks];
+  // Stream-K over (tile, k-block) units (split = 1): CTA c owns units [c U / G, (c+1) U / G),
+  // U = tiles * k_blocks, so a tile's K range may be cut between consecutive CTAs.  Every
+  // segment of a cut tile but the finisher publishes its f32 partial (128 x kPN, [col/4][row]
+  // float4s) to slot (cta, first/last segment) and counts on the tile's word; the segment that
+  // brings the count to the tile's segment count sums all partials in K order (bit-identical
+  // whoever finishes) back into its accumulator and runs the normal epilogue.
+  int split;
+  int64_t units;
+  uint32_t* counters;   // one per tile, zero on entry, zeroed again by each tile's finisher
+  float* slots;         // 2 * gridDim.x slots of 128 * kPN floats
   const float* norm_w[2];
   float eps;
   const float* cosv;
@@ -92,6 +103,64 @@ bool proj_m_fast(int64_t a_bytes, int64_t b_bytes) {
     return e == nullptr ? -1 : atoi(e);
   }();
   return v < 0 ? b_bytes > a_bytes : v != 0;
+}
+
+// A CTA's work as segments (tile, k-blocks [kb0, kb1)): whole tiles strided by the grid, or
+// its contiguous stream-K unit range.
+struct PSeg {
+  int tile, kb0, kb1;
+};
+__device__ __forceinline__ int64_t sk_begin(const ProjParams& p, int c) {
+  return int64_t(c) * p.units / gridDim.x;
+}
+__device__ __forceinline__ int sk_cta_of(const ProjParams& p, int64_t u) {
+  int c = static_cast<int>(u * gridDim.x / p.units);
+  while (c + 1 < static_cast<int>(gridDim.x) && sk_begin(p, c + 1) <= u) ++c;
+  while (c > 0 && sk_begin(p, c) > u) --c;
+  return c;
+}
+struct PIter {
+  int64_t u, end;
+  __device__ explicit PIter(const ProjParams& p) {
+    if (p.split) {
+      u = sk_begin(p, blockIdx.x);
+      end = sk_begin(p, blockIdx.x + 1);
+    } else {
+      u = blockIdx.x;
+      end = p.tiles;
+    }
+  }
+  __device__ bool next(const ProjParams& p, PSeg& g) {
+    if (u >= end) return false;
+    if (!p.split) {
+      g.tile = static_cast<int>(u);
+      g.kb0 = 0;
+      g.kb1 = p.k_blocks;
+      u += gridDim.x;
+      return true;
+    }
+    g.tile = static_cast<int>(u / p.k_blocks);
+    const int64_t t0 = int64_t(g.tile) * p.k_blocks;
+    g.kb0 = static_cast<int>(u - t0);
+    const int64_t lim = end < t0 + p.k_blocks ? end : t0 + p.k_blocks;
+    g.kb1 = static_cast<int>(lim - t0);
+    u = lim;
+    return true;
+  }
+};
+__device__ __forceinline__ uint32_t proj_atom_add_acq_rel(uint32_t* a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t proj_ld_acquire(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps
+  __syncwarp();
+  asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
 // kQkv = false: output projection, A = attention output [B][H][S][128] through a 4-D map.
@@ -130,12 +199,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
       prefetch_tmap(&tm_a);
       prefetch_tmap(&tm_b);
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      PIter pi(p);
+      PSeg g;
+      while (pi.next(p, g)) {
+        const int tile = g.tile;
         const int nt = p.m_fast ? tile / p.m_tiles : tile % p.n_tiles;
         const int mt = p.m_fast ? tile % p.m_tiles : tile / p.n_tiles;
         const int bb = mt / p.m_tiles_per_b;
         const int s0 = (mt - bb * p.m_tiles_per_b) * kPM;
-        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int st = it % kPStages;
           mbar_wait(&sm.empty[st], ((it / kPStages) & 1) ^ 1);
           mbar_expect_tx(&sm.full[st], kABytes + kPK * kPN * 2);
@@ -152,12 +224,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp walks, one lane issues) ----------------
     uint32_t it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++lt) {
+    PIter pi(p);
+    PSeg g;
+    for (; pi.next(p, g); ++lt) {
       const int ab = lt & 1;
       mbar_wait(&sm.acc_empty[ab], ((lt >> 1) & 1) ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
       const uint32_t d_tmem = tmem + ab * kPN;
-      for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+      for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
         const int st = it % kPStages;
         mbar_wait(&sm.full[st], (it / kPStages) & 1);
         tc_fence_after();
@@ -168,7 +242,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int k = 0; k < kPK / 16; ++k)
             mma_ss(d_tmem, adesc + uint64_t(k * 32 / 16), bdesc + uint64_t(k * 16 * 128 / 16), p.idesc,
-                   (kb > 0 || k > 0) ? 1u : 0u);
+                   (kb > g.kb0 || k > 0) ? 1u : 0u);
           mma_commit(&sm.empty[st]);
         }
         __syncwarp();
@@ -183,7 +257,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     uint32_t lt = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++lt) {
+    PIter pi(p);
+    PSeg g;
+    for (; pi.next(p, g); ++lt) {
+      const int tile = g.tile;
       const int ab = lt & 1;
       const int nt = p.m_fast ? tile / p.m_tiles : tile % p.n_tiles;
       const int mt = p.m_fast ? tile % p.m_tiles : tile / p.n_tiles;
@@ -191,6 +268,84 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int s = (mt - bb * p.m_tiles_per_b) * kPM + r;
       mbar_wait(&sm.acc_full[ab], (lt >> 1) & 1);
       tc_fence_after();
+      if (p.split && (g.kb0 != 0 || g.kb1 != p.k_blocks)) {
+        // a stream-K segment of a cut tile: publish, or finish (sum in K order into TMEM)
+        const int64_t u0 = int64_t(tile) * p.k_blocks;
+        const int cf = sk_cta_of(p, u0);
+        const int nseg = sk_cta_of(p, u0 + p.k_blocks - 1) - cf + 1;
+        const int kself = static_cast<int>(blockIdx.x) - cf;
+        uint32_t* cnt = p.counters + tile;
+        const uint32_t acc_col = tmem + lane_off + ab * kPN;
+        constexpr int kHalf = kPN / 2;  // columns of this warpgroup: [eg * kHalf, +kHalf)
+        auto slot_of = [&](int c) {     // the slot CTA c published this tile's segment to
+          const int which = sk_begin(p, c) >= u0 ? 0 : 1;
+          return reinterpret_cast<float4*>(p.slots + (int64_t(c) * 2 + which) * (int64_t(kPM) * kPN));
+        };
+        bool last = false;
+        if (kself == 0) {  // processed last by its CTA: usually every other segment has counted
+          if (threadIdx.x == 128) sm.ticket = proj_ld_acquire(cnt);
+          epi_bar();
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket) + 1 == static_cast<uint32_t>(nseg);
+          epi_bar();
+        }
+        if (!last) {
+          float4* q4 = slot_of(blockIdx.x);
+#pragma unroll 1
+          for (int c = 0; c < kHalf / 32; ++c) {
+            const int col = eg * kHalf + c * 32;
+            uint32_t v[32];
+            tmem_ld32(acc_col + col, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              __stcg(q4 + (col / 4 + i) * kPM + r, make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
+          }
+          epi_bar();  // every slot store happens-before thread 128's release
+          if (threadIdx.x == 128) sm.ticket = proj_atom_add_acq_rel(cnt, 1u);
+          epi_bar();
+          last = *reinterpret_cast<volatile uint32_t*>(&sm.ticket) + 1 == static_cast<uint32_t>(nseg);
+          if (!last) {
+            tc_fence_before();
+            mbar_arrive(&sm.acc_empty[ab]);
+            continue;
+          }
+        }
+        if (threadIdx.x == 128) *cnt = 0u;  // every segment has counted: zero for the next launch
+#pragma unroll 1
+        for (int c = 0; c < kHalf / 32; ++c) {
+          const int col = eg * kHalf + c * 32;
+          float v[32];
+#pragma unroll 1
+          for (int k = 0; k < nseg; ++k) {
+            float x[32];
+            if (k == kself) {
+              uint32_t o[32];
+              tmem_ld32(acc_col + col, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(o[i]);
+            } else {
+              const float4* q4 = slot_of(cf + k);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 y = __ldcg(q4 + (col / 4 + i) * kPM + r);
+                x[4 * i] = y.x; x[4 * i + 1] = y.y; x[4 * i + 2] = y.z; x[4 * i + 3] = y.w;
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = k == 0 ? x[i] : v[i] + x[i];
+          }
+          uint32_t o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(v[i]);
+          tmem_st32(acc_col + col, o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        epi_bar();  // both warpgroups' columns merged before either reads the other's head
+        tc_fence_after();
+      }
       const bool in_range = s < p.s;
       if constexpr (kQkv) {
         // two heads per 256-column tile (one per 128-column tile): RMSNorm needs the whole
@@ -327,6 +482,61 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
 }  // namespace
 
+namespace {
+// Tile width, stream-K split and grid of one projection launch.  128 x 256 tiles unless
+// 128 x 128 fills the SMs' waves clearly better; when whole tiles would leave the last wave
+// under 90 % full (the per-rank token counts of a sharded block: 576 tokens = 5 M tiles), the
+// (tile, k-block) units are split stream-K over all SMs instead (128 x 256 tiles).
+// FUSP_PROJ_SPLIT=0/1 overrides the choice.
+template <bool kQkv>
+fusp_status launch_proj_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const ProjParams& p0,
+                               int b, int n, bool allow256, uint32_t f, cudaStream_t stream,
+                               const char* name) {
+  const int sms = sm_count();
+  auto tiles_for = [&](int pn) { return b * p0.m_tiles_per_b * ((n + pn - 1) / pn); };
+  auto fill = [&](int pn) {
+    const int t = tiles_for(pn);
+    const int waves = (t + sms - 1) / sms;
+    return static_cast<double>(t) / (static_cast<double>(waves) * sms);
+  };
+  static const int mode = [] {
+    const char* e = getenv("FUSP_PROJ_SPLIT");
+    return e == nullptr ? -1 : atoi(e);
+  }();
+  const int pn_split = allow256 ? 256 : 128;
+  const bool want_split = mode == 1 || (mode < 0 && fill(pn_split) < 0.9 && p0.k_blocks >= 4);
+  const int pn_whole = (!allow256 || fill(128) > 1.15 * fill(256)) ? 128 : 256;
+  auto launch = [&](uint32_t* cnt, float* slots) -> fusp_status {
+    ProjParams p = p0;
+    int pn = pn_whole;
+    if (cnt != nullptr) {
+      pn = pn_split;
+      p.split = 1;
+      p.counters = cnt;
+      p.slots = slots;
+    }
+    p.n_tiles = (n + pn - 1) / pn;
+    p.tiles = b * p.m_tiles_per_b * p.n_tiles;
+    p.m_tiles = b * p.m_tiles_per_b;
+    p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
+    p.units = int64_t(p.tiles) * p.k_blocks;
+    const int64_t work = p.split ? p.units : p.tiles;
+    const int grid = static_cast<int>(work < sms ? work : sms);
+    const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
+    if (pn == 256) out_proj_kernel<256, kQkv><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+    else out_proj_kernel<128, kQkv><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, name);
+    return FUSP_OK;
+  };
+  if (want_split)
+    return with_proj_workspace(stream, static_cast<size_t>(tiles_for(pn_split)),
+                               size_t(2) * sms * kPM * pn_split * sizeof(float), launch);
+  return launch(nullptr, nullptr);
+}
+}  // namespace
+
 // y[B][S][N] = O[B][H][S][128] (as [B*S][H*128]) x W[H*128][N].  O and W: both bf16 or both
 // f16; y: f32 / f16 / bf16.  N a multiple of 64 (TMA row pitch), pointers 16-byte aligned.
 fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, const void* w,
@@ -364,29 +574,11 @@ fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, con
   const uint32_t f = o_dtype == FUSP_BF16 ? 1u : 0u;
   p.y = y;
   p.y_dtype = y_dtype;
-  // 128 x 256 tiles unless 128 x 128 fills the SMs' waves clearly better (small token counts)
-  const int sms = sm_count();
-  auto fill = [&](int pn) {
-    const int t = b * p.m_tiles_per_b * ((n + pn - 1) / pn);
-    const int waves = (t + sms - 1) / sms;
-    return static_cast<double>(t) / (static_cast<double>(waves) * sms);
-  };
-  const int pn = fill(128) > 1.15 * fill(256) ? 128 : 256;
-  p.n_tiles = (n + pn - 1) / pn;
-  p.tiles = b * p.m_tiles_per_b * p.n_tiles;
-  p.m_tiles = b * p.m_tiles_per_b;
   p.m_fast = proj_m_fast(int64_t(b) * s * h * 128 * 2, int64_t(h) * 128 * n * 2) ? 1 : 0;
-  p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, false>), smem, "out_proj_kernel<256>"));
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, false>), smem, "out_proj_kernel<128>"));
-  const int grid = p.tiles < sms ? p.tiles : sms;
-  if (pn == 256) out_proj_kernel<256, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
-  else out_proj_kernel<128, false><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error(e, "out_proj_kernel launch");
-  return FUSP_OK;
+  return launch_proj_kernel<false>(ta, tb, p, b, n, true, f, stream, "out_proj_kernel launch");
 }
 
 // Q, K, V [B][H][S][128] (dtype qkv_dtype: bf16 or f16) = x[B][S][C] . W[C][3*H*128], with
@@ -467,30 +659,13 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   p.cosv = cosv;
   p.sinv = sinv;
   p.pos0 = pos0;
-  const int sms = sm_count();
   // 256-column tiles hold two whole heads, 128-column tiles one (heads never straddle tiles)
-  auto fill = [&](int pn) {
-    const int t = b * p.m_tiles_per_b * ((n + pn - 1) / pn);
-    const int waves = (t + sms - 1) / sms;
-    return static_cast<double>(t) / (static_cast<double>(waves) * sms);
-  };
-  const int pn = (n % 256 != 0 || fill(128) > 1.15 * fill(256)) ? 128 : 256;
-  p.n_tiles = n / pn;
-  p.tiles = b * p.m_tiles_per_b * p.n_tiles;
-  p.m_tiles = b * p.m_tiles_per_b;
   p.m_fast = proj_m_fast(int64_t(b) * s * c * 2, int64_t(c) * n * 2) ? 1 : 0;
   const uint32_t f = x_dtype == FUSP_BF16 ? 1u : 0u;
-  p.idesc = idesc_f16(f, f, 0, 1, kPM, pn);
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, true>), smem, "out_proj_kernel<256>"));
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, true>), smem, "out_proj_kernel<128>"));
-  const int grid = p.tiles < sms ? p.tiles : sms;
-  if (pn == 256) out_proj_kernel<256, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
-  else out_proj_kernel<128, true><<<grid, kPThreads, smem, stream>>>(ta, tb, p);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error(e, "qkv_proj kernel launch");
-  return FUSP_OK;
+  return launch_proj_kernel<true>(ta, tb, p, b, n, n % 256 == 0, f, stream, "qkv_proj kernel launch");
 }
 
 // Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -148,6 +149,9 @@ struct StreamWs {
   size_t bytes = 0;
   CounterBuf cnt;  // zero-initialised words (stream-K tickets, staging amax / tickets)
   CounterBuf qw;   // zero-initialised words of the FP8 amax pass (left zero by each launch)
+  CounterBuf pc;   // projection GEMM stream-K tile counters (left zero by each launch)
+  void* pslots = nullptr;  // projection GEMM stream-K partial slots
+  size_t pbytes = 0;
 };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, std::unique_ptr<StreamWs>> g_ws;
@@ -214,6 +218,26 @@ std::string shape_str(const fusp_shape4& s) {
 
 bool valid_float_dtype(int dt) { return dt == FUSP_F32 || dt == FUSP_F16 || dt == FUSP_BF16; }
 }  // namespace
+
+fusp_status with_proj_workspace(cudaStream_t s, size_t words, size_t bytes,
+                                const std::function<fusp_status(uint32_t*, float*)>& launch) {
+  StreamWs* w = nullptr;
+  FUSP_CHECK(stream_ws(s, &w));
+  std::lock_guard<std::mutex> lk(w->mu);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+  const bool grow = w->pc.words < words || w->pc.ptr == nullptr || w->pbytes < bytes;
+  if (grow && cs != cudaStreamCaptureStatusNone) return launch(nullptr, nullptr);  // no split
+  FUSP_CHECK(ensure_counters(w->pc, words, s));
+  if (w->pbytes < bytes) {
+    if (w->pslots) FUSP_CUDA(cudaFreeAsync(w->pslots, s));  // its last users ran on `s`
+    w->pslots = nullptr;
+    w->pbytes = 0;
+    FUSP_CUDA(cudaMallocAsync(&w->pslots, bytes, s));
+    w->pbytes = bytes;
+  }
+  return launch(w->pc.ptr, static_cast<float*>(w->pslots));
+}
 
 }  // namespace fusp
 

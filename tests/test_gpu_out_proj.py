@@ -39,6 +39,24 @@ def test_out_projection_matches_reference(cuda, fu, b, h, s, n, dtype):
     assert rel_l2(yb.float().cpu().numpy(), want) <= 4e-3
 
 
+@pytest.mark.parametrize("s", [576, 1152, 2304, 300])
+def test_out_projection_stream_k_split(cuda, fu, s):
+    # per-rank token counts of a sharded FLUX block: whole 128 x 256 tiles would leave the last
+    # wave mostly empty, so the (tile, k-block) units are split stream-K over the SMs and cut
+    # tiles are summed by their finisher in K order -- same bar, and bit-identical run to run
+    # (the merge order does not depend on which CTA finishes last)
+    h, n = 24, 3072
+    g = torch.Generator(device="cuda")
+    g.manual_seed(s)
+    o = torch.empty(1, h, s, 128, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1, generator=g)
+    w = (torch.empty(h * 128, n, device="cuda", dtype=torch.bfloat16).uniform_(-1, 1, generator=g) / (h * 128) ** 0.5).to(torch.bfloat16)
+    want = ref_proj(o.float().cpu().numpy(), w.float().cpu().numpy())
+    y = fu.out_projection(o, w, out_dtype=torch.float32)
+    assert rel_l2(y.cpu().numpy(), want) <= 1e-5
+    for _ in range(3):
+        assert torch.equal(fu.out_projection(o, w, out_dtype=torch.float32), y)
+
+
 def test_out_projection_rejects_bad_shapes(cuda, fu):
     o = torch.zeros(1, 2, 64, 128, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(fu.ShapeError):
