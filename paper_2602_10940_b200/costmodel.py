@@ -21,7 +21,7 @@ ATTN_MEASURED = {"24x4608": 1299.6, "12x4608": 1229.2, "6x4608": 1049.9, "3x4608
 # tcgen05 projection GEMMs of the FLUX block (C = 3072, H = 24) at per-rank token counts S/N,
 # measured on one B200 (tools/cpp/proj_bench, profiles/r02_proj_tokens.jsonl):
 # tokens -> (QKV projection incl. the QK RMSNorm + RoPE epilogue us, output projection us)
-PROJ_MEASURED_US = {4608: (178.2, 51.4), 2304: (97.4, 35.0), 1152: (70.8, 20.6), 576: (37.0, 14.5)}
+PROJ_MEASURED_US = {4608: (178.6, 53.0), 2304: (98.4, 37.0), 1152: (66.8, 20.6), 576: (39.7, 14.5)}
 
 
 @dataclass

@@ -484,14 +484,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
 namespace {
 // Tile width, stream-K split and grid of one projection launch.  128 x 256 tiles unless
-// 128 x 128 fills the SMs' waves clearly better; when whole tiles would leave the last wave
-// under 90 % full (the per-rank token counts of a sharded block: 576 tokens = 5 M tiles), the
-// (tile, k-block) units are split stream-K over all SMs instead (128 x 256 tiles).
-// FUSP_PROJ_SPLIT=0/1 overrides the choice.
+// 128 x 128 fills the SMs' waves clearly better.  Stream-K (128 x 256 tiles, all SMs) when
+// neither whole-tile width fills the waves to 90 % and every CTA still gets at least one
+// tile's worth of units (two with a heavy epilogue: a cut tile's merge and epilogue run
+// after its last segment, unoverlapped).  Measured (profiles/r02_proj_tokens.jsonl): the QKV
+// projection at 1152 tokens 76.9 -> 56.0 us (plain epilogue) / 75.9 -> 66.4 us (RMSNorm +
+// RoPE), at 576 tokens 41.1 -> 37.0 us (plain); the output projection (12 column tiles: few
+// tiles, short segments) and the RMSNorm epilogue at 576 tokens lose, so they keep whole
+// tiles.  FUSP_PROJ_SPLIT=0/1 overrides the choice.
 template <bool kQkv>
 fusp_status launch_proj_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const ProjParams& p0,
                                int b, int n, bool allow256, uint32_t f, cudaStream_t stream,
-                               const char* name) {
+                               const char* name, bool allow_split, bool heavy_epilogue) {
   const int sms = sm_count();
   auto tiles_for = [&](int pn) { return b * p0.m_tiles_per_b * ((n + pn - 1) / pn); };
   auto fill = [&](int pn) {
@@ -504,8 +508,11 @@ fusp_status launch_proj_kernel(const CUtensorMap& ta, const CUtensorMap& tb, con
     return e == nullptr ? -1 : atoi(e);
   }();
   const int pn_split = allow256 ? 256 : 128;
-  const bool want_split = mode == 1 || (mode < 0 && fill(pn_split) < 0.9 && p0.k_blocks >= 4);
   const int pn_whole = (!allow256 || fill(128) > 1.15 * fill(256)) ? 128 : 256;
+  const double best_whole = allow256 && fill(256) > fill(128) ? fill(256) : fill(128);
+  const bool want_split =
+      mode == 1 || (mode < 0 && allow_split && p0.k_blocks >= 8 && best_whole < 0.9 &&
+                    tiles_for(pn_split) >= (heavy_epilogue ? 2 : 1) * sms);
   auto launch = [&](uint32_t* cnt, float* slots) -> fusp_status {
     ProjParams p = p0;
     int pn = pn_whole;
@@ -578,7 +585,8 @@ fusp_status launch_out_proj(const void* o, int o_dtype, int b, int h, int s, con
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, false>), smem, "out_proj_kernel<256>"));
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, false>), smem, "out_proj_kernel<128>"));
-  return launch_proj_kernel<false>(ta, tb, p, b, n, true, f, stream, "out_proj_kernel launch");
+  return launch_proj_kernel<false>(ta, tb, p, b, n, true, f, stream, "out_proj_kernel launch",
+                                   /*allow_split=*/false, false);
 }
 
 // Q, K, V [B][H][S][128] (dtype qkv_dtype: bf16 or f16) = x[B][S][C] . W[C][3*H*128], with
@@ -665,7 +673,8 @@ fusp_status launch_qkv_proj_to(const void* x, int x_dtype, int b, int s, int c, 
   const int smem = static_cast<int>(sizeof(ProjSmem)) + 1024;
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<256, true>), smem, "out_proj_kernel<256>"));
   FUSP_CHECK(ensure_smem_attr(reinterpret_cast<const void*>(out_proj_kernel<128, true>), smem, "out_proj_kernel<128>"));
-  return launch_proj_kernel<true>(ta, tb, p, b, n, n % 256 == 0, f, stream, "qkv_proj kernel launch");
+  return launch_proj_kernel<true>(ta, tb, p, b, n, n % 256 == 0, f, stream, "qkv_proj kernel launch",
+                                  /*allow_split=*/true, wq != nullptr || wk != nullptr || cosv != nullptr);
 }
 
 // Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).

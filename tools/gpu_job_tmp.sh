@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_wire.py tests/test_gpu_configs.py tests/test_gpu_protocols.py tests/test_gpu_numerics.py -q -p no:cacheprovider -x > gpurun_out/fp8_tests.log 2>&1; echo "rc=$?" >> gpurun_out/fp8_tests.log; tail -15 gpurun_out/fp8_tests.log
-timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; grep -A1 "fp8" gpurun_out/movers.jsonl | cut -c1-200
+timeout 900 python -m pytest tests/test_gpu_out_proj.py tests/test_gpu_prologue.py tests/test_gpu_peer.py -q -p no:cacheprovider > gpurun_out/proj_tests.log 2>&1; echo "rc=$?" >> gpurun_out/proj_tests.log; tail -5 gpurun_out/proj_tests.log
