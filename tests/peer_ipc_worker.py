@@ -1,0 +1,69 @@
+"""One rank of the cross-process peer-memory test (tests/test_gpu_peer.py): a separate process
+on cuda:0 whose window reaches the other rank's through CUDA IPC (cudaIpcGetMemHandle /
+cudaIpcOpenMemHandle), as one-process-per-GPU ranks do over NVLink.  Handles travel through
+files in a scratch directory (the caller's own bootstrap: fusp_ctx_peer_window / _open).
+usage: python tests/peer_ipc_worker.py RANK WORLD DIR"""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2602_10940_b200 as fu  # noqa: E402
+from oracle import restate as R  # noqa: E402
+from oracle.make_golden import qkv  # noqa: E402
+
+
+def wait_for(path, timeout=120.0):
+    t0 = time.time()
+    while not os.path.exists(path):
+        if time.time() - t0 > timeout:
+            raise TimeoutError(path)
+        time.sleep(0.01)
+
+
+def main():
+    rank, world, d = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    torch.cuda.set_device(0)
+    h, s = 8, 256 * world
+    probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(600 + i, 610 + i, 620 + i)) for i in range(3)]
+    mesh = fu.make_mesh(world, 1)
+    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float32)
+    # a fabric of `world` ranks of which this process runs one: the peer path at R = 1 moves
+    # every byte through the windows, the fabric is never entered
+    fab = fu.Fabric(world)
+    ctx = fu.WorkerContext.local(fab, rank, 0)
+    wb = fu.peer_window_bytes(world, 1, (1, h, s // world, 128), torch.bfloat16, opts)
+    mine = ctx.peer_window(wb)
+    tmp = os.path.join(d, f"h{rank}.tmp")
+    with open(tmp, "wb") as f:
+        f.write(mine)
+    os.rename(tmp, os.path.join(d, f"h{rank}"))
+    handles = []
+    for r in range(world):
+        wait_for(os.path.join(d, f"h{r}"))
+        with open(os.path.join(d, f"h{r}"), "rb") as f:
+            handles.append(f.read())
+    ctx.peer_open(handles)
+    outs = []
+    for q, k, v in probs:
+        sh = [torch.from_numpy(np.ascontiguousarray(R.split_sequence(t, world)[rank])).cuda().bfloat16()
+              for t in (q, k, v)]
+        outs.append(fu.usp_attention(ctx, *sh, mesh, opts).clone())
+    ctx.synchronize(timeout_s=60)
+    stats = ctx.peer_stats()
+    torch.save({"outs": [o.cpu() for o in outs], "stats": stats}, os.path.join(d, f"out{rank}.pt"))
+    # keep the window mapped until every rank has finished reading / writing it
+    open(os.path.join(d, f"done{rank}"), "w").close()
+    for r in range(world):
+        wait_for(os.path.join(d, f"done{r}"))
+    ctx.close()
+    fab.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -287,3 +287,29 @@ print("RESULTS", rep.results)
     assert p.returncode == 0, p.stderr[-2000:]
     line = [x for x in p.stdout.splitlines() if x.startswith("RESULTS")][0]
     assert line.count("CUDA_DEVICE_MAX_CONNECTIONS >= 8") == 4, line
+
+
+def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path):
+    # two processes on cuda:0, windows mapped through CUDA IPC (the deployment path: one process
+    # per GPU) -- the pointer path of ranks-as-threads never opens an IPC handle.  Contexts of
+    # different processes time-slice the GPU, so the spinning exchanges see each other's
+    # signals slice by slice; outputs must equal the in-process 2-rank layer bit for bit.
+    world = 2
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "peer_ipc_worker.py"), str(r),
+                               str(world), str(tmp_path)], cwd=os.path.dirname(HERE),
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                              env=dict(os.environ, FUSP_TIMEOUT_S="60"))
+             for r in range(world)]
+    errs = [p.communicate(timeout=600)[1] for p in procs]
+    assert all(p.returncode == 0 for p in procs), [e[-1500:] for e in errs]
+    got = [torch.load(tmp_path / f"out{r}.pt") for r in range(world)]
+    assert all(tuple(g["stats"]) == (3, 0) for g in got)
+    h, s = 8, 256 * world
+    mesh = fu.make_mesh(world, 1)
+    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float32)
+    for i in range(3):
+        q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(600 + i, 610 + i, 620 + i))
+        qs, ks, vs = shards(q, world), shards(k, world), shards(v, world)
+        ref = layer(fu, qs, ks, vs, mesh, opts)
+        for r in range(world):
+            assert torch.equal(got[r]["outs"][i], ref.results[r][0][0].cpu())
