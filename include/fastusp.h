@@ -346,6 +346,16 @@ fusp_status fusp_graph_capture_usp(fusp_ctx ctx, int ring_dim, const void* q, co
                                    void* out, const fusp_comm_options* opts, int layers,
                                    int64_t in_layer_stride_bytes, int64_t out_layer_stride_bytes,
                                    fusp_stream_t stream, fusp_graph* graph);
+/* The same for `layers` back-to-back fusp_usp_block calls (x / y of layer i at i * x_stride /
+ * i * y_stride bytes): the whole MMDiT attention block -- QKV projection, the USP layer and the
+ * output projection -- as one graph.  Runs layer 0 once eagerly to size the graph's own
+ * workspace.  Capturable at world > 1 through NCCL or with peer windows at ring_dim 1. */
+fusp_status fusp_graph_capture_block(fusp_ctx ctx, int ring_dim, const void* x, fusp_dtype x_dtype,
+                                     int64_t batch, int64_t s_local, int64_t channels,
+                                     const void* w_qkv, int heads, const fusp_qk_prologue* prologue,
+                                     const void* w_out, int64_t n_out, void* y, fusp_dtype y_dtype,
+                                     const fusp_comm_options* opts, int layers, int64_t x_stride,
+                                     int64_t y_stride, fusp_stream_t stream, fusp_graph* graph);
 fusp_status fusp_graph_launch(fusp_graph graph, fusp_stream_t stream);
 fusp_status fusp_graph_destroy(fusp_graph graph);
 

@@ -5,7 +5,7 @@ include/fastusp.h (libfastusp.so: hand-written sm_100a kernels + NCCL).
 """
 from ._lib import (BF16, E4M3, F16, F32, DeadlockError, FabricError, FuspError, InvalidArgument, MeshError,
                    ShapeError, build)
-from .api import (AttnResult, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGroup,
+from .api import (AttnResult, BlockGraph, CommOptions, Fabric, LayerGraph, Mesh2D, ProcessGroup,
                   QKPrologue, QuantizedTensor, rope_tables, RunReport, WorkerContext, attention_reference,
                   attention_schedule, attention_with_lse, build_mesh, decode_e4m3, dequantize, dequantize_blocks,
                   encode_e4m3, quantize_blocks, requantize,

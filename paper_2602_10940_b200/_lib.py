@@ -158,6 +158,10 @@ _SIGS = {
     "fusp_graph_capture_usp": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int, Shape4,
                                               _P, ctypes.POINTER(CommOptions), ctypes.c_int, _I64,
                                               _I64, _P, _P]),
+    "fusp_graph_capture_block": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _I64,
+                                                _P, ctypes.c_int, ctypes.POINTER(QKPrologue), _P,
+                                                _I64, _P, ctypes.c_int, ctypes.POINTER(CommOptions),
+                                                ctypes.c_int, _I64, _I64, _P, _P]),
     "fusp_ctx_peer_enable": (ctypes.c_int, [_P, ctypes.c_size_t]),
     "fusp_ctx_peer_window": (ctypes.c_int, [_P, ctypes.c_size_t, _P]),
     "fusp_ctx_peer_open": (ctypes.c_int, [_P, _P]),

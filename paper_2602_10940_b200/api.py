@@ -818,6 +818,37 @@ def usp_attention_host(ctx: WorkerContext, q, k, v, mesh: Mesh2D,
     return out
 
 
+class BlockGraph:
+    """CUDA graph of `layers` back-to-back usp_block calls (fusp_graph_capture_block): the QKV
+    projection, the USP layer and the output projection of every layer replayed as one graph.
+    x: [layers, B, S/N, C], y: [layers, B, S/N, N] (y[0] is computed once while sizing)."""
+
+    def __init__(self, ctx: WorkerContext, x, w_qkv, heads: int, w_out, y, mesh: Mesh2D,
+                 prologue: Optional[QKPrologue] = None, opts: Optional[CommOptions] = None,
+                 layers: int = 1):
+        opts = opts or CommOptions(check_finite=False)
+        co = opts._c()
+        pc = prologue._c() if prologue is not None else None
+        _, b, s_, c = x.shape
+        h = ctypes.c_void_p()
+        self._keep = (x, w_qkv, w_out, y, prologue)
+        self._ctx = ctx
+        check(lib().fusp_graph_capture_block(
+            ctx.handle, mesh.r, _ptr(x), _DT[x.dtype], b, s_, c, _ptr(w_qkv), heads,
+            ctypes.byref(pc) if pc is not None else None, _ptr(w_out), int(w_out.shape[1]), _ptr(y),
+            _DT[y.dtype], ctypes.byref(co), layers, x[0].numel() * x.element_size(),
+            y[0].numel() * y.element_size(), _stream(), ctypes.byref(h)))
+        self.handle = h
+
+    def launch(self, stream=None):
+        check(lib().fusp_graph_launch(self.handle, _stream(stream)))
+
+    def close(self):
+        if self.handle:
+            lib().fusp_graph_destroy(self.handle)
+            self.handle = None
+
+
 class LayerGraph:
     """CUDA graph of `layers` back-to-back usp_attention calls (fusp_graph_capture_usp)."""
 

@@ -226,8 +226,9 @@ fusp_status with_proj_workspace(cudaStream_t s, size_t words, size_t bytes,
   std::lock_guard<std::mutex> lk(w->mu);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
-  const bool grow = w->pc.words < words || w->pc.ptr == nullptr || w->pbytes < bytes;
-  if (grow && cs != cudaStreamCaptureStatusNone) return launch(nullptr, nullptr);  // no split
+  // under capture: whole tiles (a graph must not address this stream's workspace, which a
+  // later eager call may regrow)
+  if (cs != cudaStreamCaptureStatusNone) return launch(nullptr, nullptr);
   FUSP_CHECK(ensure_counters(w->pc, words, s));
   if (w->pbytes < bytes) {
     if (w->pslots) FUSP_CUDA(cudaFreeAsync(w->pslots, s));  // its last users ran on `s`

@@ -132,6 +132,7 @@ struct fusp_graph_s {
   int device = 0;
   fusp_ctx_s* ctx = nullptr;  // its communicators are replayed: the context must outlive it
   Workspace ws;               // the arena and words the captured kernels address
+  void* block_ws = nullptr;   // fusp_graph_capture_block: Q, K, V and attention output
 };
 
 namespace {
@@ -2071,8 +2072,88 @@ fusp_status fusp_graph_destroy(fusp_graph g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->graph) cudaGraphDestroy(g->graph);
   g->ws.release();  // cudaFree waits for a replay still in flight
+  if (g->block_ws) cudaFree(g->block_ws);
   if (g->ctx) g->ctx->live_graphs--;
   delete g;
+  return FUSP_OK;
+}
+
+// CUDA graph of `layers` back-to-back fusp_usp_block calls (the whole MMDiT attention block:
+// QKV projection -> USP layer -> output projection).  Collective like the block itself.  The
+// graph owns its layer workspace and block buffers: sized by one eager block (which also
+// computes y for layer 0), then captured; eager calls on the context may later regrow the
+// context's own without touching them.  At world > 1 only the peer-memory path (ring_dim 1)
+// or an NCCL context is capturable -- the in-process fabric's rendezvous is host code.
+fusp_status fusp_graph_capture_block(fusp_ctx c, int ring_dim, const void* x, fusp_dtype x_dtype,
+                                     int64_t batch, int64_t s_local, int64_t channels,
+                                     const void* w_qkv, int heads, const fusp_qk_prologue* prologue,
+                                     const void* w_out, int64_t n_out, void* y, fusp_dtype y_dtype,
+                                     const fusp_comm_options* opts, int layers, int64_t x_stride,
+                                     int64_t y_stride, fusp_stream_t stream, fusp_graph* graph) {
+  clear_error();
+  if (!c || !graph) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context or graph");
+  if (!c->comm->capturable() && !(c->peer && ring_dim == 1))
+    return set_error(FUSP_ERR_UNSUPPORTED,
+                     "graph capture needs an NCCL context, a world-1 local context, or peer "
+                     "windows with ring_dim 1");
+  if (opts && opts->check_finite)
+    return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
+  if (layers < 1) return set_error(FUSP_ERR_INVALID_ARGUMENT, "graph capture: layers < 1");
+  FUSP_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto* g = new fusp_graph_s;
+  g->device = c->device;
+  g->ctx = c;
+  void* own_bws = c->block_ws;
+  const size_t own_bbytes = c->block_ws_bytes;
+  c->ws = &g->ws;
+  c->block_ws = nullptr;
+  c->block_ws_bytes = 0;
+  auto restore = [&]() {
+    c->ws = &c->own;
+    g->block_ws = c->block_ws;
+    c->block_ws = own_bws;
+    c->block_ws_bytes = own_bbytes;
+  };
+  auto fail = [&](fusp_status st) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    cudaStreamSynchronize(s);
+    g->ws.release();
+    if (g->block_ws) cudaFree(g->block_ws);
+    delete g;
+    return st;
+  };
+  fusp_status st0 = fusp_usp_block(c, ring_dim, x, x_dtype, batch, s_local, channels, w_qkv, heads,
+                                   prologue, w_out, n_out, y, y_dtype, opts, stream);
+  if (st0 == FUSP_OK && cudaStreamSynchronize(s) != cudaSuccess)
+    st0 = set_cuda_error(cudaGetLastError(), "cudaStreamSynchronize");
+  if (st0 != FUSP_OK) {
+    restore();
+    return fail(st0);
+  }
+  c->capturing = true;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  fusp_status st = e == cudaSuccess ? FUSP_OK : set_cuda_error(e, "cudaStreamBeginCapture");
+  for (int i = 0; i < layers && st == FUSP_OK; ++i)
+    st = fusp_usp_block(c, ring_dim, static_cast<const char*>(x) + i * x_stride, x_dtype, batch, s_local,
+                        channels, w_qkv, heads, prologue, w_out, n_out,
+                        static_cast<char*>(y) + i * y_stride, y_dtype, opts, stream);
+  cudaGraph_t graph_raw = nullptr;
+  e = cudaStreamEndCapture(s, &graph_raw);
+  c->capturing = false;
+  restore();
+  if (st == FUSP_OK && e != cudaSuccess) st = set_cuda_error(e, "cudaStreamEndCapture");
+  if (st == FUSP_OK) {
+    g->graph = graph_raw;
+    e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) st = set_cuda_error(e, "cudaGraphInstantiate");
+  } else if (graph_raw) {
+    cudaGraphDestroy(graph_raw);
+  }
+  if (st != FUSP_OK) return fail(st);
+  c->live_graphs++;
+  *graph = g;
   return FUSP_OK;
 }
 

@@ -27,6 +27,20 @@ for name, s in (("flux", 4608), ("qwen", 7168)):
     e1.record(); e1.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     flop = 2.0 * s * c * 3 * h * 128 + 4.0 * h * s * s * 128 + 2.0 * s * h * 128 * c
+    # the same blocks replayed from one CUDA graph (fusp_graph_capture_block), 4 layers per graph
+    layers = 4
+    xl = x.unsqueeze(0).repeat(layers, 1, 1, 1).contiguous()
+    yl = torch.empty(layers, 1, s, c, device="cuda", dtype=torch.bfloat16)
+    g = fu.BlockGraph(ctx, xl, wqkv, h, wout, yl, mesh, prologue=pro, opts=opts, layers=layers)
+    for _ in range(2):
+        g.launch()
+    torch.cuda.synchronize(); e0.record()
+    for _ in range(reps):
+        g.launch()
+    e1.record(); e1.synchronize()
+    ug = e0.elapsed_time(e1) * 1e3 / (reps * layers)
+    g.close()
     print(json.dumps({"block": name, "tokens": s, "channels": c, "heads": h, "us": round(us, 1),
-                      "flop": flop, "tflops": round(flop / us / 1e6, 1)}), flush=True)
+                      "graph_us": round(ug, 1), "flop": flop, "tflops": round(flop / us / 1e6, 1),
+                      "graph_tflops": round(flop / ug / 1e6, 1)}), flush=True)
     ctx.close()
