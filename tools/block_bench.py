@@ -31,13 +31,15 @@ for name, s in (("flux", 4608), ("qwen", 7168)):
     layers = 4
     xl = x.unsqueeze(0).repeat(layers, 1, 1, 1).contiguous()
     yl = torch.empty(layers, 1, s, c, device="cuda", dtype=torch.bfloat16)
-    g = fu.BlockGraph(ctx, xl, wqkv, h, wout, yl, mesh, prologue=pro, opts=opts, layers=layers)
-    for _ in range(2):
-        g.launch()
-    torch.cuda.synchronize(); e0.record()
-    for _ in range(reps):
-        g.launch()
-    e1.record(); e1.synchronize()
+    cs = torch.cuda.Stream()  # (capture needs a stream other than the legacy default one)
+    with torch.cuda.stream(cs):
+        g = fu.BlockGraph(ctx, xl, wqkv, h, wout, yl, mesh, prologue=pro, opts=opts, layers=layers)
+        for _ in range(2):
+            g.launch()
+        torch.cuda.synchronize(); e0.record()
+        for _ in range(reps):
+            g.launch()
+        e1.record(); e1.synchronize()
     ug = e0.elapsed_time(e1) * 1e3 / (reps * layers)
     g.close()
     print(json.dumps({"block": name, "tokens": s, "channels": c, "heads": h, "us": round(us, 1),
