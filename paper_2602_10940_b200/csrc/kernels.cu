@@ -1922,8 +1922,11 @@ fusp_status try_quantize_fused(const Fp8Src* src, int parts, int64_t n, uint32_t
     FUSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBlock, 0));
     if (dev < 16) per_sm[dev][dt].store(occ);
   }
+  // at most (occupancy - 1) CTAs per SM: a cooperative grid waits until ALL its CTAs fit, so
+  // it leaves every SM room for a small kernel that may be resident meanwhile (an NCCL or
+  // exchange kernel spinning on a peer whose progress could depend on this launch)
   const int grid = a.cta0[parts];
-  if (grid > occ * sm_count() || grid >= 0xFFFF) return FUSP_OK;  // not co-resident
+  if (occ < 2 || grid > (occ - 1) * sm_count() || grid >= 0xFFFF) return FUSP_OK;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);
