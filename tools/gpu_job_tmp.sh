@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-FUSP_TIMEOUT_S=60 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
-tail -4 gpurun_out/gpu_tests.log
-timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log; tail -2 gpurun_out/smoke.log
+timeout 300 python tools/pcie_bw.py > gpurun_out/pcie.txt 2>&1; cat gpurun_out/pcie.txt
+timeout 600 python tools/e2e_probe.py > gpurun_out/e2e_probe.txt 2>&1; cat gpurun_out/e2e_probe.txt
