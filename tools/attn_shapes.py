@@ -25,6 +25,9 @@ def run(hp, span, reps=20):
     return us, 4.0 * hp * span * span * 128 / (us * 1e-6) / 1e12
 
 
+sel = os.environ.get("ATTN_SHAPES")  # comma-separated config names (default: all)
+if sel:
+    SHAPES = [x for x in SHAPES if x[0] in sel.split(",")]
 for name, hp, span in SHAPES:
     for mode in MODES:
         with fu.attention_schedule(mode, 0):

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 python tools/pcie_bw.py > gpurun_out/pcie.txt 2>&1; cat gpurun_out/pcie.txt
-timeout 600 python tools/e2e_probe.py > gpurun_out/e2e_probe.txt 2>&1; cat gpurun_out/e2e_probe.txt
+ATTN_SHAPES=qwen_u1,flux_u1 timeout 600 python tools/attn_shapes.py auto,split,whole,auto,split,whole > gpurun_out/attn_shapes2.jsonl 2>&1; cat gpurun_out/attn_shapes2.jsonl
