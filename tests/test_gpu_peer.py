@@ -358,3 +358,23 @@ def test_block_graph_replays_match_eager(cuda, fu, n):
     for r in rep.results:
         for got, eager in r:
             assert torch.equal(got, eager)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16])
+@pytest.mark.parametrize("n,r,fp8", [(4, 1, False), (4, 2, False), (4, 1, True)])
+def test_peer_input_dtypes_bit_identical(cuda, fu, dtype, n, r, fp8):
+    # the wire carries the caller's dtype (f32 inputs put exactly the reference's bytes on it;
+    # f16 as is) and the receiver stages the operands: through the windows as through the
+    # fabric, bit for bit, with the reference's TrafficLog bytes
+    h, s = 8, 128 * n
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(700 + n, 701 + r, 702 + int(fp8)))
+    qs, ks, vs = shards(q, n, dtype), shards(k, n, dtype), shards(v, n, dtype)
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float32)
+    wb = fu.peer_window_bytes(n, r, (1, h, s // n, 128), dtype, opts)
+    ref = layer(fu, qs, ks, vs, mesh, opts)
+    got = layer(fu, qs, ks, vs, mesh, opts, peer_bytes=wb)
+    for a, b in zip(got.results, ref.results):
+        assert torch.equal(a[0][0], b[0][0])
+        assert a[1] == b[1]
+        assert a[2] == (1, 0)

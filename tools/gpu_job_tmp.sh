@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-ATTN_SHAPES=qwen_u1,flux_u1 timeout 600 python tools/attn_shapes.py auto,split,whole,auto,split,whole > gpurun_out/attn_shapes2.jsonl 2>&1; cat gpurun_out/attn_shapes2.jsonl
+timeout 900 python -m pytest tests/test_gpu_peer.py -q -p no:cacheprovider -k "dtypes" > gpurun_out/pd_tests.log 2>&1; echo "rc=$?" >> gpurun_out/pd_tests.log; tail -5 gpurun_out/pd_tests.log
