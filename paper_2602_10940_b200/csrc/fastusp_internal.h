@@ -170,6 +170,12 @@ fusp_status launch_pack(const PackDesc& p, cudaStream_t s);
 // t's window) instead of t * dst_slot_stride; every CTA fences system-wide before it exits.
 fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s, bool pdl = false,
                               const int64_t* peer_slot_boff = nullptr);
+// The FP8 input reshard's amax + pack as ONE cooperative launch (pack_fp8_fused_kernel) when
+// ps = {Q plain 16-bit, K E4M3, V E4M3} with per-tensor scales fit the grid's registers and the
+// stream is not capturing; amax[p] (and amax[0][1], the barrier) zero on entry and on exit,
+// scales[p] receive the K / V scales.  *done = false: nothing launched, use the two passes.
+fusp_status try_pack_fp8_fused(const PackDesc* ps, uint32_t* const* amax, float* const* scales,
+                              const int64_t* peer_slot_boff, cudaStream_t s, bool* done);
 // Fused QK RMSNorm (w != null) + interleaved RoPE (cosv != null, rows pos0 + s) + pack into
 // slot t = h / (H/u) at t * slot_stride elements (u = 1: plain [B][H][SL][D] output).
 // One operand of a batched prologue pack (w / cos / sin null = that step skipped).

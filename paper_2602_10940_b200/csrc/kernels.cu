@@ -1428,6 +1428,124 @@ __global__ void __launch_bounds__(256, 4) quantize_fused_kernel(const __grid_con
   }
 }
 
+// ---- FP8 Ulysses pack in one cooperative launch (per-tensor scales, small tensors) ---------
+// The FP8 input reshard quantizes the whole local K and V (fp8.cpp:107-123, protocols.cpp:
+// 139-153) and packs them with Q into the slots: an amax launch, then the pack.  When K and V
+// fit the registers of the grid (every FLUX U = 8 shape) one cooperative launch does both:
+// each thread keeps its share of K or V, the CTAs reduce the two amaxes while ALL of them copy
+// Q into its slots, cross a grid barrier, then encode from the registers straight into the
+// slots (the members' windows on the peer path) and write the slot trailers.
+struct FusedPackArgs {
+  PackArgs pk;            // op[0] = Q (plain 16-bit copy), op[1] = K, op[2] = V (E4M3)
+  FDiv slab_vecs, h, hp;  // vector -> slab, slab -> head, head -> slot
+  uint32_t* amax[2];      // zero on entry and on exit
+  float* scales[2];       // out: the K and V scales
+  uint32_t* barrier;      // zero on entry and on exit (arrivals low, departures high 16 bits)
+  int64_t nvec;           // 16-byte vectors per tensor (B*H*SL*D / 8)
+  int cta0[3];            // CTAs [cta0[p], cta0[p+1]) hold part p (K, V)
+};
+__device__ __forceinline__ int64_t fused_pack_dst(const FusedPackArgs& a, int64_t v, int64_t desz,
+                                                  int64_t slot_stride) {
+  const PackArgs& k = a.pk;
+  const uint32_t slab = fdiv(a.slab_vecs, static_cast<uint32_t>(v));
+  const uint32_t off = static_cast<uint32_t>(v) - slab * a.slab_vecs.d;
+  const uint32_t bb = fdiv(a.h, slab), hh = slab - bb * a.h.d;
+  const uint32_t t = fdiv(a.hp, hh), hl = hh - t * a.hp.d;
+  return (k.peer ? k.slot_boff[t] / desz : int64_t(t) * slot_stride) +
+         (int64_t(bb) * k.hp + hl) * k.slab_elems + int64_t(off) * 8;
+}
+template <int SDT>
+__global__ void __launch_bounds__(256, 4) pack_fp8_fused_kernel(const __grid_constant__ FusedPackArgs a) {
+  const int p = blockIdx.x >= static_cast<unsigned>(a.cta0[1]) ? 1 : 0;
+  const PackOp& o = a.pk.op[1 + p];
+  const int64_t per = int64_t(a.cta0[p + 1] - a.cta0[p]) * blockDim.x;
+  const int64_t t0 = int64_t(blockIdx.x - a.cta0[p]) * blockDim.x + threadIdx.x;
+  uint4 w[kFusedHold];
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k)
+    if (t0 + k * per < a.nvec) w[k] = __ldg(reinterpret_cast<const uint4*>(o.src) + t0 + k * per);
+  float m = 0.f;
+  bool bad = false;
+  uint32_t mag = 0;
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k) {
+    if (t0 + k * per >= a.nvec) break;
+    Raw8 r;
+    r.a = w[k];
+    r.b = make_uint4(0, 0, 0, 0);
+    if (!absmax_raw8(r, SDT, mag, bad)) {
+      const Vec8 f = cvt8(r, SDT);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f.f[e]));
+    }
+  }
+  m = fmaxf(m, mag_to_f32(mag, SDT));
+  for (int q = 16; q > 0; q >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, q));
+  __shared__ float wm[kBlock / 32];
+  __shared__ float qs_sh;
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  const unsigned G = gridDim.x;
+  if (threadIdx.x == 0) {
+    float bm = 0.f;
+    for (int i = 0; i < kBlock / 32; ++i) bm = fmaxf(bm, wm[i]);
+    if (!(bm >= 0.f)) bm = 0.f;
+    atomicMax(a.amax[p], __float_as_uint(bm));
+    __threadfence();
+    atomicAdd(a.barrier, 1u);
+  }
+  // Q needs no scale: every CTA copies its share into the slots while the others arrive
+  {
+    const PackOp& qo = a.pk.op[0];
+    const int64_t qstride = int64_t(G) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < a.nvec; v += qstride)
+      reinterpret_cast<uint4*>(qo.dst)[fused_pack_dst(a, v, 2, qo.slot_stride) / 8] =
+          __ldg(reinterpret_cast<const uint4*>(qo.src) + v);
+  }
+  if (threadIdx.x == 0) {
+    uint32_t bv;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(bv) : "l"(a.barrier) : "memory");
+      if ((bv & 0xFFFFu) == G) break;
+      __nanosleep(32);
+    } while (true);
+    const float am = __uint_as_float(__ldcg(a.amax[p]));
+    const float qs = am > 0.f ? __fdiv_rn(am, 448.0f) : 1.0f;  // fp8.cpp:119
+    qs_sh = qs;
+    if (blockIdx.x == static_cast<unsigned>(a.cta0[p])) {
+      *a.scales[p] = qs;
+      // slot trailers: slice_heads keeps the tensor-wide scale (fp8.cpp:100-105)
+      const int u = a.pk.h / a.pk.hp;
+      for (int t = 0; t < u; ++t)
+        o.trailer[a.pk.peer ? a.pk.slot_boff[t] / 4 : t * o.trailer_stride] = qs;
+    }
+  }
+  __syncthreads();
+  const float qs = qs_sh;
+  (void)bad;  // (non-finite inputs are the caller's check_finite; the codes saturate like pack)
+#pragma unroll
+  for (int k = 0; k < kFusedHold; ++k) {
+    const int64_t v = t0 + k * per;
+    if (v >= a.nvec) break;
+    Raw8 r;
+    r.a = w[k];
+    r.b = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint2*>(static_cast<uint8_t*>(o.dst) + fused_pack_dst(a, v, 1, o.slot_stride)) =
+        encode8(cvt8(r, SDT), qs);
+  }
+  if (a.pk.peer) __threadfence_system();  // remote stores visible before the exchange signal
+  __syncthreads();
+  if (threadIdx.x == 0) {  // depart; the last CTA out leaves the words zero
+    const uint32_t old = atomicAdd(a.barrier, 0x10000u);
+    if ((old >> 16) == G - 1) {
+      *a.amax[0] = 0u;
+      *a.amax[1] = 0u;
+      __threadfence();
+      *a.barrier = 0u;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) dequantize_vec_kernel(const uint8_t* __restrict__ c,
                                                              const float* __restrict__ scales,
                                                              FDiv block_vecs, int64_t n_vecs,
@@ -1583,6 +1701,89 @@ fusp_status launch_pack_multi(const PackDesc* ps, int n, cudaStream_t s, bool pd
   if (pdl) FUSP_CUDA(launch_pdl(pack_slab_kernel, grid, s, a));
   else pack_slab_kernel<<<grid, kBlock, 0, s>>>(a);
   FUSP_LAUNCHED("pack_slab_kernel");
+  return FUSP_OK;
+}
+
+fusp_status try_pack_fp8_fused(const PackDesc* ps, uint32_t* const* amax, float* const* scales,
+                              const int64_t* peer_slot_boff, cudaStream_t s, bool* done) {
+  *done = false;
+  static const bool off = getenv("FUSP_FP8_FUSED") != nullptr && atoi(getenv("FUSP_FP8_FUSED")) == 0;
+  const PackDesc& q = ps[0];
+  const int dt = q.src_dtype;
+  if (off || (dt != FUSP_BF16 && dt != FUSP_F16) || q.dst_dtype != dt) return FUSP_OK;
+  const int64_t slab_elems = int64_t(q.sl) * q.d;
+  const int64_t slabs = int64_t(q.b) * q.h;
+  const int64_t n = slabs * slab_elems;
+  if (n <= 0 || n % 8 != 0 || slab_elems % 8 != 0 || q.h % q.u != 0 || n / 8 >= (int64_t(1) << 31))
+    return FUSP_OK;
+  for (int i = 0; i < 3; ++i) {
+    const PackDesc& p = ps[i];
+    if (p.src_dtype != dt || p.b != q.b || p.h != q.h || p.sl != q.sl || p.d != q.d || p.u != q.u ||
+        !aligned16(p.src) || !aligned16(p.dst))
+      return FUSP_OK;
+    if (i > 0 && (p.dst_dtype != FUSP_E4M3 || p.scale_bh_stride != 0 || p.trailer == nullptr ||
+                  p.dst_slot_stride % 16 != 0))
+      return FUSP_OK;
+  }
+  if ((q.dst_slot_stride * 2) % 16 != 0) return FUSP_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FUSP_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return FUSP_OK;
+  FusedPackArgs a{};
+  if (peer_slot_boff != nullptr) {
+    if (q.u > kMaxPeerChunks) return FUSP_OK;
+    a.pk.peer = 1;
+    for (int t = 0; t < q.u; ++t) {
+      if (peer_slot_boff[t] % 16 != 0) return FUSP_OK;
+      a.pk.slot_boff[t] = peer_slot_boff[t];
+    }
+  }
+  for (int i = 0; i < 3; ++i)
+    a.pk.op[i] = PackOp{ps[i].src, ps[i].dst, ps[i].scale, ps[i].amax_bits, ps[i].trailer,
+                        ps[i].trailer_stride, 0, ps[i].dst_slot_stride, ps[i].src_dtype, ps[i].dst_dtype};
+  a.pk.h = q.h;
+  a.pk.hp = q.h / q.u;
+  a.pk.slab_vecs = static_cast<int>(slab_elems / 8);
+  a.pk.slab_elems = slab_elems;
+  a.slab_vecs = make_fdiv(static_cast<uint32_t>(slab_elems / 8));
+  a.h = make_fdiv(static_cast<uint32_t>(q.h));
+  a.hp = make_fdiv(static_cast<uint32_t>(q.h / q.u));
+  a.nvec = n / 8;
+  a.amax[0] = amax[0];
+  a.amax[1] = amax[1];
+  a.scales[0] = scales[0];
+  a.scales[1] = scales[1];
+  a.barrier = amax[0] + 1;  // the amax pass's ticket word (zero on entry and on exit)
+  const int per_part = static_cast<int>((a.nvec + int64_t(kBlock) * kFusedHold - 1) / (int64_t(kBlock) * kFusedHold));
+  a.cta0[0] = 0;
+  a.cta0[1] = per_part;
+  a.cta0[2] = 2 * per_part;
+  void (*k)(FusedPackArgs) = dt == FUSP_BF16 ? pack_fp8_fused_kernel<FUSP_BF16> : pack_fp8_fused_kernel<FUSP_F16>;
+  int dev = 0;
+  FUSP_CUDA(cudaGetDevice(&dev));
+  int occ = 0;
+  static std::atomic<int> per_sm[16][2];
+  const int slot = dt == FUSP_BF16 ? 0 : 1;
+  if (dev < 16 && per_sm[dev][slot].load() > 0) {
+    occ = per_sm[dev][slot].load();
+  } else {
+    FUSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBlock, 0));
+    if (dev < 16) per_sm[dev][slot].store(occ);
+  }
+  const int grid = a.cta0[2];
+  if (occ < 2 || grid > (occ - 1) * sm_count() || grid >= 0xFFFF) return FUSP_OK;  // see quantize
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FUSP_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  FUSP_LAUNCHED("pack_fp8_fused_kernel");
+  *done = true;
   return FUSP_OK;
 }
 
@@ -2104,6 +2305,8 @@ void append_kernels_kernels(std::vector<const void*>& v) {
     v.push_back(k);
   v.push_back(reinterpret_cast<const void*>(dequantize_vec_kernel));
   v.push_back(reinterpret_cast<const void*>(fp8_forward_scales_kernel));
+  v.push_back(reinterpret_cast<const void*>(pack_fp8_fused_kernel<FUSP_BF16>));
+  v.push_back(reinterpret_cast<const void*>(pack_fp8_fused_kernel<FUSP_F16>));
   for (const void* k : {reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_BF16>), reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_F16>),
                         reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_F32>), reinterpret_cast<const void*>(quantize_fused_kernel<FUSP_E4M3>)})
     v.push_back(k);

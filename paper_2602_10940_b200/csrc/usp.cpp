@@ -706,7 +706,6 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
                               Fp8Src{v, l.in_dt, nullptr, 0, 0, l.D, l.SL, l.SL}};
       uint32_t* am[2] = {b.amax, b.amax + l.nsc_local + 1};
       float* sc[2] = {b.pscale, b.pscale + l.nsc_local};
-      FUSP_CHECK(launch_amax_scales(srcs, 2, block, l.nsc_local, am, sc, nullptr, s));
       for (int part = 0; part < 2; ++part) {
         p.src = srcs[part].x;
         p.src_dtype = srcs[part].dt;
@@ -720,9 +719,15 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
         p.trailer_stride = int64_t(l.slot_stride / 4);
         ops[nops++] = p;
       }
-      // programmatic dependent of the amax pass: the Q copy overlaps it, the E4M3 operands
-      // wait for its scales
-      FUSP_CHECK(launch_pack_multi(ops, nops, s, /*pdl=*/true, pboff));
+      bool fused = false;  // small per-tensor case: amax + pack in one cooperative launch
+      if (nops == 3 && !l.fp8_block)
+        FUSP_CHECK(try_pack_fp8_fused(ops, am, sc, pboff, s, &fused));
+      if (!fused) {
+        FUSP_CHECK(launch_amax_scales(srcs, 2, block, l.nsc_local, am, sc, nullptr, s));
+        // programmatic dependent of the amax pass: the Q copy overlaps it, the E4M3 operands
+        // wait for its scales
+        FUSP_CHECK(launch_pack_multi(ops, nops, s, /*pdl=*/true, pboff));
+      }
     }
   }
   if (l.peer) {

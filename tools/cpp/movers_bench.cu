@@ -116,6 +116,44 @@ int main() {
       u[t].src_slot_stride = se2; u[t].dst = t == 0 ? dq : t == 1 ? dk : dv; u[t].dst_dtype = u[t].src_dtype;
       u[t].b = 1; u[t].hp = c.h / c.u; u[t].sl = c.sl; u[t].d = 128; u[t].u = c.u;
     }
+    {  // FP8 Ulysses pack (Q bf16, K and V E4M3 with per-tensor scales + slot trailers)
+      uint32_t* w8;
+      float* sc8;
+      CK(cudaMalloc(&w8, 4096)); CK(cudaMemset(w8, 0, 4096)); CK(cudaMalloc(&sc8, 4096));
+      const int64_t blk8 = n / c.u;                       // elements per slot piece
+      const int64_t slot_bytes = blk8 * 2 + 2 * blk8 + 256;  // [Q bf16][K codes][V codes][trailers]
+      PackDesc f[3];
+      for (int t = 0; t < 3; ++t) {
+        f[t] = PackDesc{};
+        f[t].src = t == 0 ? q : t == 1 ? k : v; f[t].src_dtype = FUSP_BF16;
+        f[t].b = 1; f[t].h = c.h; f[t].sl = c.sl; f[t].d = 128; f[t].u = c.u;
+        f[t].dst = static_cast<char*>(slots) + (t == 0 ? 0 : blk8 * 2 + (t - 1) * blk8);
+        f[t].dst_dtype = t == 0 ? FUSP_BF16 : FUSP_E4M3;
+        f[t].dst_slot_stride = t == 0 ? slot_bytes / 2 : slot_bytes;
+        if (t > 0) {
+          f[t].scale = sc8 + (t - 1);
+          f[t].trailer = reinterpret_cast<float*>(static_cast<char*>(slots) + blk8 * 4) + (t - 1);
+          f[t].trailer_stride = slot_bytes / 4;
+        }
+      }
+      uint32_t* am8[2] = {w8, w8 + 2};
+      float* scs8[2] = {sc8, sc8 + 1};
+      const Fp8Src s8[2] = {Fp8Src{k, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}, Fp8Src{v, FUSP_BF16, nullptr, 0, 0, 128, c.sl, c.sl}};
+      if (int64_t(c.u) * slot_bytes <= n * 6 + 4096) {
+        snprintf(nm, sizeof nm, "%s fp8 Ulysses pack: amax pass + pack (two launches)", c.name);
+        report(nm, double(n) * (2 + 2 + 2 + 2 + 1 + 1), [&] {
+          launch_amax_scales(s8, 2, n, 1, am8, scs8, nullptr, 0);
+          launch_pack_multi(f, 3, 0, true);
+        });
+        snprintf(nm, sizeof nm, "%s fp8 Ulysses pack: one cooperative launch (when it fits)", c.name);
+        report(nm, double(n) * (2 + 2 + 2 + 2 + 1 + 1), [&] {
+          bool done = false;
+          try_pack_fp8_fused(f, am8, scs8, nullptr, 0, &done);
+          if (!done) { launch_amax_scales(s8, 2, n, 1, am8, scs8, nullptr, 0); launch_pack_multi(f, 3, 0, true); }
+        });
+      }
+      cudaFree(w8); cudaFree(sc8);
+    }
     snprintf(nm, sizeof nm, "%s unpack Q,K,V slots -> operands (one launch)", c.name);
     report(nm, 3.0 * n * 4, [&] { launch_unpack_multi(u, 3, 0); });
     // FP8: K and V amax + quantize (per-tensor block), codes into a buffer

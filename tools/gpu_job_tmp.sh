@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_peer.py -q -p no:cacheprovider -k "dtypes" > gpurun_out/pd_tests.log 2>&1; echo "rc=$?" >> gpurun_out/pd_tests.log; tail -5 gpurun_out/pd_tests.log
+timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; grep -A1 "Ulysses pack" gpurun_out/movers.jsonl | cut -c1-220
