@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; grep -A1 "Ulysses pack" gpurun_out/movers.jsonl | cut -c1-220
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 $CS --tool $tool --target-processes all --print-limit 20 python tools/sanitize_cases.py fp8pack > gpurun_out/san_${tool}_fp8pack.log 2>&1; echo "rc=$?" >> gpurun_out/san_${tool}_fp8pack.log
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|rc=|ok$" gpurun_out/san_${tool}_fp8pack.log | head -3
+done

@@ -73,7 +73,21 @@ def ulysses_fp8_u2():
     print("U=2 R=2 per-block FP8 f32-input layer with LSE ok", flush=True)
 
 
-CASES = {"attention": attention, "staging": staging, "fp8": fp8_movers, "ring": ring_fp8_4ranks,
+def fp8_pack_u4():
+    # FP8 input reshard at U = 4, per-tensor scales: the one-launch cooperative amax + pack
+    n = 4
+    q = torch.randn(1, 8, 64 * n, 128, device="cuda", dtype=torch.bfloat16)
+    k, v = torch.randn_like(q), torch.randn_like(q)
+    qs, ks, vs = ([x.contiguous() for x in t.chunk(n, dim=2)] for t in (q, k, v))
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(fp8_kv=True, check_finite=False)
+    fu.run_protocol(n, lambda ctx: fu.usp_attention(ctx, qs[ctx.rank()], ks[ctx.rank()],
+                                                    vs[ctx.rank()], mesh, opts))
+    torch.cuda.synchronize()
+    print("U=4 FP8 per-tensor layer (one-launch pack) ok", flush=True)
+
+
+CASES = {"fp8pack": fp8_pack_u4, "attention": attention, "staging": staging, "fp8": fp8_movers, "ring": ring_fp8_4ranks,
          "usp": ulysses_fp8_u2}
 
 if __name__ == "__main__":
