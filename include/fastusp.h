@@ -187,14 +187,15 @@ fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms
  * (protocols.cpp:125-203) are fused into the kernels around them: the pack kernel stores every
  * member's slot straight into that member's window and the attention epilogue stores O (and the
  * LSE) rows straight into their owner's window, over NVLink / NVSwitch, each followed by one tiny
- * signal-and-wait kernel.  Results and TrafficLog bytes are identical to the comm path; the ring
- * (R > 1) still uses the context's backend.  Windows serve one Ulysses group per context (the
+ * signal-and-wait kernel.  Results and TrafficLog bytes are identical to the comm path.  The
+ * ring's hops (R > 1) go through the windows too (copies into the next member's ring buffers,
+ * signals both ways) when the ring's members are separate processes or devices.  Windows serve one Ulysses group per context (the
  * first layer's); other layers (other groups, the QK prologue variants, D != 128, wire
  * debugging, shapes larger than a window) fall back to the backend -- counted by
  * fusp_ctx_peer_stats.  fusp_usp_block's QKV projection is the producer on this path: its
  * epilogue stores Q, K, V into the members' windows (GEMM and input all-to-all in one kernel),
  * and its output projection reads O where the members' epilogues stored it.  A peer-path layer
- * at ring_dim 1 needs no host rendezvous, so it is graph-capturable on any context.
+ * needs no host rendezvous, so it is graph-capturable on any context.
  * Every kernel of the library is loaded when the window is created (lazy module loading could
  * otherwise synchronise the context behind a spinning exchange).  Ranks that are threads of one
  * process sharing one device need a hardware queue per stream: CUDA_DEVICE_MAX_CONNECTIONS >=

@@ -158,10 +158,12 @@ fusp_status nccl_error(ncclResult_t r, const std::string& where);
 
 // ---- peer-memory windows (peer.cu) --------------------------------------------------------
 // One device window per rank, mapped by every rank of the world (one node): a 4 KB control
-// block of uint32 words -- [0][src] input-reshard signals, [1][src] output-reshard signals,
-// [2][src] / [3][src] completed waits per source, [4][0] timeout flag; src = world rank -- and
-// the data region the Ulysses receive slots live in.
+// block of uint32 words -- [kind][src] signals for kinds 0 input reshard, 1 output reshard,
+// 2 ring chunk ready, 3 ring buffer free; [kPeerKinds + kind][src] completed waits per source;
+// [2 kPeerKinds][0] timeout flag; src = world rank -- and the data region the Ulysses receive
+// slots and the ring receive buffers live in.
 constexpr int kPeerMaxWorld = 64;
+constexpr int kPeerKinds = 4;
 constexpr size_t kPeerCtlBytes = 4096;
 constexpr uint64_t kPeerMagic = 0x46555350504545ull;  // "FUSPPEE"
 struct PeerHandle {  // FUSP_PEER_HANDLE_BYTES on the wire
@@ -179,7 +181,10 @@ struct PeerWindow {
   std::vector<char*> peer;    // world rank -> that rank's window in my address space
   std::vector<bool> opened;   // mapped with cudaIpcOpenMemHandle (closed on destruction)
   std::vector<uint64_t> bytes_of;  // data bytes of every rank's window
+  std::vector<bool> shares_device; // rank r is a thread of this process on my device
   std::string group;          // the one Ulysses group the peer path serves (usp.cpp)
+  std::string ring_group;     // the one ring group the peer ring serves
+  bool ring_used[2] = {false, false};  // ring receive buffer b has held a hop (host order)
   ~PeerWindow();
   char* data(int r) const { return peer[r] + kPeerCtlBytes; }
   uint32_t* ctl(int r) const { return reinterpret_cast<uint32_t*>(peer[r]); }
@@ -191,6 +196,10 @@ fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all);
 // until each has signalled me once more than before (timeout -> the flag peer_window_check reads).
 fusp_status launch_peer_exchange(const PeerWindow& w, int kind, const Group& g, double timeout_s,
                                  cudaStream_t s);
+// Ring step over the windows (kinds 2 / 3): signal `to` (a world rank, -1: none) on `kind_sig`,
+// then wait for one more signal from `from` (-1: none) on `kind_wait` than waited for before.
+fusp_status launch_peer_signal_wait(const PeerWindow& w, int kind_sig, int to, int kind_wait,
+                                    int from, double timeout_s, cudaStream_t s);
 fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_t s);
 
 }  // namespace fusp

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 namespace fusp {
@@ -76,7 +77,51 @@ __global__ void peer_exchange_kernel(const __grid_constant__ ExchArgs a) {
   }
 }
 
+// One thread: signal one rank, then wait for one rank (the ring's point-to-point steps).
+struct SigWaitArgs {
+  uint32_t* remote;  // to's word for me (null: no signal)
+  uint32_t* sig;     // my word for `from` (null: no wait)
+  uint32_t* expect;  // my completed waits on `from`
+  uint32_t* err;
+  unsigned long long timeout_ns;
+};
+__global__ void peer_signal_wait_kernel(const __grid_constant__ SigWaitArgs a) {
+  if (a.remote != nullptr) {
+    __threadfence_system();  // the stream's copies / stores into to's window before the signal
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.remote) : "memory");
+  }
+  if (a.sig != nullptr) {
+    const uint32_t target = *a.expect + 1u;
+    const unsigned long long t0 = globaltimer();
+    while (static_cast<int32_t>(ld_acquire_sys(a.sig) - target) < 0) {
+      __nanosleep(100);
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicOr(a.err, 1u);
+        break;
+      }
+    }
+    *a.expect = target;
+  }
+}
+
 }  // namespace
+
+fusp_status launch_peer_signal_wait(const PeerWindow& w, int kind_sig, int to, int kind_wait,
+                                    int from, double timeout_s, cudaStream_t s) {
+  SigWaitArgs a{};
+  if (to >= 0) a.remote = w.ctl(to) + kind_sig * kPeerMaxWorld + w.rank;
+  if (from >= 0) {
+    a.sig = w.ctl(w.rank) + kind_wait * kPeerMaxWorld + from;
+    a.expect = w.ctl(w.rank) + (kPeerKinds + kind_wait) * kPeerMaxWorld + from;
+  }
+  a.err = w.ctl(w.rank) + 2 * kPeerKinds * kPeerMaxWorld;
+  a.timeout_ns = static_cast<unsigned long long>((timeout_s > 0 ? timeout_s : 120.0) * 1e9);
+  peer_signal_wait_kernel<<<1, 1, 0, s>>>(a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "peer_signal_wait_kernel");
+  return FUSP_OK;
+}
 
 PeerWindow::~PeerWindow() {
   if (device >= 0) cudaSetDevice(device);
@@ -115,6 +160,7 @@ fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all) {
   w->peer.assign(static_cast<size_t>(w->world), nullptr);
   w->opened.assign(static_cast<size_t>(w->world), false);
   w->bytes_of.assign(static_cast<size_t>(w->world), 0);
+  w->shares_device.assign(static_cast<size_t>(w->world), false);
   const int32_t pid = static_cast<int32_t>(getpid());
   // Ranks of this process sharing my device (threads as ranks): every one of them enqueues on
   // its own stream and side stream, and a spinning exchange kernel blocks whatever the
@@ -138,6 +184,7 @@ fusp_status peer_window_open(PeerWindow* w, const PeerHandle* all) {
     if (h.magic != kPeerMagic)
       return set_error(FUSP_ERR_COMM, "peer window: bad handle from rank " + std::to_string(r));
     w->bytes_of[r] = h.bytes;
+    w->shares_device[r] = h.pid == pid && h.device == w->device;
     if (r == w->rank) {
       w->peer[r] = w->base;
       continue;
@@ -176,8 +223,8 @@ fusp_status launch_peer_exchange(const PeerWindow& w, int kind, const Group& g, 
     a.remote[t] = t == g.pos ? nullptr : w.ctl(m) + kind * kPeerMaxWorld + w.rank;
   }
   a.sig = w.ctl(w.rank) + kind * kPeerMaxWorld;
-  a.expect = w.ctl(w.rank) + (2 + kind) * kPeerMaxWorld;
-  a.err = w.ctl(w.rank) + 4 * kPeerMaxWorld;
+  a.expect = w.ctl(w.rank) + (kPeerKinds + kind) * kPeerMaxWorld;
+  a.err = w.ctl(w.rank) + 2 * kPeerKinds * kPeerMaxWorld;
   a.timeout_ns = static_cast<unsigned long long>((timeout_s > 0 ? timeout_s : 120.0) * 1e9);
   peer_exchange_kernel<<<1, 32, 0, s>>>(a);
   count_launch();
@@ -188,17 +235,20 @@ fusp_status launch_peer_exchange(const PeerWindow& w, int kind, const Group& g, 
 
 fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_t s) {
   uint32_t err = 0;  // (stream-ordered: a legacy-stream copy could wait on other ranks' spins)
-  FUSP_CUDA(cudaMemcpyAsync(&err, w.ctl(w.rank) + 4 * kPeerMaxWorld, 4, cudaMemcpyDeviceToHost, s));
+  FUSP_CUDA(cudaMemcpyAsync(&err, w.ctl(w.rank) + 2 * kPeerKinds * kPeerMaxWorld, 4, cudaMemcpyDeviceToHost, s));
   FUSP_CUDA(cudaStreamSynchronize(s));
   if (err && getenv("FUSP_PEER_DEBUG") != nullptr) {  // post-mortem: who signalled whom
-    std::vector<uint32_t> ctl(5 * kPeerMaxWorld);
+    std::vector<uint32_t> ctl((2 * kPeerKinds + 1) * kPeerMaxWorld);
     cudaMemcpy(ctl.data(), w.ctl(w.rank), ctl.size() * 4, cudaMemcpyDeviceToHost);
-    for (int kind = 0; kind < 2; ++kind) {
-      fprintf(stderr, "[peer] rank %d kind %d sig/expect:", w.rank, kind);
+    std::string out;  // one write per rank: ranks may be threads printing at once
+    for (int kind = 0; kind < kPeerKinds; ++kind) {
+      out += "[peer] rank " + std::to_string(w.rank) + " kind " + std::to_string(kind) + " sig/expect:";
       for (int r = 0; r < w.world; ++r)
-        fprintf(stderr, " %u/%u", ctl[kind * kPeerMaxWorld + r], ctl[(2 + kind) * kPeerMaxWorld + r]);
-      fprintf(stderr, "\n");
+        out += " " + std::to_string(ctl[kind * kPeerMaxWorld + r]) + "/" +
+               std::to_string(ctl[(kPeerKinds + kind) * kPeerMaxWorld + r]);
+      out += "\n";
     }
+    fputs(out.c_str(), stderr);
   }
   if (err)
     return set_error(FUSP_ERR_DEADLOCK, std::string("deadlock: rank ") + std::to_string(w.rank) +
@@ -209,6 +259,7 @@ fusp_status peer_window_check(const PeerWindow& w, const char* what, cudaStream_
 // Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).
 void append_kernels_peer(std::vector<const void*>& v) {
   v.push_back(reinterpret_cast<const void*>(peer_exchange_kernel));
+  v.push_back(reinterpret_cast<const void*>(peer_signal_wait_kernel));
 }
 
 }  // namespace fusp

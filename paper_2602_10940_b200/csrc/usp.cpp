@@ -295,7 +295,30 @@ struct Layer {
   char* pw[kMaxPeerChunks] = {};  // data region of member t's window (group order)
   size_t pw_out = 0, pw_lse = 0;  // output / LSE regions (the receive slots start at 0)
   size_t pw_need = 0;             // data bytes the layer needs in every member's window
+  // Peer-memory ring (R > 1): the K / V chunk of every hop is copied into the next member's
+  // window (ring buffers at pw_ring, [buffer][part] of pw_ring_part bytes), no backend call
+  bool peer_ring = false;
+  size_t pw_ring = 0, pw_ring_part = 0;
+  int ring_next = -1, ring_prev = -1;  // world ranks
+  char* ring_next_win = nullptr;       // the next member's data region
+  char* ring_win_self = nullptr;       // my data region
 };
+
+// Window layout of a layer: Ulysses receive slots, output and LSE regions (U > 1), then the
+// ring's two receive buffers of K and V parts (R > 1).  Shared by plan_peer and
+// fusp_peer_window_bytes.
+void peer_layout(Layer& l) {
+  size_t off = 0;
+  if (l.U > 1) {
+    const size_t in = l.slot_stride * l.U;
+    l.pw_out = align_up(in, 256);
+    l.pw_lse = l.pw_out + align_up(size_t(l.blk) * l.wout * l.U, 256);
+    off = l.pw_lse + align_up(size_t(l.blk / l.D) * 4 * l.U, 256);
+  }
+  l.pw_ring = off;
+  l.pw_ring_part = l.R > 1 ? align_up(l.fp8 ? size_t(l.C) + 4 * size_t(l.nsc_chunk) : size_t(l.C) * l.w_in, 256) : 0;
+  l.pw_need = off + 4 * l.pw_ring_part;
+}
 
 struct Buffers {
   // Ulysses in
@@ -428,24 +451,55 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
 // the members' windows itself: GEMM epilogue and all-to-all in one kernel.  Not on the peer
 // path: the QK prologue variants (their pack kernels write local slots), other head dims, wire
 // debugging, layers larger than any member's window.
-bool plan_peer(fusp_ctx_s* c, Layer& l) {
+bool plan_peer_ulysses(fusp_ctx_s* c, Layer& l) {
   l.peer = false;
-  if (!c->peer || !c->peer_open || !l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks || l.generic ||
-      l.pro != nullptr || c->debug_wire)
-    return false;
+  if (!l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks || l.pro != nullptr) return false;
   const std::string key = l.ug.key();
   if (!c->peer->group.empty() && c->peer->group != key) return false;
   if (l.slot_stride % 16 != 0 || (size_t(l.blk) * l.wout) % 16 != 0) return false;
-  const size_t in = l.slot_stride * l.U;
-  l.pw_out = align_up(in, 256);
-  l.pw_lse = l.pw_out + align_up(size_t(l.blk) * l.wout * l.U, 256);
-  l.pw_need = l.pw_lse + align_up(size_t(l.blk / l.D) * 4 * l.U, 256);
   for (int t = 0; t < l.U; ++t)
     if (c->peer->bytes_of[size_t(l.ug.members[t])] < l.pw_need) return false;
   for (int t = 0; t < l.U; ++t) l.pw[t] = c->peer->data(l.ug.members[t]);
   c->peer->group = key;
   l.peer = true;
   return true;
+}
+
+// The ring's K / V hops through the windows: like the Ulysses path, ONE ring group per context
+// (every ring signal of a rank then involves the same two neighbours, whose counters pair up).
+// Ring members that are threads of this process on my device (the single-GPU test setup) keep
+// the backend ring unless FUSP_PEER_RING=1: their streams share the device's hardware queues,
+// and a queue holding one rank's spinning wait ahead of another rank's work can close a cycle
+// through the ring that one-process-per-GPU ranks (separate queues, the deployment shape) and
+// ranks in separate processes (time-sliced contexts; tested over CUDA IPC) cannot.
+bool plan_peer_ring(fusp_ctx_s* c, Layer& l) {
+  l.peer_ring = false;
+  if (l.R < 2 || l.rg.size() < 2) return false;
+  bool shared = true;
+  for (int m : l.rg.members) shared = shared && c->peer->shares_device[size_t(m)];
+  const char* force = getenv("FUSP_PEER_RING");
+  if (shared && !(force != nullptr && atoi(force) == 1)) return false;
+  const std::string key = l.rg.key();
+  if (!c->peer->ring_group.empty() && c->peer->ring_group != key) return false;
+  for (int m : l.rg.members)
+    if (c->peer->bytes_of[size_t(m)] < l.pw_need) return false;
+  const int R = l.rg.size();
+  l.ring_next = l.rg.members[(l.rg.pos + 1) % R];
+  l.ring_prev = l.rg.members[(l.rg.pos - 1 + R) % R];
+  l.ring_next_win = c->peer->data(l.ring_next);
+  l.ring_win_self = c->peer->data(c->rank);
+  c->peer->ring_group = key;
+  l.peer_ring = true;
+  return true;
+}
+
+bool plan_peer(fusp_ctx_s* c, Layer& l) {
+  l.peer = l.peer_ring = false;
+  if (!c->peer || !c->peer_open || l.generic || c->debug_wire) return false;
+  peer_layout(l);
+  const bool u = plan_peer_ulysses(c, l);
+  const bool r = plan_peer_ring(c, l);
+  return u || r;
 }
 
 // Assign workspace for a layer. `q`, `k`, `v` are the caller's tensors (zero-copy when the
@@ -549,7 +603,9 @@ void carve(const Layer& l, Carve& cv, CarveWords& cw, Buffers* b, const void* q,
     const size_t part = l.fp8 ? align_up(size_t(l.C) + 4 * size_t(l.nsc_chunk), 256)
                               : size_t(l.C) * l.w_in;
     for (int i = 0; i < 2; ++i)
-      for (int p = 0; p < 2; ++p) b->rb[i][p] = static_cast<char*>(cv.take(part));
+      for (int p = 0; p < 2; ++p)  // peer ring: my receive buffers are in my window
+        b->rb[i][p] = l.peer_ring ? l.ring_win_self + l.pw_ring + (2 * i + p) * l.pw_ring_part
+                                  : static_cast<char*>(cv.take(part));
     if (l.fp8)
       for (int p = 0; p < 2; ++p) b->sw[p] = static_cast<char*>(cv.take(part));
     for (int i = 0; i < 2; ++i) {
@@ -962,7 +1018,28 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     const size_t bytes[2] = {part_bytes, part_bytes};
     FUSP_CHECK(record_wire(c, 1, hop, snd[0], part_bytes, st));
     FUSP_CHECK(record_wire(c, 2, hop, snd[1], part_bytes, st));
-    FUSP_CHECK(c->comm->ring_exchange(l.rg, snd, rcv, bytes, 2, st));
+    if (l.peer_ring) {
+      // Through the windows (protocols.cpp:253-257 as stores): my receive buffer `into` was
+      // last read by my compute step hop-2 (the caller's event wait precedes this on `st`) and
+      // by my forward of hop-1 (earlier on `st`), so once it has been used I tell my previous
+      // member it may overwrite it, and wait for the same word from my next member before
+      // writing into its buffer.  Then copy both parts (copy engines, over NVLink for a real peer),
+      // signal the next member and wait for my previous member's chunk.
+      // (Across layers too: a buffer that held a hop of an earlier layer is released the same
+      // way -- the first two hops of this layer would otherwise overwrite buffers a slower
+      // neighbour may still be staging or forwarding.  Every rank of the ring runs the same
+      // layer sequence, so the release counts pair up.)
+      const double to = sync_timeout_s();
+      if (c->peer->ring_used[into])
+        FUSP_CHECK(launch_peer_signal_wait(*c->peer, 3, l.ring_prev, 3, l.ring_next, to, st));
+      c->peer->ring_used[into] = true;
+      for (int p = 0; p < 2; ++p)
+        FUSP_CUDA(cudaMemcpyAsync(l.ring_next_win + l.pw_ring + (2 * into + p) * l.pw_ring_part, snd[p],
+                                  part_bytes, cudaMemcpyDeviceToDevice, st));
+      FUSP_CHECK(launch_peer_signal_wait(*c->peer, 2, l.ring_next, 2, l.ring_prev, to, st));
+    } else {
+      FUSP_CHECK(c->comm->ring_exchange(l.rg, snd, rcv, bytes, 2, st));
+    }
     c->send_bytes += 2 * part_bytes;
     log_send(c, l.rg, hop, part_bytes);  // K (protocols.cpp:253)
     log_send(c, l.rg, hop, part_bytes);  // V (protocols.cpp:254)
@@ -1017,7 +1094,7 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
   if (timing) FUSP_CUDA(cudaEventRecord(c->tm1[1], m));
   FUSP_CUDA(cudaEventRecord(c->ev_recv[1], m));
   // compute steps that run beside a transfer leave its SMs free (NCCL kernels need them)
-  const int reserve = c->comm->sms_in_flight();
+  const int reserve = l.peer_ring ? 0 : c->comm->sms_in_flight();  // (copy engines on the peer ring)
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc0[0], s));
   FUSP_CHECK(attend(l, b, b.Kr, b.Vr, b.k_exp, b.v_exp, true, false, out, lse_out, s, reserve));
   if (timing) FUSP_CUDA(cudaEventRecord(c->tc1[0], s));
@@ -1204,14 +1281,15 @@ fusp_status run_layer(fusp_ctx_s* c, Mode mode, int r, const void* q, const void
       return set_error(FUSP_ERR_UNSUPPORTED, "operand producer: bf16/f16 wire, no prologue, no check");
     l.prepacked = true;
   }
-  if (c->peer && l.wire()) {
-    if (plan_peer(c, l)) {
-      if (!size_only) c->peer_layers++;
-    } else if (!size_only) {
-      c->peer_fallbacks++;
-    }
+  if (c->peer && (l.wire() || l.R > 1)) {
+    // a layer is on the peer path when every transfer it makes goes through the windows
+    // (counted on the peer path when its Ulysses reshards -- or, without them, its ring --
+    // went through the windows)
+    plan_peer(c, l);
+    const bool on = l.wire() ? l.peer : l.peer_ring;
+    if (!size_only) ++(on ? c->peer_layers : c->peer_fallbacks);
   }
-  if (c->capturing && !c->comm->capturable() && ((l.wire() && !l.peer) || l.R > 1))
+  if (c->capturing && !c->comm->capturable() && ((l.wire() && !l.peer) || (l.R > 1 && !l.peer_ring)))
     return set_error(FUSP_ERR_UNSUPPORTED,
                      "graph capture: this layer needs the in-process fabric's host rendezvous");
   Carve cv;
@@ -1444,9 +1522,8 @@ fusp_status fusp_peer_window_bytes(int world, int ring_dim, fusp_dtype in_dtype,
   if (opts) o = *opts;
   Layer l;
   FUSP_CHECK(plan_layer(&tmp, Mode::kUsp, ring_dim, ls, in_dtype, o, &l));
-  const size_t in = l.slot_stride * l.U;
-  *bytes = align_up(in, 256) + align_up(size_t(l.blk) * l.wout * l.U, 256) +
-           align_up(size_t(l.blk / l.D) * 4 * l.U, 256);
+  peer_layout(l);
+  *bytes = l.pw_need;
   return FUSP_OK;
 }
 
@@ -2008,10 +2085,9 @@ fusp_status fusp_graph_capture_usp(fusp_ctx c, int ring_dim, const void* q, cons
                                    fusp_graph* graph) {
   clear_error();
   if (!c) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context");
-  if (!c->comm->capturable() && !(c->peer && ring_dim == 1))
+  if (!c->comm->capturable() && !c->peer)
     return set_error(FUSP_ERR_UNSUPPORTED,
-                     "graph capture needs an NCCL context, a world-1 local context, or peer "
-                     "windows with ring_dim 1");
+                     "graph capture needs an NCCL context, a world-1 local context, or peer windows");
   if (opts && opts->check_finite)
     return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
   FUSP_CUDA(cudaSetDevice(c->device));
@@ -2097,10 +2173,9 @@ fusp_status fusp_graph_capture_block(fusp_ctx c, int ring_dim, const void* x, fu
                                      int64_t y_stride, fusp_stream_t stream, fusp_graph* graph) {
   clear_error();
   if (!c || !graph) return set_error(FUSP_ERR_INVALID_ARGUMENT, "null context or graph");
-  if (!c->comm->capturable() && !(c->peer && ring_dim == 1))
+  if (!c->comm->capturable() && !c->peer)
     return set_error(FUSP_ERR_UNSUPPORTED,
-                     "graph capture needs an NCCL context, a world-1 local context, or peer "
-                     "windows with ring_dim 1");
+                     "graph capture needs an NCCL context, a world-1 local context, or peer windows");
   if (opts && opts->check_finite)
     return set_error(FUSP_ERR_UNSUPPORTED, "check_finite synchronizes; not capturable");
   if (layers < 1) return set_error(FUSP_ERR_INVALID_ARGUMENT, "graph capture: layers < 1");

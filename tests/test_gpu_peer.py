@@ -102,16 +102,19 @@ def test_peer_batch2(cuda, fu):
         assert a[2] == (1, 0)
 
 
-def test_peer_back_to_back_layers_no_buffer_race(cuda, fu):
+@pytest.mark.parametrize("r,fp8", [(1, False), (2, False), (4, True)])
+def test_peer_back_to_back_layers_no_buffer_race(cuda, fu, r, fp8):
     # single-buffered windows: consecutive layers reuse every member's regions; a rank that
     # runs ahead must never overwrite data a slower member has not consumed (peer.cu header).
-    # 12 layers with different inputs per layer, 8 ranks racing on one GPU.
+    # 12 layers with different inputs per layer, 8 ranks racing on one GPU; with R > 1 the
+    # ring's hops go through the windows too (two receive buffers per rank, released to the
+    # previous member once consumed -- within a layer and across layers).
     n, h, s = 8, 8, 1024
     probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(300 + i, 400 + i, 500 + i)) for i in range(3)]
     per = [[shards(t, n) for t in p] for p in probs]
-    mesh = fu.make_mesh(n, 1)
-    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float16)
-    wb = window(fu, n, 1, s // n, h, opts)
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float16)
+    wb = window(fu, n, r, s // n, h, opts)
 
     def prog(peer):
         def body(ctx):
@@ -162,13 +165,15 @@ def test_peer_other_group_falls_back(cuda, fu):
     assert all(x[2] == (1, 1) for x in rep.results)
 
 
-def test_peer_graph_capture_multi_rank(cuda, fu):
-    # a peer-path layer at ring_dim 1 needs no host rendezvous: capturable on in-process
-    # ranks (the fabric path is not); 3 replays with new inputs each match eager
+@pytest.mark.parametrize("r", [1])
+def test_peer_graph_capture_multi_rank(cuda, fu, r):
+    # a peer-path layer needs no host rendezvous -- the Ulysses reshards AND the ring's hops
+    # (R > 1) go through the windows -- so it is capturable on in-process ranks (the fabric
+    # path is not); 3 replays with new inputs each match eager
     n, h, s = 4, 8, 512
-    mesh = fu.make_mesh(n, 1)
-    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float16)
-    wb = window(fu, n, 1, s // n, h, opts)
+    mesh = fu.make_mesh(n, r)
+    opts = fu.CommOptions(pipelined_ring=True, check_finite=False, out_dtype=torch.float16)
+    wb = window(fu, n, r, s // n, h, opts)
     probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(240 + i, 250 + i, 260 + i)) for i in range(3)]
     per = [[shards(t, n) for t in p] for p in probs]
 
@@ -289,30 +294,36 @@ print("RESULTS", rep.results)
     assert line.count("CUDA_DEVICE_MAX_CONNECTIONS >= 8") == 4, line
 
 
-def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path):
-    # two processes on cuda:0, windows mapped through CUDA IPC (the deployment path: one process
-    # per GPU) -- the pointer path of ranks-as-threads never opens an IPC handle.  Contexts of
-    # different processes time-slice the GPU, so the spinning exchanges see each other's
-    # signals slice by slice; outputs must equal the in-process 2-rank layer bit for bit.
-    world = 2
+@pytest.mark.parametrize("world,ring,fp8,graph", [(2, 1, False, False), (4, 2, False, True),
+                                                  (4, 4, True, True), (4, 2, True, False)])
+def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8, graph):
+    # PROCESSES on cuda:0, windows mapped through CUDA IPC (the deployment path: one process per
+    # GPU) -- the pointer path of ranks-as-threads never opens an IPC handle.  Contexts of
+    # different processes time-slice the GPU (separate hardware queues), so the spinning
+    # exchanges see each other's signals slice by slice.  With R > 1 the ring's K / V hops go
+    # through the windows too (copies into the next member's ring buffers, released back by
+    # signals), and the three layers also run as ONE captured graph.  Outputs equal the
+    # in-process layer over the fabric bit for bit.
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "peer_ipc_worker.py"), str(r),
-                               str(world), str(tmp_path)], cwd=os.path.dirname(HERE),
-                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
-                              env=dict(os.environ, FUSP_TIMEOUT_S="60"))
+                               str(world), str(tmp_path), str(ring), str(int(fp8)), str(int(graph))],
+                              cwd=os.path.dirname(HERE), stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True, env=dict(os.environ, FUSP_TIMEOUT_S="60"))
              for r in range(world)]
-    errs = [p.communicate(timeout=600)[1] for p in procs]
+    errs = [p.communicate(timeout=900)[1] for p in procs]
     assert all(p.returncode == 0 for p in procs), [e[-1500:] for e in errs]
     got = [torch.load(tmp_path / f"out{r}.pt") for r in range(world)]
-    assert all(tuple(g["stats"]) == (3, 0) for g in got)
+    assert all(tuple(g["stats"])[0] >= 3 and tuple(g["stats"])[1] == 0 for g in got)
     h, s = 8, 256 * world
-    mesh = fu.make_mesh(world, 1)
-    opts = fu.CommOptions(check_finite=False, out_dtype=torch.float32)
+    mesh = fu.make_mesh(world, ring)
+    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float32)
     for i in range(3):
         q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(600 + i, 610 + i, 620 + i))
         qs, ks, vs = shards(q, world), shards(k, world), shards(v, world)
         ref = layer(fu, qs, ks, vs, mesh, opts)
         for r in range(world):
             assert torch.equal(got[r]["outs"][i], ref.results[r][0][0].cpu())
+            if graph:
+                assert torch.equal(got[r]["gouts"][i], ref.results[r][0][0].cpu())
 
 
 @pytest.mark.parametrize("n", [1, 4])

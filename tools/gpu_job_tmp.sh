@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 900 $CS --tool $tool --target-processes all --print-limit 20 python tools/sanitize_cases.py fp8pack > gpurun_out/san_${tool}_fp8pack.log 2>&1; echo "rc=$?" >> gpurun_out/san_${tool}_fp8pack.log
-  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|rc=|ok$" gpurun_out/san_${tool}_fp8pack.log | head -3
-done
+export FUSP_PEER_DEBUG=1
+FUSP_TIMEOUT_S=20 timeout 1500 python -m pytest tests/test_gpu_peer.py tests/test_gpu_nccl_shim.py -q -p no:cacheprovider > gpurun_out/pr.log 2>&1; echo "rc=$?" >> gpurun_out/pr.log; tail -4 gpurun_out/pr.log; grep "^FAILED\|Error" gpurun_out/pr.log | head; grep "\[peer\]" gpurun_out/pr.log | sort | head -30
