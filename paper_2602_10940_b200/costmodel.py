@@ -160,7 +160,8 @@ def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipeli
     peer=True models the peer-memory transport (csrc/peer.cu): the input reshard is the pack
     kernel's own stores into the members' windows (its bytes at link bandwidth plus one
     signal kernel, no NCCL group call), and the output reshard is the attention epilogue's
-    stores -- overlapped with the compute of later tiles except for the last wave's."""
+    stores -- overlapped with the compute of later tiles except for the last wave's; the ring's
+    rounds are copy-engine copies into the next member's window plus one signal kernel."""
     if n % r or w.H % (n // r) or w.S % n:
         raise ValueError(f"infeasible mesh N={n} R={r} for H={w.H}, S={w.S}")
     u = n // r
@@ -176,8 +177,10 @@ def step_latency(hw: HardwareProfile, w: WorkloadProfile, n: int, r: int, pipeli
     else:
         a2a = comm_volume_ulysses(w, u, hw.element_width, fp8, out_width=ow, n=n) / hw.link_bandwidth
         a2a += (2 * hw.link_latency) if u > 1 else 0.0
+    # ring round: the K / V chunk over the link, plus an NCCL group call -- or, on the peer
+    # ring, a copy-engine copy into the next member's window and one signal kernel
     per_round_comm = (comm_volume_ring(w, r, u, hw.element_width, fp8) / max(r - 1, 1)
-                      / hw.link_bandwidth + hw.link_latency) if r > 1 else 0.0
+                      / hw.link_bandwidth + (hw.peer_signal if peer else hw.link_latency)) if r > 1 else 0.0
     tl = pipeline_timeline(step_compute, per_round_comm, r)
     ring_total = tl["pipelined_total"] if pipelined else tl["serial_total"]
     compute = r * step_compute
