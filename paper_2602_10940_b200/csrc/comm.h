@@ -184,7 +184,6 @@ struct PeerWindow {
   std::vector<bool> shares_device; // rank r is a thread of this process on my device
   std::string group;          // the one Ulysses group the peer path serves (usp.cpp)
   std::string ring_group;     // the one ring group the peer ring serves
-  bool ring_used[2] = {false, false};  // ring receive buffer b has held a hop (host order)
   ~PeerWindow();
   char* data(int r) const { return peer[r] + kPeerCtlBytes; }
   uint32_t* ctl(int r) const { return reinterpret_cast<uint32_t*>(peer[r]); }

@@ -1021,18 +1021,15 @@ fusp_status ring(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* k_src, c
     if (l.peer_ring) {
       // Through the windows (protocols.cpp:253-257 as stores): my receive buffer `into` was
       // last read by my compute step hop-2 (the caller's event wait precedes this on `st`) and
-      // by my forward of hop-1 (earlier on `st`), so once it has been used I tell my previous
-      // member it may overwrite it, and wait for the same word from my next member before
-      // writing into its buffer.  Then copy both parts (copy engines, over NVLink for a real peer),
+      // by my forward of hop-1 (earlier on `st`), so I tell my previous member it may overwrite
+      // it, and wait for the same word from my next member before writing into its buffer.  Then copy both parts (copy engines, over NVLink for a real peer),
       // signal the next member and wait for my previous member's chunk.
-      // (Across layers too: a buffer that held a hop of an earlier layer is released the same
-      // way -- the first two hops of this layer would otherwise overwrite buffers a slower
-      // neighbour may still be staging or forwarding.  Every rank of the ring runs the same
-      // layer sequence, so the release counts pair up.)
+      // Released at EVERY hop, also for a buffer no hop has used yet (the pair of signals is
+      // then a plain handshake): the first hops of a layer reuse the buffers of the previous
+      // layer, and a captured graph replays the same kernels whatever ran before, so no host
+      // state may decide which hops release.
       const double to = sync_timeout_s();
-      if (c->peer->ring_used[into])
-        FUSP_CHECK(launch_peer_signal_wait(*c->peer, 3, l.ring_prev, 3, l.ring_next, to, st));
-      c->peer->ring_used[into] = true;
+      FUSP_CHECK(launch_peer_signal_wait(*c->peer, 3, l.ring_prev, 3, l.ring_next, to, st));
       for (int p = 0; p < 2; ++p)
         FUSP_CUDA(cudaMemcpyAsync(l.ring_next_win + l.pw_ring + (2 * into + p) * l.pw_ring_part, snd[p],
                                   part_bytes, cudaMemcpyDeviceToDevice, st));

@@ -324,6 +324,8 @@ def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8,
             assert torch.equal(got[r]["outs"][i], ref.results[r][0][0].cpu())
             if graph:
                 assert torch.equal(got[r]["gouts"][i], ref.results[r][0][0].cpu())
+                if i == 0:  # the eager layer after the replays
+                    assert torch.equal(got[r]["outs"][3], ref.results[r][0][0].cpu())
 
 
 @pytest.mark.parametrize("n", [1, 4])
