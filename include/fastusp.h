@@ -350,7 +350,7 @@ fusp_status fusp_graph_capture_usp(fusp_ctx ctx, int ring_dim, const void* q, co
 /* The same for `layers` back-to-back fusp_usp_block calls (x / y of layer i at i * x_stride /
  * i * y_stride bytes): the whole MMDiT attention block -- QKV projection, the USP layer and the
  * output projection -- as one graph.  Runs layer 0 once eagerly to size the graph's own
- * workspace.  Capturable at world > 1 through NCCL or with peer windows at ring_dim 1. */
+ * workspace.  Capturable at world > 1 through NCCL or with peer windows (see above). */
 fusp_status fusp_graph_capture_block(fusp_ctx ctx, int ring_dim, const void* x, fusp_dtype x_dtype,
                                      int64_t batch, int64_t s_local, int64_t channels,
                                      const void* w_qkv, int heads, const fusp_qk_prologue* prologue,
