@@ -30,7 +30,10 @@ class HardwareProfile:
     link_bandwidth: float = 770e9       # B/s per direction per GPU (measured peer copy)
     link_latency: float = 6e-6          # s per NCCL group call (launch + handshake)
     peer_signal: float = 2e-6           # s per peer-window signal-and-wait kernel (fused path)
-    launch_overhead: float = 4e-6       # s per kernel launch, eager
+    # per kernel launch, eager: calibrated on the 60-layer Qwen stack at world 1 (2 kernels a
+    # layer; profiles/r02_vmesh.jsonl "cuda_graph_stack": 34.29 ms eager vs 33.40 ms replayed
+    # = 14.8 us a layer), with graph_residual assumed (one measurement cannot separate them)
+    launch_overhead: float = 7.8e-6
     graph_residual: float = 0.05        # fraction of launch cost left under graph replay
     element_width: int = 2              # bytes per Q/K/V element on the wire (bf16/f16)
     peak_tflops: float = 1618.9         # measured dense bf16 burst (MEASURED_PEAKS.json)
