@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -1513,10 +1514,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- host-side schedule ------------------------------------------------------------------
-int g_sched_mode = 0;  // 0 auto, 1 whole q-blocks, 2 stream-K split
+// (tuning knobs set by fusp_attention_schedule from any thread: atomics, read once per plan)
+std::atomic<int> g_sched_mode{0};  // 0 auto, 1 whole q-blocks, 2 stream-K split, 3-5 variants
 unsigned long long* g_trace = nullptr;  // debug event buffer (attention_trace), device memory
 bool g_trace_on = false;
-int g_max_ctas = 0;    // 0 = every SM
+std::atomic<int> g_max_ctas{0};    // 0 = every SM
 
 }  // namespace
 int sm_count() {
@@ -1544,6 +1546,8 @@ struct Plan {
 
 Plan plan_attention(int heads, int sq, int skv, bool have_ws, int max_ctas) {
   Plan pl{};
+  const int g_sched_mode = fusp::g_sched_mode.load(std::memory_order_relaxed);
+  const int g_max_ctas = fusp::g_max_ctas.load(std::memory_order_relaxed);
   int sms = sm_count();
   if (g_max_ctas > 0 && g_max_ctas < sms) sms = g_max_ctas;
   if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
