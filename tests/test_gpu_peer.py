@@ -391,3 +391,34 @@ def test_peer_input_dtypes_bit_identical(cuda, fu, dtype, n, r, fp8):
         assert torch.equal(a[0][0], b[0][0])
         assert a[1] == b[1]
         assert a[2] == (1, 0)
+
+
+def test_peer_check_finite_rejects_before_any_exchange(cuda, fu):
+    # check_finite validates the local inputs before the pack (protocols.cpp:97-105): every rank
+    # raises InvalidArgument with the reference's message and no rank is left in an exchange
+    n, h, s = 4, 4, 512
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(801, 802, 803))
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    for t in ks:
+        t[0, 0, 3, 5] = float("nan")
+    mesh = fu.make_mesh(n, 1)
+    opts = fu.CommOptions(check_finite=True)
+    wb = window(fu, n, 1, s // n, h, opts)
+
+    def prog(ctx):
+        ctx.enable_peer_memory(wb)
+        try:
+            fu.usp_attention(ctx, qs[ctx.rank()], ks[ctx.rank()], vs[ctx.rank()], mesh, opts)
+        except fu.InvalidArgument as e:
+            msg = str(e)
+        else:
+            msg = "no error"
+        # the windows still work afterwards (nothing half-exchanged)
+        ok = fu.usp_attention(ctx, qs[ctx.rank()], qs[ctx.rank()], vs[ctx.rank()], mesh,
+                              fu.CommOptions(check_finite=False))
+        ctx.synchronize()
+        return msg, bool(torch.isfinite(ok).all())
+
+    rep = fu.run_protocol(n, prog)
+    for msg, finite in rep.results:
+        assert "non-finite" in msg and finite
