@@ -2,7 +2,8 @@
 on cuda:0 whose window reaches the other rank's through CUDA IPC (cudaIpcGetMemHandle /
 cudaIpcOpenMemHandle), as one-process-per-GPU ranks do over NVLink.  Handles travel through
 files in a scratch directory (the caller's own bootstrap: fusp_ctx_peer_window / _open).
-usage: python tests/peer_ipc_worker.py RANK WORLD DIR [RING_DIM FP8 GRAPH]"""
+usage: python tests/peer_ipc_worker.py RANK WORLD DIR [RING_DIM FP8 GRAPH BATCH]
+(FP8: 0 off, 1 per tensor, 2 per (b,h) block)"""
 import os
 import sys
 import time
@@ -29,18 +30,20 @@ def wait_for(path, timeout=120.0):
 def main():
     rank, world, d = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
     r = int(sys.argv[4]) if len(sys.argv) > 4 else 1
-    fp8 = len(sys.argv) > 5 and sys.argv[5] == "1"
+    fp8 = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     graph = len(sys.argv) > 6 and sys.argv[6] == "1"
+    bsz = int(sys.argv[7]) if len(sys.argv) > 7 else 1
     torch.cuda.set_device(0)
     h, s = 8, 256 * world
-    probs = [qkv((1, h, s, 128), (1, h, s, 128), seeds=(600 + i, 610 + i, 620 + i)) for i in range(3)]
+    probs = [qkv((bsz, h, s, 128), (bsz, h, s, 128), seeds=(600 + i, 610 + i, 620 + i)) for i in range(3)]
     mesh = fu.make_mesh(world, r)
-    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float32)
+    opts = fu.CommOptions(fp8_kv=fp8 > 0, fp8_block=int(fp8 == 2), pipelined_ring=True,
+                          check_finite=False, out_dtype=torch.float32)
     # a fabric of `world` ranks of which this process runs one: the peer path at R = 1 moves
     # every byte through the windows, the fabric is never entered
     fab = fu.Fabric(world)
     ctx = fu.WorkerContext.local(fab, rank, 0)
-    wb = fu.peer_window_bytes(world, r, (1, h, s // world, 128), torch.bfloat16, opts)
+    wb = fu.peer_window_bytes(world, r, (bsz, h, s // world, 128), torch.bfloat16, opts)
     mine = ctx.peer_window(wb)
     tmp = os.path.join(d, f"h{rank}.tmp")
     with open(tmp, "wb") as f:

@@ -294,9 +294,10 @@ print("RESULTS", rep.results)
     assert line.count("CUDA_DEVICE_MAX_CONNECTIONS >= 8") == 4, line
 
 
-@pytest.mark.parametrize("world,ring,fp8,graph", [(2, 1, False, False), (4, 2, False, True),
-                                                  (4, 4, True, True), (4, 2, True, False)])
-def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8, graph):
+@pytest.mark.parametrize("world,ring,fp8,graph,bsz", [(2, 1, 0, False, 1), (4, 2, 0, True, 1),
+                                                      (4, 4, 1, True, 1), (4, 2, 1, False, 1),
+                                                      (4, 2, 2, False, 1), (4, 2, 0, False, 2)])
+def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8, graph, bsz):
     # PROCESSES on cuda:0, windows mapped through CUDA IPC (the deployment path: one process per
     # GPU) -- the pointer path of ranks-as-threads never opens an IPC handle.  Contexts of
     # different processes time-slice the GPU (separate hardware queues), so the spinning
@@ -305,7 +306,7 @@ def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8,
     # signals), and the three layers also run as ONE captured graph.  Outputs equal the
     # in-process layer over the fabric bit for bit.
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "peer_ipc_worker.py"), str(r),
-                               str(world), str(tmp_path), str(ring), str(int(fp8)), str(int(graph))],
+                               str(world), str(tmp_path), str(ring), str(fp8), str(int(graph)), str(bsz)],
                               cwd=os.path.dirname(HERE), stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                               text=True, env=dict(os.environ, FUSP_TIMEOUT_S="60"))
              for r in range(world)]
@@ -315,9 +316,10 @@ def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8,
     assert all(tuple(g["stats"])[0] >= 3 and tuple(g["stats"])[1] == 0 for g in got)
     h, s = 8, 256 * world
     mesh = fu.make_mesh(world, ring)
-    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float32)
+    opts = fu.CommOptions(fp8_kv=fp8 > 0, fp8_block=int(fp8 == 2), pipelined_ring=True,
+                          check_finite=False, out_dtype=torch.float32)
     for i in range(3):
-        q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(600 + i, 610 + i, 620 + i))
+        q, k, v = qkv((bsz, h, s, 128), (bsz, h, s, 128), seeds=(600 + i, 610 + i, 620 + i))
         qs, ks, vs = shards(q, world), shards(k, world), shards(v, world)
         ref = layer(fu, qs, ks, vs, mesh, opts)
         for r in range(world):
