@@ -330,8 +330,8 @@ def test_peer_windows_across_processes_ipc(cuda, fu, tmp_path, world, ring, fp8,
                     assert torch.equal(got[r]["outs"][3], ref.results[r][0][0].cpu())
 
 
-@pytest.mark.parametrize("n", [1, 4])
-def test_block_graph_replays_match_eager(cuda, fu, n):
+@pytest.mark.parametrize("n,fp8", [(1, False), (4, False), (1, True), (2, True)])
+def test_block_graph_replays_match_eager(cuda, fu, n, fp8):
     # the whole MMDiT attention block (QKV projection -> USP layer -> output projection) of 3
     # layers captured as ONE CUDA graph (fusp_graph_capture_block), replayed with new inputs:
     # bit-identical to eager blocks.  n = 4: ranks as threads with peer windows -- the fused
@@ -344,9 +344,11 @@ def test_block_graph_replays_match_eager(cuda, fu, n):
     w_d, wo_d = torch.from_numpy(w).cuda().bfloat16(), torch.from_numpy(wo).cuda().bfloat16()
     xs = [R.round_bf16(rs.uniform(-1, 1, (layers, 1, s, c)).astype(np.float32)) for _ in range(2)]
     mesh = fu.make_mesh(n, 1)
-    opts = fu.CommOptions(check_finite=False)
+    # (FP8: the block stages Q, K, V and the layer quantizes K, V -- the two-pass form under
+    # capture, the one-launch form eager: the same codes)
+    opts = fu.CommOptions(fp8_kv=fp8, check_finite=False)
     wb = fu.peer_window_bytes(n, 1, (1, heads, s // n, 128), torch.bfloat16,
-                              fu.CommOptions(check_finite=False, out_dtype=torch.bfloat16))
+                              fu.CommOptions(fp8_kv=fp8, check_finite=False, out_dtype=torch.bfloat16))
 
     def prog(ctx):
         if n > 1:
