@@ -607,10 +607,38 @@ __device__ __forceinline__ uint32_t enc_pair_finite(float a, float b) {
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
   return r;
 }
+// x * inv for a pair with one FFMA2 (c = -0: RN(a b + -0) = RN(a b), signed zeros included).
+__device__ __forceinline__ float2 fmul2_rn(float2 a, float b) {
+  const float2 bb = make_float2(b, b), zz = make_float2(-0.f, -0.f);
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(reinterpret_cast<unsigned long long&>(r))
+      : "l"(reinterpret_cast<const unsigned long long&>(a)),
+        "l"(reinterpret_cast<const unsigned long long&>(bb)),
+        "l"(reinterpret_cast<const unsigned long long&>(zz)));
+  return r;
+}
+// As qdiv on 8 values: the products packed in pairs, and one branch per vector to the exact
+// divisions -- taken only when some product is in the E4M3 subnormal range or near a rounding
+// boundary (then every element of the vector goes through qdiv, with the same results).
 __device__ __forceinline__ uint2 encode8_finite(const Vec8& v, float qs, float inv) {
   float q[8];
+  uint32_t slow = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) q[e] = qdiv(v.f[e], qs, inv);
+  for (int e = 0; e < 8; e += 2) {
+    const float2 p = fmul2_rn(make_float2(v.f[e], v.f[e + 1]), inv);
+    q[e] = p.x;
+    q[e + 1] = p.y;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t b = __float_as_uint(q[e]) & 0x7fffffffu;
+    slow |= static_cast<uint32_t>(b < 0x3c800000u) | static_cast<uint32_t>(((b & 0xFFFFFu) - 0x7FFF8u) < 16u);
+  }
+  if (slow) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] = qdiv(v.f[e], qs, inv);
+  }
   return make_uint2(enc_pair_finite(q[0], q[1]) | (enc_pair_finite(q[2], q[3]) << 16),
                     enc_pair_finite(q[4], q[5]) | (enc_pair_finite(q[6], q[7]) << 16));
 }
