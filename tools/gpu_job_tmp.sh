@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_wire.py tests/test_gpu_configs.py -q -p no:cacheprovider > gpurun_out/k.log 2>&1; echo "rc=$?" >> gpurun_out/k.log; tail -3 gpurun_out/k.log
-timeout 300 tools/cpp/movers_bench > gpurun_out/movers.jsonl 2>&1; grep -A1 "fp8" gpurun_out/movers.jsonl | cut -c1-200
+SHAPES=flux_u1,qwen_u1,flux_u2 timeout 900 python tools/ab_attn.py main p40 u4 e5 > gpurun_out/ab_var.jsonl 2>&1; cat gpurun_out/ab_var.jsonl | cut -c1-400
