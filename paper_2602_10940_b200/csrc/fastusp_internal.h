@@ -189,11 +189,13 @@ struct ProPack {
 };
 fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_stride, int b,
                                         int h, int sl, int d, int u, float eps, int64_t pos0,
-                                        cudaStream_t s);
+                                        cudaStream_t s,
+                                        const int64_t* peer_slot_boff = nullptr);
 fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
                                   int64_t slot_stride, int b, int h, int sl, int d, int u,
                                   const float* w, float eps, const float* cosv, const float* sinv,
-                                  int64_t pos0, cudaStream_t s);
+                                  int64_t pos0, cudaStream_t s,
+                                  const int64_t* peer_slot_boff = nullptr);
 // Ulysses unpack: src slots [U][B][hp][SL][D] -> dst [B][hp][U*SL][D]; e4m3 src uses per-slot
 // scales scale[j] (device) -- value = decode(code) * scale[j] in f32, then cast to dst dtype.
 struct UnpackDesc {

@@ -68,6 +68,8 @@ struct ProArgs {
   int rows;             // B * H * SL
   float eps;
   int64_t pos0;
+  int peer;             // slot t at slot_boff[t] bytes from slot 0 (the members' peer windows)
+  int64_t slot_boff[kMaxPeerChunks];
 };
 
 // src [B][H][SL][D] -> dst slot t = h / hp: [B][hp][SL][D] at t * slot_stride (elements);
@@ -104,16 +106,18 @@ __global__ void __launch_bounds__(256) norm_rope_pack_kernel(const __grid_consta
       x[0] = y0; x[1] = y1; x[2] = y2; x[3] = y3;
     }
     const int t = hh / a.hp, hl = hh - t * a.hp;
-    const int64_t dst = t * a.slot_stride + ((int64_t(bb) * a.hp + hl) * a.sl + s) * D + lane * 4;
+    const int64_t slot0 = a.peer ? a.slot_boff[t] / (o.ddt == FUSP_F32 ? 4 : 2) : t * a.slot_stride;
+    const int64_t dst = slot0 + ((int64_t(bb) * a.hp + hl) * a.sl + s) * D + lane * 4;
     store4(o.dst, o.ddt, dst, x);
   }
+  if (a.peer) __threadfence_system();  // remote stores visible before the exchange signal
 }
 
 }  // namespace
 
 fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_stride, int b,
                                         int h, int sl, int d, int u, float eps, int64_t pos0,
-                                        cudaStream_t s) {
+                                        cudaStream_t s, const int64_t* peer_slot_boff) {
   if (d != 128) return set_error(FUSP_ERR_SHAPE, "qk prologue: head dim must be 128");
   if (n < 1 || n > 3) return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: 1..3 operands");
   const int64_t rows = int64_t(b) * h * sl;
@@ -129,6 +133,14 @@ fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_
   a.rows = static_cast<int>(rows);
   a.eps = eps;
   a.pos0 = pos0;
+  if (peer_slot_boff != nullptr) {
+    if (u > kMaxPeerChunks) return set_error(FUSP_ERR_UNSUPPORTED, "qk prologue: too many peer slots");
+    a.peer = 1;
+    for (int t = 0; t < u; ++t) {
+      if (peer_slot_boff[t] % 16 != 0) return set_error(FUSP_ERR_INVALID_ARGUMENT, "qk prologue: misaligned peer slot");
+      a.slot_boff[t] = peer_slot_boff[t];
+    }
+  }
   int64_t grid = (rows * 32 + 255) / 256;
   const int64_t cap = (int64_t(sm_count()) * 16 + n - 1) / n;
   if (grid > cap) grid = cap;
@@ -142,9 +154,9 @@ fusp_status launch_norm_rope_pack_multi(const ProPack* ops, int n, int64_t slot_
 fusp_status launch_norm_rope_pack(const void* src, int sdt, void* dst, int ddt,
                                   int64_t slot_stride, int b, int h, int sl, int d, int u,
                                   const float* w, float eps, const float* cosv, const float* sinv,
-                                  int64_t pos0, cudaStream_t s) {
+                                  int64_t pos0, cudaStream_t s, const int64_t* peer_slot_boff) {
   const ProPack op{src, dst, w, cosv, sinv, sdt, ddt};
-  return launch_norm_rope_pack_multi(&op, 1, slot_stride, b, h, sl, d, u, eps, pos0, s);
+  return launch_norm_rope_pack_multi(&op, 1, slot_stride, b, h, sl, d, u, eps, pos0, s, peer_slot_boff);
 }
 
 // Every kernel of this file, for preload_kernels() (lazy module loading, see runtime.cpp).

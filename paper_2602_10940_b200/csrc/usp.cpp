@@ -448,12 +448,12 @@ fusp_status plan_layer(fusp_ctx_s* c, Mode mode, int r, const fusp_shape4& ls, i
 // stores) or through c->comm.  The windows serve ONE Ulysses group per context (the hazard
 // argument in peer.cu needs every peer-path exchange of a rank to involve the same members):
 // the first eligible layer's group.  A producer (fusp_usp_block's QKV projection) stores into
-// the members' windows itself: GEMM epilogue and all-to-all in one kernel.  Not on the peer
-// path: the QK prologue variants (their pack kernels write local slots), other head dims, wire
-// debugging, layers larger than any member's window.
+// the members' windows itself: GEMM epilogue and all-to-all in one kernel, and so do the fused
+// QK RMSNorm + RoPE packs.  Not on the peer path: other head dims, wire debugging, layers
+// larger than any member's window.
 bool plan_peer_ulysses(fusp_ctx_s* c, Layer& l) {
   l.peer = false;
-  if (!l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks || l.pro != nullptr) return false;
+  if (!l.wire() || l.force_wire || l.U < 2 || l.U > kMaxPeerChunks) return false;
   const std::string key = l.ug.key();
   if (!c->peer->group.empty() && c->peer->group != key) return false;
   if (l.slot_stride % 16 != 0 || (size_t(l.blk) * l.wout) % 16 != 0) return false;
@@ -734,13 +734,14 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
     if (!l.fp8 && (l.pro_q || l.pro_k)) {
       // one norm/RoPE/pack launch whose V operand is a plain pack
       const fusp_qk_prologue& pr = *l.pro;
+      // (peer path: the fused prologue stores into the members' windows like the plain pack)
       const ProPack pops[3] = {
-          {q, b.send_in, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
+          {q, sbase, l.pro_q ? pr.q_norm_weight : nullptr, l.pro_q ? pr.rope_cos : nullptr,
            l.pro_q ? pr.rope_sin : nullptr, l.in_dt, l.in_dt},
-          {k, b.send_in + l.off_k, l.pro_k ? pr.k_norm_weight : nullptr,
+          {k, sbase + l.off_k, l.pro_k ? pr.k_norm_weight : nullptr,
            l.pro_k ? pr.rope_cos : nullptr, l.pro_k ? pr.rope_sin : nullptr, l.in_dt, l.in_dt},
-          {v, b.send_in + l.off_v, nullptr, nullptr, nullptr, l.in_dt, l.in_dt}};
-      FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, sew, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s));
+          {v, sbase + l.off_v, nullptr, nullptr, nullptr, l.in_dt, l.in_dt}};
+      FUSP_CHECK(launch_norm_rope_pack_multi(pops, 3, sew, l.B, l.H, l.SL, l.D, l.U, pr.eps, l.pos0, s, pboff));
     } else if (!l.fp8) {
       ops[nops++] = p;
       p.src = k;
@@ -751,7 +752,11 @@ fusp_status ulysses_in(fusp_ctx_s* c, const Layer& l, Buffers& b, const void* q,
       ops[nops++] = p;
       FUSP_CHECK(launch_pack_multi(ops, nops, s, false, pboff));
     } else {
-      if (l.pro_q) FUSP_CHECK(prologue(true, q, b.send_in, l.in_dt, sew, l.U));
+      if (l.pro_q) {
+        const fusp_qk_prologue& pr = *l.pro;
+        FUSP_CHECK(launch_norm_rope_pack(q, l.in_dt, sbase, l.in_dt, sew, l.B, l.H, l.SL, l.D, l.U,
+                                         pr.q_norm_weight, pr.eps, pr.rope_cos, pr.rope_sin, l.pos0, s, pboff));
+      }
       else ops[nops++] = p;
       // per-tensor scale over ALL local heads (fp8.cpp:107-123) -- or one per (b,h) slab --:
       // one amax launch for K and V, then Q, K, V leave in one pack launch whose E4M3

@@ -426,3 +426,35 @@ def test_peer_check_finite_rejects_before_any_exchange(cuda, fu):
     rep = fu.run_protocol(n, prog)
     for msg, finite in rep.results:
         assert "non-finite" in msg and finite
+
+
+@pytest.mark.parametrize("n,r,fp8", [(4, 1, False), (8, 2, False), (4, 1, True)])
+def test_peer_qk_prologue_bit_identical(cuda, fu, n, r, fp8):
+    # the fused QK RMSNorm + RoPE pack stores into the members' windows like the plain pack
+    h, s = 8, 128 * n
+    q, k, v = qkv((1, h, s, 128), (1, h, s, 128), seeds=(900 + n, 901 + r, 902 + int(fp8)))
+    qs, ks, vs = shards(q, n), shards(k, n), shards(v, n)
+    mesh = fu.make_mesh(n, r)
+    cos, sin = fu.rope_tables(s)
+    rs = np.random.RandomState(n + r)
+    pro = fu.QKPrologue(q_norm_weight=torch.from_numpy(rs.uniform(0.5, 1.5, 128).astype(np.float32)).cuda(),
+                        k_norm_weight=torch.from_numpy(rs.uniform(0.5, 1.5, 128).astype(np.float32)).cuda(),
+                        eps=1e-6, rope_cos=cos, rope_sin=sin)
+    opts = fu.CommOptions(fp8_kv=fp8, pipelined_ring=True, check_finite=False, out_dtype=torch.float32)
+    wb = window(fu, n, r, s // n, h, opts)
+
+    def run(peer):
+        def prog(ctx):
+            if peer:
+                ctx.enable_peer_memory(wb)
+            i = ctx.rank()
+            out = fu.usp_attention(ctx, qs[i], ks[i], vs[i], mesh, opts, prologue=pro).clone()
+            ctx.synchronize()
+            return out, ctx.traffic(), ctx.peer_stats() if peer else None
+        return fu.run_protocol(n, prog)
+
+    ref, got = run(False), run(True)
+    for a, b in zip(got.results, ref.results):
+        assert torch.equal(a[0], b[0])
+        assert a[1] == b[1]
+        assert a[2] == (1, 0)

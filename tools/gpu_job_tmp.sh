@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-SHAPES=flux_u1,qwen_u1,flux_u2 timeout 900 python tools/ab_attn.py main p40 u4 e5 > gpurun_out/ab_var.jsonl 2>&1; cat gpurun_out/ab_var.jsonl | cut -c1-400
+FUSP_TIMEOUT_S=30 timeout 900 python -m pytest tests/test_gpu_peer.py tests/test_gpu_prologue.py -q -p no:cacheprovider > gpurun_out/pro.log 2>&1; echo "rc=$?" >> gpurun_out/pro.log; tail -15 gpurun_out/pro.log
