@@ -190,9 +190,10 @@ fusp_status fusp_ctx_ring_timings(fusp_ctx ctx, int max_steps, float* compute_ms
  * signal-and-wait kernel.  Results and TrafficLog bytes are identical to the comm path.  The
  * ring's hops (R > 1) go through the windows too (copies into the next member's ring buffers,
  * signals both ways) when the ring's members are separate processes or devices.  Windows
- * serve one Ulysses group and one ring group per context (the first layer's); other layers (other groups, D != 128, wire
- * debugging, shapes larger than a window) fall back to the backend -- counted by
- * fusp_ctx_peer_stats.  fusp_usp_block's QKV projection is the producer on this path: its
+ * serve one Ulysses group and one ring group per context (the first layer's); other layers
+ * (other groups, D != 128, wire debugging, shapes larger than a window) fall back to the
+ * backend -- counted by fusp_ctx_peer_stats.  The fused QK RMSNorm + RoPE packs store into the
+ * windows like the plain pack.  fusp_usp_block's QKV projection is the producer on this path: its
  * epilogue stores Q, K, V into the members' windows (GEMM and input all-to-all in one kernel),
  * and its output projection reads O where the members' epilogues stored it.  A peer-path layer
  * needs no host rendezvous, so it is graph-capturable on any context.
