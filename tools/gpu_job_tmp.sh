@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-FUSP_TIMEOUT_S=30 timeout 900 python -m pytest tests/test_gpu_peer.py tests/test_gpu_prologue.py -q -p no:cacheprovider > gpurun_out/pro.log 2>&1; echo "rc=$?" >> gpurun_out/pro.log; tail -15 gpurun_out/pro.log
+FUSP_TIMEOUT_S=60 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log; tail -3 gpurun_out/gpu_tests.log; grep "^FAILED" gpurun_out/gpu_tests.log | head
+timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; cut -c1-300 gpurun_out/bench.json
